@@ -1,0 +1,196 @@
+// bfs.cu -- level-synchronous BFS driver over the adaptive
+// multiply: x = frontier, y = A x (A as stored), next frontier =
+// {i : y_i != identity and level[i] unset}.  The frontier update is one fused
+// compaction kernel over y (dense or sparse view) that writes the next
+// frontier's index list + values and the levels in the same pass; only the
+// frontier size crosses to the host per level.
+//
+// Semirings: PLUS_TIMES with frontier values 1.0 is the reference-spec
+// driver; OR_AND is the pattern-only boolean BFS; MIN_PLUS
+// carries levels as values (y_i = min_j level_j + a_ij).
+#include <chrono>
+
+#include "device.cuh"
+#include "internal.hpp"
+#include "kernels.hpp"
+#include "prims.cuh"
+
+namespace ada {
+
+namespace {
+
+using clk = std::chrono::steady_clock;
+
+double secs(clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); }
+
+__global__ void init_levels_kernel(int32_t* lv, int64_t n, int64_t source) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) lv[i] = i == source ? 0 : -1;
+}
+
+template <class V, int SR>
+struct DenseFrontierIn {
+    const V* y;
+    const int32_t* lv;
+    __device__ int64_t operator()(int64_t i) const {
+        return (y[i] != Semiring<SR, V>::zero() && lv[i] < 0) ? 1 : 0;
+    }
+};
+
+template <class V, int SR>
+struct SparseFrontierIn {
+    const int32_t* yi;
+    const V* yv;
+    const int32_t* lv;
+    __device__ int64_t operator()(int64_t k) const {
+        return (yv[k] != Semiring<SR, V>::zero() && lv[yi[k]] < 0) ? 1 : 0;
+    }
+};
+
+template <class V>
+struct FrontierEpi {
+    const int32_t* yi;  // null for the dense view (row = i)
+    int32_t* lv;
+    int32_t* xi;
+    V* xv;
+    int32_t level;
+    V value;
+    __device__ void operator()(int64_t i, int64_t p, int64_t v) const {
+        if (!v) return;
+        const int32_t row = yi ? yi[i] : static_cast<int32_t>(i);
+        lv[row] = level;
+        xi[p] = row;
+        xv[p] = value;
+    }
+};
+
+template <class V, int SR>
+int64_t next_frontier(Context& ctx, Output& y, Vector& x, int32_t* lv, int32_t level) {
+    x.invalidate();
+    int32_t* xi = static_cast<int32_t*>(x.sp_idx.ensure(sizeof(int32_t) * static_cast<size_t>(x.n)));
+    V* xv = static_cast<V*>(x.sp_val.ensure(sizeof(V) * static_cast<size_t>(x.n)));
+    const V value = SR == SR_MIN_PLUS ? V(level) : V(1);
+    if (y.has_sparse) {
+        const int64_t nnz = output_nnz(ctx, y);
+        scan3(ctx, nnz, SparseFrontierIn<V, SR>{y.sp_idx.as<int32_t>(), y.sp_val.as<V>(), lv},
+              FrontierEpi<V>{y.sp_idx.as<int32_t>(), lv, xi, xv, level, value}, ctx.dscal(2),
+              ctx.scratch[4]);
+    } else {
+        scan3(ctx, y.n, DenseFrontierIn<V, SR>{y.dense.as<V>(), lv},
+              FrontierEpi<V>{nullptr, lv, xi, xv, level, value}, ctx.dscal(2), ctx.scratch[4]);
+    }
+    x.nnz = ctx.fetch_scalar(ctx.dscal(2));
+    x.has_sparse = true;
+    return x.nnz;
+}
+
+// Push vs pull by the algorithmic-bytes model of SURVEY.md section 8(d):
+// column-major reads ~ nnz_s entries, row-major (validated) reads every index.
+int heuristic_kernel(Context& ctx, const Matrix& m, Vector& x) {
+    const int64_t nnz_s = vector_nnz_s(ctx, x, m);
+    const double vb = m.vbytes();
+    const double push = static_cast<double>(x.nnz) * 20.0 + static_cast<double>(nnz_s) * (4.0 + vb) +
+                        (nnz_s <= 4096 ? 0.0 : static_cast<double>(m.rows) * vb);
+    const double pull = static_cast<double>(m.rows + 1) * 8.0 + static_cast<double>(m.nnz) * 4.0 +
+                        static_cast<double>(nnz_s) * vb + static_cast<double>(m.cols) * vb;
+    if (push <= pull) return nnz_s <= 4096 ? 7 : 6;
+    return 3;
+}
+
+template <class V, int SR>
+void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int forced,
+           int64_t* levels, int64_t* n_levels, adaspmv_iteration_report* reports,
+           int64_t max_reports) {
+    const int64_t n = m.rows;
+    DevBuf lvb;
+    int32_t* lv = static_cast<int32_t*>(lvb.ensure(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(n, 1))));
+    init_levels_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx.stream>>>(lv, n, source);
+    ADA_LAUNCHED(ctx);
+    Vector x;
+    x.ctx = &ctx;
+    x.n = n;
+    x.dtype = m.dtype;
+    {
+        int32_t* xi = static_cast<int32_t*>(x.sp_idx.ensure(sizeof(int32_t) * static_cast<size_t>(n)));
+        V* xv = static_cast<V*>(x.sp_val.ensure(sizeof(V) * static_cast<size_t>(n)));
+        const int32_t s32 = static_cast<int32_t>(source);
+        const V one = SR == SR_MIN_PLUS ? V(0) : V(1);
+        ADA_CUDA(cudaMemcpyAsync(xi, &s32, sizeof(s32), cudaMemcpyHostToDevice, ctx.stream));
+        ADA_CUDA(cudaMemcpyAsync(xv, &one, sizeof(one), cudaMemcpyHostToDevice, ctx.stream));
+        x.nnz = 1;
+        x.has_sparse = true;
+        ctx.sync();
+    }
+    Output y;
+    y.ctx = &ctx;
+    adaspmv_config cfg{};
+    cfg.semiring = SR;
+    int64_t it = 0;
+    while (x.nnz > 0) {
+        const auto t0 = clk::now();
+        int k;
+        if (b) k = predict(ctx, m, x, *b, nullptr, nullptr);
+        else if (forced >= 0) k = forced;
+        else k = heuristic_kernel(ctx, m, x);
+        const auto t1 = clk::now();
+        if (k <= 3) {
+            vector_ensure_dense(ctx, x);
+            if (k >= 2) vector_ensure_mask(ctx, x);
+        } else if (k == 6 || k == 7) {
+            vector_ensure_eff(ctx, x, m);
+        }
+        ctx.sync();
+        const auto t2 = clk::now();
+        const int64_t nnz_x = x.nnz;
+        run_kernel(ctx, m, x, k, cfg, y);
+        ctx.sync();
+        const auto t3 = clk::now();
+        next_frontier<V, SR>(ctx, y, x, lv, static_cast<int32_t>(it + 1));
+        if (reports && it < max_reports) {
+            adaspmv_iteration_report& r = reports[it];
+            r.iteration = it;
+            r.nnz_x = nnz_x;
+            r.kernel = k;
+            r.pad = 0;
+            r.predict_s = secs(t0, t1);
+            r.feature_s = 0;  // features are pulled inside predict (lazy)
+            r.convert_s = secs(t1, t2);
+            r.kernel_s = secs(t2, t3);
+        }
+        ++it;
+    }
+    std::vector<int32_t> h(static_cast<size_t>(n));
+    ADA_CUDA(cudaMemcpyAsync(h.data(), lv, sizeof(int32_t) * static_cast<size_t>(n), cudaMemcpyDeviceToHost,
+                             ctx.stream));
+    ctx.sync();
+    for (int64_t i = 0; i < n; ++i) levels[i] = h[static_cast<size_t>(i)];
+    *n_levels = it;
+}
+
+}  // namespace
+
+void bfs(Context& ctx, const Matrix& m, int64_t source, int semiring, const Bundle* b, int forced,
+         int64_t* levels, int64_t* n_levels, adaspmv_iteration_report* reports,
+         int64_t max_reports) {
+    if (m.rows != m.cols) invalid("bfs: matrix must be square");
+    if (source < 0 || source >= m.rows) invalid("bfs: source out of range");
+    if (forced < -1 || forced > 7) invalid("bfs: forced kernel out of range");
+    const bool f64 = m.dtype == ADASPMV_F64;
+    switch (semiring) {
+        case ADASPMV_PLUS_TIMES:
+            f64 ? bfs_t<double, SR_PLUS_TIMES>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports)
+                : bfs_t<float, SR_PLUS_TIMES>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports);
+            break;
+        case ADASPMV_OR_AND:
+            f64 ? bfs_t<double, SR_OR_AND>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports)
+                : bfs_t<float, SR_OR_AND>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports);
+            break;
+        case ADASPMV_MIN_PLUS:
+            f64 ? bfs_t<double, SR_MIN_PLUS>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports)
+                : bfs_t<float, SR_MIN_PLUS>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports);
+            break;
+        default: invalid("unknown semiring");
+    }
+}
+
+}  // namespace ada

@@ -1,0 +1,231 @@
+// internal.hpp -- host-side object model of libadaspmv_cuda (not installed).
+//
+// Objects behind the C-ABI handles of include/adaspmv_cuda.h:
+//   Context  one device + one stream + grow-only scratch (parallel.hpp's
+//            ThreadPool is replaced by CUDA grids on this stream)
+//   Matrix   device-resident DualMatrix (sparse.hpp:204-259): CSR + CSC,
+//            int64 offsets, int32 indices, fp32/fp64 values; matrix-static
+//            LB tile heads; the 9 matrix features
+//   Vector   one operand x with its lazily-built representations
+//            (OperandViews, kernels.hpp:171-175)
+//   Output   MultiplyOutput (kernels.hpp:116-152)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/adaspmv_cuda.h"
+
+namespace ada {
+
+// Status-carrying exception; converted to adaspmv_status at the C-ABI.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void invalid(const std::string& m) { throw Error(ADASPMV_ERR_INVALID_ARGUMENT, m); }
+[[noreturn]] inline void out_of_range(const std::string& m) { throw Error(ADASPMV_ERR_OUT_OF_RANGE, m); }
+
+#define ADA_CUDA(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t e_ = (expr);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            throw ::ada::Error(e_ == cudaErrorMemoryAllocation ? ADASPMV_ERR_NOMEM          \
+                                                               : ADASPMV_ERR_CUDA,          \
+                               std::string(#expr) + ": " + cudaGetErrorString(e_));        \
+    } while (0)
+
+// After every kernel launch: catches configuration errors immediately.
+#define ADA_LAUNCHED(ctx)                                                                   \
+    do {                                                                                    \
+        ADA_CUDA(cudaGetLastError());                                                       \
+        (ctx).launches++;                                                                   \
+    } while (0)
+
+inline int value_bytes(int dtype) { return dtype == ADASPMV_F64 ? 8 : 4; }
+
+// Grow-only device allocation.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), cap(o.cap) { o.p = nullptr; o.cap = 0; }
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    void* ensure(size_t bytes) {
+        if (bytes <= cap && p) return p;
+        release();
+        size_t want = bytes < 256 ? 256 : bytes;
+        ADA_CUDA(cudaMalloc(&p, want));
+        cap = want;
+        return p;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct Context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 148;
+    int64_t launches = 0;
+    // general scratch (reused by every call; calls on a context are serialised)
+    DevBuf scratch[6];
+    // pinned host scalars for D2H of counts (nnz_s, nnz_y, ...)
+    int64_t* h_scalars = nullptr;
+    DevBuf d_scalars;  // 64 int64 slots
+    // pinned staging for host vector uploads
+    void* h_stage = nullptr;
+    size_t h_stage_cap = 0;
+    void* stage(size_t bytes);  // pinned host buffer of >= bytes
+    void sync() { ADA_CUDA(cudaStreamSynchronize(stream)); }
+    int64_t* dscal(int i) { return d_scalars.as<int64_t>() + i; }
+    // D2H one device int64 (synchronises the stream)
+    int64_t fetch_scalar(const int64_t* d);
+};
+
+// LB tiles of the row-major kernels: fixed TILE nonzeros per CTA
+// (make_partition's equal-item split, partition.hpp:37-56, with W = ceil(nnz/TILE)).
+constexpr int kRowTile = 2048;
+
+struct Matrix {
+    Context* ctx = nullptr;
+    int64_t rows = 0, cols = 0, nnz = 0;
+    int dtype = ADASPMV_F64;
+    uint64_t id = 0;
+    DevBuf row_off, col_idx, vals;   // CSR
+    DevBuf col_off, row_idx, cvals;  // CSC
+    int64_t n_row_tiles = 0;
+    DevBuf tile_head;       // int64 [n_row_tiles+1]: segment_of(row_off, t*kRowTile)
+    DevBuf tile_rs;         // int64 [n_row_tiles+1]: first row with row_off >= t*kRowTile
+    DevBuf tile_partials;   // per tile: head partial, tail partial (V) + tail row (int64)
+    double feat[9] = {0};
+    int64_t max_col_deg = 0;
+    double avg_col = 0;
+    bool pattern = false;   // created without values (all 1.0)
+    int vbytes() const { return value_bytes(dtype); }
+};
+
+struct Vector {
+    Context* ctx = nullptr;
+    int64_t n = 0;
+    int dtype = ADASPMV_F64;
+    uint64_t version = 0;
+    // representations (kernels.hpp:171-175)
+    DevBuf dense;   bool has_dense = false;
+    DevBuf sp_idx;  DevBuf sp_val; bool has_sparse = false;
+    int64_t nnz = -1;  // |supp x| when known on host (sparse input, or counted)
+    DevBuf mask;    bool has_mask = false;   // (n+31)/32 u32 words == (n+63)/64 u64 LSB-first
+    // effective-nnz prefix (eff_offsets, kernels.hpp:400-404) for one matrix
+    DevBuf eff;     uint64_t eff_matrix = 0; bool has_eff = false;
+    int64_t nnz_s = -1; uint64_t nnz_s_matrix = 0;
+    DevBuf stage_idx;  // int64 staging for host index uploads
+    void invalidate() {
+        has_dense = has_sparse = has_mask = has_eff = false;
+        nnz = -1;
+        nnz_s = -1;
+        nnz_s_matrix = 0;
+        eff_matrix = 0;
+        ++version;
+    }
+};
+
+struct Output {
+    Context* ctx = nullptr;
+    int64_t n = 0;
+    int dtype = ADASPMV_F64;
+    DevBuf dense;   bool has_dense = false;
+    DevBuf sp_idx;  DevBuf sp_val; bool has_sparse = false;
+    int64_t nnz = -1;      // host-known nnz_y (-1 = only on device, slot d_nnz)
+    DevBuf d_nnz;          // device int64 nnz_y
+    int semiring = ADASPMV_PLUS_TIMES;  // identity of absent entries
+    void reset(int64_t len, int dt) {
+        n = len;
+        dtype = dt;
+        has_dense = has_sparse = false;
+        nnz = -1;
+    }
+};
+
+// One decision tree: flat node array.
+struct Tree {
+    int target = 0;          // 0 pattern, 1 workload, 2 write-back
+    uint32_t mask = 0x1fff;  // features the tree may read
+    std::vector<int32_t> feature, left, right, leaf;
+    std::vector<double> threshold;
+};
+
+struct Bundle {
+    int schema_version = 1;
+    std::string hardware_tag;
+    std::string feature_order_hash;
+    Tree trees[3];
+};
+
+// ---- entry points implemented in the .cu/.cpp files ------------------------
+Matrix* matrix_create_device(Context& ctx, int64_t rows, int64_t cols, int64_t nnz,
+                             const int64_t* d_ro, const int32_t* d_ci, const void* d_vals,
+                             int dtype, bool pattern);
+Matrix* matrix_transpose(Context& ctx, const Matrix& m);
+
+void vector_set_dense_device(Context& ctx, Vector& v, const void* d_vals);
+void vector_set_sparse_device(Context& ctx, Vector& v, int64_t nnz, const int32_t* d_idx,
+                              const void* d_vals);
+void vector_ensure_dense(Context& ctx, Vector& v);
+void vector_ensure_sparse(Context& ctx, Vector& v);
+void vector_ensure_mask(Context& ctx, Vector& v);
+void vector_ensure_eff(Context& ctx, Vector& v, const Matrix& m);  // also sparse
+int64_t vector_nnz(Context& ctx, Vector& v);
+int64_t vector_nnz_s(Context& ctx, Vector& v, const Matrix& m);
+
+void run_kernel(Context& ctx, const Matrix& m, Vector& x, int kernel, const adaspmv_config& cfg,
+                Output& y);
+void output_ensure_dense(Context& ctx, Output& y);
+void output_ensure_sparse(Context& ctx, Output& y);
+int64_t output_nnz(Context& ctx, Output& y);
+
+// device sort_reduce_pairs: keys int32 rows in [0, nrows); returns nnz
+int64_t sort_reduce_pairs_device(Context& ctx, int64_t npairs, const int32_t* d_rows,
+                                 const void* d_vals, int dtype, int64_t nrows, int32_t* d_out_idx,
+                                 void* d_out_val);
+
+// features / selector (selector.cpp)
+void features(Context& ctx, const Matrix& m, Vector& v, uint32_t mask, double* out13);
+int predict(Context& ctx, const Matrix& m, Vector& v, const Bundle& b, uint32_t* used,
+            int* trees);
+Bundle* bundle_load(const std::string& path);
+
+// host I/O (mmio.cpp): CSR in the reference layout
+struct HostCsr {
+    int64_t rows = 0, cols = 0;
+    std::vector<int64_t> row_offsets, col_indices;
+    std::vector<double> values;  // widened; narrowed per dtype at upload
+};
+HostCsr csr_from_triplets(int64_t rows, int64_t cols, int64_t count, const int64_t* tr,
+                          const int64_t* tc, const double* tv, bool round_f32);
+HostCsr load_matrix_file(const std::string& path, int dtype);
+void write_matrix_market_file(const std::string& path, int64_t rows, int64_t cols,
+                              const std::vector<int64_t>& ro, const std::vector<int64_t>& ci,
+                              const std::vector<double>& vals);
+void save_binary_file(const std::string& path, int64_t rows, int64_t cols,
+                      const std::vector<int64_t>& ro, const std::vector<int64_t>& ci,
+                      const void* vals, int dtype);
+
+// BFS (bfs.cu)
+void bfs(Context& ctx, const Matrix& m, int64_t source, int semiring, const Bundle* b,
+         int forced, int64_t* levels, int64_t* n_levels, adaspmv_iteration_report* reports,
+         int64_t max_reports);
+
+}  // namespace ada

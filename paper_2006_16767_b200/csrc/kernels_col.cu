@@ -1,0 +1,463 @@
+// kernels_col.cu -- the four column-major kernels (CSC scatter driven by the
+// nonzeros of x; spmspv_col, kernels.hpp:377-514).  Only the effective
+// nonzeros (sparse.hpp:346-359) are read.
+//
+//   K4 col_direct_atomic  whole support columns per lane group (:394-398),
+//                         atomic write-back into a dense y (:436-451)
+//   K5 col_direct_sort    same distribution, sort write-back (:489-513)
+//   K6 col_lb_atomic      equal effective-nnz tiles over eff_offsets
+//                         (:399-432), atomic write-back
+//   K7 col_lb_sort        LB distribution, sort write-back
+//
+// Sort write-back (emit pairs, sort, reduce-by-key):
+// (row, a_rj * x_j) pairs are emitted at position eff_offsets[s] + (k -
+// col_offsets[j]) -- a deterministic order -- then stably radix-sorted by row
+// and reduced by key in order, exact-zero sums dropped (kernels.hpp:331), so
+// the sparse y is bitwise reproducible run to run (kernels.hpp:374-376).
+// Inputs whose pair count fits one CTA (kSmallPairs) run emit + sort + reduce
+// + compaction in a single launch with no host synchronisation: the
+// latency-bound sparse end of the sweep.
+#include <algorithm>
+
+#include "device.cuh"
+#include "internal.hpp"
+#include "kernels.hpp"
+#include "prims.cuh"
+
+namespace ada {
+
+namespace {
+
+constexpr int kNT = 256;
+constexpr int kU = 4;
+constexpr int kColTile = 2048;           // effective entries per LB tile
+constexpr int kColIPT = kColTile / kNT;  // 8 consecutive entries per thread
+constexpr int kSmallPairs = 4096;        // single-CTA sort path capacity
+constexpr int kSmallNT = 1024;
+
+int blocks_for(int64_t work, int t) {
+    return static_cast<int>(std::max<int64_t>(1, (work + t - 1) / t));
+}
+
+// ---------------------------------------------------------------------------
+// K4: G lanes per support column, atomic scatter
+// ---------------------------------------------------------------------------
+template <class V, int G, int SR>
+__global__ void __launch_bounds__(kNT) col_direct_atomic_kernel(
+    int64_t nnz_x, const int32_t* __restrict__ xi, const V* __restrict__ xv,
+    const int64_t* __restrict__ co, const int32_t* __restrict__ ri, const V* __restrict__ cv,
+    V* __restrict__ y) {
+    using S = Semiring<SR, V>;
+    const int64_t gid = static_cast<int64_t>(blockIdx.x) * kNT + threadIdx.x;
+    const int64_t s = gid / G;
+    const int lg = threadIdx.x & (G - 1);
+    if (s >= nnz_x) return;  // no cross-lane communication below
+    const int32_t col = __ldg(xi + s);
+    const V xval = __ldg(xv + s);
+    const int64_t b = __ldg(co + col), e = __ldg(co + col + 1);
+    for (int64_t k0 = b + lg; k0 < e; k0 += G * kU) {
+        int r[kU];
+        V a[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            const int64_t k = k0 + j * G;
+            if (k < e) {
+                r[j] = __ldg(ri + k);
+                a[j] = S::kUsesValues ? __ldg(cv + k) : V(1);
+            } else {
+                r[j] = -1;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kU; ++j)
+            if (r[j] >= 0) AtomicCombine<SR>::apply(y + r[j], S::mul(a[j], xval));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6: equal effective-nnz tiles; each thread owns 8 consecutive effective
+// entries located by segment_of over eff_offsets (partition.hpp:30-33) and a
+// forward walk (entry_range clipping, kernels.hpp:422-432).
+// ---------------------------------------------------------------------------
+template <class V, int SR, bool EMIT>
+__global__ void __launch_bounds__(kNT) col_lb_kernel(
+    int64_t nnz_x, int64_t nnz_s, const int64_t* __restrict__ eff, const int32_t* __restrict__ xi,
+    const V* __restrict__ xv, const int64_t* __restrict__ co, const int32_t* __restrict__ ri,
+    const V* __restrict__ cv, V* __restrict__ y, uint32_t* __restrict__ keys,
+    V* __restrict__ pvals) {
+    using S = Semiring<SR, V>;
+    __shared__ int64_t s_range[2];
+    const int64_t tb = static_cast<int64_t>(blockIdx.x) * kColTile;
+    const int64_t te = min(tb + static_cast<int64_t>(kColTile), nnz_s);
+    if (threadIdx.x < 2) {  // support span of the tile
+        const int64_t pos = threadIdx.x == 0 ? tb : te - 1;
+        s_range[threadIdx.x] = segment_search(eff, 0, nnz_x + 1, pos);
+    }
+    __syncthreads();
+    const int64_t s_lo = s_range[0], s_hi = s_range[1] + 1;
+    const int64_t p0 = tb + static_cast<int64_t>(threadIdx.x) * kColIPT;
+    if (p0 >= te) return;
+    const int64_t p1 = min(p0 + kColIPT, te);
+    int64_t s = segment_search(eff, s_lo, s_hi, p0);
+    int64_t s_end = __ldg(eff + s + 1);
+    int32_t col = __ldg(xi + s);
+    V xval = __ldg(xv + s);
+    int64_t base = __ldg(co + col) - __ldg(eff + s);
+    for (int64_t p = p0; p < p1; ++p) {
+        while (p >= s_end) {
+            ++s;
+            s_end = __ldg(eff + s + 1);
+            col = __ldg(xi + s);
+            xval = __ldg(xv + s);
+            base = __ldg(co + col) - __ldg(eff + s);
+        }
+        const int64_t k = base + p;
+        const int32_t r = __ldg(ri + k);
+        const V a = S::kUsesValues ? __ldg(cv + k) : V(1);
+        if (EMIT) {
+            keys[p] = static_cast<uint32_t>(r);
+            pvals[p] = S::mul(a, xval);
+        } else {
+            AtomicCombine<SR>::apply(y + r, S::mul(a, xval));
+        }
+    }
+}
+
+// K5 emission: G lanes per support column write pairs at eff[s] + offset.
+template <class V, int G, int SR>
+__global__ void __launch_bounds__(kNT) col_direct_emit_kernel(
+    int64_t nnz_x, const int64_t* __restrict__ eff, const int32_t* __restrict__ xi,
+    const V* __restrict__ xv, const int64_t* __restrict__ co, const int32_t* __restrict__ ri,
+    const V* __restrict__ cv, uint32_t* __restrict__ keys, V* __restrict__ pvals) {
+    using S = Semiring<SR, V>;
+    const int64_t gid = static_cast<int64_t>(blockIdx.x) * kNT + threadIdx.x;
+    const int64_t s = gid / G;
+    const int lg = threadIdx.x & (G - 1);
+    if (s >= nnz_x) return;
+    const int32_t col = __ldg(xi + s);
+    const V xval = __ldg(xv + s);
+    const int64_t b = __ldg(co + col), e = __ldg(co + col + 1);
+    const int64_t out = __ldg(eff + s) - b;
+    for (int64_t k = b + lg; k < e; k += G) {
+        keys[out + k] = static_cast<uint32_t>(__ldg(ri + k));
+        pvals[out + k] = S::mul(S::kUsesValues ? __ldg(cv + k) : V(1), xval);
+    }
+}
+
+// Segment sums of the row-sorted pair stream (reduce_sorted_pairs,
+// kernels.hpp:323-337): each head sums its run in order; flag = sum != zero.
+template <class V, int SR>
+__global__ void seg_reduce_kernel(int64_t n, const uint32_t* __restrict__ keys,
+                                  const V* __restrict__ vals, V* __restrict__ sums,
+                                  uint8_t* __restrict__ keep) {
+    using S = Semiring<SR, V>;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = keys[i];
+    if (i > 0 && keys[i - 1] == k) {
+        keep[i] = 0;
+        return;
+    }
+    V acc = vals[i];
+    for (int64_t j = i + 1; j < n && keys[j] == k; ++j) acc = S::add(acc, vals[j]);
+    sums[i] = acc;
+    keep[i] = acc != S::zero() ? 1 : 0;
+}
+
+struct KeepIn {
+    const uint8_t* keep;
+    __device__ int64_t operator()(int64_t i) const { return keep[i]; }
+};
+
+template <class V>
+struct KeepEpi {
+    const uint32_t* keys;
+    const V* sums;
+    int32_t* out_idx;
+    V* out_val;
+    __device__ void operator()(int64_t i, int64_t p, int64_t v) const {
+        if (v) {
+            out_idx[p] = static_cast<int32_t>(keys[i]);
+            out_val[p] = sums[i];
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Single-CTA sort write-back for <= kSmallPairs pairs: degrees + scan of the
+// support, emission into shared memory, bitonic sort on (row, emission index)
+// -- unique keys, hence stable --, reduce-by-key and compaction.
+// ---------------------------------------------------------------------------
+template <class V, int SR>
+__global__ void __launch_bounds__(kSmallNT) col_sort_small_kernel(
+    int64_t nnz_x, const int32_t* __restrict__ xi, const V* __restrict__ xv,
+    const int64_t* __restrict__ co, const int32_t* __restrict__ ri, const V* __restrict__ cv,
+    int32_t* __restrict__ out_idx, V* __restrict__ out_val, int64_t* __restrict__ d_nnz) {
+    using S = Semiring<SR, V>;
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* skey = reinterpret_cast<uint64_t*>(smem);                  // kSmallPairs
+    V* sval = reinterpret_cast<V*>(skey + kSmallPairs);                  // kSmallPairs
+    int* sflag = reinterpret_cast<int*>(sval + kSmallPairs);             // kSmallPairs
+    __shared__ int64_t sm_scan[kSmallNT / 32 + 1];
+
+    // 1. emit: support processed in chunks of kSmallNT columns; one thread per
+    //    support column walks its entries (columns are short on this path).
+    int64_t base = 0;
+    for (int64_t c0 = 0; c0 < nnz_x; c0 += kSmallNT) {
+        const int64_t s = c0 + threadIdx.x;
+        int64_t deg = 0, b = 0;
+        int32_t col = 0;
+        if (s < nnz_x) {
+            col = xi[s];
+            b = co[col];
+            deg = co[col + 1] - b;
+        }
+        int64_t tot;
+        const int64_t off = block_exclusive_sum<kSmallNT>(deg, sm_scan, &tot) + base;
+        if (s < nnz_x) {
+            const V xval = xv[s];
+            for (int64_t k = 0; k < deg; ++k) {
+                const int64_t o = off + k;
+                skey[o] = (static_cast<uint64_t>(static_cast<uint32_t>(ri[b + k])) << 32) |
+                          static_cast<uint64_t>(o);
+                sval[o] = S::mul(S::kUsesValues ? cv[b + k] : V(1), xval);
+            }
+        }
+        base += tot;
+    }
+    const int n = static_cast<int>(base);
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    for (int i = n + threadIdx.x; i < np2; i += kSmallNT) skey[i] = ~0ull;
+    __syncthreads();
+    // 2. bitonic sort (ascending) of keys with values
+    for (int k = 2; k <= np2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < np2; i += kSmallNT) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k) == 0;
+                    const uint64_t a = skey[i], b = skey[ixj];
+                    if ((a > b) == up) {
+                        skey[i] = b;
+                        skey[ixj] = a;
+                        const V t = sval[i];  // padded slots carry garbage values
+                        sval[i] = sval[ixj];
+                        sval[ixj] = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // 3. reduce by key: heads sum their run in order
+    for (int i = threadIdx.x; i < n; i += kSmallNT) {
+        const uint32_t r = static_cast<uint32_t>(skey[i] >> 32);
+        int keep = 0;
+        if (i == 0 || static_cast<uint32_t>(skey[i - 1] >> 32) != r) {
+            V acc = sval[i];
+            for (int j = i + 1; j < n && static_cast<uint32_t>(skey[j] >> 32) == r; ++j)
+                acc = S::add(acc, sval[j]);
+            keep = acc != S::zero();
+            if (keep) sval[i] = acc;  // only heads are read back
+        }
+        sflag[i] = keep;
+    }
+    __syncthreads();
+    // 4. compaction in row order
+    int64_t outbase = 0;
+    for (int c0 = 0; c0 < n; c0 += kSmallNT) {
+        const int i = c0 + threadIdx.x;
+        const int64_t f = i < n ? sflag[i] : 0;
+        int64_t tot;
+        const int64_t p = block_exclusive_sum<kSmallNT>(f, sm_scan, &tot) + outbase;
+        if (f) {
+            out_idx[p] = static_cast<int32_t>(skey[i] >> 32);
+            out_val[p] = sval[i];
+        }
+        outbase += tot;
+    }
+    if (threadIdx.x == 0) *d_nnz = outbase;
+}
+
+template <class V, int SR>
+size_t small_smem_bytes() {
+    return kSmallPairs * (sizeof(uint64_t) + sizeof(V) + sizeof(int));
+}
+
+template <class V, int SR>
+void launch_small_sort(Context& ctx, const Matrix& m, Vector& x, int32_t* y_idx, V* y_val,
+                       int64_t* d_nnz) {
+    const size_t smem = small_smem_bytes<V, SR>();
+    // per device; a host-side attribute write, no synchronisation
+    ADA_CUDA(cudaFuncSetAttribute(col_sort_small_kernel<V, SR>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    col_sort_small_kernel<V, SR><<<1, kSmallNT, smem, ctx.stream>>>(
+        x.nnz, x.sp_idx.as<int32_t>(), x.sp_val.as<V>(), m.col_off.as<int64_t>(),
+        m.row_idx.as<int32_t>(), m.cvals.as<V>(), y_idx, y_val, d_nnz);
+    ADA_LAUNCHED(ctx);
+}
+
+template <class V, int SR>
+void launch_direct_atomic(Context& ctx, const Matrix& m, Vector& x, int G, V* y) {
+    const unsigned blocks = static_cast<unsigned>(blocks_for(x.nnz * G, kNT));
+#define ADA_G(GG)                                                                            \
+    case GG:                                                                                 \
+        col_direct_atomic_kernel<V, GG, SR><<<blocks, kNT, 0, ctx.stream>>>(                 \
+            x.nnz, x.sp_idx.as<int32_t>(), x.sp_val.as<V>(), m.col_off.as<int64_t>(),        \
+            m.row_idx.as<int32_t>(), m.cvals.as<V>(), y);                                    \
+        break;
+    switch (G) {
+        ADA_G(1) ADA_G(2) ADA_G(4) ADA_G(8) ADA_G(16) ADA_G(32)
+        default: invalid("lanes_per_row must be a power of two <= 32");
+    }
+#undef ADA_G
+    ADA_LAUNCHED(ctx);
+}
+
+template <class V, int SR>
+void launch_direct_emit(Context& ctx, const Matrix& m, Vector& x, int G, uint32_t* keys, V* pv) {
+    const unsigned blocks = static_cast<unsigned>(blocks_for(x.nnz * G, kNT));
+#define ADA_G(GG)                                                                            \
+    case GG:                                                                                 \
+        col_direct_emit_kernel<V, GG, SR><<<blocks, kNT, 0, ctx.stream>>>(                   \
+            x.nnz, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),            \
+            m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), keys, pv);    \
+        break;
+    switch (G) {
+        ADA_G(1) ADA_G(2) ADA_G(4) ADA_G(8) ADA_G(16) ADA_G(32)
+        default: invalid("lanes_per_row must be a power of two <= 32");
+    }
+#undef ADA_G
+    ADA_LAUNCHED(ctx);
+}
+
+}  // namespace
+
+template <class V, int SR>
+void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort, bool private_acc,
+                   int lanes, V* y_dense, int32_t* y_idx, V* y_val, int64_t* d_nnz,
+                   int64_t* h_nnz) {
+    (void)private_acc;
+    vector_ensure_sparse(ctx, x);
+    const int G = lanes > 0 ? lanes : default_lanes_per_row(m.avg_col);
+    *h_nnz = -1;
+    if (!sort) {
+        // atomic write-back into a dense y initialised to the identity
+        fill_value<V, SR>(ctx, y_dense, m.rows);
+        if (x.nnz == 0 || m.nnz == 0) return;
+        if (!lb) {
+            launch_direct_atomic<V, SR>(ctx, m, x, G, y_dense);
+            return;
+        }
+        const int64_t nnz_s = vector_nnz_s(ctx, x, m);
+        if (nnz_s == 0) return;
+        const unsigned tiles = static_cast<unsigned>((nnz_s + kColTile - 1) / kColTile);
+        col_lb_kernel<V, SR, false><<<tiles, kNT, 0, ctx.stream>>>(
+            x.nnz, nnz_s, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
+            m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), y_dense, nullptr,
+            nullptr);
+        ADA_LAUNCHED(ctx);
+        return;
+    }
+    // ---- sort write-back -> sparse y ---------------------------------------
+    if (x.nnz == 0 || m.nnz == 0) {
+        ADA_CUDA(cudaMemsetAsync(d_nnz, 0, sizeof(int64_t), ctx.stream));
+        *h_nnz = 0;
+        return;
+    }
+    // pair-count bound without a device round trip when possible
+    int64_t bound = m.max_col_deg > 0 && x.nnz <= kSmallPairs ? x.nnz * m.max_col_deg : INT64_MAX;
+    if (x.nnz_s >= 0 && x.nnz_s_matrix == m.id) bound = x.nnz_s;
+    if (bound > kSmallPairs) bound = vector_nnz_s(ctx, x, m);
+    if (bound <= kSmallPairs && x.nnz <= kSmallPairs) {
+        launch_small_sort<V, SR>(ctx, m, x, y_idx, y_val, d_nnz);
+        return;
+    }
+    const int64_t nnz_s = vector_nnz_s(ctx, x, m);
+    DevBuf& kb0 = ctx.scratch[0];
+    DevBuf& kb1 = ctx.scratch[1];
+    DevBuf& vb0 = ctx.scratch[2];
+    DevBuf& vb1 = ctx.scratch[3];
+    const size_t z = static_cast<size_t>(nnz_s);
+    uint32_t* k0 = static_cast<uint32_t*>(kb0.ensure(sizeof(uint32_t) * z));
+    uint32_t* k1 = static_cast<uint32_t*>(kb1.ensure(sizeof(uint32_t) * z));
+    V* v0 = static_cast<V*>(vb0.ensure(sizeof(V) * z));
+    V* v1 = static_cast<V*>(vb1.ensure(sizeof(V) * z));
+    if (!lb) {
+        launch_direct_emit<V, SR>(ctx, m, x, G, k0, v0);
+    } else {
+        const unsigned tiles = static_cast<unsigned>((nnz_s + kColTile - 1) / kColTile);
+        col_lb_kernel<V, SR, true><<<tiles, kNT, 0, ctx.stream>>>(
+            x.nnz, nnz_s, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
+            m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), nullptr, k0, v0);
+        ADA_LAUNCHED(ctx);
+    }
+    static thread_local DevBuf counts, scan_tmp, sums, keep;
+    const int which = radix_sort_pairs<V>(ctx, k0, v0, k1, v1, nnz_s, bits_for(m.rows), counts,
+                                          scan_tmp);
+    const uint32_t* sk = which ? k1 : k0;
+    const V* sv = which ? v1 : v0;
+    V* ssum = static_cast<V*>(sums.ensure(sizeof(V) * z));
+    uint8_t* kp = static_cast<uint8_t*>(keep.ensure(z));
+    seg_reduce_kernel<V, SR><<<blocks_for(nnz_s, 256), 256, 0, ctx.stream>>>(nnz_s, sk, sv, ssum, kp);
+    ADA_LAUNCHED(ctx);
+    scan3(ctx, nnz_s, KeepIn{kp}, KeepEpi<V>{sk, ssum, y_idx, y_val}, d_nnz, scan_tmp);
+}
+
+namespace {
+__global__ void rows_to_keys_kernel(int64_t n, const int32_t* __restrict__ rows,
+                                    uint32_t* __restrict__ keys) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) keys[i] = static_cast<uint32_t>(rows[i]);
+}
+
+template <class V>
+int64_t sort_reduce_t(Context& ctx, int64_t n, const int32_t* d_rows, const void* d_vals,
+                      int64_t nrows, int32_t* out_idx, V* out_val) {
+    if (n == 0) return 0;
+    const size_t z = static_cast<size_t>(n);
+    DevBuf k0, k1, v0, v1, counts, scan_tmp, sums, keep;
+    uint32_t* pk0 = static_cast<uint32_t*>(k0.ensure(sizeof(uint32_t) * z));
+    uint32_t* pk1 = static_cast<uint32_t*>(k1.ensure(sizeof(uint32_t) * z));
+    V* pv0 = static_cast<V*>(v0.ensure(sizeof(V) * z));
+    V* pv1 = static_cast<V*>(v1.ensure(sizeof(V) * z));
+    rows_to_keys_kernel<<<blocks_for(n, 256), 256, 0, ctx.stream>>>(n, d_rows, pk0);
+    ADA_LAUNCHED(ctx);
+    ADA_CUDA(cudaMemcpyAsync(pv0, d_vals, sizeof(V) * z, cudaMemcpyDeviceToDevice, ctx.stream));
+    const int which = radix_sort_pairs<V>(ctx, pk0, pv0, pk1, pv1, n, bits_for(nrows), counts, scan_tmp);
+    const uint32_t* sk = which ? pk1 : pk0;
+    const V* sv = which ? pv1 : pv0;
+    V* ssum = static_cast<V*>(sums.ensure(sizeof(V) * z));
+    uint8_t* kp = static_cast<uint8_t*>(keep.ensure(z));
+    seg_reduce_kernel<V, SR_PLUS_TIMES><<<blocks_for(n, 256), 256, 0, ctx.stream>>>(n, sk, sv, ssum, kp);
+    ADA_LAUNCHED(ctx);
+    scan3(ctx, n, KeepIn{kp}, KeepEpi<V>{sk, ssum, out_idx, out_val}, ctx.dscal(1), scan_tmp);
+    const int64_t r = ctx.fetch_scalar(ctx.dscal(1));
+    return r;
+}
+}  // namespace
+
+int64_t sort_reduce_pairs_device(Context& ctx, int64_t npairs, const int32_t* d_rows,
+                                 const void* d_vals, int dtype, int64_t nrows, int32_t* d_out_idx,
+                                 void* d_out_val) {
+    if (dtype == ADASPMV_F64)
+        return sort_reduce_t<double>(ctx, npairs, d_rows, d_vals, nrows, d_out_idx,
+                                     static_cast<double*>(d_out_val));
+    return sort_reduce_t<float>(ctx, npairs, d_rows, d_vals, nrows, d_out_idx,
+                                static_cast<float*>(d_out_val));
+}
+
+#define ADA_INST(V, SR)                                                                       \
+    template void run_col_major<V, SR>(Context&, const Matrix&, Vector&, bool, bool, bool, int, \
+                                       V*, int32_t*, V*, int64_t*, int64_t*);
+ADA_INST(float, SR_PLUS_TIMES)
+ADA_INST(double, SR_PLUS_TIMES)
+ADA_INST(float, SR_OR_AND)
+ADA_INST(double, SR_OR_AND)
+ADA_INST(float, SR_MIN_PLUS)
+ADA_INST(double, SR_MIN_PLUS)
+#undef ADA_INST
+
+}  // namespace ada

@@ -1,0 +1,373 @@
+// matrix.cu -- device-resident DualMatrix (sparse.hpp:204-259).
+//
+// Upload keeps the CSR as given (int64 offsets, indices narrowed to int32)
+// and builds the CSC on the device with the reference's stable order
+// (csr_to_csc, sparse.hpp:157-178: rows ascending within each column) by a
+// stable LSD radix sort of (column, (row, value)) in CSR order.  The matrix
+// features and the LB tile heads (partition.hpp:30-33) are
+// computed once here ("computed only once at the beginning").
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "device.cuh"
+#include "internal.hpp"
+#include "prims.cuh"
+
+namespace ada {
+
+namespace {
+
+std::atomic<uint64_t> g_matrix_ids{1};
+
+template <class V>
+struct RowVal {
+    int32_t row;
+    V val;
+};
+
+__global__ void fill_ones_kernel(void* vals, int64_t n, int vbytes) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t k = i; k < n; k += stride) {
+        if (vbytes == 8) static_cast<double*>(vals)[k] = 1.0;
+        else static_cast<float*>(vals)[k] = 1.0f;
+    }
+}
+
+// one warp per row: keys = column, payload = (row, value) in CSR order
+template <class V>
+__global__ void csr_expand_kernel(const int64_t* __restrict__ ro, const int32_t* __restrict__ ci,
+                                  const V* __restrict__ vals, int64_t rows,
+                                  uint32_t* __restrict__ keys, RowVal<V>* __restrict__ pay) {
+    const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = warp; r < rows; r += nwarps) {
+        const int64_t b = ro[r], e = ro[r + 1];
+        for (int64_t k = b + lane; k < e; k += 32) {
+            keys[k] = static_cast<uint32_t>(ci[k]);
+            pay[k] = RowVal<V>{static_cast<int32_t>(r), vals[k]};
+        }
+    }
+}
+
+template <class V>
+__global__ void csc_unpack_kernel(const RowVal<V>* __restrict__ pay, int64_t nnz,
+                                  int32_t* __restrict__ ri, V* __restrict__ cv) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t k = i; k < nnz; k += stride) {
+        RowVal<V> p = pay[k];
+        ri[k] = p.row;
+        cv[k] = p.val;
+    }
+}
+
+__global__ void col_count_kernel(const int32_t* __restrict__ ci, int64_t nnz,
+                                 unsigned long long* __restrict__ counts) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t k = i; k < nnz; k += stride) atomicAdd(counts + ci[k], 1ull);
+}
+
+struct U64In {
+    const unsigned long long* c;
+    __device__ int64_t operator()(int64_t i) const { return static_cast<int64_t>(c[i]); }
+};
+
+// tile_head[t] = segment_of(ro, t * kRowTile) for t < ntiles; [ntiles] = rows
+__global__ void tile_head_kernel(const int64_t* __restrict__ ro, int64_t rows, int64_t ntiles,
+                                 int64_t* __restrict__ head) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t > ntiles) return;
+    if (t == ntiles) {
+        head[t] = rows;
+        return;
+    }
+    head[t] = segment_search(ro, 0, rows + 1, t * static_cast<int64_t>(kRowTile));
+}
+
+// tile_rs[t] = lower_bound(ro, t * kRowTile): rows whose start lies in tile t
+// are owned by it (it writes their y when they are empty); [ntiles] = rows.
+__global__ void tile_rs_kernel(const int64_t* __restrict__ ro, int64_t rows, int64_t ntiles,
+                               int64_t* __restrict__ rs) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t > ntiles) return;
+    if (t == ntiles) {
+        rs[t] = rows;
+        return;
+    }
+    const int64_t pos = t * static_cast<int64_t>(kRowTile);
+    int64_t lo = 0, hi = rows + 1;  // first index with ro[i] >= pos
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ro[mid] < pos) lo = mid + 1;
+        else hi = mid;
+    }
+    rs[t] = lo;
+}
+
+void build_tiles(Context& ctx, Matrix& m) {
+    m.n_row_tiles = (m.nnz + kRowTile - 1) / kRowTile;
+    const size_t n = static_cast<size_t>(m.n_row_tiles + 1);
+    m.tile_head.ensure(sizeof(int64_t) * n);
+    m.tile_rs.ensure(sizeof(int64_t) * n);
+    const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+    tile_head_kernel<<<blocks, 256, 0, ctx.stream>>>(m.row_off.as<int64_t>(), m.rows,
+                                                     m.n_row_tiles, m.tile_head.as<int64_t>());
+    ADA_LAUNCHED(ctx);
+    tile_rs_kernel<<<blocks, 256, 0, ctx.stream>>>(m.row_off.as<int64_t>(), m.rows, m.n_row_tiles,
+                                                   m.tile_rs.as<int64_t>());
+    ADA_LAUNCHED(ctx);
+    // head partial, tail partial (V) and tail row (int64) per tile
+    m.tile_partials.ensure((2 * static_cast<size_t>(m.vbytes()) + sizeof(int64_t)) *
+                           static_cast<size_t>(std::max<int64_t>(m.n_row_tiles, 1)));
+}
+
+// degree statistics: slot[0] = max, [1] = min, [2] = sum of squares (u64)
+__global__ void degree_stats_kernel(const int64_t* __restrict__ off, int64_t n,
+                                    unsigned long long* __restrict__ slot) {
+    unsigned long long mx = 0, mn = ~0ull, sq = 0;
+    const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t r = i0; r < n; r += stride) {
+        const unsigned long long d = static_cast<unsigned long long>(off[r + 1] - off[r]);
+        mx = d > mx ? d : mx;
+        mn = d < mn ? d : mn;
+        sq += d * d;
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        mx = max(mx, __shfl_xor_sync(kFull, mx, s));
+        mn = min(mn, __shfl_xor_sync(kFull, mn, s));
+        sq += __shfl_xor_sync(kFull, sq, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(slot + 0, mx);
+        atomicMin(slot + 1, mn);
+        atomicAdd(slot + 2, sq);
+    }
+}
+
+// histogram of row degrees (for the Gini coefficient by the sorted identity)
+constexpr int kHistSmem = 2048;
+__global__ void degree_hist_kernel(const int64_t* __restrict__ off, int64_t n, int64_t nbins,
+                                   unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int sh[kHistSmem];
+    for (int i = threadIdx.x; i < kHistSmem; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t r = i0; r < n; r += stride) {
+        const int64_t d = off[r + 1] - off[r];
+        if (d < kHistSmem) atomicAdd(&sh[d], 1u);
+        else atomicAdd(hist + d, 1ull);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHistSmem && i < nbins; i += blockDim.x)
+        if (sh[i]) atomicAdd(hist + i, static_cast<unsigned long long>(sh[i]));
+}
+
+int grid_for(const Context& ctx, int64_t work, int threads) {
+    int64_t g = (work + threads - 1) / threads;
+    const int64_t cap = static_cast<int64_t>(ctx.sm_count) * 32;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return static_cast<int>(g);
+}
+
+template <class V>
+void build_csc(Context& ctx, Matrix& m) {
+    const int64_t nnz = m.nnz;
+    m.col_off.ensure(sizeof(int64_t) * static_cast<size_t>(m.cols + 1));
+    m.row_idx.ensure(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+    m.cvals.ensure(sizeof(V) * static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+    // column counts -> col_offsets (exclusive scan; [cols] = nnz)
+    DevBuf counts;
+    counts.ensure(sizeof(unsigned long long) * static_cast<size_t>(std::max<int64_t>(m.cols, 1)));
+    ADA_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(unsigned long long) * static_cast<size_t>(m.cols),
+                             ctx.stream));
+    if (nnz > 0) {
+        col_count_kernel<<<grid_for(ctx, nnz, 256), 256, 0, ctx.stream>>>(
+            m.col_idx.as<int32_t>(), nnz, counts.as<unsigned long long>());
+        ADA_LAUNCHED(ctx);
+    }
+    int64_t* co = m.col_off.as<int64_t>();
+    scan3(ctx, m.cols, U64In{counts.as<unsigned long long>()}, WriteExclusive{co}, co + m.cols,
+          ctx.scratch[5]);
+    if (m.cols == 0) ADA_CUDA(cudaMemsetAsync(co, 0, sizeof(int64_t), ctx.stream));
+    if (nnz == 0) return;
+    // stable sort of CSR-order entries by column
+    DevBuf k0, k1, p0, p1, cnt;
+    k0.ensure(sizeof(uint32_t) * static_cast<size_t>(nnz));
+    k1.ensure(sizeof(uint32_t) * static_cast<size_t>(nnz));
+    p0.ensure(sizeof(RowVal<V>) * static_cast<size_t>(nnz));
+    p1.ensure(sizeof(RowVal<V>) * static_cast<size_t>(nnz));
+    csr_expand_kernel<V><<<grid_for(ctx, m.rows * 32, 256), 256, 0, ctx.stream>>>(
+        m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), m.vals.as<V>(), m.rows,
+        k0.as<uint32_t>(), p0.as<RowVal<V>>());
+    ADA_LAUNCHED(ctx);
+    const int which = radix_sort_pairs<RowVal<V>>(ctx, k0.as<uint32_t>(), p0.as<RowVal<V>>(),
+                                                  k1.as<uint32_t>(), p1.as<RowVal<V>>(), nnz,
+                                                  bits_for(m.cols), cnt, ctx.scratch[5]);
+    const RowVal<V>* sorted = which ? p1.as<RowVal<V>>() : p0.as<RowVal<V>>();
+    csc_unpack_kernel<V><<<grid_for(ctx, nnz, 256), 256, 0, ctx.stream>>>(
+        sorted, nnz, m.row_idx.as<int32_t>(), m.cvals.as<V>());
+    ADA_LAUNCHED(ctx);
+    ctx.sync();  // scratch buffers are released on return
+}
+
+// Matrix features.
+void compute_features(Context& ctx, Matrix& m) {
+    double* f = m.feat;
+    f[0] = static_cast<double>(m.rows);
+    f[1] = static_cast<double>(m.cols);
+    f[2] = static_cast<double>(m.nnz);
+    if (m.rows == 0) {
+        for (int i = 3; i < 9; ++i) f[i] = 0;
+        return;
+    }
+    DevBuf slots;
+    slots.ensure(sizeof(unsigned long long) * 8);
+    unsigned long long init[8] = {0, ~0ull, 0, 0, 0, ~0ull, 0, 0};
+    ADA_CUDA(cudaMemcpyAsync(slots.p, init, sizeof(init), cudaMemcpyHostToDevice, ctx.stream));
+    degree_stats_kernel<<<grid_for(ctx, m.rows, 256), 256, 0, ctx.stream>>>(
+        m.row_off.as<int64_t>(), m.rows, slots.as<unsigned long long>());
+    ADA_LAUNCHED(ctx);
+    if (m.cols > 0) {  // column degree max (slot 4) for the column kernels' sizing
+        degree_stats_kernel<<<grid_for(ctx, m.cols, 256), 256, 0, ctx.stream>>>(
+            m.col_off.as<int64_t>(), m.cols, slots.as<unsigned long long>() + 4);
+        ADA_LAUNCHED(ctx);
+    }
+    unsigned long long h[8];
+    ADA_CUDA(cudaMemcpyAsync(h, slots.p, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    const uint64_t mx = h[0], mn = h[1], sq = h[2];
+    m.max_col_deg = m.cols > 0 ? static_cast<int64_t>(h[4]) : 0;
+    m.avg_col = m.cols > 0 ? static_cast<double>(m.nnz) / static_cast<double>(m.cols) : 0.0;
+    const double avg = static_cast<double>(m.nnz) / static_cast<double>(m.rows);
+    double var = static_cast<double>(sq) / static_cast<double>(m.rows) - avg * avg;
+    if (var < 0) var = 0;
+    f[3] = static_cast<double>(mx);
+    f[4] = static_cast<double>(mn);
+    f[5] = avg;
+    f[6] = m.cols > 0 ? static_cast<double>(mx - mn) / static_cast<double>(m.cols) : 0.0;
+    f[7] = std::sqrt(var);
+    // Gini: G = 2*sum_i i*d_(i) / (k*sum d) - (k+1)/k with d sorted ascending.
+    // From the degree histogram c_v: positions C_<v + 1 .. C_<v + c_v carry v.
+    const int64_t nbins = static_cast<int64_t>(mx) + 1;
+    DevBuf hist;
+    hist.ensure(sizeof(unsigned long long) * static_cast<size_t>(nbins));
+    ADA_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(unsigned long long) * static_cast<size_t>(nbins),
+                             ctx.stream));
+    degree_hist_kernel<<<grid_for(ctx, m.rows, 256), 256, 0, ctx.stream>>>(
+        m.row_off.as<int64_t>(), m.rows, nbins, hist.as<unsigned long long>());
+    ADA_LAUNCHED(ctx);
+    std::vector<unsigned long long> hh(static_cast<size_t>(nbins));
+    ADA_CUDA(cudaMemcpyAsync(hh.data(), hist.p, sizeof(unsigned long long) * hh.size(),
+                             cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    unsigned __int128 wsum = 0, total = 0, before = 0;
+    for (int64_t v = 0; v < nbins; ++v) {
+        const unsigned __int128 c = hh[static_cast<size_t>(v)];
+        if (!c) continue;
+        // sum of positions before+1 .. before+c
+        const unsigned __int128 pos_sum = c * before + c * (c + 1) / 2;
+        wsum += pos_sum * static_cast<unsigned __int128>(v);
+        total += c * static_cast<unsigned __int128>(v);
+        before += c;
+    }
+    const double k = static_cast<double>(m.rows);
+    f[8] = total == 0 ? 0.0
+                      : (2.0 * static_cast<double>(wsum)) / (k * static_cast<double>(total)) -
+                            (k + 1.0) / k;
+}
+
+template <class V>
+void finish_matrix(Context& ctx, Matrix& m) {
+    build_csc<V>(ctx, m);
+    build_tiles(ctx, m);
+    compute_features(ctx, m);
+}
+
+}  // namespace
+
+Matrix* matrix_create_device(Context& ctx, int64_t rows, int64_t cols, int64_t nnz,
+                             const int64_t* d_ro, const int32_t* d_ci, const void* d_vals,
+                             int dtype, bool pattern) {
+    if (rows < 0 || cols < 0) invalid("negative matrix dimension");
+    if (rows >= (int64_t(1) << 31) || cols >= (int64_t(1) << 31))
+        invalid("matrix dimension exceeds the device int32 index range");
+    auto* m = new Matrix();
+    try {
+        m->ctx = &ctx;
+        m->rows = rows;
+        m->cols = cols;
+        m->nnz = nnz;
+        m->dtype = dtype;
+        m->pattern = pattern;
+        m->id = g_matrix_ids.fetch_add(1);
+        const int vb = m->vbytes();
+        m->row_off.ensure(sizeof(int64_t) * static_cast<size_t>(rows + 1));
+        m->col_idx.ensure(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+        m->vals.ensure(static_cast<size_t>(vb) * static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+        ADA_CUDA(cudaMemcpyAsync(m->row_off.p, d_ro, sizeof(int64_t) * static_cast<size_t>(rows + 1),
+                                 cudaMemcpyDeviceToDevice, ctx.stream));
+        if (nnz > 0) {
+            ADA_CUDA(cudaMemcpyAsync(m->col_idx.p, d_ci, sizeof(int32_t) * static_cast<size_t>(nnz),
+                                     cudaMemcpyDeviceToDevice, ctx.stream));
+            if (d_vals) {
+                ADA_CUDA(cudaMemcpyAsync(m->vals.p, d_vals, static_cast<size_t>(vb) * static_cast<size_t>(nnz),
+                                         cudaMemcpyDeviceToDevice, ctx.stream));
+            } else {
+                fill_ones_kernel<<<grid_for(ctx, nnz, 256), 256, 0, ctx.stream>>>(m->vals.p, nnz, vb);
+                ADA_LAUNCHED(ctx);
+            }
+        }
+        if (dtype == ADASPMV_F64) finish_matrix<double>(ctx, *m);
+        else finish_matrix<float>(ctx, *m);
+        ctx.sync();
+        return m;
+    } catch (...) {
+        delete m;
+        throw;
+    }
+}
+
+// transpose (sparse.hpp:262-275): the two layouts swap roles.
+Matrix* matrix_transpose(Context& ctx, const Matrix& src) {
+    auto* m = new Matrix();
+    try {
+        m->ctx = &ctx;
+        m->rows = src.cols;
+        m->cols = src.rows;
+        m->nnz = src.nnz;
+        m->dtype = src.dtype;
+        m->pattern = src.pattern;
+        m->id = g_matrix_ids.fetch_add(1);
+        const size_t vb = static_cast<size_t>(src.vbytes());
+        const size_t z = static_cast<size_t>(std::max<int64_t>(src.nnz, 1));
+        auto copy = [&](DevBuf& dst, const DevBuf& s, size_t bytes) {
+            dst.ensure(bytes);
+            ADA_CUDA(cudaMemcpyAsync(dst.p, s.p, bytes, cudaMemcpyDeviceToDevice, ctx.stream));
+        };
+        copy(m->row_off, src.col_off, sizeof(int64_t) * static_cast<size_t>(src.cols + 1));
+        copy(m->col_idx, src.row_idx, sizeof(int32_t) * z);
+        copy(m->vals, src.cvals, vb * z);
+        copy(m->col_off, src.row_off, sizeof(int64_t) * static_cast<size_t>(src.rows + 1));
+        copy(m->row_idx, src.col_idx, sizeof(int32_t) * z);
+        copy(m->cvals, src.vals, vb * z);
+        build_tiles(ctx, *m);
+        compute_features(ctx, *m);
+        ctx.sync();
+        return m;
+    } catch (...) {
+        delete m;
+        throw;
+    }
+}
+
+}  // namespace ada

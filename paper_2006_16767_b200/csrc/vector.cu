@@ -1,0 +1,210 @@
+// vector.cu -- the operand cache of one input vector x (OperandViews,
+// kernels.hpp:171-175) and the format conversions the runtime performs only
+// when the chosen kernel needs another representation:
+//   sparse_to_dense  sparse.hpp:323-331  memset + scatter
+//   dense_to_sparse  sparse.hpp:283-321  stream compaction (drops exact zeros)
+//   build_bitmask    sparse.hpp:333-344  atomicOr from indices / warp ballot
+//   effective_nnz    sparse.hpp:348-359  degree gather + exclusive scan (the
+//                    scan is the eff_offsets of kernels.hpp:400-404)
+#include <algorithm>
+
+#include "device.cuh"
+#include "internal.hpp"
+#include "prims.cuh"
+
+namespace ada {
+
+namespace {
+
+template <class V>
+__global__ void scatter_kernel(int64_t nnz, const int32_t* __restrict__ idx,
+                               const V* __restrict__ val, V* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < nnz) out[idx[i]] = val[i];
+}
+
+__global__ void mask_from_indices_kernel(int64_t nnz, const int32_t* __restrict__ idx,
+                                         uint32_t* __restrict__ words) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < nnz) {
+        const int32_t c = idx[i];
+        atomicOr(words + (c >> 5), 1u << (c & 31));
+    }
+}
+
+// one u32 word per warp-iteration from 32 consecutive values (LSB-first)
+template <class V>
+__global__ void mask_from_dense_kernel(int64_t n, const V* __restrict__ x,
+                                       uint32_t* __restrict__ words) {
+    const int64_t nw = (n + 31) / 32;
+    const int64_t warp0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = warp0; w < nw; w += nwarps) {
+        const int64_t i = w * 32 + lane;
+        const bool nz = i < n && x[i] != V(0);
+        const unsigned b = __ballot_sync(kFull, nz);
+        if (lane == 0) words[w] = b;
+    }
+}
+
+template <class V>
+struct NonzeroIn {
+    const V* x;
+    __device__ int64_t operator()(int64_t i) const { return x[i] != V(0) ? 1 : 0; }
+};
+
+template <class V>
+struct CompactEpi {
+    const V* x;
+    int32_t* idx;
+    V* val;
+    __device__ void operator()(int64_t i, int64_t p, int64_t v) const {
+        if (v) {
+            idx[p] = static_cast<int32_t>(i);
+            val[p] = x[i];
+        }
+    }
+};
+
+struct NoEpi {
+    __device__ void operator()(int64_t, int64_t, int64_t) const {}
+};
+
+struct DegreeIn {
+    const int64_t* co;
+    const int32_t* xi;
+    __device__ int64_t operator()(int64_t s) const {
+        const int32_t c = xi[s];
+        return co[c + 1] - co[c];
+    }
+};
+
+int blocks_for(int64_t n, int t) { return static_cast<int>(std::max<int64_t>(1, (n + t - 1) / t)); }
+
+template <class V>
+void ensure_dense_t(Context& ctx, Vector& v) {
+    V* d = static_cast<V*>(v.dense.ensure(sizeof(V) * static_cast<size_t>(std::max<int64_t>(v.n, 1))));
+    ADA_CUDA(cudaMemsetAsync(d, 0, sizeof(V) * static_cast<size_t>(v.n), ctx.stream));
+    if (v.nnz > 0) {
+        scatter_kernel<V><<<blocks_for(v.nnz, 256), 256, 0, ctx.stream>>>(
+            v.nnz, v.sp_idx.as<int32_t>(), v.sp_val.as<V>(), d);
+        ADA_LAUNCHED(ctx);
+    }
+}
+
+template <class V>
+void ensure_sparse_t(Context& ctx, Vector& v) {
+    const size_t cap = static_cast<size_t>(std::max<int64_t>(v.n, 1));
+    v.sp_idx.ensure(sizeof(int32_t) * cap);
+    v.sp_val.ensure(sizeof(V) * cap);
+    const V* x = v.dense.as<V>();
+    scan3(ctx, v.n, NonzeroIn<V>{x}, CompactEpi<V>{x, v.sp_idx.as<int32_t>(), v.sp_val.as<V>()},
+          ctx.dscal(0), ctx.scratch[4]);
+    v.nnz = ctx.fetch_scalar(ctx.dscal(0));
+}
+
+template <class V>
+int64_t count_nonzero_t(Context& ctx, const Vector& v) {
+    scan3(ctx, v.n, NonzeroIn<V>{v.dense.as<V>()}, NoEpi{}, ctx.dscal(0), ctx.scratch[4]);
+    return ctx.fetch_scalar(ctx.dscal(0));
+}
+
+}  // namespace
+
+void vector_set_dense_device(Context& ctx, Vector& v, const void* d_vals) {
+    v.invalidate();
+    const size_t bytes = static_cast<size_t>(value_bytes(v.dtype)) * static_cast<size_t>(v.n);
+    v.dense.ensure(std::max<size_t>(bytes, 1));
+    if (bytes)
+        ADA_CUDA(cudaMemcpyAsync(v.dense.p, d_vals, bytes, cudaMemcpyDeviceToDevice, ctx.stream));
+    v.has_dense = true;
+}
+
+void vector_set_sparse_device(Context& ctx, Vector& v, int64_t nnz, const int32_t* d_idx,
+                              const void* d_vals) {
+    if (nnz < 0 || nnz > v.n) invalid("sparse vector: nnz out of range");
+    v.invalidate();
+    const size_t vb = static_cast<size_t>(value_bytes(v.dtype));
+    v.sp_idx.ensure(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+    v.sp_val.ensure(vb * static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+    if (nnz > 0) {
+        ADA_CUDA(cudaMemcpyAsync(v.sp_idx.p, d_idx, sizeof(int32_t) * static_cast<size_t>(nnz),
+                                 cudaMemcpyDeviceToDevice, ctx.stream));
+        ADA_CUDA(cudaMemcpyAsync(v.sp_val.p, d_vals, vb * static_cast<size_t>(nnz),
+                                 cudaMemcpyDeviceToDevice, ctx.stream));
+    }
+    v.nnz = nnz;
+    v.has_sparse = true;
+}
+
+void vector_ensure_dense(Context& ctx, Vector& v) {
+    if (v.has_dense) return;
+    if (!v.has_sparse) invalid("vector has no value set");
+    if (v.dtype == ADASPMV_F64) ensure_dense_t<double>(ctx, v);
+    else ensure_dense_t<float>(ctx, v);
+    v.has_dense = true;
+}
+
+void vector_ensure_sparse(Context& ctx, Vector& v) {
+    if (v.has_sparse) return;
+    if (!v.has_dense) invalid("vector has no value set");
+    if (v.dtype == ADASPMV_F64) ensure_sparse_t<double>(ctx, v);
+    else ensure_sparse_t<float>(ctx, v);
+    v.has_sparse = true;
+}
+
+void vector_ensure_mask(Context& ctx, Vector& v) {
+    if (v.has_mask) return;
+    const int64_t nw = (v.n + 31) / 32;
+    // u64-granular allocation so host reads of (n+63)/64 words stay in bounds
+    uint32_t* w = static_cast<uint32_t*>(v.mask.ensure(sizeof(uint64_t) * static_cast<size_t>(std::max<int64_t>((v.n + 63) / 64, 1))));
+    if (v.has_sparse) {
+        ADA_CUDA(cudaMemsetAsync(w, 0, sizeof(uint64_t) * static_cast<size_t>((v.n + 63) / 64), ctx.stream));
+        if (v.nnz > 0) {
+            mask_from_indices_kernel<<<blocks_for(v.nnz, 256), 256, 0, ctx.stream>>>(
+                v.nnz, v.sp_idx.as<int32_t>(), w);
+            ADA_LAUNCHED(ctx);
+        }
+    } else if (v.has_dense) {
+        ADA_CUDA(cudaMemsetAsync(w, 0, sizeof(uint64_t) * static_cast<size_t>((v.n + 63) / 64), ctx.stream));
+        if (nw > 0) {
+            const int blocks = static_cast<int>(std::min<int64_t>(blocks_for(nw * 32, 256), ctx.sm_count * 16));
+            if (v.dtype == ADASPMV_F64)
+                mask_from_dense_kernel<double><<<blocks, 256, 0, ctx.stream>>>(v.n, v.dense.as<double>(), w);
+            else
+                mask_from_dense_kernel<float><<<blocks, 256, 0, ctx.stream>>>(v.n, v.dense.as<float>(), w);
+            ADA_LAUNCHED(ctx);
+        }
+    } else {
+        invalid("vector has no value set");
+    }
+    v.has_mask = true;
+}
+
+void vector_ensure_eff(Context& ctx, Vector& v, const Matrix& m) {
+    if (v.has_eff && v.eff_matrix == m.id) return;
+    vector_ensure_sparse(ctx, v);
+    int64_t* eff = static_cast<int64_t*>(v.eff.ensure(sizeof(int64_t) * static_cast<size_t>(v.nnz + 1)));
+    scan3(ctx, v.nnz, DegreeIn{m.col_off.as<int64_t>(), v.sp_idx.as<int32_t>()},
+          WriteExclusive{eff}, eff + v.nnz, ctx.scratch[4]);
+    v.has_eff = true;
+    v.eff_matrix = m.id;
+}
+
+int64_t vector_nnz(Context& ctx, Vector& v) {
+    if (v.nnz >= 0) return v.nnz;
+    if (!v.has_dense) invalid("vector has no value set");
+    v.nnz = v.dtype == ADASPMV_F64 ? count_nonzero_t<double>(ctx, v) : count_nonzero_t<float>(ctx, v);
+    return v.nnz;
+}
+
+int64_t vector_nnz_s(Context& ctx, Vector& v, const Matrix& m) {
+    if (v.nnz_s >= 0 && v.nnz_s_matrix == m.id) return v.nnz_s;
+    vector_ensure_eff(ctx, v, m);
+    v.nnz_s = ctx.fetch_scalar(v.eff.as<int64_t>() + v.nnz);
+    v.nnz_s_matrix = m.id;
+    return v.nnz_s;
+}
+
+}  // namespace ada

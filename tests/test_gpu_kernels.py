@@ -1,0 +1,263 @@
+"""GPU parity of the eight kernels and the operand conversions against the CPU
+oracle (oracle/adaspmv_oracle.c), through the C-ABI (ctypes mirror).
+
+Edge cases follow SURVEY.md section 4 (probe-verified reference behaviour) and
+SPEC.md:156-186: all-zero matrix, a dense 1x100 row, a 100x1 column, empty x,
+dense x, explicit zero in x, rows spanning several LB tiles, empty rows at
+tile boundaries.
+"""
+import numpy as np
+import pytest
+
+from paper_2006_16767_b200 import adaspmv as A
+from paper_2006_16767_b200 import synth
+from tests.util import assert_dense_close, assert_sparse_match, ref_and_bound
+
+pytestmark = pytest.mark.gpu
+
+DTYPES = [np.float64, np.float32]
+
+
+def _matrix_cases():
+    cases = []
+    for seed, (r, c, d) in enumerate([(300, 200, 0.05), (1000, 1000, 0.01), (64, 500, 0.2),
+                                      (2000, 3000, 0.004), (1, 1, 1.0), (3, 3, 0.0)]):
+        cases.append(("rand%d" % seed, synth.random_csr(r, c, d, seed=seed)))
+    # all-zero 5x7
+    cases.append(("zero5x7", (5, 7, np.zeros(6, np.int64), np.zeros(0, np.int64), np.zeros(0))))
+    # one dense row 1x100 and one dense column 100x1
+    cases.append(("row1x100", (1, 100, np.array([0, 100]), np.arange(100), np.linspace(-1, 1, 100))))
+    cases.append(("col100x1", (100, 1, np.arange(101), np.zeros(100, np.int64), np.linspace(-1, 1, 100))))
+    # long rows spanning LB tiles + empty rows around tile boundaries
+    rng = np.random.default_rng(7)
+    deg = rng.integers(0, 6, size=4000)
+    deg[[10, 11, 12, 500]] = 0
+    deg[100] = 9000   # spans several 2048-item tiles
+    deg[2000] = 5000
+    deg[1500:1600] = 0
+    cols = 12000
+    ro = np.zeros(len(deg) + 1, np.int64)
+    ro[1:] = np.cumsum(deg)
+    ci = np.concatenate([np.sort(rng.choice(cols, size=d, replace=False)) for d in deg]).astype(np.int64)
+    cases.append(("skewed", (len(deg), cols, ro, ci, rng.uniform(-1, 1, ro[-1]))))
+    # trailing and leading empty rows
+    ro2 = np.array([0, 0, 0, 3, 3, 5, 5, 5], np.int64)
+    cases.append(("emptyends", (7, 4, ro2, np.array([0, 1, 3, 0, 2]), np.array([1., 2., 3., 4., 5.]))))
+    return cases
+
+
+CASES = _matrix_cases()
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
+@pytest.mark.parametrize("name,case", CASES, ids=[c[0] for c in CASES])
+def test_all_kernels_vs_oracle(ctx, port, name, case, dt):
+    rows, cols, ro, ci, vals = case
+    vals = np.asarray(vals, dt)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    for nx in sorted({0, 1, max(1, cols // 50), max(1, cols // 3), cols}):
+        xi, xv = synth.sparse_vector(cols, nx, seed=nx + 3, dtype=dt)
+        xd = port.sparse_to_dense(cols, xi, xv)
+        y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, xd)
+        for k in range(8):
+            x = A.SparseVector(cols, xi, xv) if k >= 4 else A.DenseVector(xd)
+            out = A.run_kernel(m, k, x)
+            what = f"{name} k={k} nnz_x={nx} {np.dtype(dt).name}"
+            assert_dense_close(out.dense().values, y_ref, bound, dt, what)
+            s = out.sparse()
+            assert_sparse_match(s.indices, s.values, y_ref, bound, dt, what)
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
+def test_lanes_override_and_workers_invariance(ctx, port, dt):
+    rows, cols, ro, ci, vals = synth.random_csr(700, 900, 0.02, seed=3, dtype=dt)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    xi, xv = synth.sparse_vector(cols, 300, seed=1, dtype=dt)
+    xd = port.sparse_to_dense(cols, xi, xv)
+    y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, xd)
+    for lanes in (1, 2, 4, 8, 16, 32):
+        for k in (0, 2, 4, 5):
+            x = A.SparseVector(cols, xi, xv) if k >= 4 else A.DenseVector(xd)
+            out = A.run_kernel(m, k, x, A.KernelConfig(lanes_per_row=lanes, workers=lanes))
+            assert_dense_close(out.dense().values, y_ref, bound, dt, f"lanes={lanes} k={k}")
+
+
+def test_explicit_zero_in_x_drops_zero_sums(ctx):
+    # A = {(0,0),(1,1),(2,0)}, x = {0: 0.0, 1: 5.0} -> sparse y = {1}
+    ro = np.array([0, 1, 2, 3])
+    ci = np.array([0, 1, 0])
+    m = A.DualMatrix.from_csr(3, 2, ro, ci, np.array([1.0, 1.0, 1.0]), ctx=ctx)
+    for k in range(8):
+        out = A.run_kernel(m, k, A.SparseVector(2, [0, 1], [0.0, 5.0]))
+        assert out.sparse().indices.tolist() == [1], k
+        assert out.sparse().values.tolist() == [5.0], k
+
+
+def test_sort_writeback_bitwise_deterministic(ctx):
+    rows, cols, ro, ci, vals = synth.random_csr(20000, 20000, 0.002, seed=9, dtype=np.float32)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    for nx in (50, 5000):  # single-CTA path and multi-kernel radix path
+        xi, xv = synth.sparse_vector(cols, nx, seed=2, dtype=np.float32)
+        for k in (5, 7):
+            runs = [A.run_kernel(m, k, A.SparseVector(cols, xi, xv)).sparse() for _ in range(3)]
+            for r in runs[1:]:
+                assert np.array_equal(r.indices, runs[0].indices)
+                assert r.values.tobytes() == runs[0].values.tobytes()
+        # Direct and LB sort paths emit identical pair streams -> identical bits
+        a = A.run_kernel(m, 5, A.SparseVector(cols, xi, xv)).sparse()
+        b = A.run_kernel(m, 7, A.SparseVector(cols, xi, xv)).sparse()
+        assert a.values.tobytes() == b.values.tobytes()
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
+def test_device_csc_is_bit_exact_csr_to_csc(ctx, port, dt):
+    for seed, (r, c, d) in enumerate([(500, 700, 0.03), (4000, 100, 0.1), (1, 1000, 0.5)]):
+        rows, cols, ro, ci, vals = synth.random_csr(r, c, d, seed=seed, dtype=dt)
+        m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+        ro2, ci2, v2, co, ri, cv = m.download()
+        eco, eri, ecv = port.csr_to_csc(rows, cols, ro, ci, vals)
+        assert np.array_equal(ro2, ro) and np.array_equal(ci2, ci) and v2.tobytes() == vals.tobytes()
+        assert np.array_equal(co, eco)
+        assert np.array_equal(ri, eri)
+        assert cv.tobytes() == ecv.tobytes()
+        t = m.transpose()
+        tro, tci, tv, tco, tri, tcv = t.download()
+        assert np.array_equal(tro, eco) and np.array_equal(tci, eri) and tv.tobytes() == ecv.tobytes()
+        assert np.array_equal(tco, ro) and np.array_equal(tri, ci)
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
+def test_vector_conversions(ctx, port, dt):
+    n = 10000
+    rng = np.random.default_rng(4)
+    xd = rng.uniform(-1, 1, n).astype(dt)
+    xd[rng.random(n) < 0.7] = 0
+    xd[5] = -0.0  # negative zero is a zero (sparse.hpp:291)
+    v = A.DeviceVector(n, dt, ctx).set_dense(xd)
+    s = v.sparse()
+    ei, ev = port.dense_to_sparse(xd)
+    assert np.array_equal(s.indices, ei) and s.values.tobytes() == ev.tobytes()
+    assert np.array_equal(v.bitmask().words, port.build_bitmask_dense(xd))
+    assert v.nnz() == len(ei)
+    # sparse -> dense, bitmask across the 63/64 word boundary
+    v2 = A.DeviceVector(65, dt, ctx).set_sparse([0, 63, 64], np.array([1, 2, 3], dt))
+    w = v2.bitmask().words
+    assert w.tolist() == [1 | (1 << 63), 1]
+    assert v2.dense().values.tolist() == [1] + [0] * 62 + [2, 3]
+    # explicit zero stays a structural nonzero in the mask
+    v3 = A.DeviceVector(10, dt, ctx).set_sparse([2, 4], np.array([0, 1], dt))
+    assert v3.bitmask().words.tolist() == [(1 << 2) | (1 << 4)]
+
+
+def test_effective_nnz_and_features(ctx, port):
+    rows, cols, ro, ci, vals = synth.random_csr(800, 600, 0.02, seed=8)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    co, ri, cv = port.csr_to_csc(rows, cols, ro, ci, vals)
+    fm = port.matrix_features(rows, cols, ro)
+    got = m.features()
+    assert np.allclose(got, fm, rtol=1e-12, atol=0)
+    for nx in (0, 1, 57, 600):
+        xi, xv = synth.sparse_vector(cols, nx, seed=nx)
+        assert A.effective_nnz(m, A.SparseVector(cols, xi, xv)) == port.effective_nnz(co, xi)
+        f = A.features(m, A.SparseVector(cols, xi, xv))
+        exp = np.concatenate([fm, port.vector_features_sparse(cols, co, xi)])
+        assert np.allclose(f, exp, rtol=1e-12, atol=0)
+    # dense input: nnz_x counts nonzero entries
+    xd = np.zeros(cols)
+    xd[[3, 7, 100]] = 1.0
+    f = A.features(m, A.DenseVector(xd))
+    assert np.allclose(f[9:], port.vector_features_dense(co, xd))
+
+
+def test_selector_cascade_stub_bundles(ctx):
+    rows, cols, ro, ci, vals = synth.random_csr(100, 100, 0.05, seed=1)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    x = A.SparseVector(cols, [1, 5], [1.0, 2.0])
+    # constant (SpMV, Direct, -) -> SpMV/Direct; write-back tree not evaluated
+    k, used, nt = A.predict_kernel(m, x, A.SelectorBundle.constant(2, 0, 1))
+    assert k.index() == 0 and nt == 2 and used == 0
+    # (ColSpMSpV, LoadBalanced, Sort) -> that exact KernelId
+    k, used, nt = A.predict_kernel(m, x, A.SelectorBundle.constant(0, 1, 1))
+    assert k.name() == "col_lb_sort" and nt == 3
+    # a real split on x_sparsity (feature 10): <= 0.05 -> ColSpMSpV else SpMV
+    pat = {"feature": [10, -1, -1], "threshold": [0.05, 0, 0], "left": [1, -1, -1],
+           "right": [2, -1, -1], "leaf": [0, 0, 2]}
+    wl = {"feature": [-1], "threshold": [0.0], "left": [-1], "right": [-1], "leaf": [1]}
+    wb = {"feature": [11, -1, -1], "threshold": [10.0, 0, 0], "left": [1, -1, -1],
+          "right": [2, -1, -1], "leaf": [1, 1, 0]}
+    b = A.SelectorBundle.from_trees([pat, wl, wb])
+    k, used, _ = A.predict_kernel(m, x, b)
+    assert k.index() == 7 and used == (1 << 10) | (1 << 11)  # lazy: only the features walked
+    k, used, _ = A.predict_kernel(m, A.DenseVector(np.ones(cols)), b)
+    assert k.index() == 1 and used == (1 << 10)
+    out, kk = A.run_adaptive(m, x, b)
+    assert kk.index() == 7
+
+
+@pytest.mark.parametrize("semiring", [A.PLUS_TIMES, A.OR_AND, A.MIN_PLUS])
+def test_bfs_levels_match_queue_bfs(ctx, port, semiring):
+    # path graph 0-1-2-3 -> levels [0,1,2,3], 4 iterations
+    ro = np.array([0, 1, 3, 5, 6])
+    ci = np.array([1, 0, 2, 1, 3, 2])
+    m = A.DualMatrix.from_csr(4, 4, ro, ci, None, dtype=np.float32, ctx=ctx)
+    lv, reps = A.bfs(m, 0, semiring)
+    assert lv.tolist() == [0, 1, 2, 3] and len(reps) == 4
+    for seed, scale in ((1, 10), (2, 12)):
+        n, _, ro, ci, vals = synth.rmat(scale, 8, seed=seed)
+        m = A.DualMatrix.from_csr(n, n, ro, ci, None, dtype=np.float32, ctx=ctx)
+        co, ri, _ = port.csr_to_csc(n, n, ro, ci, np.ones(len(ci)))
+        exp, nl = port.bfs_queue(n, co, ri, 0)
+        for forced in (-1, 1, 3, 4, 7):
+            lv, reps = A.bfs(m, 0, semiring, force_kernel=forced)
+            assert np.array_equal(lv, exp), (scale, forced)
+
+
+def test_sort_reduce_pairs_known_answer(ctx):
+    # [(2,1.0),(0,2.0),(2,3.0)] -> {0: 2.0, 2: 4.0}
+    s = A.sort_reduce_pairs([2, 0, 2], np.array([1.0, 2.0, 3.0]), 3, ctx)
+    assert s.indices.tolist() == [0, 2] and s.values.tolist() == [2.0, 4.0]
+    # exact-zero sums dropped (kernels.hpp:331)
+    s = A.sort_reduce_pairs([1, 1, 0], np.array([1.5, -1.5, 2.0]), 2, ctx)
+    assert s.indices.tolist() == [0]
+
+
+def test_errors_map_to_reference_exceptions(ctx, tmp_path):
+    m = A.DualMatrix.from_csr(2, 2, [0, 1, 2], [0, 1], [1.0, 2.0], ctx=ctx)
+    with pytest.raises(A.InvalidArgument):
+        A.run_kernel(m, 0, A.DenseVector(np.ones(3)))
+    with pytest.raises(A.InvalidArgument):
+        A.run_kernel(m, 0, A.OperandViews(sparse=A.SparseVector(2, [0], [1.0])))
+    with pytest.raises(A.InvalidArgument):
+        A.DualMatrix.from_csr(2, 2, [0, 2, 2], [1, 0], [1.0, 2.0], ctx=ctx)  # unsorted columns
+    with pytest.raises(A.InvalidArgument):
+        A.run_kernel(m, 4, A.SparseVector(2, [1, 0], [1.0, 1.0]))
+    p = tmp_path / "bad.mtx"
+    p.write_text("%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n")
+    with pytest.raises(A.ParseError) as e:
+        A.load_matrix(p, ctx=ctx)
+    assert e.value.line == 3
+    with pytest.raises(A.FormatError):
+        A.load_matrix(tmp_path / "missing.mtx", ctx=ctx)
+
+
+def test_matrix_market_and_binary_round_trip(ctx, tmp_path):
+    rows, cols, ro, ci, vals = synth.random_csr(50, 40, 0.1, seed=2)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    p = tmp_path / "a.mtx"
+    m.write_matrix_market(p)
+    m2 = A.load_matrix(p, ctx=ctx)
+    a, b = m.download(), m2.download()
+    for u, v in zip(a, b):
+        assert u.tobytes() == v.tobytes()
+    pb = tmp_path / "a.bin"
+    m.save_binary(pb)
+    m3 = A.load_matrix(pb, ctx=ctx)
+    for u, v in zip(a, m3.download()):
+        assert u.tobytes() == v.tobytes()
+    with pytest.raises(A.FormatError):
+        A.load_matrix(pb, dtype=np.float32, ctx=ctx)  # width mismatch
+    # symmetric + pattern + duplicates
+    q = tmp_path / "s.mtx"
+    q.write_text("%%MatrixMarket matrix coordinate pattern symmetric\n3 3 3\n2 1\n3 3\n2 1\n")
+    s = A.load_matrix(q, ctx=ctx).download()
+    assert s[0].tolist() == [0, 1, 2, 3] and s[1].tolist() == [1, 0, 2] and s[2].tolist() == [2.0, 2.0, 1.0]
