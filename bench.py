@@ -1,0 +1,443 @@
+#!/usr/bin/env python3
+"""bench.py -- BASELINE.json metric on its 1-GPU configuration (configs[1]):
+
+  "GFLOP/s and HBM GB/s (% of roofline) vs x sparsity; selector regret vs best"
+  workload C2: uniform random 4M x 4M, 2^26 iid draws (~64M nnz), fp32,
+  x-sparsity sweep 0.001 % .. 100 % across all 8 kernels + the selector.
+
+A *step* is one adaptive pass over the sweep: for each of the 7 x-sparsity
+points, select a kernel (C++ decision-tree hook) and run it, inputs resident
+in HBM.  value = total useful GFLOP/s of the step = sum(2 nnz_s) / sum(t).
+Every point is also timed with all 8 kernels (best-of-8, regret).
+
+  --impl ours       (default) the CUDA library through its C-ABI
+  --impl reference  the reference's own CPU implementation (oracle/_ref: the
+                    unmodified reference headers) on the host cores
+
+Timing: CUDA events on the library's stream around each multiply, medians
+over K steps after W warm-up steps; an L2 flush (256 MiB write) precedes every
+timed multiply whose working set fits in L2.  e2e repeats the step through
+the public API with host buffers (pinned), H2D of x and D2H of y inside the
+timed region, wall clock with a synchronize at the end of each point.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SPARSITIES = (0.00001, 0.0001, 0.001, 0.01, 0.1, 0.5, 1.0)
+N = 1 << int(os.environ.get("ADASPMV_BENCH_LOG2N", "22"))  # override only for dry runs
+DRAWS = 16 * N
+METRIC = "GFLOP/s and HBM GB/s (% of roofline) vs x sparsity; selector regret vs best"
+WORKLOAD = "C2 uniform random 4M x 4M, 2^26 draws (~64M nnz) fp32, x-sparsity sweep 0.001%-100%"
+I_B, O_B = 4, 8  # device index / offset bytes (SURVEY.md section 8 symbols)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def alg_bytes(rows, cols, nnz, nnz_x, nnz_s, nnz_y, V=4):
+    """SURVEY.md section 8(d) algorithmic bytes per multiply."""
+    b_spmv = (rows + 1) * O_B + nnz * (I_B + V) + cols * V + rows * V
+    b_row = (rows + 1) * O_B + nnz * I_B + nnz_s * V + ((cols + 31) // 32) * 4 + nnz_x * V + rows * V
+    b_col_atomic = nnz_x * (I_B + V) + 2 * nnz_x * O_B + nnz_s * (I_B + V) + rows * V
+    b_col_sort = nnz_x * (I_B + V) + 2 * nnz_x * O_B + nnz_s * (I_B + V) + nnz_y * (I_B + V)
+    fam = {0: b_spmv, 1: b_spmv, 2: b_row, 3: b_row, 4: b_col_atomic, 5: b_col_sort, 6: b_col_atomic,
+           7: b_col_sort}
+    return min(b_spmv, b_row, b_col_atomic, b_col_sort), fam
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device=0):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_matrix():
+    from paper_2006_16767_b200 import synth
+    t0 = time.time()
+    m = synth.uniform_random(N, DRAWS, seed=1, dtype=np.float32)
+    return m, time.time() - t0
+
+
+def make_vectors(n):
+    from paper_2006_16767_b200 import synth
+    out = []
+    for i, s in enumerate(SPARSITIES):
+        k = max(1, int(round(s * n)))
+        out.append(synth.sparse_vector(n, k, seed=1000 + i, dtype=np.float32))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm
+# ---------------------------------------------------------------------------
+def ref_sweep_times(ref_m, vecs, kernels_per_point, repeats=1, warmup=0):
+    """Times the given kernel per point with the reference's run_kernel."""
+    ts = []
+    for (xi, xv), k in zip(vecs, kernels_per_point):
+        dense = None
+        if len(xi) == ref_m.cols:
+            dense = np.zeros(ref_m.cols, np.float32)
+            dense[xi] = xv
+        t = ref_m.bench_kernel(k, x_dense=dense, x_sparse=None if dense is not None else (xi, xv),
+                               warmup=warmup, repeats=repeats)
+        ts.append(float(np.median(t)))
+    return ts
+
+
+def cpu_choose(ref_m, vecs):
+    """Best reference kernel per point (1 warm-up + 1 run each); the sort
+    write-back is skipped where nnz_x >= 1 % (seconds per call on CPU)."""
+    best = []
+    for (xi, xv) in vecs:
+        dense = None
+        if len(xi) == ref_m.cols:
+            dense = np.zeros(ref_m.cols, np.float32)
+            dense[xi] = xv
+        cand = range(8) if len(xi) < 0.01 * ref_m.cols else (0, 1, 2, 3, 4, 6)
+        tk = {}
+        for k in cand:
+            t = ref_m.bench_kernel(k, x_dense=dense, x_sparse=None if dense is not None else (xi, xv),
+                                   warmup=1, repeats=1)
+            tk[k] = float(t[0])
+        best.append(min(tk, key=tk.get))
+    return best
+
+
+def run_reference(args, rank, world):
+    from oracle.oracle import Ref
+
+    if rank != 0:
+        return None
+    (rows, cols, ro, ci, vals), gen_s = make_matrix()
+    nnz = int(ro[-1])
+    vecs = make_vectors(cols)
+    ref = Ref(np.float32)
+    threads = os.cpu_count() or 1
+    ref.set_threads(threads)
+    M = ref.matrix(rows, cols, ro, ci, vals)
+    del ci
+    col_off = M.export()[3]
+    nnz_s = [int(np.sum(col_off[xi + 1] - col_off[xi])) for xi, _ in vecs]
+    best = cpu_choose(M, vecs)
+    for _ in range(args.warmup):
+        ref_sweep_times(M, vecs, best)
+    steps = [ref_sweep_times(M, vecs, best) for _ in range(args.steps)]
+    t_step = [sum(s) for s in steps]
+    flops = sum(2 * s for s in nnz_s)
+    v = flops / statistics.median(t_step) / 1e9
+    line = {
+        "metric": METRIC, "value": round(v, 4), "unit": "GFLOP/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(statistics.median(t_step) * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "rows": rows, "cols": cols, "nnz": nnz,
+                   "x_sparsity": list(SPARSITIES), "kernel_per_point": best},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+                         "sample": "full C2 sweep, best reference kernel per point (chosen by one timed "
+                                   "pass; sort write-back skipped at >=1 % density)"},
+        "e2e": {"value": round(v, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "per_point_ms": [round(statistics.median([s[i] for s in steps]) * 1e3, 4) for i in range(len(vecs))],
+        "generation_s": round(gen_s, 1),
+    }
+    return line
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world):
+    import torch
+
+    from paper_2006_16767_b200 import adaspmv as A
+    from paper_2006_16767_b200 import selector as S
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = A.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    (rows, cols, ro, ci, vals), gen_s = make_matrix()
+    nnz = int(ro[-1])
+    vecs = make_vectors(cols)
+    t0 = time.time()
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    upload_s = time.time() - t0
+    bundle_path = Path(args.bundle) if args.bundle else S.DEFAULT_PATH
+    bundle = A.SelectorBundle.load(bundle_path)
+    # device-resident operands: one DeviceVector per sweep point
+    dvs = []
+    for xi, xv in vecs:
+        dv = A.DeviceVector(cols, np.float32, ctx)
+        if len(xi) == cols:
+            d = np.zeros(cols, np.float32)
+            d[xi] = xv
+            dv.set_dense(d)
+        else:
+            dv.set_sparse(xi, xv)
+        dvs.append(dv)
+    nnz_s = [A.effective_nnz(m, dv) for dv in dvs]
+    nnz_x = [len(xi) for xi, _ in vecs]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    out = A.MultiplyOutput(ctx)
+
+    def timed(fn, n_rep, need_flush):
+        ts = []
+        for _ in range(n_rep):
+            if need_flush:
+                with torch.cuda.stream(stream):
+                    flush.add_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        return ts
+
+    # ---- per point: every kernel (best-of-8, regret) -------------------------
+    small = [alg_bytes(rows, cols, nnz, nx, ns, 0)[0] < 64e6 for nx, ns in zip(nnz_x, nnz_s)]
+    kernel_t = []
+    for i, dv in enumerate(dvs):
+        row = []
+        for k in range(8):
+            dv.prepare(k)
+            run = lambda k=k, dv=dv: A.run_kernel(m, k, dv, out=out)  # noqa: E731
+            timed(run, args.warmup, small[i])
+            row.append(statistics.median(timed(run, max(args.steps, 3), small[i])))
+        kernel_t.append(row)
+    # ---- the adaptive step ----------------------------------------------------
+    chosen = []
+    for dv in dvs:
+        k, _, _ = A.predict_kernel(m, dv, bundle)
+        chosen.append(k.index())
+    for i, dv in enumerate(dvs):  # operand conversions happen once, untimed
+        dv.prepare(chosen[i])
+    l0 = ctx.launches
+
+    def step_times():
+        per = []
+        for i, dv in enumerate(dvs):
+            per.append(timed(lambda dv=dv: A.run_adaptive(m, dv, bundle, out=out), 1, small[i])[0])
+        return per
+
+    for _ in range(args.warmup):
+        step_times()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        steps = [step_times() for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    launches = (ctx.launches - l0) // max(1, args.steps + args.warmup)
+    t_step = [sum(s) for s in steps]
+    t_med = statistics.median(t_step)
+    if dist:
+        tt = torch.tensor([t_med], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_med = float(tt.item())
+    flops = sum(2 * s for s in nnz_s)
+    value = world * flops / t_med / 1e9
+    # ---- e2e through the public API with host buffers ----------------------
+    pinned = []
+    for xi, xv in vecs:
+        if len(xi) == cols:
+            d = torch.zeros(cols, dtype=torch.float32).pin_memory()
+            d[torch.from_numpy(xi)] = torch.from_numpy(xv)
+            pinned.append(("dense", d.numpy()))
+        else:
+            pinned.append(("sparse", (torch.from_numpy(xi).pin_memory().numpy(),
+                                      torch.from_numpy(xv).pin_memory().numpy())))
+    ybuf = torch.zeros(rows, dtype=torch.float32).pin_memory().numpy()
+    e2e_x = A.DeviceVector(cols, np.float32, ctx)
+    h2d = d2h = 0
+    for kind, payload in pinned:
+        h2d += payload.nbytes if kind == "dense" else payload[0].nbytes + payload[1].nbytes
+    e2e_times = []
+    for it in range(args.warmup + args.steps):
+        tsum = 0.0
+        d2h_step = 0
+        for i, (kind, payload) in enumerate(pinned):
+            t0 = time.perf_counter()
+            if kind == "dense":
+                e2e_x.set_dense(payload)
+            else:
+                e2e_x.set_sparse(*payload)
+            y, k = A.run_adaptive(m, e2e_x, bundle, out=out)
+            if k.index() in (5, 7):
+                s = y.sparse()
+                d2h_step += s.indices.nbytes // 2 + s.values.nbytes  # int32 indices cross the bus
+            else:
+                A._check(A._lib.adaspmv_output_dense(ctx.h, y.h, A._ptr(ybuf)))
+                d2h_step += ybuf.nbytes
+            tsum += time.perf_counter() - t0
+        if it >= args.warmup:
+            e2e_times.append(tsum)
+            d2h = d2h_step
+    e2e_v = world * flops / statistics.median(e2e_times) / 1e9
+    # ---- roofline of the dominant kernel (the largest share of the step) ----
+    per_point = [statistics.median([s[i] for s in steps]) for i in range(len(dvs))]
+    dom = int(np.argmax(per_point))
+    k_dom = chosen[dom]
+    out_nnz = nnz_x[dom]
+    _, fam = alg_bytes(rows, cols, nnz, nnz_x[dom], nnz_s[dom], out_nnz)
+    hbm, src = peaks()
+    achieved = fam[k_dom] / per_point[dom] / 1e9
+    prof = ROOT / "profiles" / "r01_roofline_traffic.json"
+    traffic = None
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("traffic_bytes_per_launch")
+        except Exception:
+            traffic = None
+    points = []
+    for i in range(len(dvs)):
+        b_alg, fam_i = alg_bytes(rows, cols, nnz, nnz_x[i], nnz_s[i], 0)
+        tb = min(kernel_t[i])
+        points.append({
+            "x_sparsity": SPARSITIES[i], "nnz_x": nnz_x[i], "nnz_s": nnz_s[i],
+            "selected": A.KernelId.from_index(chosen[i]).name(), "t_sel_us": round(per_point[i] * 1e6, 2),
+            "best": A.KernelId.from_index(int(np.argmin(kernel_t[i]))).name(), "t_best_us": round(tb * 1e6, 2),
+            "regret": round(per_point[i] / tb, 3),
+            "gflops_sel": round(2 * nnz_s[i] / per_point[i] / 1e9, 2),
+            "alg_GBps_sel": round(b_alg / per_point[i] / 1e9, 1),
+            "pct_roofline_sel": round(100 * b_alg / per_point[i] / 1e9 / hbm, 1),
+            "t_kernels_us": [round(t * 1e6, 2) for t in kernel_t[i]],
+        })
+    regret_total = sum(per_point) / sum(min(r) for r in kernel_t)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_med * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded numpy generator, SURVEY.md 8(d) C2)",
+        "config": {"workload": WORKLOAD, "rows": rows, "cols": cols, "nnz": nnz,
+                   "x_sparsity": list(SPARSITIES), "l2": "256 MiB flush before timed multiplies with "
+                   "working set < 64 MB; larger inputs exceed L2", "selector": str(bundle_path.name),
+                   "parallelism": f"row-replicated x{world}" if world > 1 else "1 GPU"},
+        "e2e": {"value": round(e2e_v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "roofline": {"bound": "hbm", "kernel": A.KernelId.from_index(k_dom).name(),
+                     "x_sparsity": SPARSITIES[dom], "achieved": round(achieved, 1), "peak": hbm,
+                     "peak_source": src, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                     "traffic": traffic, "alg_bytes": int(fam[k_dom])},
+        "selector_regret": round(regret_total, 4),
+        "gpu_launches": int(launches),
+        "points": points,
+        "setup_s": {"generate": round(gen_s, 1), "upload_csc_features": round(upload_s, 2)},
+    }
+    line["clocks"] = clk.summary()
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(rows, cols, ro, ci, vals, vecs)
+    if dist:
+        dist.destroy_process_group()
+    return line if rank == 0 else None
+
+
+def cpu_baseline(rows, cols, ro, ci, vals, vecs):
+    """The reference CPU implementation (oracle/_ref) on a bounded sample:
+    one pass over the sweep, every point with its best reference kernel."""
+    try:
+        from oracle.oracle import Ref, have_ref
+        if not have_ref(np.float32):
+            return {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference",
+                    "sample": "oracle/_ref not built"}
+        ref = Ref(np.float32)
+        threads = os.cpu_count() or 1
+        ref.set_threads(threads)
+        M = ref.matrix(rows, cols, ro, ci, vals)
+        col_off = M.export()[3]
+        nnz_s = [int(np.sum(col_off[xi + 1] - col_off[xi])) for xi, _ in vecs]
+        best = cpu_choose(M, vecs)
+        ts = ref_sweep_times(M, vecs, best, repeats=3, warmup=1)
+        v = sum(2 * s for s in nnz_s) / sum(ts) / 1e9
+        return {"value": round(v, 4), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+                "sample": "one C2 sweep (7 points), best reference kernel per point, median of 3",
+                "per_point_ms": [round(t * 1e3, 3) for t in ts],
+                "kernel_per_point": best}
+    except Exception as e:  # never fail the GPU line on the baseline
+        return {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--bundle", default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_ours(args, rank, world)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -134,7 +134,7 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         else k = heuristic_kernel(ctx, m, x);
         const auto t1 = clk::now();
         if (k <= 3) {
-            vector_ensure_dense(ctx, x);
+            vector_ensure_dense(ctx, x, SR);
             if (k >= 2) vector_ensure_mask(ctx, x);
         } else if (k == 6 || k == 7) {
             vector_ensure_eff(ctx, x, m);

@@ -125,6 +125,7 @@ struct Vector {
     uint64_t version = 0;
     // representations (kernels.hpp:171-175)
     DevBuf dense;   bool has_dense = false;
+    int dense_fill = -1;  // semiring whose identity filled absent entries (-1: user dense)
     DevBuf sp_idx;  DevBuf sp_val; bool has_sparse = false;
     int64_t nnz = -1;  // |supp x| when known on host (sparse input, or counted)
     DevBuf mask;    bool has_mask = false;   // (n+31)/32 u32 words == (n+63)/64 u64 LSB-first
@@ -134,6 +135,7 @@ struct Vector {
     DevBuf stage_idx;  // int64 staging for host index uploads
     void invalidate() {
         has_dense = has_sparse = has_mask = has_eff = false;
+        dense_fill = -1;
         nnz = -1;
         nnz_s = -1;
         nnz_s_matrix = 0;
@@ -183,7 +185,9 @@ Matrix* matrix_transpose(Context& ctx, const Matrix& m);
 void vector_set_dense_device(Context& ctx, Vector& v, const void* d_vals);
 void vector_set_sparse_device(Context& ctx, Vector& v, int64_t nnz, const int32_t* d_idx,
                               const void* d_vals);
-void vector_ensure_dense(Context& ctx, Vector& v);
+// dense view; entries absent from a sparse input hold the identity of
+// `semiring` (0 for plus-times / or-and, +inf for min-plus)
+void vector_ensure_dense(Context& ctx, Vector& v, int semiring = ADASPMV_PLUS_TIMES);
 void vector_ensure_sparse(Context& ctx, Vector& v);
 void vector_ensure_mask(Context& ctx, Vector& v);
 void vector_ensure_eff(Context& ctx, Vector& v, const Matrix& m);  // also sparse

@@ -47,7 +47,7 @@ void run_t(Context& ctx, const Matrix& m, Vector& x, int kernel, const adaspmv_c
         case 1:
         case 2:
         case 3: {
-            vector_ensure_dense(ctx, x);
+            vector_ensure_dense(ctx, x, SR);
             const uint32_t* mask = nullptr;
             if (kernel >= 2) {
                 vector_ensure_mask(ctx, x);

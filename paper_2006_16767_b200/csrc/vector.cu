@@ -10,6 +10,7 @@
 
 #include "device.cuh"
 #include "internal.hpp"
+#include "kernels.hpp"
 #include "prims.cuh"
 
 namespace ada {
@@ -83,9 +84,10 @@ struct DegreeIn {
 int blocks_for(int64_t n, int t) { return static_cast<int>(std::max<int64_t>(1, (n + t - 1) / t)); }
 
 template <class V>
-void ensure_dense_t(Context& ctx, Vector& v) {
+void ensure_dense_t(Context& ctx, Vector& v, int semiring) {
     V* d = static_cast<V*>(v.dense.ensure(sizeof(V) * static_cast<size_t>(std::max<int64_t>(v.n, 1))));
-    ADA_CUDA(cudaMemsetAsync(d, 0, sizeof(V) * static_cast<size_t>(v.n), ctx.stream));
+    if (semiring == ADASPMV_MIN_PLUS) fill_value<V, SR_MIN_PLUS>(ctx, d, v.n);
+    else ADA_CUDA(cudaMemsetAsync(d, 0, sizeof(V) * static_cast<size_t>(v.n), ctx.stream));
     if (v.nnz > 0) {
         scatter_kernel<V><<<blocks_for(v.nnz, 256), 256, 0, ctx.stream>>>(
             v.nnz, v.sp_idx.as<int32_t>(), v.sp_val.as<V>(), d);
@@ -138,12 +140,14 @@ void vector_set_sparse_device(Context& ctx, Vector& v, int64_t nnz, const int32_
     v.has_sparse = true;
 }
 
-void vector_ensure_dense(Context& ctx, Vector& v) {
-    if (v.has_dense) return;
+void vector_ensure_dense(Context& ctx, Vector& v, int semiring) {
+    const int fill = semiring == ADASPMV_MIN_PLUS ? ADASPMV_MIN_PLUS : ADASPMV_PLUS_TIMES;
+    if (v.has_dense && (v.dense_fill < 0 || v.dense_fill == fill)) return;
     if (!v.has_sparse) invalid("vector has no value set");
-    if (v.dtype == ADASPMV_F64) ensure_dense_t<double>(ctx, v);
-    else ensure_dense_t<float>(ctx, v);
+    if (v.dtype == ADASPMV_F64) ensure_dense_t<double>(ctx, v, fill);
+    else ensure_dense_t<float>(ctx, v, fill);
     v.has_dense = true;
+    v.dense_fill = fill;
 }
 
 void vector_ensure_sparse(Context& ctx, Vector& v) {
