@@ -102,6 +102,10 @@ void* adaspmv_ctx_stream(adaspmv_ctx* ctx);
 const char* adaspmv_last_error(void);
 /* Number of kernels this library launched on `ctx` so far (bench evidence). */
 int64_t adaspmv_ctx_launch_count(adaspmv_ctx* ctx);
+/* When enabled, every run is bracketed by CUDA events on the context stream
+ * (device time of the multiply incl. conversions it triggers, excluding host
+ * time before the first launch); read with adaspmv_output_elapsed. */
+int adaspmv_ctx_set_timing(adaspmv_ctx* ctx, int enable);
 const char* adaspmv_version(void);
 
 /* ---- matrices: DualMatrix (sparse.hpp:204-259) ------------------------------ */
@@ -220,6 +224,8 @@ int adaspmv_output_dense(adaspmv_ctx* ctx, adaspmv_output* y, void* values);
  * Writes nnz_y; copies up to `capacity` entries when indices/values != NULL. */
 int adaspmv_output_sparse(adaspmv_ctx* ctx, adaspmv_output* y, int64_t capacity,
                           int64_t* indices, void* values, int64_t* nnz_y);
+/* Seconds between the events of the last timed run of `y` (synchronises). */
+int adaspmv_output_elapsed(adaspmv_ctx* ctx, adaspmv_output* y, double* seconds);
 /* Device pointers of the views (materialised on demand). */
 int adaspmv_output_device_dense(adaspmv_ctx* ctx, adaspmv_output* y, const void** d_values);
 int adaspmv_output_device_sparse(adaspmv_ctx* ctx, adaspmv_output* y, const int32_t** d_indices,

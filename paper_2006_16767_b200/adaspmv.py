@@ -126,6 +126,8 @@ def load(path: Optional[os.PathLike] = None):
         "adaspmv_ctx_synchronize": [vp],
         "adaspmv_ctx_stream": [vp],
         "adaspmv_ctx_launch_count": [vp],
+        "adaspmv_ctx_set_timing": [vp, C.c_int],
+        "adaspmv_output_elapsed": [vp, vp, P(C.c_double)],
         "adaspmv_matrix_create_csr": [vp, i64, i64, vp, vp, vp, C.c_int, P(vp)],
         "adaspmv_matrix_create_csr_device": [vp, i64, i64, i64, vp, vp, vp, C.c_int, P(vp)],
         "adaspmv_matrix_from_triplets": [vp, i64, i64, i64, vp, vp, vp, C.c_int, P(vp)],
@@ -386,6 +388,10 @@ class Context:
     @property
     def launches(self) -> int:
         return int(_lib.adaspmv_ctx_launch_count(self.h))
+
+    def set_timing(self, enable: bool = True):
+        """Bracket every multiply with CUDA events (MultiplyOutput.elapsed())."""
+        _check(_lib.adaspmv_ctx_set_timing(self.h, int(bool(enable))))
 
     def close(self):
         if getattr(self, "h", None):
@@ -657,6 +663,12 @@ class MultiplyOutput:
         kk = C.c_int64()
         _check(_lib.adaspmv_output_sparse(self.ctx.h, self.h, k, _ptr(idx), _ptr(val), C.byref(kk)))
         return SparseVector(n, idx[:k], val[:k])
+
+    def elapsed(self) -> float:
+        """Device seconds of the last timed run (Context.set_timing)."""
+        s = C.c_double()
+        _check(_lib.adaspmv_output_elapsed(self.ctx.h, self.h, C.byref(s)))
+        return s.value
 
     def device_dense(self) -> int:
         p = C.c_void_p()

@@ -173,6 +173,26 @@ void* adaspmv_ctx_stream(adaspmv_ctx* ctx) { return ctx ? static_cast<void*>(ctx
 
 int64_t adaspmv_ctx_launch_count(adaspmv_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int adaspmv_ctx_set_timing(adaspmv_ctx* ctx, int enable) {
+    return guarded([&] {
+        need(ctx, "context");
+        ctx->timing = enable != 0;
+    });
+}
+
+int adaspmv_output_elapsed(adaspmv_ctx* ctx, adaspmv_output* y, double* seconds) {
+    return guarded([&] {
+        bind(ctx);
+        need(y, "output");
+        need(seconds, "out");
+        if (!y->timed || !y->ev[0] || !y->ev[1]) ada::invalid("output was not produced by a timed run");
+        ADA_CUDA(cudaEventSynchronize(y->ev[1]));
+        float ms = 0;
+        ADA_CUDA(cudaEventElapsedTime(&ms, y->ev[0], y->ev[1]));
+        *seconds = static_cast<double>(ms) * 1e-3;
+    });
+}
+
 // ---- matrices -------------------------------------------------------------------
 int adaspmv_matrix_create_csr(adaspmv_ctx* ctx, int64_t rows, int64_t cols,
                               const int64_t* row_offsets, const int64_t* col_indices,

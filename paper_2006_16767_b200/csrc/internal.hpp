@@ -81,6 +81,7 @@ struct Context {
     bool own_stream = false;
     int sm_count = 148;
     int64_t launches = 0;
+    bool timing = false;  // bracket every run with CUDA events (adaspmv_output_elapsed)
     // general scratch (reused by every call; calls on a context are serialised)
     DevBuf scratch[6];
     // pinned host scalars for D2H of counts (nnz_s, nnz_y, ...)
@@ -96,9 +97,9 @@ struct Context {
     int64_t fetch_scalar(const int64_t* d);
 };
 
-// LB tiles of the row-major kernels: fixed TILE nonzeros per CTA
-// (make_partition's equal-item split, partition.hpp:37-56, with W = ceil(nnz/TILE)).
-constexpr int kRowTile = 2048;
+// LB tiles of the row-major kernels: fixed kRowTile nonzeros per warp
+// (make_partition's equal-item split, partition.hpp:37-56, W = ceil(nnz/kRowTile)).
+constexpr int kRowTile = 256;
 
 struct Matrix {
     Context* ctx = nullptr;
@@ -108,8 +109,12 @@ struct Matrix {
     DevBuf row_off, col_idx, vals;   // CSR
     DevBuf col_off, row_idx, cvals;  // CSC
     int64_t n_row_tiles = 0;
-    DevBuf tile_head;       // int64 [n_row_tiles+1]: segment_of(row_off, t*kRowTile)
-    DevBuf tile_rs;         // int64 [n_row_tiles+1]: first row with row_off >= t*kRowTile
+    // int64 [n_row_tiles+2]: [t] = first row of tile t's row window: the row
+    // holding item t*kRowTile, or the first row starting there (so empty rows
+    // starting at the tile boundary are inside the window); [n] = rows;
+    // [n+1] = first row starting at nnz (trailing empty rows)
+    DevBuf tile_head;
+    int64_t trail_start = 0;  // host copy of tile_head[n+1]
     DevBuf tile_partials;   // per tile: head partial, tail partial (V) + tail row (int64)
     double feat[9] = {0};
     int64_t max_col_deg = 0;
@@ -153,6 +158,13 @@ struct Output {
     int64_t nnz = -1;      // host-known nnz_y (-1 = only on device, slot d_nnz)
     DevBuf d_nnz;          // device int64 nnz_y
     int semiring = ADASPMV_PLUS_TIMES;  // identity of absent entries
+    // device-time bracket of the last run (recorded when Context::timing)
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    bool timed = false;
+    ~Output() {
+        if (ev[0]) cudaEventDestroy(ev[0]);
+        if (ev[1]) cudaEventDestroy(ev[1]);
+    }
     void reset(int64_t len, int dt) {
         n = len;
         dtype = dt;

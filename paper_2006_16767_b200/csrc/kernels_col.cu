@@ -199,31 +199,46 @@ __global__ void __launch_bounds__(kSmallNT) col_sort_small_kernel(
     V* sval = reinterpret_cast<V*>(skey + kSmallPairs);                  // kSmallPairs
     int* sflag = reinterpret_cast<int*>(sval + kSmallPairs);             // kSmallPairs
     __shared__ int64_t sm_scan[kSmallNT / 32 + 1];
+    __shared__ int64_t s_base[kSmallNT];   // col_offsets[col] of the chunk's columns
+    __shared__ int s_off[kSmallNT + 1];    // chunk-relative emission offsets
+    __shared__ V s_xv[kSmallNT];
 
-    // 1. emit: support processed in chunks of kSmallNT columns; one thread per
-    //    support column walks its entries (columns are short on this path).
+    // 1. emit: support processed in chunks of kSmallNT columns.  The chunk's
+    //    degrees are scanned, then every thread emits pairs o = tid, tid+NT, ...
+    //    (support position by binary search over the offsets), so all matrix
+    //    loads of a chunk are independent and in flight together.
     int64_t base = 0;
     for (int64_t c0 = 0; c0 < nnz_x; c0 += kSmallNT) {
         const int64_t s = c0 + threadIdx.x;
-        int64_t deg = 0, b = 0;
-        int32_t col = 0;
+        int64_t deg = 0;
         if (s < nnz_x) {
-            col = xi[s];
-            b = co[col];
+            const int32_t col = xi[s];
+            const int64_t b = co[col];
             deg = co[col + 1] - b;
+            s_base[threadIdx.x] = b;
+            s_xv[threadIdx.x] = xv[s];
         }
         int64_t tot;
-        const int64_t off = block_exclusive_sum<kSmallNT>(deg, sm_scan, &tot) + base;
-        if (s < nnz_x) {
-            const V xval = xv[s];
-            for (int64_t k = 0; k < deg; ++k) {
-                const int64_t o = off + k;
-                skey[o] = (static_cast<uint64_t>(static_cast<uint32_t>(ri[b + k])) << 32) |
-                          static_cast<uint64_t>(o);
-                sval[o] = S::mul(S::kUsesValues ? cv[b + k] : V(1), xval);
+        const int64_t off = block_exclusive_sum<kSmallNT>(deg, sm_scan, &tot);
+        s_off[threadIdx.x] = static_cast<int>(off);
+        if (threadIdx.x == 0) s_off[kSmallNT] = static_cast<int>(tot);
+        __syncthreads();
+        const int ncols = static_cast<int>(nnz_x - c0 < kSmallNT ? nnz_x - c0 : kSmallNT);
+        for (int o = threadIdx.x; o < tot; o += kSmallNT) {
+            int lo = 0, hi = ncols;  // largest c with s_off[c] <= o
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_off[mid] <= o) lo = mid;
+                else hi = mid;
             }
+            const int64_t k = s_base[lo] + (o - s_off[lo]);
+            const int64_t g = base + o;
+            skey[g] = (static_cast<uint64_t>(static_cast<uint32_t>(ri[k])) << 32) |
+                      static_cast<uint64_t>(g);
+            sval[g] = S::mul(S::kUsesValues ? cv[k] : V(1), s_xv[lo]);
         }
         base += tot;
+        __syncthreads();
     }
     const int n = static_cast<int>(base);
     int np2 = 1;

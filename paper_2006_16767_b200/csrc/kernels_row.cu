@@ -76,11 +76,21 @@ __global__ void __launch_bounds__(kNT) row_direct_kernel(int64_t rows,
 }
 
 // ---------------------------------------------------------------------------
-// LB tile kernel
+// LB warp-tile kernel.  Warp w of the grid owns items [w*T, (w+1)*T), T =
+// kRowTile = 256: two rounds of 128 items, lane l holding the 4 consecutive
+// items 4l..4l+3 of each round (one 128-bit load of columns, one/two of
+// values: fully coalesced).  All 8 x gathers per lane are issued before any
+// is consumed.  The row window of the tile (<= 33 offsets) sits in shared
+// memory; lanes find their row by binary search there and walk their 4
+// items; runs are joined across lanes by a warp segmented scan (no block
+// barriers).  Tiles whose window exceeds 33 rows take the same code path
+// with the offsets read from global memory.
 // ---------------------------------------------------------------------------
-constexpr int kIPT = 4;                     // items per thread per round
-constexpr int kRound = kNT * kIPT;          // 1024
-constexpr int kRounds = kRowTile / kRound;  // 2
+constexpr int kIPT = 4;                       // items per lane per round
+constexpr int kRound = 32 * kIPT;             // 128
+constexpr int kRounds = kRowTile / kRound;    // 2
+constexpr int kWin = 33;                      // offsets held per warp window
+constexpr int kWarps = kNT / 32;
 static_assert(kRounds * kRound == kRowTile, "tile shape");
 
 template <class V>
@@ -101,23 +111,39 @@ struct Vec4<double> {
     }
 };
 
+// Row offsets as seen by one warp tile: a shared-memory window [ws, ws+33)
+// when it covers the tile, else global memory.
+struct RowWindow {
+    const int64_t* __restrict__ ro;
+    const int64_t* win;  // smem, valid when fast
+    int64_t ws, rows;
+    bool fast;
+    __device__ int64_t off(int64_t r) const { return fast ? win[r - ws] : __ldg(ro + r); }
+    // segment_of (partition.hpp:30-33) for a position inside the tile
+    __device__ int64_t row_of(int64_t pos, int64_t hi) const {
+        int64_t lo = ws;  // off(ws) <= pos
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (off(mid) <= pos) lo = mid;
+            else hi = mid;
+        }
+        return lo;
+    }
+};
+
 template <class V, bool VALIDATE, int SR>
 __global__ void __launch_bounds__(kNT) row_lb_kernel(
-    int64_t rows, int64_t nnz, const int64_t* __restrict__ ro, const int32_t* __restrict__ ci,
-    const V* __restrict__ vals, const V* __restrict__ x, const uint32_t* __restrict__ mask,
-    const int64_t* __restrict__ tile_head, const int64_t* __restrict__ tile_rs, V* __restrict__ y,
+    int64_t rows, int64_t nnz, int64_t ntiles, const int64_t* __restrict__ ro,
+    const int32_t* __restrict__ ci, const V* __restrict__ vals, const V* __restrict__ x,
+    const uint32_t* __restrict__ mask, const int64_t* __restrict__ tile_head, V* __restrict__ y,
     V* __restrict__ head_part, V* __restrict__ tail_part, int64_t* __restrict__ tail_row) {
     using S = Semiring<SR, V>;
-    __shared__ int sf[kNT / 32];
-    __shared__ V sv[kNT / 32];
-    __shared__ V sp[kNT / 32 + 1];
-
-    const int64_t t = blockIdx.x;
+    __shared__ int64_t swin[kWarps][kWin];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+    if (t >= ntiles) return;  // whole warp; no block barriers below
     const int64_t tb = t * kRowTile;
     const int64_t te = min(tb + static_cast<int64_t>(kRowTile), nnz);
-    const int64_t h = tile_head[t];
-    const int64_t hi = min(tile_head[t + 1] + 1, rows);  // search bound (exclusive)
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     // ---- stream the tile: all loads of both rounds issued before use -------
     int c[kRounds][kIPT];
@@ -125,7 +151,7 @@ __global__ void __launch_bounds__(kNT) row_lb_kernel(
     V xv[kRounds][kIPT];
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
-        const int64_t p0 = tb + r * kRound + threadIdx.x * kIPT;
+        const int64_t p0 = tb + r * kRound + lane * kIPT;
         if (p0 + kIPT <= te) {
             int4 cc = ld_stream(reinterpret_cast<const int4*>(ci + p0));
             c[r][0] = cc.x; c[r][1] = cc.y; c[r][2] = cc.z; c[r][3] = cc.w;
@@ -145,7 +171,7 @@ __global__ void __launch_bounds__(kNT) row_lb_kernel(
     }
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
-        const int64_t p0 = tb + r * kRound + threadIdx.x * kIPT;
+        const int64_t p0 = tb + r * kRound + lane * kIPT;
 #pragma unroll
         for (int j = 0; j < kIPT; ++j) {
             bool ok = p0 + j < te;
@@ -155,29 +181,50 @@ __global__ void __launch_bounds__(kNT) row_lb_kernel(
         }
     }
 
-    // ---- rows owned by this tile that are empty: y = zero (SR identity) ----
+    // ---- row window ----------------------------------------------------------
+    const int64_t ws = __ldg(tile_head + t);
+    const int64_t wlast = min(ws + kWin - 1, rows);  // last offset index held
     {
-        const int64_t rs = tile_rs[t], re = tile_rs[t + 1];
-        for (int64_t r = rs + threadIdx.x; r < re; r += kNT)
-            if (__ldg(ro + r) == __ldg(ro + r + 1)) y[r] = S::zero();
+        const int64_t r = ws + lane;
+        swin[warp][lane] = r <= rows ? __ldg(ro + r) : nnz;
+        if (lane == 0) swin[warp][32] = ws + 32 <= rows ? __ldg(ro + ws + 32) : nnz;
+    }
+    __syncwarp();
+    // fast iff every item's row and row end lies in the window
+    const bool fast = swin[warp][wlast - ws] >= te || wlast == rows;
+    RowWindow W{ro, &swin[warp][0], ws, rows, fast};
+    const int64_t hi = fast ? wlast : rows;  // exclusive bound of row_of results (< rows)
+    const int64_t row_hi = min(hi, rows);
+
+    // ---- empty rows starting in [tb, te) belong to this tile ----------------
+    if (fast) {
+        const int64_t r = ws + lane;
+        if (r < rows && lane < kWin - 1) {
+            const int64_t o0 = swin[warp][lane], o1 = swin[warp][lane + 1];
+            if (o0 == o1 && o0 >= tb && o0 < te) y[r] = S::zero();
+        }
+    } else {
+        for (int64_t r = ws + lane; r < rows; r += 32) {
+            const int64_t o0 = __ldg(ro + r);
+            if (o0 >= te) break;
+            if (o0 >= tb && o0 == __ldg(ro + r + 1)) y[r] = S::zero();
+        }
     }
 
     V carry = S::zero();  // value of the row open at the start of the round
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
-        const int64_t p0 = tb + r * kRound + threadIdx.x * kIPT;
+        const int64_t p0 = tb + r * kRound + lane * kIPT;
         const int64_t p1 = min(p0 + kIPT, te);
         const bool active = p0 < te;
-        int64_t row = 0;
-        bool cont = false, head_closed = false, last_open = false;
+        int64_t row = 0, first_row = 0;
+        bool cont = false, head_closed = false, last_open = false, first = true;
         V head_val = S::zero(), acc = S::zero();
-        bool first = true;
-        int64_t first_row = 0;
         if (active) {
-            row = segment_search(ro, h, hi, p0);
+            row = W.row_of(p0, row_hi);
             first_row = row;
-            cont = __ldg(ro + row) < p0;
-            int64_t row_end = __ldg(ro + row + 1);
+            cont = W.off(row) < p0;
+            int64_t row_end = W.off(row + 1);
 #pragma unroll
             for (int j = 0; j < kIPT; ++j) {
                 const int64_t p = p0 + j;
@@ -186,19 +233,19 @@ __global__ void __launch_bounds__(kNT) row_lb_kernel(
                         if (first && cont) {
                             head_closed = true;
                             head_val = acc;
-                        } else if (__ldg(ro + row) < row_end) {
-                            y[row] = acc;  // complete inside this thread
+                        } else if (W.off(row) < row_end) {
+                            y[row] = acc;  // complete inside this lane
                         }
                         first = false;
                         ++row;
-                        row_end = __ldg(ro + row + 1);
+                        row_end = W.off(row + 1);
                         acc = S::zero();
                     }
                     if (c[r][j] >= 0) acc = S::fma(a[r][j], xv[r][j], acc);
                 }
             }
             last_open = row_end > p1;
-            if (!last_open) {  // last run closes exactly at the thread end
+            if (!last_open) {  // last run closes exactly at the lane's end
                 if (first && cont) {
                     head_closed = true;
                     head_val = acc;
@@ -209,49 +256,28 @@ __global__ void __launch_bounds__(kNT) row_lb_kernel(
                 first = false;
             }
         }
-        // segmented-scan element: pass-through only if the thread is inside
-        // one continuing row that stays open.
+        // segmented-scan element: pass-through only inside one open continuing row
         SegPair<V> e;
-        e.f = (active && first && cont && last_open) ? 0 : 1;
+        e.f = (active && !(first && cont && last_open)) ? 1 : 0;
         e.v = (active && last_open) ? acc : S::zero();
-        if (!active) e.f = 0, e.v = S::zero();  // neutral
         SegPair<V> inc = warp_seg_inclusive(e, [](V u, V w) { return S::add(u, w); });
-        if (lane == 31) {
-            sf[warp] = inc.f;
-            sv[warp] = inc.v;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            V pcur = carry;
-            sp[0] = pcur;
-#pragma unroll
-            for (int w = 0; w < kNT / 32; ++w) {
-                pcur = sf[w] ? sv[w] : S::add(pcur, sv[w]);
-                sp[w + 1] = pcur;
-            }
-        }
-        __syncthreads();
-        const V wpre = sp[warp];
-        const V incl = inc.f ? inc.v : S::add(wpre, inc.v);
+        const V incl = inc.f ? inc.v : S::add(carry, inc.v);
         V excl = __shfl_up_sync(kFull, incl, 1);
-        if (lane == 0) excl = wpre;
-        const V round_carry = sp[kNT / 32];
+        if (lane == 0) excl = carry;
         if (active && head_closed) {
             const V total = S::add(excl, head_val);
-            if (__ldg(ro + first_row) >= tb) y[first_row] = total;  // row began in this tile
-            else head_part[t] = total;                               // shared head row
+            if (W.off(first_row) >= tb) y[first_row] = total;  // row began in this tile
+            else head_part[t] = total;                           // shared head row
         }
-        carry = round_carry;
-        __syncthreads();  // sf/sv/sp reuse
+        carry = __shfl_sync(kFull, incl, 31);
     }
 
     // ---- tile epilogue: the row open at te ----------------------------------
-    if (threadIdx.x == 0) {
-        const int64_t R = segment_search(ro, h, hi, te - 1);
-        const int64_t rend = __ldg(ro + R + 1);
+    if (lane == 0) {
+        const int64_t R = W.row_of(te - 1, row_hi);
         int64_t tr = -1;
-        if (rend > te) {
-            if (__ldg(ro + R) >= tb) {
+        if (W.off(R + 1) > te) {
+            if (W.off(R) >= tb) {
                 tail_part[t] = carry;
                 tr = R;
             } else {
@@ -308,15 +334,16 @@ void launch_lb(Context& ctx, const Matrix& m, const V* x, const uint32_t* mask, 
     V* head = reinterpret_cast<V*>(m.tile_partials.p);
     V* tail = head + T;
     int64_t* trow = reinterpret_cast<int64_t*>(tail + T);
-    row_lb_kernel<V, VALIDATE, SR><<<static_cast<unsigned>(T), kNT, 0, ctx.stream>>>(
-        m.rows, m.nnz, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), m.vals.as<V>(), x, mask,
-        m.tile_head.as<int64_t>(), m.tile_rs.as<int64_t>(), y, head, tail, trow);
+    row_lb_kernel<V, VALIDATE, SR><<<static_cast<unsigned>((T + kWarps - 1) / kWarps), kNT, 0, ctx.stream>>>(
+        m.rows, m.nnz, T, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), m.vals.as<V>(), x, mask,
+        m.tile_head.as<int64_t>(), y, head, tail, trow);
     ADA_LAUNCHED(ctx);
     if (T > 1) {
         row_lb_fixup_kernel<V, SR><<<static_cast<unsigned>((T + 255) / 256), 256, 0, ctx.stream>>>(
             T, m.row_off.as<int64_t>(), head, tail, trow, y);
         ADA_LAUNCHED(ctx);
     }
+    if (m.trail_start < m.rows) fill_value<V, SR>(ctx, y + m.trail_start, m.rows - m.trail_start);
 }
 
 }  // namespace

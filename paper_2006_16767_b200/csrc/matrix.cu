@@ -78,50 +78,47 @@ struct U64In {
     __device__ int64_t operator()(int64_t i) const { return static_cast<int64_t>(c[i]); }
 };
 
-// tile_head[t] = segment_of(ro, t * kRowTile) for t < ntiles; [ntiles] = rows
-__global__ void tile_head_kernel(const int64_t* __restrict__ ro, int64_t rows, int64_t ntiles,
-                                 int64_t* __restrict__ head) {
-    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t > ntiles) return;
-    if (t == ntiles) {
-        head[t] = rows;
-        return;
-    }
-    head[t] = segment_search(ro, 0, rows + 1, t * static_cast<int64_t>(kRowTile));
-}
-
-// tile_rs[t] = lower_bound(ro, t * kRowTile): rows whose start lies in tile t
-// are owned by it (it writes their y when they are empty); [ntiles] = rows.
-__global__ void tile_rs_kernel(const int64_t* __restrict__ ro, int64_t rows, int64_t ntiles,
-                               int64_t* __restrict__ rs) {
-    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t > ntiles) return;
-    if (t == ntiles) {
-        rs[t] = rows;
-        return;
-    }
-    const int64_t pos = t * static_cast<int64_t>(kRowTile);
-    int64_t lo = 0, hi = rows + 1;  // first index with ro[i] >= pos
+// lower_bound: first index i in [0, rows] with ro[i] >= pos
+__device__ int64_t lower_row(const int64_t* __restrict__ ro, int64_t rows, int64_t pos) {
+    int64_t lo = 0, hi = rows + 1;
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
         if (ro[mid] < pos) lo = mid + 1;
         else hi = mid;
     }
-    rs[t] = lo;
+    return lo;
+}
+
+// Row window start of each LB warp tile (see Matrix::tile_head): the row that
+// holds item t*kRowTile when the tile starts mid-row, else the first row
+// starting at the tile boundary (empty rows there are owned by this tile).
+__global__ void tile_head_kernel(const int64_t* __restrict__ ro, int64_t rows, int64_t nnz,
+                                 int64_t ntiles, int64_t* __restrict__ head) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t > ntiles + 1) return;
+    if (t == ntiles) {
+        head[t] = rows;
+        return;
+    }
+    if (t == ntiles + 1) {
+        head[t] = lower_row(ro, rows, nnz);
+        return;
+    }
+    const int64_t pos = t * static_cast<int64_t>(kRowTile);
+    const int64_t lb = lower_row(ro, rows, pos);
+    head[t] = (lb <= rows && ro[lb] == pos) ? lb : lb - 1;
 }
 
 void build_tiles(Context& ctx, Matrix& m) {
     m.n_row_tiles = (m.nnz + kRowTile - 1) / kRowTile;
-    const size_t n = static_cast<size_t>(m.n_row_tiles + 1);
+    const size_t n = static_cast<size_t>(m.n_row_tiles + 2);
     m.tile_head.ensure(sizeof(int64_t) * n);
-    m.tile_rs.ensure(sizeof(int64_t) * n);
-    const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
-    tile_head_kernel<<<blocks, 256, 0, ctx.stream>>>(m.row_off.as<int64_t>(), m.rows,
-                                                     m.n_row_tiles, m.tile_head.as<int64_t>());
+    tile_head_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx.stream>>>(
+        m.row_off.as<int64_t>(), m.rows, m.nnz, m.n_row_tiles, m.tile_head.as<int64_t>());
     ADA_LAUNCHED(ctx);
-    tile_rs_kernel<<<blocks, 256, 0, ctx.stream>>>(m.row_off.as<int64_t>(), m.rows, m.n_row_tiles,
-                                                   m.tile_rs.as<int64_t>());
-    ADA_LAUNCHED(ctx);
+    ADA_CUDA(cudaMemcpyAsync(&m.trail_start, m.tile_head.as<int64_t>() + m.n_row_tiles + 1,
+                             sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
     // head partial, tail partial (V) and tail row (int64) per tile
     m.tile_partials.ensure((2 * static_cast<size_t>(m.vbytes()) + sizeof(int64_t)) *
                            static_cast<size_t>(std::max<int64_t>(m.n_row_tiles, 1)));

@@ -127,8 +127,15 @@ void run_kernel(Context& ctx, const Matrix& m, Vector& x, int kernel, const adas
     y.ctx = &ctx;
     y.reset(m.rows, m.dtype);
     y.semiring = cfg.semiring;
+    y.timed = ctx.timing;
+    if (y.timed) {
+        for (auto& e : y.ev)
+            if (!e) ADA_CUDA(cudaEventCreate(&e));
+        ADA_CUDA(cudaEventRecord(y.ev[0], ctx.stream));
+    }
     if (m.dtype == ADASPMV_F64) run_v<double>(ctx, m, x, kernel, cfg, y);
     else run_v<float>(ctx, m, x, kernel, cfg, y);
+    if (y.timed) ADA_CUDA(cudaEventRecord(y.ev[1], ctx.stream));
 }
 
 int64_t output_nnz(Context& ctx, Output& y) {
