@@ -40,6 +40,7 @@ sys.path.insert(0, str(ROOT))
 SPARSITIES = (0.00001, 0.0001, 0.001, 0.01, 0.1, 0.5, 1.0)
 N = 1 << int(os.environ.get("ADASPMV_BENCH_LOG2N", "22"))  # override only for dry runs
 DRAWS = 16 * N
+GATE_CYCLES = 400_000  # ~0.2 ms at 1.9 GHz
 METRIC = "GFLOP/s and HBM GB/s (% of roofline) vs x sparsity; selector regret vs best"
 WORKLOAD = "C2 uniform random 4M x 4M, 2^26 draws (~64M nnz) fp32, x-sparsity sweep 0.001%-100%"
 I_B, O_B = 4, 8  # device index / offset bytes (SURVEY.md section 8 symbols)
@@ -247,9 +248,12 @@ def run_ours(args, rank, world):
     def timed(fn, n_rep, need_flush):
         ts = []
         for _ in range(n_rep):
-            if need_flush:
-                with torch.cuda.stream(stream):
+            with torch.cuda.stream(stream):
+                if need_flush:
                     flush.add_(1)
+                # the GPU spins while the host enqueues the multiply, so the
+                # library's events see device time, not host launch latency
+                torch.cuda._sleep(GATE_CYCLES)
             y = fn()
             if isinstance(y, tuple):
                 y = y[0]

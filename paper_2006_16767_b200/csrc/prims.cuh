@@ -158,7 +158,9 @@ __global__ void __launch_bounds__(kRsThreads) radix_downsweep_kernel(
         __syncwarp();
     }
     __syncthreads();
-    {   // per-digit exclusive prefix over warps (thread = digit)
+    __shared__ int toff[kRsRadix];
+    __shared__ int sm_scan[kRsThreads / 32 + 1];
+    {   // per-digit exclusive prefix over warps (thread = digit), then over digits
         const int d = threadIdx.x;
         int run = 0;
 #pragma unroll
@@ -167,17 +169,33 @@ __global__ void __launch_bounds__(kRsThreads) radix_downsweep_kernel(
             wh[w][d] = run;
             run += t;
         }
+        int total;
+        toff[d] = block_exclusive_sum<kRsThreads>(run, sm_scan, &total);
     }
     __syncthreads();
+    // stage the tile in digit order in shared memory, then write each digit's
+    // run contiguously (coalesced) instead of scattering item by item
+    extern __shared__ __align__(16) unsigned char rs_smem[];
+    uint32_t* skey = reinterpret_cast<uint32_t*>(rs_smem);
+    P* spay = reinterpret_cast<P*>(rs_smem + kRsTile * sizeof(uint32_t));
 #pragma unroll
     for (int r = 0; r < kRsRounds; ++r) {
         const int64_t i = wbase + r * 32 + lane;
         if (i < n) {
             const int d = (key[r] >> shift) & (kRsRadix - 1);
-            const int64_t o = sbase[d] + wh[warp][d] + pos[r];
-            kout[o] = key[r];
-            pout[o] = pay[r];
+            const int p = toff[d] + wh[warp][d] + pos[r];
+            skey[p] = key[r];
+            spay[p] = pay[r];
         }
+    }
+    __syncthreads();
+    const int tile_n = static_cast<int>(min(static_cast<int64_t>(kRsTile), n - tile * kRsTile));
+    for (int i = threadIdx.x; i < tile_n; i += kRsThreads) {
+        const uint32_t k = skey[i];
+        const int d = (k >> shift) & (kRsRadix - 1);
+        const int64_t o = sbase[d] + (i - toff[d]);
+        kout[o] = k;
+        pout[o] = spay[i];
     }
 }
 
@@ -196,6 +214,9 @@ int radix_sort_pairs(Context& ctx, uint32_t* k0, P* p0, uint32_t* k1, P* p1, int
     const int64_t ntiles = (n + kRsTile - 1) / kRsTile;
     int64_t* counts = static_cast<int64_t*>(
         counts_buf.ensure(sizeof(int64_t) * static_cast<size_t>(kRsRadix * ntiles)));
+    const size_t smem = kRsTile * (sizeof(uint32_t) + sizeof(P));
+    ADA_CUDA(cudaFuncSetAttribute(radix_downsweep_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
     int cur = 0;
     for (int shift = 0; shift < bits; shift += 8) {
         uint32_t* kin = cur ? k1 : k0;
@@ -206,7 +227,7 @@ int radix_sort_pairs(Context& ctx, uint32_t* k0, P* p0, uint32_t* k1, P* p1, int
             kin, n, shift, ntiles, counts);
         ADA_LAUNCHED(ctx);
         scan3(ctx, kRsRadix * ntiles, CountsIn{counts}, WriteExclusive{counts}, nullptr, scan_tmp);
-        radix_downsweep_kernel<P><<<static_cast<unsigned>(ntiles), kRsThreads, 0, ctx.stream>>>(
+        radix_downsweep_kernel<P><<<static_cast<unsigned>(ntiles), kRsThreads, smem, ctx.stream>>>(
             kin, pin, kout, pout, n, shift, ntiles, counts);
         ADA_LAUNCHED(ctx);
         cur ^= 1;

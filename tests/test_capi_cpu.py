@@ -80,10 +80,17 @@ def test_shard_rows_balanced_and_whole_rows():
 
 
 def test_bundle_files(tmp_path):
-    # default bundle loads; host mirror of the cascade agrees with node arrays
+    # the shipped (trained) bundle loads and predicts valid kernels
     b = A.SelectorBundle.load(S.DEFAULT_PATH)
     assert b.h
-    trees = S.read_bundle(S.DEFAULT_PATH)
+    shipped = S.read_bundle(S.DEFAULT_PATH)
+    rng = np.random.default_rng(0)
+    for _ in range(100):
+        assert 0 <= S.predict(shipped, rng.random(13) * 1e6) <= 7
+    # hand-set cascade: host mirror agrees with the node arrays
+    p0 = tmp_path / "default.txt"
+    S.write_bundle(p0, S.default_trees())
+    trees = S.read_bundle(p0)
     f = np.zeros(13)
     f[12] = 0.01
     f[11] = 100

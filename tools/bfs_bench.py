@@ -1,0 +1,84 @@
+"""C3: R-MAT scale-22 BFS (BASELINE.json configs[2]) through the adaptive
+executor: levels checked against a queue BFS (CPU oracle), total time for the
+trained selector, the built-in push/pull heuristic and every fixed kernel,
+per-level kernel choices, GTEPS (edges of the reached component / time).
+
+  python tools/bfs_bench.py --scale 22 --semiring or_and
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2006_16767_b200 import adaspmv as A  # noqa: E402
+from paper_2006_16767_b200 import selector as S  # noqa: E402
+from paper_2006_16767_b200 import synth  # noqa: E402
+
+SR = {"or_and": A.OR_AND, "min_plus": A.MIN_PLUS, "plus_times": A.PLUS_TIMES}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--scale", type=int, default=22)
+    ap.add_argument("--semiring", default="or_and")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    t0 = time.time()
+    n, _, ro, ci, vals = synth.rmat(a.scale, 16, seed=2)
+    gen = time.time() - t0
+    ctx = A.Context(0)
+    m = A.DualMatrix.from_csr(n, n, ro, ci, None, dtype=np.float32, ctx=ctx)
+    sr = SR[a.semiring]
+    # oracle levels (queue BFS over the same pattern)
+    from oracle.oracle import Port
+    port = Port()
+    co, ri, _ = port.csr_to_csc(n, n, ro, ci, np.ones(len(ci), np.float32))
+    exp, nl = port.bfs_queue(n, co, ri, 0)
+    reached = exp >= 0
+    edges = int(np.sum(np.diff(ro)[reached]))
+    bundle = A.SelectorBundle.load(S.DEFAULT_PATH)
+    res = {"scale": a.scale, "n": n, "nnz": int(ro[-1]), "levels": nl, "reached": int(reached.sum()),
+           "edges_traversed": edges, "semiring": a.semiring, "generate_s": round(gen, 1), "runs": {}}
+    modes = [("selector", bundle, -1), ("heuristic", None, -1)] + [(f"fixed_{k}", None, k) for k in range(8)]
+    for name, b, forced in modes:
+        ts = []
+        ok = True
+        reps = None
+        for _ in range(a.reps):
+            ctx.synchronize()
+            t1 = time.perf_counter()
+            lv, reps = A.bfs(m, 0, sr, bundle=b, force_kernel=forced)
+            ts.append(time.perf_counter() - t1)
+            ok = ok and bool(np.array_equal(lv, exp))
+        t = float(np.median(ts))
+        res["runs"][name] = {"seconds": round(t, 6), "gteps": round(edges / t / 1e9, 3), "levels_match": ok,
+                             "per_level": [{"nnz_x": r["nnz_x"], "kernel": A.KernelId.from_index(r["kernel"]).name(),
+                                            "kernel_ms": round(r["kernel_s"] * 1e3, 4),
+                                            "select_ms": round(r["predict_s"] * 1e3, 4),
+                                            "convert_ms": round(r["convert_s"] * 1e3, 4)} for r in reps]}
+        print(f"{name:10s} {t * 1e3:9.3f} ms  {edges / t / 1e9:7.3f} GTEPS  levels_ok={ok}", flush=True)
+    fixed = {k: v["seconds"] for k, v in res["runs"].items() if k.startswith("fixed_")}
+    best_fixed = min(fixed, key=fixed.get)
+    oracle_levels = []
+    # per-level best-of-8 from the fixed runs' kernel times (same frontiers)
+    for lvl in range(len(res["runs"]["selector"]["per_level"])):
+        oracle_levels.append(min(res["runs"][f"fixed_{k}"]["per_level"][lvl]["kernel_ms"] for k in range(8)))
+    sel_k = sum(p["kernel_ms"] for p in res["runs"]["selector"]["per_level"])
+    res["summary"] = {"best_fixed": best_fixed, "best_fixed_s": fixed[best_fixed],
+                      "selector_s": res["runs"]["selector"]["seconds"],
+                      "selector_kernel_ms": round(sel_k, 4),
+                      "per_level_oracle_kernel_ms": round(sum(oracle_levels), 4),
+                      "kernel_regret": round(sel_k / max(sum(oracle_levels), 1e-12), 3)}
+    print(json.dumps(res["summary"]))
+    if a.out:
+        Path(a.out).write_text(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
