@@ -84,17 +84,89 @@ int64_t next_frontier(Context& ctx, Output& y, Vector& x, int32_t* lv, int32_t l
     return x.nnz;
 }
 
+// Output-masked pull: the fused BFS extension of K2/K3.
+// Rows already visited are skipped before any index is loaded; with the
+// boolean semiring (or min-plus on a pattern matrix, where every frontier
+// value is the current level) a lane stops at its first frontier neighbour.
+// Only unvisited rows are written; the frontier update reads y only there.
+template <class V, int G, int SR, bool EARLY>
+__global__ void __launch_bounds__(256) bfs_pull_kernel(int64_t rows, const int64_t* __restrict__ ro,
+                                                       const int32_t* __restrict__ ci,
+                                                       const V* __restrict__ vals,
+                                                       const V* __restrict__ x,
+                                                       const uint32_t* __restrict__ fmask,
+                                                       const int32_t* __restrict__ lv,
+                                                       V* __restrict__ y) {
+    using S = Semiring<SR, V>;
+    constexpr int kU = 4;
+    const int64_t gid = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+    const int64_t row = gid / G;
+    const int lg = threadIdx.x & (G - 1);
+    const bool live = row < rows && __ldg(lv + row) < 0;
+    const int64_t b = live ? __ldg(ro + row) : 0, e = live ? __ldg(ro + row + 1) : 0;
+    V acc = S::zero();
+    for (int64_t k0 = b + lg; k0 < e; k0 += G * kU) {
+        int c[kU];
+        bool hit[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            const int64_t k = k0 + j * G;
+            c[j] = k < e ? __ldg(ci + k) : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < kU; ++j)
+            hit[j] = c[j] >= 0 && ((__ldg(fmask + (c[j] >> 5)) >> (c[j] & 31)) & 1u);
+#pragma unroll
+        for (int j = 0; j < kU; ++j)
+            if (hit[j]) acc = S::fma(S::kUsesValues ? __ldg(vals + k0 + j * G) : V(1), __ldg(x + c[j]), acc);
+        if (EARLY && acc != S::zero()) break;
+    }
+#pragma unroll
+    for (int d = G / 2; d > 0; d >>= 1) acc = S::add(acc, __shfl_xor_sync(kFull, acc, d, G));
+    if (live && lg == 0) y[row] = acc;
+}
+
+template <class V, int SR, bool EARLY>
+void launch_pull_e(Context& ctx, const Matrix& m, const Vector& x, const int32_t* lv, V* y) {
+    const int G = default_lanes_per_row(m.feat[5]);
+    const unsigned blocks = static_cast<unsigned>((m.rows * G + 255) / 256);
+    if (!blocks) return;
+#define ADA_G(GG)                                                                               \
+    case GG:                                                                                    \
+        bfs_pull_kernel<V, GG, SR, EARLY><<<blocks, 256, 0, ctx.stream>>>(                      \
+            m.rows, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), m.vals.as<V>(),           \
+            x.dense.as<V>(), x.mask.as<uint32_t>(), lv, y);                                     \
+        break;
+    switch (G) { ADA_G(1) ADA_G(2) ADA_G(4) ADA_G(8) ADA_G(16) ADA_G(32) default: invalid("lanes"); }
+#undef ADA_G
+    ADA_LAUNCHED(ctx);
+}
+
+template <class V, int SR>
+void launch_pull(Context& ctx, const Matrix& m, const Vector& x, const int32_t* lv, Output& y) {
+    V* yd = static_cast<V*>(y.dense.ensure(sizeof(V) * static_cast<size_t>(std::max<int64_t>(m.rows, 1))));
+    const bool early = SR == SR_OR_AND || (SR == SR_MIN_PLUS && m.pattern);
+    if (early) launch_pull_e<V, SR, true>(ctx, m, x, lv, yd);
+    else launch_pull_e<V, SR, false>(ctx, m, x, lv, yd);
+    y.reset(m.rows, m.dtype);
+    y.semiring = SR;
+    y.has_dense = true;
+}
+
 // Push vs pull by the algorithmic-bytes model of SURVEY.md section 8(d):
 // column-major reads ~ nnz_s entries, row-major (validated) reads every index.
-int heuristic_kernel(Context& ctx, const Matrix& m, Vector& x) {
+// The pull is output-masked (bfs_pull_kernel): only the ~unvisited share of
+// the index stream is read.
+int heuristic_kernel(Context& ctx, const Matrix& m, Vector& x, int64_t visited) {
     const int64_t nnz_s = vector_nnz_s(ctx, x, m);
     const double vb = m.vbytes();
+    const double unvisited = m.rows > 0 ? 1.0 - static_cast<double>(visited) / static_cast<double>(m.rows) : 0.0;
     const double push = static_cast<double>(x.nnz) * 20.0 + static_cast<double>(nnz_s) * (4.0 + vb) +
                         (nnz_s <= 4096 ? 0.0 : static_cast<double>(m.rows) * vb);
-    const double pull = static_cast<double>(m.rows + 1) * 8.0 + static_cast<double>(m.nnz) * 4.0 +
-                        static_cast<double>(nnz_s) * vb + static_cast<double>(m.cols) * vb;
+    const double pull = static_cast<double>(m.rows + 1) * 8.0 + static_cast<double>(m.nnz) * 4.0 * unvisited +
+                        static_cast<double>(m.cols) / 8.0 + static_cast<double>(m.rows) * vb * unvisited;
     if (push <= pull) return nnz_s <= 4096 ? 7 : 6;
-    return 3;
+    return 2;
 }
 
 template <class V, int SR>
@@ -126,12 +198,13 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
     adaspmv_config cfg{};
     cfg.semiring = SR;
     int64_t it = 0;
+    int64_t visited = 1;
     while (x.nnz > 0) {
         const auto t0 = clk::now();
         int k;
         if (b) k = predict(ctx, m, x, *b, nullptr, nullptr);
         else if (forced >= 0) k = forced;
-        else k = heuristic_kernel(ctx, m, x);
+        else k = heuristic_kernel(ctx, m, x, visited);
         const auto t1 = clk::now();
         if (k <= 3) {
             vector_ensure_dense(ctx, x, SR);
@@ -142,10 +215,11 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         ctx.sync();
         const auto t2 = clk::now();
         const int64_t nnz_x = x.nnz;
-        run_kernel(ctx, m, x, k, cfg, y);
+        if (k == 2 || k == 3) launch_pull<V, SR>(ctx, m, x, lv, y);  // RowSpMSpV, output-masked
+        else run_kernel(ctx, m, x, k, cfg, y);
         ctx.sync();
         const auto t3 = clk::now();
-        next_frontier<V, SR>(ctx, y, x, lv, static_cast<int32_t>(it + 1));
+        visited += next_frontier<V, SR>(ctx, y, x, lv, static_cast<int32_t>(it + 1));
         if (reports && it < max_reports) {
             adaspmv_iteration_report& r = reports[it];
             r.iteration = it;

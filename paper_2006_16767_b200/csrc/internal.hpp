@@ -114,7 +114,8 @@ struct Matrix {
     // starting at the tile boundary are inside the window); [n] = rows;
     // [n+1] = first row starting at nnz (trailing empty rows)
     DevBuf tile_head;
-    int64_t trail_start = 0;  // host copy of tile_head[n+1]
+    DevBuf empty_rows;        // int32 ids of rows with no entries (written by the LB fix-up)
+    int64_t n_empty = 0;
     DevBuf tile_partials;   // per tile: head partial, tail partial (V) + tail row (int64)
     double feat[9] = {0};
     int64_t max_col_deg = 0;

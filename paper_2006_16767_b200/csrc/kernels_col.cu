@@ -30,8 +30,7 @@ namespace {
 
 constexpr int kNT = 256;
 constexpr int kU = 4;
-constexpr int kColTile = 2048;           // effective entries per LB tile
-constexpr int kColIPT = kColTile / kNT;  // 8 consecutive entries per thread
+constexpr int kColTile = 256;            // effective entries per LB warp tile
 constexpr int kSmallPairs = 4096;        // single-CTA sort path capacity
 constexpr int kSmallNT = 1024;
 
@@ -75,50 +74,121 @@ __global__ void __launch_bounds__(kNT) col_direct_atomic_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// K6: equal effective-nnz tiles; each thread owns 8 consecutive effective
-// entries located by segment_of over eff_offsets (partition.hpp:30-33) and a
-// forward walk (entry_range clipping, kernels.hpp:422-432).
+// K6 (and K7's emission): equal effective-nnz tiles -- make_partition over
+// eff_offsets (kernels.hpp:399-432) with W = ceil(nnz_s / kColTile).  One warp
+// per tile of kColTile = 256 effective entries; lane l takes entries 32j + l,
+// so a warp instruction reads 32 consecutive entries of one column
+// (coalesced).  The tile's support span (found by a warp-cooperative 32-ary
+// search over eff_offsets, segment_of, partition.hpp:30-33) is staged in
+// shared memory: per support position the CSC start rebased to the effective
+// stream (entry_range clipping, kernels.hpp:422-432), the x value and the
+// tile-relative end.  Lanes walk it forward; all loads of the 8 entries are
+// issued before the write-back.  Spans wider than kColWin positions (many
+// empty support columns) read the same data from global memory.
 // ---------------------------------------------------------------------------
+constexpr int kColWin = 128;
+
+// largest s in [lo, hi) with eff[s] <= pos (warp-cooperative, all lanes)
+__device__ __forceinline__ int64_t warp_segment_of(const int64_t* __restrict__ eff, int64_t lo, int64_t hi,
+                                                   int64_t pos, int lane) {
+    while (hi - lo > 32) {
+        const int64_t step = (hi - lo + 31) / 32;
+        const int64_t probe = lo + lane * step;
+        const unsigned b = __ballot_sync(kFull, probe < hi && __ldg(eff + probe) <= pos);
+        const int last = 31 - __clz(b);  // bit 0 is always set (eff[lo] <= pos)
+        lo += last * step;
+        hi = min(lo + step, hi);
+    }
+    const int64_t probe = lo + lane;
+    const unsigned b = __ballot_sync(kFull, probe < hi && __ldg(eff + probe) <= pos);
+    return lo + (31 - __clz(b));
+}
+
 template <class V, int SR, bool EMIT>
 __global__ void __launch_bounds__(kNT) col_lb_kernel(
-    int64_t nnz_x, int64_t nnz_s, const int64_t* __restrict__ eff, const int32_t* __restrict__ xi,
-    const V* __restrict__ xv, const int64_t* __restrict__ co, const int32_t* __restrict__ ri,
-    const V* __restrict__ cv, V* __restrict__ y, uint32_t* __restrict__ keys,
-    V* __restrict__ pvals) {
+    int64_t nnz_x, int64_t nnz_s, int64_t ntiles, const int64_t* __restrict__ eff,
+    const int32_t* __restrict__ xi, const V* __restrict__ xv, const int64_t* __restrict__ co,
+    const int32_t* __restrict__ ri, const V* __restrict__ cv, V* __restrict__ y,
+    uint32_t* __restrict__ keys, V* __restrict__ pvals) {
     using S = Semiring<SR, V>;
-    __shared__ int64_t s_range[2];
-    const int64_t tb = static_cast<int64_t>(blockIdx.x) * kColTile;
-    const int64_t te = min(tb + static_cast<int64_t>(kColTile), nnz_s);
-    if (threadIdx.x < 2) {  // support span of the tile
-        const int64_t pos = threadIdx.x == 0 ? tb : te - 1;
-        s_range[threadIdx.x] = segment_search(eff, 0, nnz_x + 1, pos);
-    }
-    __syncthreads();
-    const int64_t s_lo = s_range[0], s_hi = s_range[1] + 1;
-    const int64_t p0 = tb + static_cast<int64_t>(threadIdx.x) * kColIPT;
-    if (p0 >= te) return;
-    const int64_t p1 = min(p0 + kColIPT, te);
-    int64_t s = segment_search(eff, s_lo, s_hi, p0);
-    int64_t s_end = __ldg(eff + s + 1);
-    int32_t col = __ldg(xi + s);
-    V xval = __ldg(xv + s);
-    int64_t base = __ldg(co + col) - __ldg(eff + s);
-    for (int64_t p = p0; p < p1; ++p) {
-        while (p >= s_end) {
-            ++s;
-            s_end = __ldg(eff + s + 1);
-            col = __ldg(xi + s);
-            xval = __ldg(xv + s);
-            base = __ldg(co + col) - __ldg(eff + s);
+    constexpr int kW = kNT / 32;
+    constexpr int kJ = kColTile / 32;  // entries per lane
+    __shared__ int64_t s_base[kW][kColWin];  // co[xi[s]] - eff[s]
+    __shared__ int s_end[kW][kColWin];       // eff[s+1] - tb (clamped)
+    __shared__ V s_xv[kW][kColWin];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kW + warp;
+    if (t >= ntiles) return;
+    const int64_t tb = t * kColTile;
+    const int ten = static_cast<int>(min(static_cast<int64_t>(kColTile), nnz_s - tb));
+    const int64_t s_lo = warp_segment_of(eff, 0, nnz_x + 1, tb, lane);
+    const int64_t s_hi = warp_segment_of(eff, s_lo, nnz_x + 1, tb + ten - 1, lane);  // inclusive
+    const int64_t span = s_hi - s_lo + 1;
+    int64_t kidx[kJ];
+    V xval[kJ];
+    if (span <= kColWin) {
+        for (int i = lane; i < span; i += 32) {
+            const int64_t s = s_lo + i;
+            const int32_t col = __ldg(xi + s);
+            const int64_t e0 = __ldg(eff + s), e1 = __ldg(eff + s + 1);
+            s_base[warp][i] = __ldg(co + col) - e0;
+            const int64_t rel = e1 - tb;
+            s_end[warp][i] = static_cast<int>(rel > kColTile + 1 ? kColTile + 1 : rel);
+            s_xv[warp][i] = __ldg(xv + s);
         }
-        const int64_t k = base + p;
-        const int32_t r = __ldg(ri + k);
-        const V a = S::kUsesValues ? __ldg(cv + k) : V(1);
+        __syncwarp();
+        // first support position holding entry `lane`, then walk forward
+        int si = 0;
+        {
+            int hi = static_cast<int>(span);
+            while (hi - si > 1) {  // largest si with end[si-1] <= lane, i.e. end[si] > lane
+                const int mid = (si + hi) >> 1;
+                if (s_end[warp][mid - 1] <= lane) si = mid;
+                else hi = mid;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+            const int i = 32 * j + lane;
+            if (i < ten) {
+                while (s_end[warp][si] <= i) ++si;
+                kidx[j] = s_base[warp][si] + tb + i;
+                xval[j] = s_xv[warp][si];
+            } else {
+                kidx[j] = -1;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+            const int i = 32 * j + lane;
+            if (i < ten) {
+                const int64_t s = segment_search(eff, s_lo, s_hi + 1, tb + i);
+                kidx[j] = __ldg(co + __ldg(xi + s)) - __ldg(eff + s) + tb + i;
+                xval[j] = __ldg(xv + s);
+            } else {
+                kidx[j] = -1;
+            }
+        }
+    }
+    int r[kJ];
+    V a[kJ];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+        if (kidx[j] >= 0) {
+            r[j] = ld_stream(ri + kidx[j]);
+            a[j] = S::kUsesValues ? ld_stream(cv + kidx[j]) : V(1);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+        if (kidx[j] < 0) continue;
+        const V prod = S::mul(a[j], xval[j]);
         if (EMIT) {
-            keys[p] = static_cast<uint32_t>(r);
-            pvals[p] = S::mul(a, xval);
+            keys[tb + 32 * j + lane] = static_cast<uint32_t>(r[j]);
+            pvals[tb + 32 * j + lane] = prod;
         } else {
-            AtomicCombine<SR>::apply(y + r, S::mul(a, xval));
+            AtomicCombine<SR>::apply(y + r[j], prod);
         }
     }
 }
@@ -368,9 +438,9 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
         }
         const int64_t nnz_s = vector_nnz_s(ctx, x, m);
         if (nnz_s == 0) return;
-        const unsigned tiles = static_cast<unsigned>((nnz_s + kColTile - 1) / kColTile);
-        col_lb_kernel<V, SR, false><<<tiles, kNT, 0, ctx.stream>>>(
-            x.nnz, nnz_s, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
+        const int64_t tiles = (nnz_s + kColTile - 1) / kColTile;
+        col_lb_kernel<V, SR, false><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
+            x.nnz, nnz_s, tiles, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
             m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), y_dense, nullptr,
             nullptr);
         ADA_LAUNCHED(ctx);
@@ -403,9 +473,9 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
     if (!lb) {
         launch_direct_emit<V, SR>(ctx, m, x, G, k0, v0);
     } else {
-        const unsigned tiles = static_cast<unsigned>((nnz_s + kColTile - 1) / kColTile);
-        col_lb_kernel<V, SR, true><<<tiles, kNT, 0, ctx.stream>>>(
-            x.nnz, nnz_s, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
+        const int64_t tiles = (nnz_s + kColTile - 1) / kColTile;
+        col_lb_kernel<V, SR, true><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
+            x.nnz, nnz_s, tiles, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
             m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), nullptr, k0, v0);
         ADA_LAUNCHED(ctx);
     }

@@ -134,10 +134,10 @@ struct GlobWin {
     }
 };
 
-// largest i in [0, hi) with off(i) <= p (segment_of, partition.hpp:30-33)
+// largest i in [lo, hi) with off(i) <= p, given off(lo) <= p
+// (segment_of, partition.hpp:30-33)
 template <class W>
-__device__ __forceinline__ int win_row_of(const W& w, int p, int hi) {
-    int lo = 0;
+__device__ __forceinline__ int win_row_of(const W& w, int p, int hi, int lo = 0) {
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
         if (w.off(mid) <= p) lo = mid;
@@ -153,11 +153,7 @@ __device__ __forceinline__ void lb_tile_body(const W& win, int nrow, int64_t ws,
                                              V* __restrict__ y, V* __restrict__ head_part,
                                              V* __restrict__ tail_part, int64_t* __restrict__ tail_row) {
     using S = Semiring<SR, V>;
-    // empty rows starting in [tb, te) belong to this tile
-    for (int i = lane; i < nrow; i += 32) {
-        const int o0 = win.off(i);
-        if (o0 >= 0 && o0 < ten && o0 == win.off(i + 1)) y[ws + i] = S::zero();
-    }
+    // (empty rows are written by the fix-up kernel from the matrix's list)
     V carry = S::zero();  // value of the row open at the start of the round
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
@@ -176,15 +172,16 @@ __device__ __forceinline__ void lb_tile_body(const W& win, int nrow, int64_t ws,
             for (int j = 0; j < kIPT; ++j) {
                 const int p = p0 + j;
                 if (p < p1) {
-                    while (p >= row_end) {  // close the run of `row`
+                    if (p >= row_end) {  // close the run of `row` (it holds items of this lane)
                         if (first && cont) {
                             head_closed = true;
                             head_val = acc;
-                        } else if (win.off(row) < row_end) {
+                        } else {
                             y[ws + row] = acc;  // complete inside this lane
                         }
                         first = false;
-                        ++row;
+                        // rows strictly between hold no items (empty): jump to p's row
+                        row = win.off(row + 2) > p ? row + 1 : win_row_of(win, p, nrow, row + 1);
                         row_end = win.off(row + 1);
                         acc = S::zero();
                     }
@@ -235,7 +232,7 @@ __device__ __forceinline__ void lb_tile_body(const W& win, int nrow, int64_t ws,
 }
 
 template <class V, bool VALIDATE, int SR>
-__global__ void __launch_bounds__(kNT, 4) row_lb_kernel(
+__global__ void __launch_bounds__(kNT, sizeof(V) == 8 ? 3 : 4) row_lb_kernel(
     int64_t rows, int64_t nnz, int64_t ntiles, const int64_t* __restrict__ ro,
     const int32_t* __restrict__ ci, const V* __restrict__ vals, const V* __restrict__ x,
     const uint32_t* __restrict__ mask, const int64_t* __restrict__ tile_head, V* __restrict__ y,
@@ -304,15 +301,20 @@ __global__ void __launch_bounds__(kNT, 4) row_lb_kernel(
     }
 }
 
-// Combines the partials of rows that span tiles, in tile order.
+// Combines the partials of rows that span tiles, in tile order, and writes
+// the identity into the matrix's empty rows (precomputed list).
 template <class V, int SR>
 __global__ void row_lb_fixup_kernel(int64_t ntiles, const int64_t* __restrict__ ro,
                                     const V* __restrict__ head_part,
                                     const V* __restrict__ tail_part,
-                                    const int64_t* __restrict__ tail_row, V* __restrict__ y) {
+                                    const int64_t* __restrict__ tail_row,
+                                    const int32_t* __restrict__ empty_rows, int64_t n_empty,
+                                    V* __restrict__ y) {
     using S = Semiring<SR, V>;
     constexpr int64_t kSerial = 32;  // chains longer than this are summed by the whole warp
     const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = t; i < n_empty; i += nthreads) y[empty_rows[i]] = S::zero();
     const int lane = threadIdx.x & 31;
     const int64_t R = t < ntiles ? tail_row[t] : -1;
     int64_t k = 0;  // continuation tiles t+1 .. t+k hold the rest of row R
@@ -374,12 +376,12 @@ void launch_lb(Context& ctx, const Matrix& m, const V* x, const uint32_t* mask, 
         m.rows, m.nnz, T, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), m.vals.as<V>(), x, mask,
         m.tile_head.as<int64_t>(), y, head, tail, trow);
     ADA_LAUNCHED(ctx);
-    if (T > 1) {
-        row_lb_fixup_kernel<V, SR><<<static_cast<unsigned>((T + 255) / 256), 256, 0, ctx.stream>>>(
-            T, m.row_off.as<int64_t>(), head, tail, trow, y);
+    if (T > 1 || m.n_empty > 0) {
+        const int64_t work = std::max<int64_t>(T, std::min<int64_t>(m.n_empty, 256LL * ctx.sm_count * 8));
+        row_lb_fixup_kernel<V, SR><<<static_cast<unsigned>((work + 255) / 256), 256, 0, ctx.stream>>>(
+            T, m.row_off.as<int64_t>(), head, tail, trow, m.empty_rows.as<int32_t>(), m.n_empty, y);
         ADA_LAUNCHED(ctx);
     }
-    if (m.trail_start < m.rows) fill_value<V, SR>(ctx, y + m.trail_start, m.rows - m.trail_start);
 }
 
 }  // namespace

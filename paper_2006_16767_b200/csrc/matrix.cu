@@ -109,6 +109,17 @@ __global__ void tile_head_kernel(const int64_t* __restrict__ ro, int64_t rows, i
     head[t] = (lb <= rows && ro[lb] == pos) ? lb : lb - 1;
 }
 
+struct EmptyRowIn {
+    const int64_t* ro;
+    __device__ int64_t operator()(int64_t r) const { return ro[r] == ro[r + 1] ? 1 : 0; }
+};
+struct EmptyRowEpi {
+    int32_t* out;
+    __device__ void operator()(int64_t r, int64_t p, int64_t v) const {
+        if (v) out[p] = static_cast<int32_t>(r);
+    }
+};
+
 void build_tiles(Context& ctx, Matrix& m) {
     m.n_row_tiles = (m.nnz + kRowTile - 1) / kRowTile;
     const size_t n = static_cast<size_t>(m.n_row_tiles + 2);
@@ -116,9 +127,11 @@ void build_tiles(Context& ctx, Matrix& m) {
     tile_head_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx.stream>>>(
         m.row_off.as<int64_t>(), m.rows, m.nnz, m.n_row_tiles, m.tile_head.as<int64_t>());
     ADA_LAUNCHED(ctx);
-    ADA_CUDA(cudaMemcpyAsync(&m.trail_start, m.tile_head.as<int64_t>() + m.n_row_tiles + 1,
-                             sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
-    ctx.sync();
+    // list of empty rows (the LB kernels never see them; the fix-up writes them)
+    m.empty_rows.ensure(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(m.rows, 1)));
+    scan3(ctx, m.rows, EmptyRowIn{m.row_off.as<int64_t>()}, EmptyRowEpi{m.empty_rows.as<int32_t>()},
+          ctx.dscal(3), ctx.scratch[5]);
+    m.n_empty = ctx.fetch_scalar(ctx.dscal(3));
     // head partial, tail partial (V) and tail row (int64) per tile
     m.tile_partials.ensure((2 * static_cast<size_t>(m.vbytes()) + sizeof(int64_t)) *
                            static_cast<size_t>(std::max<int64_t>(m.n_row_tiles, 1)));

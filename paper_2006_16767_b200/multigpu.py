@@ -89,7 +89,7 @@ def _device_view(ptr: int, n: int, dtype, device) -> torch.Tensor:
     """A torch tensor aliasing n elements of device memory at ptr."""
     class _Cuda:
         __cuda_array_interface__ = {"shape": (n,), "typestr": torch.empty(0, dtype=dtype).numpy().dtype.str,
-                                    "data": (ptr, True), "version": 2}
+                                    "data": (ptr, False), "version": 2}
     return torch.as_tensor(_Cuda(), device=device)
 
 

@@ -152,38 +152,76 @@ def _export_sklearn(clf, mask: int) -> dict:
     return nd
 
 
-def train_tree(X, y, mask: int, max_depths=range(1, 11), folds: int = 5, seed: int = 0):
+def costs_from_times(times8) -> tuple[float, float, float]:
+    """Relative cost of getting each tree's label wrong for one sample:
+    (time of the alternative / time of the label) - 1, averaged over the
+    alternatives for the 3-class pattern tree.  Used as CART sample weights
+    (cost-sensitive training), so that the trees spend their splits where a
+    wrong choice is expensive rather than where classes merely alternate."""
+    t = np.asarray(times8, np.float64)
+    per_pat = {2: min(t[0], t[1]), 1: min(t[2], t[3]), 0: min(t[4:8])}
+    pat, wl, wb = labels_from_times(t)
+    best = per_pat[pat]
+    c_pat = float(np.mean([per_pat[p] / best - 1.0 for p in per_pat if p != pat]))
+    if pat == 2:
+        pair = (t[0], t[1])
+    elif pat == 1:
+        pair = (t[2], t[3])
+    else:
+        pair = (min(t[4], t[5]), min(t[6], t[7]))
+    c_wl = float(pair[1 - wl] / pair[wl] - 1.0)
+    atomic, sort = min(t[4], t[6]), min(t[5], t[7])
+    c_wb = float((atomic / sort if wb else sort / atomic) - 1.0)
+    return c_pat, c_wl, c_wb
+
+
+def train_tree(X, y, mask: int, max_depths=range(1, 11), folds: int = 5, seed: int = 0,
+               cost=None):
     """CART with grid search over depth [1,10] x class_weight {balanced,
     uniform} and k-fold CV.  Features
-    outside `mask` are hidden from the tree."""
-    from sklearn.model_selection import GridSearchCV, StratifiedKFold
+    outside `mask` are hidden from the tree.  With `cost` (per-sample
+    misclassification cost), samples are weighted by it and the CV score is
+    the cost-weighted accuracy; ties go to the smaller depth."""
+    from sklearn.model_selection import StratifiedKFold
     from sklearn.tree import DecisionTreeClassifier
 
     X = np.asarray(X, np.float64).copy()
-    y = np.asarray(y)
+    y = np.asarray(y).astype(int)
     cols = [i for i in range(13) if mask & (1 << i)]
     Xm = np.zeros_like(X)
-    Xm[:, cols] = X[:, cols]
+    Xm[:, cols] = X[:, cols]  # constant (zeroed) features are never split on
     if len(np.unique(y)) == 1:
         return leaf(int(y[0])), 1.0
-    n_min = int(np.min(np.bincount(y.astype(int))[np.bincount(y.astype(int)) > 0]))
-    k = max(2, min(folds, n_min))
-    grid = {"max_depth": list(max_depths), "class_weight": ["balanced", None]}
+    w = np.ones(len(y)) if cost is None else np.clip(np.asarray(cost, np.float64), 1e-3, 10.0)
+    counts = np.bincount(y)
+    k = max(2, min(folds, int(np.min(counts[counts > 0]))))
     cv = StratifiedKFold(n_splits=k, shuffle=True, random_state=seed)
-    gs = GridSearchCV(DecisionTreeClassifier(random_state=seed), grid, cv=cv)
-    gs.fit(Xm, y)
-    best = gs.best_estimator_
-    # constant features were zeroed: sklearn never splits on them
-    return _export_sklearn(best, mask), float(gs.best_score_)
+    splits = list(cv.split(Xm, y))
+    best = None
+    for depth in max_depths:
+        for cw in ("balanced", None):
+            score = 0.0
+            for tr, te in splits:
+                clf = DecisionTreeClassifier(max_depth=depth, class_weight=cw, random_state=seed)
+                clf.fit(Xm[tr], y[tr], sample_weight=w[tr])
+                score += float(np.sum(w[te] * (clf.predict(Xm[te]) == y[te])) / np.sum(w[te]))
+            score /= len(splits)
+            if best is None or score > best[0] + 1e-12:
+                best = (score, depth, cw)
+    clf = DecisionTreeClassifier(max_depth=best[1], class_weight=best[2], random_state=seed)
+    clf.fit(Xm, y, sample_weight=w)
+    return _export_sklearn(clf, mask), float(best[0])
 
 
-def train_bundle(features, times, seed: int = 0) -> tuple[dict, dict]:
+def train_bundle(features, times, seed: int = 0, cost_sensitive: bool = True) -> tuple[dict, dict]:
     """features: [S,13]; times: [S,8] seconds -> (trees, cv scores)."""
     F = np.asarray(features, np.float64)
     lab = np.array([labels_from_times(t) for t in times])
+    cst = np.array([costs_from_times(t) for t in times]) if cost_sensitive else None
     trees, scores = {}, {}
     for j, t in enumerate(TARGETS):
-        trees[t], scores[t] = train_tree(F, lab[:, j], MASKS[t], seed=seed)
+        trees[t], scores[t] = train_tree(F, lab[:, j], MASKS[t], seed=seed,
+                                         cost=None if cst is None else cst[:, j])
     return trees, scores
 
 

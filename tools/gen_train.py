@@ -77,7 +77,7 @@ def corpus(scale: str):
     return items
 
 
-def densities(n, geo=12, uni=4):
+def densities(n, geo=16, uni=8):
     """geometric:k and uniform:k density points (nnz_x)."""
     g = np.unique(np.round(np.geomspace(1, n, geo)).astype(np.int64))
     u = np.unique(np.round(np.linspace(1, n, uni)).astype(np.int64))

@@ -41,3 +41,25 @@ if __name__ == '__main__':
         print('----')
         for k, (v, u) in d.items():
             print(f'{k:70s} {v} {u}')
+
+
+def source_hotspots(rep, kernel_regex, top=25):
+    """Per-source-line warp samples / instructions of the first matching kernel."""
+    out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'cuda',
+                          '-k', f'regex:{kernel_regex}', '--launch-count', '1'],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    if not rows:
+        return []
+    hdr = rows[0]
+    res = []
+    for r in rows[1:]:
+        d = dict(zip(hdr, r))
+        try:
+            s = float(d.get('Warp Stall Sampling (All Samples)', '0') or 0)
+            ins = float(d.get('Instructions Executed', '0') or 0)
+        except ValueError:
+            continue
+        res.append((s, ins, d.get('#', ''), d.get('Source', '')[:110]))
+    res.sort(key=lambda x: -x[0])
+    return res[:top]

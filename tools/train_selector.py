@@ -4,10 +4,13 @@ runtime loads (paper_2006_16767_b200/selector/b200_bundle.txt).
 
   7:3 train/test split by seeded shuffle, CART grid search over
   depth [1,10] x class_weight {balanced, uniform} with 5-fold CV per tree.
-  Reports per-tree held-out accuracy and the held-out kernel-time regret
-  (chosen / best-of-8), plus the same for a cheap-feature variant that never
-  reads nnz_s / m_sparsity (no device round trip per call, PAPER.md:691-696);
-  the cheap variant is kept when its held-out regret is within 2 %.
+  Four variants are fitted: all features vs a cheap-feature set that never
+  reads nnz_s / m_sparsity (no device round trip per call),
+  each with plain labels or cost-sensitive sample weights (the relative time
+  lost by a wrong label, selector.costs_from_times).  The variant with the
+  lowest held-out per-input regret (chosen / best-of-8) is written; a cheap
+  variant within 2 % of it is preferred.  Per-tree held-out accuracies are
+  reported for comparison with PAPER.md:582-593.
 """
 from __future__ import annotations
 
@@ -70,14 +73,14 @@ def main():
     perm = rng.permutation(len(F))
     ntr = int(round(0.7 * len(F)))
     tr, te = perm[:ntr], perm[ntr:]
-    cheap = (1 << 12) - 1 & ~((1 << 11) | (1 << 12)) | ((1 << 9) | (1 << 10))  # no nnz_s / m_sparsity
     results = {}
-    for variant, hide in (("full", 0), ("cheap", (1 << 11) | (1 << 12))):
+    for variant, hide, cs in (("full", 0, False), ("cheap", (1 << 11) | (1 << 12), False),
+                              ("full_cost", 0, True), ("cheap_cost", (1 << 11) | (1 << 12), True)):
         saved = dict(S.MASKS)
         try:
             for t in S.TARGETS:
                 S.MASKS[t] = saved[t] & ~hide
-            trees, cv = S.train_bundle(F[tr], T[tr], seed=a.seed)
+            trees, cv = S.train_bundle(F[tr], T[tr], seed=a.seed, cost_sensitive=cs)
         finally:
             S.MASKS.update(saved)
         rg_tot, rg_mean, rg_max, _ = regret(trees, F[te], T[te])
@@ -86,7 +89,15 @@ def main():
                             "test_regret_max": rg_max,
                             "train_regret_total": regret(trees, F[tr], T[tr])[0],
                             "nodes": {t: len(trees[t]["feature"]) for t in S.TARGETS}}
-    pick = "cheap" if results["cheap"]["test_regret_total"] <= 1.02 * results["full"]["test_regret_total"] else "full"
+    # per-input regret (north_star: "within 10 % of the best of the eight per
+    # input"); a cheap-feature variant wins ties within 2 % (no device round trip)
+    order = sorted(results, key=lambda v: results[v]["test_regret_mean"])
+    best_v = order[0]
+    for v in order:
+        if v.startswith("cheap") and results[v]["test_regret_mean"] <= 1.02 * results[best_v]["test_regret_mean"]:
+            best_v = v
+            break
+    pick = best_v
     S.write_bundle(a.out, results[pick]["trees"], hardware_tag=f"B200-trained-{pick}")
     oracle_best = T.min(axis=1)
     fixed = {k: float(T[:, k].sum() / oracle_best.sum()) for k in range(8)}
@@ -99,7 +110,6 @@ def main():
                                                                "test_regret_mean", "test_regret_max", "nodes")}
                       for v in rep["variants"]}, indent=1))
     print("picked", pick, "-> wrote", a.out)
-    _ = cheap
 
 
 if __name__ == "__main__":
