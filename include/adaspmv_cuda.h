@@ -255,6 +255,15 @@ typedef struct {
     double feature_s, predict_s, convert_s, kernel_s; /* IterationReport */
 } adaspmv_iteration_report;
 
+/* execute_iteration: lazy features -> predict_kernel (or
+ * `forced_kernel` >= 0) -> convert x iff the kernel needs another format ->
+ * run.  Fills `report` (IterationReport): host seconds of
+ * the feature pulls and the tree walk, device seconds of the conversion and
+ * of the multiply (CUDA events; synchronises once at the end). */
+int adaspmv_execute_iteration(adaspmv_ctx* ctx, const adaspmv_matrix* m, adaspmv_vector* x,
+                              const adaspmv_bundle* b, int forced_kernel, const adaspmv_config* cfg,
+                              adaspmv_output* y, adaspmv_iteration_report* report);
+
 /* Level-synchronous BFS from `source` over y = A x (A as stored, square).
  * `semiring` selects the multiply's algebra; `bundle` (may be NULL) selects
  * a kernel per level, else `forced_kernel` (0..7) is used for every level,

@@ -170,6 +170,7 @@ def load(path: Optional[os.PathLike] = None):
         "adaspmv_sort_reduce_pairs": [vp, i64, vp, vp, C.c_int, i64, vp, vp, P(i64)],
         "adaspmv_shard_rows": [vp, i64, C.c_int, vp],
         "adaspmv_bfs": [vp, vp, i64, C.c_int, vp, C.c_int, vp, P(i64), vp, i64],
+        "adaspmv_execute_iteration": [vp, vp, vp, vp, C.c_int, vp, vp, vp],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -834,6 +835,21 @@ def run_adaptive(m: DualMatrix, x, bundle: SelectorBundle, cfg: Optional[KernelC
     _check(_lib.adaspmv_run_adaptive(m.ctx.h, m.h, v.h, bundle.h, C.byref(c), out.h, C.byref(k)))
     out._operand = v
     return out, KernelId.from_index(k.value)
+
+
+def execute_iteration(m: DualMatrix, x, bundle: Optional[SelectorBundle] = None, force_kernel: int = -1,
+                      cfg: Optional[KernelConfig] = None, out: Optional[MultiplyOutput] = None):
+    """execute_iteration (SPEC.md:410-418) -> (MultiplyOutput, IterationReport
+    dict: kernel, feature_s, predict_s, convert_s (device), kernel_s (device))."""
+    v = _as_device_vector(m, x)
+    out = out or MultiplyOutput(m.ctx)
+    c = (cfg or KernelConfig())._c()
+    rep = _IterReport()
+    _check(_lib.adaspmv_execute_iteration(m.ctx.h, m.h, v.h, bundle.h if bundle else None, int(force_kernel),
+                                          C.byref(c), out.h, C.byref(rep)))
+    out._operand = v
+    return out, dict(kernel=KernelId.from_index(rep.kernel), nnz_x=rep.nnz_x, feature_s=rep.feature_s,
+                     predict_s=rep.predict_s, convert_s=rep.convert_s, kernel_s=rep.kernel_s)
 
 
 def effective_nnz(m: DualMatrix, x) -> int:

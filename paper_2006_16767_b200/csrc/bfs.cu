@@ -199,6 +199,16 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
     cfg.semiring = SR;
     int64_t it = 0;
     int64_t visited = 1;
+    // device-side phase timing without extra synchronisation: events around
+    // the conversion and the multiply, read after the frontier-size fetch
+    cudaEvent_t ev[3];
+    for (auto& e : ev) ADA_CUDA(cudaEventCreate(&e));
+    struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() {
+            for (int i = 0; i < 3; ++i) cudaEventDestroy(e[i]);
+        }
+    } guard{ev};
     while (x.nnz > 0) {
         const auto t0 = clk::now();
         int k;
@@ -206,30 +216,32 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         else if (forced >= 0) k = forced;
         else k = heuristic_kernel(ctx, m, x, visited);
         const auto t1 = clk::now();
+        ADA_CUDA(cudaEventRecord(ev[0], ctx.stream));
         if (k <= 3) {
             vector_ensure_dense(ctx, x, SR);
             if (k >= 2) vector_ensure_mask(ctx, x);
         } else if (k == 6 || k == 7) {
             vector_ensure_eff(ctx, x, m);
         }
-        ctx.sync();
-        const auto t2 = clk::now();
+        ADA_CUDA(cudaEventRecord(ev[1], ctx.stream));
         const int64_t nnz_x = x.nnz;
         if (k == 2 || k == 3) launch_pull<V, SR>(ctx, m, x, lv, y);  // RowSpMSpV, output-masked
         else run_kernel(ctx, m, x, k, cfg, y);
-        ctx.sync();
-        const auto t3 = clk::now();
-        visited += next_frontier<V, SR>(ctx, y, x, lv, static_cast<int32_t>(it + 1));
+        ADA_CUDA(cudaEventRecord(ev[2], ctx.stream));
+        visited += next_frontier<V, SR>(ctx, y, x, lv, static_cast<int32_t>(it + 1));  // syncs
         if (reports && it < max_reports) {
+            float c_ms = 0, k_ms = 0;
+            ADA_CUDA(cudaEventElapsedTime(&c_ms, ev[0], ev[1]));
+            ADA_CUDA(cudaEventElapsedTime(&k_ms, ev[1], ev[2]));
             adaspmv_iteration_report& r = reports[it];
             r.iteration = it;
             r.nnz_x = nnz_x;
             r.kernel = k;
             r.pad = 0;
-            r.predict_s = secs(t0, t1);
-            r.feature_s = 0;  // features are pulled inside predict (lazy)
-            r.convert_s = secs(t1, t2);
-            r.kernel_s = secs(t2, t3);
+            r.predict_s = secs(t0, t1);  // host: tree walk + lazy features (nnz_s fetch)
+            r.feature_s = 0;             // folded into predict_s (features pulled lazily)
+            r.convert_s = c_ms * 1e-3;
+            r.kernel_s = k_ms * 1e-3;
         }
         ++it;
     }

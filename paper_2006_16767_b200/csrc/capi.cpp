@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -53,6 +54,24 @@ void need(const void* p, const char* what) {
 void bind(ada::Context* ctx) {
     need(ctx, "context");
     ADA_CUDA(cudaSetDevice(ctx->device));
+    ada::g_alloc_stream = ctx->stream;
+}
+
+// Objects are freed on the stream of the context that made them.
+void bind_quiet(ada::Context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    ada::g_alloc_stream = ctx->stream;
+}
+
+// Blocking copy ordered on the context stream (device memory is allocated
+// stream-ordered on it, see DevBuf).
+cudaError_t copy_sync(ada::Context& c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, c.stream);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(c.stream);
+}
+cudaError_t copy_sync(ada::Context* c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    return copy_sync(*c, dst, src, bytes, kind);
 }
 
 void check_dtype(int dtype) {
@@ -83,10 +102,10 @@ ada::Matrix* upload_host_csr(ada::Context& ctx, int64_t rows, int64_t cols, cons
     d_ro.ensure(sizeof(int64_t) * static_cast<size_t>(rows + 1));
     d_ci.ensure(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(nnz, 1)));
     d_v.ensure(vb * static_cast<size_t>(std::max<int64_t>(nnz, 1)));
-    ADA_CUDA(cudaMemcpy(d_ro.p, ro, sizeof(int64_t) * static_cast<size_t>(rows + 1), cudaMemcpyHostToDevice));
+    ADA_CUDA(copy_sync(ctx, d_ro.p, ro, sizeof(int64_t) * static_cast<size_t>(rows + 1), cudaMemcpyHostToDevice));
     if (nnz > 0) {
-        ADA_CUDA(cudaMemcpy(d_ci.p, ci32.data(), sizeof(int32_t) * ci32.size(), cudaMemcpyHostToDevice));
-        if (vals) ADA_CUDA(cudaMemcpy(d_v.p, vals, vb * static_cast<size_t>(nnz), cudaMemcpyHostToDevice));
+        ADA_CUDA(copy_sync(ctx, d_ci.p, ci32.data(), sizeof(int32_t) * ci32.size(), cudaMemcpyHostToDevice));
+        if (vals) ADA_CUDA(copy_sync(ctx, d_v.p, vals, vb * static_cast<size_t>(nnz), cudaMemcpyHostToDevice));
     }
     return ada::matrix_create_device(ctx, rows, cols, nnz, d_ro.as<int64_t>(), d_ci.as<int32_t>(),
                                      vals ? d_v.p : nullptr, dtype, vals == nullptr);
@@ -143,6 +162,13 @@ int adaspmv_ctx_create(int device, void* stream, adaspmv_ctx** out) {
         ADA_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
         ADA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_scalars), 64 * sizeof(int64_t),
                                cudaHostAllocDefault));
+        // keep freed blocks in the device's default pool instead of returning
+        // them to the driver at every synchronisation
+        cudaMemPool_t pool;
+        ADA_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t threshold = UINT64_MAX;
+        ADA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+        ada::g_alloc_stream = ctx->stream;
         ctx->d_scalars.ensure(64 * sizeof(int64_t));
         *out = ctx.release();
     });
@@ -151,7 +177,7 @@ int adaspmv_ctx_create(int device, void* stream, adaspmv_ctx** out) {
 int adaspmv_ctx_destroy(adaspmv_ctx* ctx) {
     if (!ctx) return ADASPMV_OK;
     return guarded([&] {
-        cudaSetDevice(ctx->device);
+        bind_quiet(ctx);
         cudaStreamSynchronize(ctx->stream);
         for (auto& b : ctx->scratch) b.release();
         ctx->d_scalars.release();
@@ -321,7 +347,7 @@ int adaspmv_matrix_destroy(adaspmv_matrix* m) {
     if (!m) return ADASPMV_OK;
     return guarded([&] {
         if (m->ctx) {
-            cudaSetDevice(m->ctx->device);
+            bind_quiet(m->ctx);
             cudaStreamSynchronize(m->ctx->stream);
         }
         delete static_cast<ada::Matrix*>(m);
@@ -348,20 +374,20 @@ int adaspmv_matrix_download(adaspmv_ctx* ctx, const adaspmv_matrix* m, int64_t* 
         const size_t vb = static_cast<size_t>(m->vbytes());
         std::vector<int32_t> tmp(z);
         if (row_offsets)
-            ADA_CUDA(cudaMemcpy(row_offsets, m->row_off.p, sizeof(int64_t) * static_cast<size_t>(m->rows + 1), cudaMemcpyDeviceToHost));
+            ADA_CUDA(copy_sync(ctx, row_offsets, m->row_off.p, sizeof(int64_t) * static_cast<size_t>(m->rows + 1), cudaMemcpyDeviceToHost));
         if (col_offsets)
-            ADA_CUDA(cudaMemcpy(col_offsets, m->col_off.p, sizeof(int64_t) * static_cast<size_t>(m->cols + 1), cudaMemcpyDeviceToHost));
+            ADA_CUDA(copy_sync(ctx, col_offsets, m->col_off.p, sizeof(int64_t) * static_cast<size_t>(m->cols + 1), cudaMemcpyDeviceToHost));
         if (z == 0) return;
         if (col_indices) {
-            ADA_CUDA(cudaMemcpy(tmp.data(), m->col_idx.p, sizeof(int32_t) * z, cudaMemcpyDeviceToHost));
+            ADA_CUDA(copy_sync(ctx, tmp.data(), m->col_idx.p, sizeof(int32_t) * z, cudaMemcpyDeviceToHost));
             for (size_t k = 0; k < z; ++k) col_indices[k] = tmp[k];
         }
         if (row_indices) {
-            ADA_CUDA(cudaMemcpy(tmp.data(), m->row_idx.p, sizeof(int32_t) * z, cudaMemcpyDeviceToHost));
+            ADA_CUDA(copy_sync(ctx, tmp.data(), m->row_idx.p, sizeof(int32_t) * z, cudaMemcpyDeviceToHost));
             for (size_t k = 0; k < z; ++k) row_indices[k] = tmp[k];
         }
-        if (values) ADA_CUDA(cudaMemcpy(values, m->vals.p, vb * z, cudaMemcpyDeviceToHost));
-        if (csc_values) ADA_CUDA(cudaMemcpy(csc_values, m->cvals.p, vb * z, cudaMemcpyDeviceToHost));
+        if (values) ADA_CUDA(copy_sync(ctx, values, m->vals.p, vb * z, cudaMemcpyDeviceToHost));
+        if (csc_values) ADA_CUDA(copy_sync(ctx, csc_values, m->cvals.p, vb * z, cudaMemcpyDeviceToHost));
     });
 }
 
@@ -393,7 +419,7 @@ int adaspmv_vector_destroy(adaspmv_vector* v) {
     if (!v) return ADASPMV_OK;
     return guarded([&] {
         if (v->ctx) {
-            cudaSetDevice(v->ctx->device);
+            bind_quiet(v->ctx);
             cudaStreamSynchronize(v->ctx->stream);
         }
         delete v;
@@ -516,11 +542,11 @@ int adaspmv_vector_get_sparse(adaspmv_ctx* ctx, adaspmv_vector* v, int64_t capac
         if (n <= 0) return;
         if (indices) {
             std::vector<int32_t> tmp(static_cast<size_t>(n));
-            ADA_CUDA(cudaMemcpy(tmp.data(), v->sp_idx.p, sizeof(int32_t) * tmp.size(), cudaMemcpyDeviceToHost));
+            ADA_CUDA(copy_sync(ctx, tmp.data(), v->sp_idx.p, sizeof(int32_t) * tmp.size(), cudaMemcpyDeviceToHost));
             for (int64_t k = 0; k < n; ++k) indices[k] = tmp[static_cast<size_t>(k)];
         }
         if (values)
-            ADA_CUDA(cudaMemcpy(values, v->sp_val.p, static_cast<size_t>(ada::value_bytes(v->dtype)) * static_cast<size_t>(n),
+            ADA_CUDA(copy_sync(ctx, values, v->sp_val.p, static_cast<size_t>(ada::value_bytes(v->dtype)) * static_cast<size_t>(n),
                                 cudaMemcpyDeviceToHost));
     });
 }
@@ -532,7 +558,7 @@ int adaspmv_vector_get_dense(adaspmv_ctx* ctx, adaspmv_vector* v, void* values) 
         ada::vector_ensure_dense(*ctx, *v);
         ctx->sync();
         if (values && v->n > 0)
-            ADA_CUDA(cudaMemcpy(values, v->dense.p, static_cast<size_t>(ada::value_bytes(v->dtype)) * static_cast<size_t>(v->n),
+            ADA_CUDA(copy_sync(ctx, values, v->dense.p, static_cast<size_t>(ada::value_bytes(v->dtype)) * static_cast<size_t>(v->n),
                                 cudaMemcpyDeviceToHost));
     });
 }
@@ -544,7 +570,7 @@ int adaspmv_vector_get_bitmask(adaspmv_ctx* ctx, adaspmv_vector* v, uint64_t* wo
         ada::vector_ensure_mask(*ctx, *v);
         ctx->sync();
         const size_t nw = static_cast<size_t>((v->n + 63) / 64);
-        if (words && nw) ADA_CUDA(cudaMemcpy(words, v->mask.p, sizeof(uint64_t) * nw, cudaMemcpyDeviceToHost));
+        if (words && nw) ADA_CUDA(copy_sync(ctx, words, v->mask.p, sizeof(uint64_t) * nw, cudaMemcpyDeviceToHost));
     });
 }
 
@@ -649,7 +675,7 @@ int adaspmv_output_destroy(adaspmv_output* y) {
     if (!y) return ADASPMV_OK;
     return guarded([&] {
         if (y->ctx) {
-            cudaSetDevice(y->ctx->device);
+            bind_quiet(y->ctx);
             cudaStreamSynchronize(y->ctx->stream);
         }
         delete y;
@@ -684,6 +710,62 @@ int adaspmv_run_adaptive(adaspmv_ctx* ctx, const adaspmv_matrix* m, adaspmv_vect
         if (cfg) c = *cfg;
         ada::run_kernel(*ctx, *m, *x, k, c, *y);
         if (chosen) *chosen = k;
+    });
+}
+
+int adaspmv_execute_iteration(adaspmv_ctx* ctx, const adaspmv_matrix* m, adaspmv_vector* x,
+                              const adaspmv_bundle* b, int forced_kernel, const adaspmv_config* cfg,
+                              adaspmv_output* y, adaspmv_iteration_report* report) {
+    return guarded([&] {
+        bind(ctx);
+        need(m, "matrix");
+        need(x, "vector");
+        need(y, "output");
+        if (x->n != m->cols) ada::invalid("execute_iteration: vector length != matrix columns");
+        if (forced_kernel < 0 && !b) ada::invalid("execute_iteration: untrained bundle without override");
+        if (forced_kernel > 7) ada::invalid("kernel index out of range");
+        using clk = std::chrono::steady_clock;
+        double feature_s = 0;
+        const auto t0 = clk::now();
+        const int k = forced_kernel >= 0 ? forced_kernel
+                                         : ada::predict(*ctx, *m, *x, *b, nullptr, nullptr, &feature_s);
+        const double select_s = std::chrono::duration<double>(clk::now() - t0).count();
+        cudaEvent_t ev[3];
+        for (auto& e : ev) ADA_CUDA(cudaEventCreate(&e));
+        struct Guard {
+            cudaEvent_t* e;
+            ~Guard() {
+                for (int i = 0; i < 3; ++i) cudaEventDestroy(e[i]);
+            }
+        } guard{ev};
+        adaspmv_config c{};
+        if (cfg) c = *cfg;
+        ADA_CUDA(cudaEventRecord(ev[0], ctx->stream));
+        // convert iff the kernel needs another representation
+        if (k <= 3) {
+            ada::vector_ensure_dense(*ctx, *x, c.semiring);
+            if (k >= 2) ada::vector_ensure_mask(*ctx, *x);
+        } else {
+            ada::vector_ensure_sparse(*ctx, *x);
+            if (k == 6 || k == 7) ada::vector_ensure_eff(*ctx, *x, *m);
+        }
+        ADA_CUDA(cudaEventRecord(ev[1], ctx->stream));
+        ada::run_kernel(*ctx, *m, *x, k, c, *y);
+        ADA_CUDA(cudaEventRecord(ev[2], ctx->stream));
+        ADA_CUDA(cudaEventSynchronize(ev[2]));
+        float conv_ms = 0, kern_ms = 0;
+        ADA_CUDA(cudaEventElapsedTime(&conv_ms, ev[0], ev[1]));
+        ADA_CUDA(cudaEventElapsedTime(&kern_ms, ev[1], ev[2]));
+        if (report) {
+            report->iteration = 0;
+            report->nnz_x = x->nnz;
+            report->kernel = k;
+            report->pad = 0;
+            report->feature_s = feature_s;
+            report->predict_s = select_s - feature_s;
+            report->convert_s = conv_ms * 1e-3;
+            report->kernel_s = kern_ms * 1e-3;
+        }
     });
 }
 
@@ -799,17 +881,17 @@ int adaspmv_sort_reduce_pairs(adaspmv_ctx* ctx, int64_t npairs, const int64_t* r
         oi.ensure(sizeof(int32_t) * std::max<size_t>(r32.size(), 1));
         ov.ensure(vb * std::max<size_t>(r32.size(), 1));
         if (npairs > 0) {
-            ADA_CUDA(cudaMemcpy(dr.p, r32.data(), sizeof(int32_t) * r32.size(), cudaMemcpyHostToDevice));
-            ADA_CUDA(cudaMemcpy(dv.p, values, vb * r32.size(), cudaMemcpyHostToDevice));
+            ADA_CUDA(copy_sync(ctx, dr.p, r32.data(), sizeof(int32_t) * r32.size(), cudaMemcpyHostToDevice));
+            ADA_CUDA(copy_sync(ctx, dv.p, values, vb * r32.size(), cudaMemcpyHostToDevice));
         }
         const int64_t k = ada::sort_reduce_pairs_device(*ctx, npairs, dr.as<int32_t>(), dv.p, dtype, nrows,
                                                         oi.as<int32_t>(), ov.p);
         *nnz_out = k;
         if (k > 0) {
             std::vector<int32_t> t(static_cast<size_t>(k));
-            ADA_CUDA(cudaMemcpy(t.data(), oi.p, sizeof(int32_t) * t.size(), cudaMemcpyDeviceToHost));
+            ADA_CUDA(copy_sync(ctx, t.data(), oi.p, sizeof(int32_t) * t.size(), cudaMemcpyDeviceToHost));
             for (int64_t i = 0; i < k; ++i) out_indices[i] = t[static_cast<size_t>(i)];
-            ADA_CUDA(cudaMemcpy(out_values, ov.p, vb * static_cast<size_t>(k), cudaMemcpyDeviceToHost));
+            ADA_CUDA(copy_sync(ctx, out_values, ov.p, vb * static_cast<size_t>(k), cudaMemcpyDeviceToHost));
         }
     });
 }

@@ -49,17 +49,24 @@ struct Error : std::runtime_error {
 
 inline int value_bytes(int dtype) { return dtype == ADASPMV_F64 ? 8 : 4; }
 
+// Stream of the context bound by the current C-ABI call: device memory is
+// stream-ordered (cudaMallocAsync from the device's pool, release threshold
+// raised at context creation), so temporaries and growth never synchronise
+// the device or return memory to the driver.
+inline thread_local cudaStream_t g_alloc_stream = nullptr;
+
 // Grow-only device allocation.
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    cudaStream_t s = nullptr;  // stream the allocation is ordered on
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), cap(o.cap) { o.p = nullptr; o.cap = 0; }
+    DevBuf(DevBuf&& o) noexcept : p(o.p), cap(o.cap), s(o.s) { o.p = nullptr; o.cap = 0; }
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
         p = nullptr;
         cap = 0;
     }
@@ -67,7 +74,8 @@ struct DevBuf {
         if (bytes <= cap && p) return p;
         release();
         size_t want = bytes < 256 ? 256 : bytes;
-        ADA_CUDA(cudaMalloc(&p, want));
+        s = g_alloc_stream;
+        ADA_CUDA(cudaMallocAsync(&p, want, s));
         cap = want;
         return p;
     }
@@ -83,7 +91,9 @@ struct Context {
     int64_t launches = 0;
     bool timing = false;  // bracket every run with CUDA events (adaspmv_output_elapsed)
     // general scratch (reused by every call; calls on a context are serialised)
-    DevBuf scratch[6];
+    // [0..3] sort write-back keys/values (double buffered), [4] vector scans,
+    // [5] matrix build scans, [6..9] radix counts / scan / segment sums / flags
+    DevBuf scratch[10];
     // pinned host scalars for D2H of counts (nnz_s, nnz_y, ...)
     int64_t* h_scalars = nullptr;
     DevBuf d_scalars;  // 64 int64 slots
@@ -221,7 +231,7 @@ int64_t sort_reduce_pairs_device(Context& ctx, int64_t npairs, const int32_t* d_
 // features / selector (selector.cpp)
 void features(Context& ctx, const Matrix& m, Vector& v, uint32_t mask, double* out13);
 int predict(Context& ctx, const Matrix& m, Vector& v, const Bundle& b, uint32_t* used,
-            int* trees);
+            int* trees, double* feature_s = nullptr);
 Bundle* bundle_load(const std::string& path);
 
 // host I/O (mmio.cpp): CSR in the reference layout

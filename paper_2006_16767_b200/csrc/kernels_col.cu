@@ -479,7 +479,10 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
             m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), nullptr, k0, v0);
         ADA_LAUNCHED(ctx);
     }
-    static thread_local DevBuf counts, scan_tmp, sums, keep;
+    DevBuf& counts = ctx.scratch[6];
+    DevBuf& scan_tmp = ctx.scratch[7];
+    DevBuf& sums = ctx.scratch[8];
+    DevBuf& keep = ctx.scratch[9];
     const int which = radix_sort_pairs<V>(ctx, k0, v0, k1, v1, nnz_s, bits_for(m.rows), counts,
                                           scan_tmp);
     const uint32_t* sk = which ? k1 : k0;

@@ -6,6 +6,7 @@
 // sparse input is known on the host for free; nnz_s / m_sparsity (and nnz_x
 // of a dense input) take one device reduction and a scalar D2H -- the only
 // per-iteration device round trip of the selection.
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -50,13 +51,17 @@ namespace {
 
 // Walks one tree (routing "value <= threshold -> left"),
 // pulling features lazily into `f` / `have`.
-int walk(Context& ctx, const Matrix& m, Vector& v, const Tree& t, double* f, uint32_t& have) {
+int walk(Context& ctx, const Matrix& m, Vector& v, const Tree& t, double* f, uint32_t& have,
+         double* feature_s) {
     int32_t i = 0;
     for (int guard = 0; guard < 1 << 20; ++guard) {
         const int32_t feat = t.feature[static_cast<size_t>(i)];
         if (feat < 0) return t.leaf[static_cast<size_t>(i)];
         if (!(have & (1u << feat))) {
+            const auto t0 = std::chrono::steady_clock::now();
             features(ctx, m, v, 1u << feat, f);
+            if (feature_s)
+                *feature_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             have |= 1u << feat;
         }
         i = f[feat] <= t.threshold[static_cast<size_t>(i)] ? t.left[static_cast<size_t>(i)]
@@ -71,20 +76,21 @@ int walk(Context& ctx, const Matrix& m, Vector& v, const Tree& t, double* f, uin
 // ColSpMSpV.  Classes: pattern {0 ColSpMSpV, 1 RowSpMSpV, 2 SpMV}
 // (kernels.hpp:34), workload {0 Direct, 1 LoadBalanced}, write-back
 // {0 Atomic, 1 Sort}; returns KernelId::index() (kernels.hpp:52-60).
-int predict(Context& ctx, const Matrix& m, Vector& v, const Bundle& b, uint32_t* used, int* trees) {
+int predict(Context& ctx, const Matrix& m, Vector& v, const Bundle& b, uint32_t* used, int* trees,
+            double* feature_s) {
     double f[ADASPMV_NUM_FEATURES] = {0};
     uint32_t have = 0;
     int nt = 0;
-    const int pattern = walk(ctx, m, v, b.trees[0], f, have);
+    const int pattern = walk(ctx, m, v, b.trees[0], f, have, feature_s);
     ++nt;
-    const int lb = walk(ctx, m, v, b.trees[1], f, have) == 1 ? 1 : 0;
+    const int lb = walk(ctx, m, v, b.trees[1], f, have, feature_s) == 1 ? 1 : 0;
     ++nt;
     int k;
     switch (pattern) {
         case 2: k = lb; break;      // SpMV
         case 1: k = 2 + lb; break;  // RowSpMSpV
         case 0: {
-            const int sort = walk(ctx, m, v, b.trees[2], f, have) == 1 ? 1 : 0;
+            const int sort = walk(ctx, m, v, b.trees[2], f, have, feature_s) == 1 ? 1 : 0;
             ++nt;
             k = 4 + 2 * lb + sort;
             break;

@@ -194,6 +194,24 @@ def test_selector_cascade_stub_bundles(ctx):
     assert kk.index() == 7
 
 
+def test_execute_iteration_reports_and_forced_override(ctx, port):
+    # forced override = each of the 8 KernelIds -> all within tolerance
+    rows, cols, ro, ci, vals = synth.random_csr(400, 300, 0.03, seed=12)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    xi, xv = synth.sparse_vector(cols, 30, seed=4)
+    y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, port.sparse_to_dense(cols, xi, xv))
+    for k in range(8):
+        out, rep = A.execute_iteration(m, A.SparseVector(cols, xi, xv), force_kernel=k)
+        assert rep["kernel"].index() == k and rep["kernel_s"] > 0 and rep["convert_s"] >= 0
+        assert_dense_close(out.dense().values, y_ref, bound, np.float64, f"execute k={k}")
+    # empty sparse x -> zero output
+    out, rep = A.execute_iteration(m, A.SparseVector(cols, [], []), bundle=A.SelectorBundle.load(
+        __import__("paper_2006_16767_b200.selector", fromlist=["x"]).DEFAULT_PATH))
+    assert not out.dense().values.any()
+    with pytest.raises(A.InvalidArgument):  # untrained bundle without override
+        A.execute_iteration(m, A.SparseVector(cols, xi, xv))
+
+
 @pytest.mark.parametrize("semiring", [A.PLUS_TIMES, A.OR_AND, A.MIN_PLUS])
 def test_bfs_levels_match_queue_bfs(ctx, port, semiring):
     # path graph 0-1-2-3 -> levels [0,1,2,3], 4 iterations
