@@ -205,6 +205,134 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def run_ours_multi(args, rank, world):
+    """N > 1: the row-partitioned mode (north_star), weak
+    scaling.  Rank g owns a C2-sized row block (4M rows x 4M columns, 2^26
+    draws, seed 1+g) of a (N*4M) x 4M matrix; every step broadcasts each sweep
+    point's x from rank 0 over NCCL straight into device buffers handed to the
+    library, then every rank runs its own selector + kernel on its block.
+    Step time = max over ranks (CUDA events on the shared stream, barrier on
+    both sides); value = all ranks' useful flops / step time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2006_16767_b200 import adaspmv as A
+    from paper_2006_16767_b200 import selector as S
+    from paper_2006_16767_b200 import synth
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)  # collectives order against it; the library launches on it
+    ctx = A.Context(local, stream=stream.cuda_stream)
+    rows, cols, ro, ci, vals = synth.uniform_random(N, DRAWS, seed=1 + rank, dtype=np.float32)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    del ci
+    bundle = A.SelectorBundle.load(Path(args.bundle) if args.bundle else S.DEFAULT_PATH)
+    vecs = make_vectors(cols) if rank == 0 else None
+    sizes = torch.tensor([len(v[0]) for v in vecs] if rank == 0 else [0] * len(SPARSITIES), device=dev)
+    dist.broadcast(sizes, 0)
+    bufs = []
+    for i, k in enumerate(sizes.tolist()):
+        dense = k == cols
+        idx = torch.empty(0 if dense else k, dtype=torch.int32, device=dev)
+        val = torch.empty(cols if dense else k, dtype=torch.float32, device=dev)
+        if rank == 0:
+            xi, xv = vecs[i]
+            if dense:
+                d = np.zeros(cols, np.float32)
+                d[xi] = xv
+                val.copy_(torch.from_numpy(d))
+            else:
+                idx.copy_(torch.from_numpy(xi.astype(np.int32)))
+                val.copy_(torch.from_numpy(xv))
+        bufs.append((dense, idx, val))
+    x = A.DeviceVector(cols, np.float32, ctx)
+    out = A.MultiplyOutput(ctx)
+    pinned = [(i.cpu().pin_memory(), v.cpu().pin_memory()) for _, i, v in bufs] if rank == 0 else None
+
+    def step(from_host=False):
+        for p, (dense, idx, val) in enumerate(bufs):
+            if from_host and rank == 0:  # e2e: this point's x comes from host memory
+                idx.copy_(pinned[p][0], non_blocking=True)
+                val.copy_(pinned[p][1], non_blocking=True)
+            if not dense:
+                dist.broadcast(idx, 0)
+            dist.broadcast(val, 0)
+            if dense:
+                x.set_dense_device(val.data_ptr())
+            else:
+                x.set_sparse_device(idx.numel(), idx.data_ptr(), val.data_ptr())
+            A.run_adaptive(m, x, bundle, out=out)
+            if from_host:
+                out.dense()  # D2H of this rank's y block
+
+    flops_local = 0
+    for dense, idx, val in bufs:  # useful work per point (outside any timed region)
+        dist.broadcast(idx, 0) if not dense else None
+        dist.broadcast(val, 0)
+        if dense:
+            x.set_dense_device(val.data_ptr())
+        else:
+            x.set_sparse_device(idx.numel(), idx.data_ptr(), val.data_ptr())
+        flops_local += 2 * A.effective_nnz(m, x)
+    for _ in range(args.warmup):
+        step()
+    l0 = ctx.launches
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = (ctx.launches - l0) // max(1, args.steps)
+    dist.barrier()
+    t_local = e0.elapsed_time(e1) * 1e-3 / args.steps
+    # e2e: x from pinned host memory on rank 0, y blocks back to host
+    e2e_t = []
+    for _ in range(max(2, args.steps // 2)):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step(from_host=True)
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t0)
+    tt = torch.tensor([t_local, float(flops_local), statistics.median(e2e_t)], dtype=torch.float64, device=dev)
+    tmax = tt.clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    fl = tt[1:2].clone()
+    dist.all_reduce(fl, op=dist.ReduceOp.SUM)
+    t_step = float(tmax[0].item())
+    value = float(fl.item()) / t_step / 1e9
+    e2e_v = float(fl.item()) / float(tmax[2].item()) / 1e9
+    line = None
+    if rank == 0:
+        xbytes = sum((int(v.numel()) * 4 + int(i.numel()) * 4) for _, i, v in bufs)
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded numpy generator, SURVEY.md 8(d) C2 per rank)",
+            "config": {"workload": WORKLOAD + ", row-partitioned: one C2-sized row block per GPU",
+                       "rows_per_gpu": rows, "cols": cols, "x_sparsity": list(SPARSITIES),
+                       "parallelism": f"row-partitioned x{world} (NCCL broadcast of x per point)",
+                       "exchange_bytes_per_step": xbytes, "l2": "inputs larger than L2 at the dense points"},
+            "e2e": {"value": round(e2e_v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(xbytes),
+                    "d2h_bytes_per_step": int(rows * 4 * len(bufs)),
+                    "note": "x H2D on rank 0 then NCCL broadcast; each rank's y block D2H; max over ranks"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+    dist.destroy_process_group()
+    return line
+
+
 def run_ours(args, rank, world):
     import torch
 
@@ -437,7 +565,8 @@ def main():
     if args.impl == "reference":
         line = run_reference(args, rank, world)
     else:
-        line = run_ours(args, rank, world)
+        multi = world > 1 or os.environ.get("ADASPMV_BENCH_FORCE_MULTI") == "1"  # 1-GPU test of the N>1 path
+        line = run_ours_multi(args, rank, world) if multi else run_ours(args, rank, world)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
 
