@@ -476,11 +476,16 @@ def run_ours(args, rank, world):
     _, fam = alg_bytes(rows, cols, nnz, nnz_x[dom], nnz_s[dom], out_nnz)
     hbm, src = peaks()
     achieved = fam[k_dom] / per_point[dom] / 1e9
+    # DRAM bytes of the same kernel + input from the committed ncu --set full
+    # capture (only when it is the kernel that dominates this run)
     prof = ROOT / "profiles" / "r01_roofline_traffic.json"
     traffic = None
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("traffic_bytes_per_launch")
+            pj = json.loads(prof.read_text())
+            if A.KernelId.from_index(k_dom).name() in pj.get("kernel", "") and \
+                    f"x = {int(SPARSITIES[dom] * 100)} %" in pj.get("kernel", ""):
+                traffic = pj.get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
     points = []

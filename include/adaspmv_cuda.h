@@ -267,7 +267,8 @@ int adaspmv_execute_iteration(adaspmv_ctx* ctx, const adaspmv_matrix* m, adaspmv
 /* Level-synchronous BFS from `source` over y = A x (A as stored, square).
  * `semiring` selects the multiply's algebra; `bundle` (may be NULL) selects
  * a kernel per level, else `forced_kernel` (0..7) is used for every level,
- * or -1 = built-in direction heuristic.  levels[n] gets the level or -1.
+ * or -1 = built-in direction heuristic.  levels[n] gets the level or -1
+ * (levels may be NULL: traversal only, no device-to-host copy).
  * reports (optional, capacity max_reports) gets one row per level. */
 int adaspmv_bfs(adaspmv_ctx* ctx, const adaspmv_matrix* m, int64_t source, int semiring,
                 const adaspmv_bundle* b, int forced_kernel, int64_t* levels, int64_t* n_levels,

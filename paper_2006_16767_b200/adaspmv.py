@@ -892,9 +892,9 @@ def shard_rows(row_offsets, nshards: int) -> np.ndarray:
 
 
 def bfs(m: DualMatrix, source: int = 0, semiring: int = OR_AND, bundle: Optional[SelectorBundle] = None,
-        force_kernel: int = -1, max_reports: int = 4096):
-    """Level-synchronous BFS -> (levels int64[n], reports list)."""
-    levels = np.zeros(m.rows(), np.int64)
+        force_kernel: int = -1, max_reports: int = 4096, download_levels: bool = True):
+    """Level-synchronous BFS -> (levels int64[n] or None, reports list)."""
+    levels = np.empty(m.rows(), np.int64) if download_levels else None
     nl = C.c_int64()
     reps = (_IterReport * max_reports)()
     _check(_lib.adaspmv_bfs(m.ctx.h, m.h, int(source), int(semiring), bundle.h if bundle else None,

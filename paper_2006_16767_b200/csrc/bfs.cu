@@ -28,6 +28,11 @@ __global__ void init_levels_kernel(int32_t* lv, int64_t n, int64_t source) {
     if (i < n) lv[i] = i == source ? 0 : -1;
 }
 
+__global__ void widen_levels_kernel(const int32_t* __restrict__ lv, int64_t n, int64_t* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] = lv[i];
+}
+
 template <class V, int SR>
 struct DenseFrontierIn {
     const V* y;
@@ -245,12 +250,16 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         }
         ++it;
     }
-    std::vector<int32_t> h(static_cast<size_t>(n));
-    ADA_CUDA(cudaMemcpyAsync(h.data(), lv, sizeof(int32_t) * static_cast<size_t>(n), cudaMemcpyDeviceToHost,
+    *n_levels = it;
+    if (!levels) return;  // traversal only (levels stay on the device)
+    // widen on the device, one D2H of the caller's int64 array
+    DevBuf l64;
+    int64_t* d64 = static_cast<int64_t*>(l64.ensure(sizeof(int64_t) * static_cast<size_t>(std::max<int64_t>(n, 1))));
+    widen_levels_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx.stream>>>(lv, n, d64);
+    ADA_LAUNCHED(ctx);
+    ADA_CUDA(cudaMemcpyAsync(levels, d64, sizeof(int64_t) * static_cast<size_t>(n), cudaMemcpyDeviceToHost,
                              ctx.stream));
     ctx.sync();
-    for (int64_t i = 0; i < n; ++i) levels[i] = h[static_cast<size_t>(i)];
-    *n_levels = it;
 }
 
 }  // namespace

@@ -921,7 +921,6 @@ int adaspmv_bfs(adaspmv_ctx* ctx, const adaspmv_matrix* m, int64_t source, int s
     return guarded([&] {
         bind(ctx);
         need(m, "matrix");
-        need(levels, "levels");
         need(n_levels, "n_levels");
         ada::bfs(*ctx, *m, source, semiring, b, forced_kernel, levels, n_levels, reports, max_reports);
     });
