@@ -852,6 +852,29 @@ def execute_iteration(m: DualMatrix, x, bundle: Optional[SelectorBundle] = None,
                      predict_s=rep.predict_s, convert_s=rep.convert_s, kernel_s=rep.kernel_s)
 
 
+def run_trace(m: DualMatrix, xs, bundle: Optional[SelectorBundle] = None, force_kernel: int = -1,
+              cfg: Optional[KernelConfig] = None, oracle_times=None) -> dict:
+    """run_trace: execute_iteration over a sequence of
+    vectors -> TraceStats: per-iteration reports, overhead fraction
+    (feature + predict + convert over total), kernel-switch
+    count, and regret = sum(chosen kernel time) / sum(best time) when
+    `oracle_times[i][k]` (seconds of kernel k on vector i) is supplied."""
+    out = MultiplyOutput(m.ctx)
+    reports = []
+    for x in xs:
+        _, rep = execute_iteration(m, x, bundle, force_kernel, cfg, out)
+        reports.append(rep)
+    over = sum(r["feature_s"] + r["predict_s"] + r["convert_s"] for r in reports)
+    total = over + sum(r["kernel_s"] for r in reports)
+    ks = [r["kernel"].index() for r in reports]
+    stats = {"iterations": reports, "overhead_fraction": (over / total) if total > 0 else 0.0,
+             "kernel_switches": sum(1 for a, b in zip(ks, ks[1:]) if a != b)}
+    if oracle_times is not None and len(reports):
+        ot = np.asarray(oracle_times, np.float64)
+        stats["regret"] = float(ot[np.arange(len(ks)), ks].sum() / ot.min(axis=1).sum())
+    return stats
+
+
 def effective_nnz(m: DualMatrix, x) -> int:
     v = _as_device_vector(m, x)
     k = C.c_int64()

@@ -418,13 +418,89 @@ void launch_direct_emit(Context& ctx, const Matrix& m, Vector& x, int G, uint32_
     ADA_LAUNCHED(ctx);
 }
 
+// KernelConfig::atomic_private_accumulators (kernels.hpp:152-162, :452-478):
+// each CTA accumulates its share into a shared-memory copy of y (all rows fit),
+// then flushes the touched rows with one global atomic each.  Shares follow
+// the reference: Direct = chunk_range of support positions (parallel.hpp:153),
+// LoadBalanced = make_partition of the effective entries with W = #CTAs.
+// (On the GPU the flush is atomic, so like the plain atomic path the result is
+// deterministic only up to summation order.)
+template <class V, int SR, bool LB>
+__global__ void __launch_bounds__(kNT) col_private_kernel(
+    int64_t nnz_x, int64_t nnz_s, int64_t rows, const int64_t* __restrict__ eff,
+    const int32_t* __restrict__ xi, const V* __restrict__ xv, const int64_t* __restrict__ co,
+    const int32_t* __restrict__ ri, const V* __restrict__ cv, V* __restrict__ y) {
+    using S = Semiring<SR, V>;
+    extern __shared__ __align__(16) unsigned char priv_smem[];
+    V* acc = reinterpret_cast<V*>(priv_smem);
+    for (int64_t r = threadIdx.x; r < rows; r += kNT) acc[r] = S::zero();
+    __syncthreads();
+    const int64_t W = gridDim.x, c = blockIdx.x;
+    if (LB) {
+        const int64_t ib = nnz_s * c / W, ie = nnz_s * (c + 1) / W;
+        const int64_t len = ie - ib;
+        const int64_t p0 = ib + len * threadIdx.x / kNT, p1 = ib + len * (threadIdx.x + 1) / kNT;
+        if (p0 < p1) {
+            int64_t s = segment_search(eff, 0, nnz_x + 1, p0);
+            int64_t s_end = __ldg(eff + s + 1);
+            int64_t base = __ldg(co + __ldg(xi + s)) - __ldg(eff + s);
+            V xval = __ldg(xv + s);
+            for (int64_t p = p0; p < p1; ++p) {
+                while (p >= s_end) {
+                    ++s;
+                    s_end = __ldg(eff + s + 1);
+                    base = __ldg(co + __ldg(xi + s)) - __ldg(eff + s);
+                    xval = __ldg(xv + s);
+                }
+                const int64_t k = base + p;
+                AtomicCombine<SR>::apply(acc + __ldg(ri + k), S::mul(S::kUsesValues ? __ldg(cv + k) : V(1), xval));
+            }
+        }
+    } else {
+        const int64_t sb = nnz_x * c / W, se = nnz_x * (c + 1) / W;
+        for (int64_t s = sb + threadIdx.x; s < se; s += kNT) {
+            const int32_t col = __ldg(xi + s);
+            const V xval = __ldg(xv + s);
+            for (int64_t k = __ldg(co + col); k < __ldg(co + col + 1); ++k)
+                AtomicCombine<SR>::apply(acc + __ldg(ri + k), S::mul(S::kUsesValues ? __ldg(cv + k) : V(1), xval));
+        }
+    }
+    __syncthreads();
+    for (int64_t r = threadIdx.x; r < rows; r += kNT)
+        if (acc[r] != S::zero()) AtomicCombine<SR>::apply(y + r, acc[r]);
+}
+
+constexpr size_t kPrivateSmem = 200 * 1024;
+
+template <class V, int SR>
+bool launch_private(Context& ctx, const Matrix& m, Vector& x, bool lb, V* y) {
+    const size_t smem = sizeof(V) * static_cast<size_t>(m.rows);
+    if (smem > kPrivateSmem || m.rows == 0) return false;  // y does not fit: plain atomic path
+    const int64_t nnz_s = lb ? vector_nnz_s(ctx, x, m) : 0;
+    const unsigned grid = static_cast<unsigned>(2 * ctx.sm_count);
+    if (lb) {
+        ADA_CUDA(cudaFuncSetAttribute(col_private_kernel<V, SR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kPrivateSmem)));
+        col_private_kernel<V, SR, true><<<grid, kNT, smem, ctx.stream>>>(
+            x.nnz, nnz_s, m.rows, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
+            m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), y);
+    } else {
+        ADA_CUDA(cudaFuncSetAttribute(col_private_kernel<V, SR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kPrivateSmem)));
+        col_private_kernel<V, SR, false><<<grid, kNT, smem, ctx.stream>>>(
+            x.nnz, 0, m.rows, nullptr, x.sp_idx.as<int32_t>(), x.sp_val.as<V>(), m.col_off.as<int64_t>(),
+            m.row_idx.as<int32_t>(), m.cvals.as<V>(), y);
+    }
+    ADA_LAUNCHED(ctx);
+    return true;
+}
+
 }  // namespace
 
 template <class V, int SR>
 void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort, bool private_acc,
                    int lanes, V* y_dense, int32_t* y_idx, V* y_val, int64_t* d_nnz,
                    int64_t* h_nnz) {
-    (void)private_acc;
     vector_ensure_sparse(ctx, x);
     const int G = lanes > 0 ? lanes : default_lanes_per_row(m.avg_col);
     *h_nnz = -1;
@@ -432,6 +508,7 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
         // atomic write-back into a dense y initialised to the identity
         fill_value<V, SR>(ctx, y_dense, m.rows);
         if (x.nnz == 0 || m.nnz == 0) return;
+        if (private_acc && launch_private<V, SR>(ctx, m, x, lb, y_dense)) return;
         if (!lb) {
             launch_direct_atomic<V, SR>(ctx, m, x, G, y_dense);
             return;

@@ -82,6 +82,26 @@ def test_lanes_override_and_workers_invariance(ctx, port, dt):
             assert_dense_close(out.dense().values, y_ref, bound, dt, f"lanes={lanes} k={k}")
 
 
+@pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
+def test_private_accumulators(ctx, port, dt):
+    # KernelConfig::atomic_private_accumulators (kernels.hpp:161, :452-478): few rows
+    for r, c, d in ((64, 5000, 0.05), (3000, 800, 0.01)):
+        rows, cols, ro, ci, vals = synth.random_csr(r, c, d, seed=r, dtype=dt)
+        m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+        for nx in (1, 100, cols):
+            xi, xv = synth.sparse_vector(cols, nx, seed=nx, dtype=dt)
+            y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, port.sparse_to_dense(cols, xi, xv))
+            for k in (4, 6):
+                out = A.run_kernel(m, k, A.SparseVector(cols, xi, xv),
+                                   A.KernelConfig(atomic_private_accumulators=True))
+                assert_dense_close(out.dense().values, y_ref, bound, dt, f"private k={k} rows={r} nnz_x={nx}")
+                for sr in (A.OR_AND,):
+                    o2 = A.run_kernel(m, k, A.SparseVector(cols, xi, xv),
+                                      A.KernelConfig(atomic_private_accumulators=True, semiring=sr))
+                    o3 = A.run_kernel(m, k, A.SparseVector(cols, xi, xv), A.KernelConfig(semiring=sr))
+                    assert np.array_equal(o2.dense().values, o3.dense().values)
+
+
 def test_explicit_zero_in_x_drops_zero_sums(ctx):
     # A = {(0,0),(1,1),(2,0)}, x = {0: 0.0, 1: 5.0} -> sparse y = {1}
     ro = np.array([0, 1, 2, 3])
@@ -210,6 +230,23 @@ def test_execute_iteration_reports_and_forced_override(ctx, port):
     assert not out.dense().values.any()
     with pytest.raises(A.InvalidArgument):  # untrained bundle without override
         A.execute_iteration(m, A.SparseVector(cols, xi, xv))
+
+
+def test_run_trace_contracts(ctx):
+    # identical vectors -> at most 1 switch; empty trace -> overhead 0;
+    # an oracle-faithful stub (constant per density class) has regret 1.0 on its own timings
+    rows, cols, ro, ci, vals = synth.random_csr(2000, 2000, 0.005, seed=3)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    from paper_2006_16767_b200 import selector as S
+    b = A.SelectorBundle.load(S.DEFAULT_PATH)
+    xi, xv = synth.sparse_vector(cols, 20, seed=1)
+    st = A.run_trace(m, [A.SparseVector(cols, xi, xv)] * 4, b)
+    assert st["kernel_switches"] <= 1 and 0 <= st["overhead_fraction"] <= 1
+    assert A.run_trace(m, [], b)["overhead_fraction"] == 0.0
+    sparse = A.SparseVector(cols, xi, xv)
+    dense = A.DenseVector(np.random.default_rng(0).uniform(-1, 1, cols))
+    st = A.run_trace(m, [sparse, dense, sparse], force_kernel=6, oracle_times=[[2] * 6 + [1, 2]] * 3)
+    assert st["regret"] == 1.0 and st["kernel_switches"] == 0
 
 
 @pytest.mark.parametrize("semiring", [A.PLUS_TIMES, A.OR_AND, A.MIN_PLUS])
