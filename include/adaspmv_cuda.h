@@ -87,8 +87,15 @@ typedef struct {
     int32_t atomic_private_accumulators; /* kernels.hpp:161: CTA-private accumulators */
     int32_t semiring;                    /* adaspmv_semiring */
     int32_t lanes_per_row;               /* 0 = auto; direct kernels' lanes per row/column */
-    int32_t reserved[4];
+    /* Execution of the Direct row-major kernels K0/K2: 0 = auto (row bins when
+     * the matrix's x gathers are scattered), 1 = CSR
+     * gather, 2 = row bins (column-sorted entries, shared-memory y segment). */
+    int32_t row_layout;
+    int32_t bin_rows;                    /* rows per bin override (0 = auto) */
+    int64_t bin_tile_nnz;                /* entries per bin tile override (0 = auto) */
 } adaspmv_config;
+
+enum { ADASPMV_ROW_LAYOUT_AUTO = 0, ADASPMV_ROW_LAYOUT_CSR = 1, ADASPMV_ROW_LAYOUT_BINNED = 2 };
 
 /* ---- context -------------------------------------------------------------- */
 /* Binds `device` and a stream (NULL = a new non-blocking stream owned by the
@@ -142,6 +149,9 @@ int adaspmv_matrix_download(adaspmv_ctx* ctx, const adaspmv_matrix* m, int64_t* 
                             int64_t* row_indices, void* csc_values);
 /* Matrix features ids 0..8, computed once at creation. */
 int adaspmv_matrix_features(const adaspmv_matrix* m, double out9[9]);
+/* Mean |col - row*cols/rows| over the nonzeros, in columns: how scattered the
+ * x gathers of the row-major kernels are (drives row_layout = AUTO). */
+int adaspmv_matrix_gather_spread(const adaspmv_matrix* m, double* out);
 
 /* ---- vectors (DenseVector / SparseVector / BitMask, sparse.hpp:99-151) ------ */
 /* A vector is one logical operand x of length n with a device cache of the

@@ -169,12 +169,18 @@ struct KernelConfig {
     bool atomic_private_accumulators = false;
     int semiring = ADASPMV_PLUS_TIMES;
     int lanes_per_row = 0;
+    int row_layout = ADASPMV_ROW_LAYOUT_AUTO;  // K0/K2 execution (adaspmv_cuda.h)
+    int bin_rows = 0;
+    long long bin_tile_nnz = 0;
     adaspmv_config c() const {
         adaspmv_config r{};
         r.workers = workers;
         r.atomic_private_accumulators = atomic_private_accumulators ? 1 : 0;
         r.semiring = semiring;
         r.lanes_per_row = lanes_per_row;
+        r.row_layout = row_layout;
+        r.bin_rows = bin_rows;
+        r.bin_tile_nnz = bin_tile_nnz;
         return r;
     }
 };

@@ -102,7 +102,8 @@ class _IterReport(C.Structure):
 class _Config(C.Structure):
     _fields_ = [("workers", C.c_int32), ("atomic_private_accumulators", C.c_int32),
                 ("semiring", C.c_int32), ("lanes_per_row", C.c_int32),
-                ("reserved", C.c_int32 * 4)]
+                ("row_layout", C.c_int32), ("bin_rows", C.c_int32),
+                ("bin_tile_nnz", C.c_int64)]
 
 
 _lib = None
@@ -139,6 +140,7 @@ def load(path: Optional[os.PathLike] = None):
         "adaspmv_matrix_dims": [vp, P(i64), P(i64), P(i64), P(C.c_int)],
         "adaspmv_matrix_download": [vp, vp, vp, vp, vp, vp, vp, vp],
         "adaspmv_matrix_features": [vp, vp],
+        "adaspmv_matrix_gather_spread": [vp, vp],
         "adaspmv_vector_create": [vp, i64, C.c_int, P(vp)],
         "adaspmv_vector_destroy": [vp],
         "adaspmv_vector_set_sparse": [vp, vp, i64, vp, vp],
@@ -349,6 +351,9 @@ class KernelConfig:  # kernels.hpp:154-162 (+ device knobs)
     atomic_private_accumulators: bool = False
     semiring: int = PLUS_TIMES
     lanes_per_row: int = 0
+    row_layout: int = 0       # K0/K2: 0 auto, 1 CSR gather, 2 row bins
+    bin_rows: int = 0         # rows per bin override (0 = auto)
+    bin_tile_nnz: int = 0     # entries per bin tile override (0 = auto)
 
     def _c(self) -> _Config:
         c = _Config()
@@ -356,6 +361,9 @@ class KernelConfig:  # kernels.hpp:154-162 (+ device knobs)
         c.atomic_private_accumulators = int(bool(self.atomic_private_accumulators))
         c.semiring = int(self.semiring)
         c.lanes_per_row = int(self.lanes_per_row)
+        c.row_layout = int(self.row_layout)
+        c.bin_rows = int(self.bin_rows)
+        c.bin_tile_nnz = int(self.bin_tile_nnz)
         return c
 
 
@@ -505,6 +513,11 @@ class DualMatrix:
         out = np.zeros(9, np.float64)
         _check(_lib.adaspmv_matrix_features(self.h, _ptr(out)))
         return out
+
+    def gather_spread(self) -> float:
+        out = C.c_double()
+        _check(_lib.adaspmv_matrix_gather_spread(self.h, C.byref(out)))
+        return out.value
 
     def transpose(self) -> "DualMatrix":
         h = C.c_void_p()

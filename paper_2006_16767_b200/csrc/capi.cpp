@@ -399,6 +399,14 @@ int adaspmv_matrix_features(const adaspmv_matrix* m, double out9[9]) {
     });
 }
 
+int adaspmv_matrix_gather_spread(const adaspmv_matrix* m, double* out) {
+    return guarded([&] {
+        need(m, "matrix");
+        need(out, "out");
+        *out = m->gather_spread;
+    });
+}
+
 // ---- vectors ----------------------------------------------------------------------
 int adaspmv_vector_create(adaspmv_ctx* ctx, int64_t length, int dtype, adaspmv_vector** out) {
     return guarded([&] {

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -111,6 +112,23 @@ struct Context {
 // (make_partition's equal-item split, partition.hpp:37-56, W = ceil(nnz/kRowTile)).
 constexpr int kRowTile = 256;
 
+// Row-bin layout of the binned K0/K2 execution (kernels_binned.cu): the CSC
+// order stably partitioned by bins of R rows; entry = (col & (2^cw-1)) <<
+// rbits | row - bin*R; chunk_off[b*nchunks + c] = first entry of bin b with
+// col >> cw == c ([nbins*nchunks] = nnz).  Tiles: CTA work units.
+struct BinLayout {
+    bool built = false;
+    int dtype = -1;
+    int64_t force_rows = 0;   // rows-per-bin override it was built with
+    int64_t R = 0, nbins = 0, nchunks = 0;
+    int rbits = 0, cw = 0;
+    DevBuf pk, bv, chunk_off;
+    std::vector<int64_t> bin_start;  // host: first entry of each bin, [nbins] = nnz
+    int64_t tile_cap = -1, ntiles = 0;
+    bool multi = false;       // some bin is split into several tiles
+    DevBuf tiles, tile_bin, tile_multi;
+};
+
 struct Matrix {
     Context* ctx = nullptr;
     int64_t rows = 0, cols = 0, nnz = 0;
@@ -131,6 +149,8 @@ struct Matrix {
     int64_t max_col_deg = 0;
     double avg_col = 0;
     bool pattern = false;   // created without values (all 1.0)
+    double gather_spread = 0;  // mean |col - row*n/m| over the nonzeros (columns)
+    mutable std::unique_ptr<BinLayout> bins{new BinLayout()};
     int vbytes() const { return value_bytes(dtype); }
 };
 
@@ -219,6 +239,9 @@ int64_t vector_nnz_s(Context& ctx, Vector& v, const Matrix& m);
 
 void run_kernel(Context& ctx, const Matrix& m, Vector& x, int kernel, const adaspmv_config& cfg,
                 Output& y);
+// binned K0/K2 (kernels_binned.cu)
+double matrix_gather_spread(Context& ctx, const Matrix& m);
+bool binned_preferred(const Matrix& m);
 void output_ensure_dense(Context& ctx, Output& y);
 void output_ensure_sparse(Context& ctx, Output& y);
 int64_t output_nnz(Context& ctx, Output& y);

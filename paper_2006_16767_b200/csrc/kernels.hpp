@@ -37,6 +37,12 @@ template <class V, int SR>
 void run_row_major(Context& ctx, const Matrix& m, const V* x, const uint32_t* mask, bool lb,
                    int lanes, V* y);
 
+// K0/K2 on the row-bin layout (kernels_binned.cu); builds the layout on
+// first use.  mask == nullptr -> SpMV.
+template <class V, int SR>
+void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* mask, V* y,
+                    int64_t force_rows, int64_t tile_cap, int variant = 0);
+
 // K4-K7 (kernels_col.cu).  Atomic -> dense y (y_dense); sort -> sparse y
 // (y_idx, y_val, *d_nnz on device).  x is the sparse operand.
 template <class V, int SR>

@@ -1,0 +1,393 @@
+// kernels_binned.cu -- row-block ("binned") execution of the row-major
+// kernels K0 spmv_direct / K2 row_direct for matrices whose x gathers are
+// scattered.
+//
+// Why: in CSR order every nonzero gathers x[col] on its own; for a matrix
+// whose columns are spread (uniform random, R-MAT) each gather is a separate
+// 128-B L1TEX wavefront and L2 request, and the SM's ~1 wavefront/cycle
+// bounds the multiply at ~35 % of HBM.  Here the rows
+// are cut into bins of R rows (R*V bytes fit one CTA's shared memory); the
+// entries of a bin are stored in COLUMN order, so the 32 gathers of a warp
+// instruction fall on a few consecutive lines of x (~9 instead of 32 at C2),
+// and each product is accumulated into the bin's y segment held in shared
+// memory.  One CTA owns a bin (the reference's Direct distribution: every
+// worker a contiguous block of rows, kernels.hpp:242-250); bins heavier than
+// the tile cap are split into column-contiguous tiles whose partial segments
+// are combined with global atomics (y pre-filled with the identity).
+//
+// Layout (Matrix::BinLayout, built once on the device from the CSC): the CSC
+// order (columns ascending, rows ascending within a column: csr_to_csc,
+// sparse.hpp:157-178) stably partitioned by bin.  Entry word =
+// (col & (2^cw - 1)) << rbits | (row - bin_row0); columns are split in chunks
+// of 2^cw (cw = 32 - rbits) whose offsets per bin are stored, so an entry is
+// 4 B of index + V of value -- the same bytes per nonzero as the CSR.
+//
+// Summation order inside a row is not the reference's (shared-memory atomics
+// in column order), so results match within the floating-point tolerance of
+// SURVEY.md 8(c) and are not run-to-run bitwise reproducible, like the
+// atomic column kernels.  OR_AND and MIN_PLUS are exact.
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "device.cuh"
+#include "internal.hpp"
+#include "kernels.hpp"
+#include "prims.cuh"
+
+namespace ada {
+
+namespace {
+
+constexpr uint32_t kBinSmemBytes = 114688;  // 112 KiB of y segment per CTA (1 CTA / SM)
+
+template <class V>
+struct PkVal {
+    uint32_t pk;
+    V val;
+};
+
+// One warp per column of the CSC: key = bin of the row, payload = packed
+// entry; counts per (bin, chunk) for the chunk offsets.
+template <class V>
+__global__ void bin_expand_kernel(const int64_t* __restrict__ co, const int32_t* __restrict__ ri,
+                                  const V* __restrict__ cv, int64_t cols, int64_t R, int rbits,
+                                  int cw, int64_t nchunks, uint32_t* __restrict__ keys,
+                                  PkVal<V>* __restrict__ pay,
+                                  unsigned long long* __restrict__ counts) {
+    const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const uint32_t cmask = cw >= 32 ? 0xffffffffu : ((1u << cw) - 1u);
+    for (int64_t j = warp; j < cols; j += nwarps) {
+        const int64_t b = co[j], e = co[j + 1];
+        const int64_t chunk = j >> cw;
+        int64_t prev_bin = -1;
+        int run = 0;
+        for (int64_t k = b + lane; k < e; k += 32) {
+            const int64_t row = ri[k];
+            const int64_t bin = row / R;
+            keys[k] = static_cast<uint32_t>(bin);
+            const uint32_t rl = static_cast<uint32_t>(row - bin * R);
+            pay[k] = PkVal<V>{((static_cast<uint32_t>(j) & cmask) << rbits) | rl, cv[k]};
+            // rows ascend within the column: count runs of equal bins per lane
+            if (bin != prev_bin) {
+                if (run) atomicAdd(counts + prev_bin * nchunks + chunk, static_cast<unsigned long long>(run));
+                prev_bin = bin;
+                run = 0;
+            }
+            ++run;
+        }
+        if (run) atomicAdd(counts + prev_bin * nchunks + chunk, static_cast<unsigned long long>(run));
+    }
+}
+
+template <class V>
+__global__ void bin_unpack_kernel(const PkVal<V>* __restrict__ pay, int64_t nnz,
+                                  uint32_t* __restrict__ pk, V* __restrict__ bv) {
+    const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t k = i0; k < nnz; k += stride) {
+        const PkVal<V> p = pay[k];
+        pk[k] = p.pk;
+        bv[k] = p.val;
+    }
+}
+
+struct U64Counts {
+    const unsigned long long* c;
+    __device__ int64_t operator()(int64_t i) const { return static_cast<int64_t>(c[i]); }
+};
+
+// mean |col - row * n/m| over the nonzeros (x-gather spread, in columns),
+// accumulated as double per block.
+__global__ void gather_spread_kernel(const int64_t* __restrict__ ro, const int32_t* __restrict__ ci,
+                                     int64_t rows, double slope, double* __restrict__ out) {
+    double s = 0;
+    const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = warp; r < rows; r += nwarps) {
+        const double d = static_cast<double>(r) * slope;
+        for (int64_t k = ro[r] + lane; k < ro[r + 1]; k += 32) s += fabs(static_cast<double>(ci[k]) - d);
+    }
+    s = warp_sum(s);
+    if (lane == 0) atomicAdd(out, s);
+}
+
+// ---------------------------------------------------------------------------
+// The multiply.  CTA = one tile (bin, entry range [e0, e1)).  Thread t of the
+// CTA handles entries e0 + i*NT*U + j*NT + t: each warp instruction covers 32
+// consecutive (column-sorted) entries.  Each thread walks the bin's chunk
+// offsets monotonically to know the chunk (high column bits) of its entries.
+// ---------------------------------------------------------------------------
+// 1024 threads x 8 entries in flight per thread: measured best on C2 (B200):
+// 1024x8 170 us, 1024x6 174, 1024x4 197, 512x16 217, 512x12 227, 256x32 363.
+template <class V, int SR, bool MASKED, int kBinUnroll = 8, bool NOALLOC = false, int kBinThreads = 1024>
+__global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
+    int64_t rows, int64_t R, int rbits, int cw, int64_t nchunks,
+    const int64_t* __restrict__ tiles, const int32_t* __restrict__ tile_bin,
+    const int32_t* __restrict__ tile_multi, const int64_t* __restrict__ chunk_off,
+    const uint32_t* __restrict__ pk, const V* __restrict__ bv, const V* __restrict__ x,
+    const uint32_t* __restrict__ mask, V* __restrict__ y) {
+    using S = Semiring<SR, V>;
+    extern __shared__ __align__(16) unsigned char bin_smem[];
+    V* ys = reinterpret_cast<V*>(bin_smem);
+    const int64_t t = blockIdx.x;
+    const int64_t bin = tile_bin[t];
+    const int64_t e0 = tiles[2 * t], e1 = tiles[2 * t + 1];
+    const int64_t r0 = bin * R;
+    const int nr = static_cast<int>(min(R, rows - r0));
+    for (int i = threadIdx.x; i < nr; i += kBinThreads) ys[i] = S::zero();
+    __syncthreads();
+
+    const int64_t* __restrict__ co = chunk_off + bin * nchunks;
+    const uint32_t rmask = (1u << rbits) - 1u;
+    if (e0 < e1) {
+        // chunk of the thread's first entry: largest c with co[c] <= e (binary search)
+        const int64_t efirst = e0 + threadIdx.x;
+        int64_t lo = 0, hi = nchunks;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (__ldg(co + mid) <= efirst) lo = mid;
+            else hi = mid;
+        }
+        int64_t c = lo;
+        int64_t nb = __ldg(co + c + 1);  // end of chunk c
+        for (int64_t base = e0; base < e1; base += static_cast<int64_t>(kBinThreads) * kBinUnroll) {
+            uint32_t p[kBinUnroll];
+            V a[kBinUnroll];
+            int col[kBinUnroll];
+            bool ok[kBinUnroll];
+#pragma unroll
+            for (int j = 0; j < kBinUnroll; ++j) {
+                const int64_t e = base + j * kBinThreads + threadIdx.x;
+                ok[j] = e < e1;
+                p[j] = ok[j] ? ld_stream(reinterpret_cast<const int*>(pk) + e) : 0;
+                if (S::kUsesValues) a[j] = ok[j] ? ld_stream(bv + e) : V(0);
+                else a[j] = V(1);
+            }
+#pragma unroll
+            for (int j = 0; j < kBinUnroll; ++j) {
+                const int64_t e = base + j * kBinThreads + threadIdx.x;
+                if (ok[j]) {
+                    while (e >= nb) {
+                        ++c;
+                        nb = __ldg(co + c + 1);
+                    }
+                }
+                col[j] = static_cast<int>((static_cast<uint32_t>(c) << cw) + (p[j] >> rbits));
+            }
+            if (MASKED) {
+#pragma unroll
+                for (int j = 0; j < kBinUnroll; ++j)
+                    if (ok[j]) ok[j] = (__ldg(mask + (col[j] >> 5)) >> (col[j] & 31)) & 1u;
+            }
+            V xv[kBinUnroll];
+#pragma unroll
+            for (int j = 0; j < kBinUnroll; ++j) xv[j] = ok[j] ? (NOALLOC ? ld_stream(x + col[j]) : __ldg(x + col[j])) : S::zero();
+#pragma unroll
+            for (int j = 0; j < kBinUnroll; ++j) {
+                if (!ok[j]) continue;
+                V* slot = ys + (p[j] & rmask);
+                if (SR == SR_PLUS_TIMES) {
+                    const V prod = a[j] * xv[j];
+                    // adding +-0 never changes a sum that starts at +0
+                    if (prod != V(0)) atomicAdd(slot, prod);
+                } else if (SR == SR_OR_AND) {
+                    if (xv[j] != V(0)) *reinterpret_cast<volatile V*>(slot) = V(1);
+                } else {
+                    const V v = a[j] + xv[j];
+                    if (v < *slot) AtomicCombine<SR_MIN_PLUS>::apply(slot, v);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (!tile_multi[t]) {  // the tile owns its bin's rows: plain coalesced stores
+        for (int i = threadIdx.x; i < nr; i += kBinThreads) y[r0 + i] = ys[i];
+    } else {               // partial segment: combine into the identity-filled y
+        for (int i = threadIdx.x; i < nr; i += kBinThreads) {
+            const V v = ys[i];
+            if (v != S::zero()) AtomicCombine<SR>::apply(y + r0 + i, v);
+        }
+    }
+}
+
+template <class V>
+void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
+    const int vb = sizeof(V);
+    const int64_t rmax = kBinSmemBytes / vb;
+    int rbits = 0;
+    while ((int64_t(1) << rbits) < rmax) ++rbits;
+    int64_t nbins;
+    if (L.force_rows > 0) {
+        nbins = (m.rows + L.force_rows - 1) / L.force_rows;
+    } else {
+        nbins = (m.rows + rmax - 1) / rmax;
+        // at least one bin per SM when rows allow bins of >= 1024 rows
+        nbins = std::max<int64_t>(nbins, std::min<int64_t>(ctx.sm_count, (m.rows + 1023) / 1024));
+    }
+    nbins = std::max<int64_t>(nbins, 1);
+    const int64_t R = std::max<int64_t>((m.rows + nbins - 1) / nbins, 1);
+    if (R > rmax) invalid("binned layout: rows per bin exceed the shared-memory segment");
+    nbins = std::max<int64_t>((m.rows + R - 1) / R, 1);
+    if (nbins >= (int64_t(1) << 31)) invalid("binned layout: too many bins");
+    const int cw = 32 - rbits;
+    const int64_t nchunks = std::max<int64_t>((m.cols + (int64_t(1) << cw) - 1) >> cw, 1);
+    L.R = R;
+    L.rbits = rbits;
+    L.cw = cw;
+    L.nbins = nbins;
+    L.nchunks = nchunks;
+    const int64_t nnz = m.nnz;
+    const size_t z = static_cast<size_t>(std::max<int64_t>(nnz, 1));
+    L.pk.ensure(sizeof(uint32_t) * z);
+    L.bv.ensure(sizeof(V) * z);
+    const int64_t nkeys = nbins * nchunks;
+    L.chunk_off.ensure(sizeof(int64_t) * static_cast<size_t>(nkeys + 1));
+    DevBuf counts;
+    counts.ensure(sizeof(unsigned long long) * static_cast<size_t>(nkeys));
+    ADA_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(unsigned long long) * static_cast<size_t>(nkeys), ctx.stream));
+    if (nnz > 0) {
+        DevBuf k0, k1, p0, p1, cnt;
+        k0.ensure(sizeof(uint32_t) * z);
+        k1.ensure(sizeof(uint32_t) * z);
+        p0.ensure(sizeof(PkVal<V>) * z);
+        p1.ensure(sizeof(PkVal<V>) * z);
+        const int64_t warps = std::min<int64_t>(m.cols, static_cast<int64_t>(ctx.sm_count) * 64);
+        bin_expand_kernel<V><<<static_cast<unsigned>(std::max<int64_t>((warps * 32 + 255) / 256, 1)), 256, 0,
+                               ctx.stream>>>(m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(),
+                                             m.cvals.as<V>(), m.cols, R, rbits, cw, nchunks,
+                                             k0.as<uint32_t>(), p0.as<PkVal<V>>(),
+                                             counts.as<unsigned long long>());
+        ADA_LAUNCHED(ctx);
+        const int which = radix_sort_pairs<PkVal<V>>(ctx, k0.as<uint32_t>(), p0.as<PkVal<V>>(),
+                                                     k1.as<uint32_t>(), p1.as<PkVal<V>>(), nnz,
+                                                     bits_for(nbins), cnt, ctx.scratch[5]);
+        const PkVal<V>* sorted = which ? p1.as<PkVal<V>>() : p0.as<PkVal<V>>();
+        const int64_t g = std::min<int64_t>((nnz + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 32);
+        bin_unpack_kernel<V><<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(sorted, nnz, L.pk.as<uint32_t>(),
+                                                                              L.bv.as<V>());
+        ADA_LAUNCHED(ctx);
+        ctx.sync();  // the sort buffers are released on return
+    }
+    int64_t* off = L.chunk_off.as<int64_t>();
+    scan3(ctx, nkeys, U64Counts{counts.as<unsigned long long>()}, WriteExclusive{off}, off + nkeys,
+          ctx.scratch[5]);
+    // per-bin entry counts on the host (tile planning)
+    std::vector<int64_t> all(static_cast<size_t>(nkeys + 1));
+    ADA_CUDA(cudaMemcpyAsync(all.data(), off, sizeof(int64_t) * all.size(), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    L.bin_start.resize(static_cast<size_t>(nbins + 1));
+    for (int64_t b = 0; b <= nbins; ++b) L.bin_start[static_cast<size_t>(b)] = all[static_cast<size_t>(b * nchunks)];
+    L.tile_cap = -1;
+    L.built = true;
+}
+
+// Tiles: every bin gets ceil(count / cap) equal column-contiguous tiles (at
+// least one, so its rows are written); heaviest first (longest-processing-
+// time order for the hardware block scheduler).
+void plan_tiles(Context& ctx, const Matrix& m, BinLayout& L, int64_t cap_req) {
+    int64_t cap = cap_req;
+    if (cap <= 0) {
+        const double fair = static_cast<double>(m.nnz) / static_cast<double>(ctx.sm_count);
+        cap = std::max<int64_t>(static_cast<int64_t>(fair * 1.25), 16384);
+    }
+    if (L.tile_cap == cap) return;
+    struct T { int64_t e0, e1; int32_t bin, multi; };
+    std::vector<T> ts;
+    bool multi = false;
+    for (int64_t b = 0; b < L.nbins; ++b) {
+        const int64_t s = L.bin_start[static_cast<size_t>(b)], e = L.bin_start[static_cast<size_t>(b + 1)];
+        const int64_t k = std::max<int64_t>((e - s + cap - 1) / cap, 1);
+        for (int64_t i = 0; i < k; ++i)
+            ts.push_back(T{s + (e - s) * i / k, s + (e - s) * (i + 1) / k, static_cast<int32_t>(b), k > 1});
+        multi = multi || k > 1;
+    }
+    std::stable_sort(ts.begin(), ts.end(), [](const T& a, const T& b) { return a.e1 - a.e0 > b.e1 - b.e0; });
+    const size_t nt = ts.size();
+    std::vector<int64_t> h_t(2 * nt);
+    std::vector<int32_t> h_b(nt), h_m(nt);
+    for (size_t i = 0; i < nt; ++i) {
+        h_t[2 * i] = ts[i].e0;
+        h_t[2 * i + 1] = ts[i].e1;
+        h_b[i] = ts[i].bin;
+        h_m[i] = ts[i].multi;
+    }
+    L.tiles.ensure(sizeof(int64_t) * h_t.size());
+    L.tile_bin.ensure(sizeof(int32_t) * nt);
+    L.tile_multi.ensure(sizeof(int32_t) * nt);
+    ADA_CUDA(cudaMemcpyAsync(L.tiles.p, h_t.data(), sizeof(int64_t) * h_t.size(), cudaMemcpyHostToDevice, ctx.stream));
+    ADA_CUDA(cudaMemcpyAsync(L.tile_bin.p, h_b.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, ctx.stream));
+    ADA_CUDA(cudaMemcpyAsync(L.tile_multi.p, h_m.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, ctx.stream));
+    ctx.sync();  // host vectors go out of scope
+    L.ntiles = static_cast<int64_t>(nt);
+    L.multi = multi;
+    L.tile_cap = cap;
+}
+
+}  // namespace
+
+double matrix_gather_spread(Context& ctx, const Matrix& m) {
+    if (m.nnz == 0 || m.rows == 0) return 0.0;
+    DevBuf acc;
+    acc.ensure(sizeof(double));
+    ADA_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double), ctx.stream));
+    const double slope = static_cast<double>(m.cols) / static_cast<double>(m.rows);
+    const int64_t warps = std::min<int64_t>(m.rows, static_cast<int64_t>(ctx.sm_count) * 64);
+    gather_spread_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, ctx.stream>>>(
+        m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), m.rows, slope, acc.as<double>());
+    ADA_LAUNCHED(ctx);
+    double h = 0;
+    ADA_CUDA(cudaMemcpyAsync(&h, acc.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    return h / static_cast<double>(m.nnz);
+}
+
+bool binned_preferred(const Matrix& m) {
+    // scattered gathers (mean distance from the diagonal > 64 KiB of x) on a
+    // matrix large enough to fill the GPU with 1024-thread CTAs
+    return m.nnz >= (int64_t(1) << 20) && m.gather_spread * m.vbytes() > 65536.0;
+}
+
+template <class V, int SR>
+void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* mask, V* y,
+                    int64_t force_rows, int64_t tile_cap, int variant) {
+    if (!m.bins->built || m.bins->force_rows != force_rows || m.bins->dtype != m.dtype) {
+        m.bins.reset(new BinLayout());
+        m.bins->force_rows = force_rows;
+        m.bins->dtype = m.dtype;
+        build_layout<V>(ctx, m, *m.bins);
+    }
+    BinLayout& L = *m.bins;
+    plan_tiles(ctx, m, L, tile_cap);
+    if (m.rows == 0) return;
+    if (L.multi) fill_value<V, SR>(ctx, y, m.rows);
+    const size_t smem = sizeof(V) * static_cast<size_t>(L.R);
+    const int nt = 1024;
+    auto launch = [&](auto kern) {
+        ADA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<static_cast<unsigned>(L.ntiles), nt, smem, ctx.stream>>>(
+            m.rows, L.R, L.rbits, L.cw, L.nchunks, L.tiles.as<int64_t>(), L.tile_bin.as<int32_t>(),
+            L.tile_multi.as<int32_t>(), L.chunk_off.as<int64_t>(), L.pk.as<uint32_t>(), L.bv.as<V>(), x,
+            mask, y);
+        ADA_LAUNCHED(ctx);
+    };
+    (void)variant;
+    if (mask) launch(binned_row_kernel<V, SR, true>);
+    else launch(binned_row_kernel<V, SR, false>);
+}
+
+#define ADA_INST(V, SR)                                                                                \
+    template void run_row_binned<V, SR>(Context&, const Matrix&, const V*, const uint32_t*, V*, int64_t, \
+                                        int64_t, int);
+ADA_INST(float, SR_PLUS_TIMES)
+ADA_INST(double, SR_PLUS_TIMES)
+ADA_INST(float, SR_OR_AND)
+ADA_INST(double, SR_OR_AND)
+ADA_INST(float, SR_MIN_PLUS)
+ADA_INST(double, SR_MIN_PLUS)
+#undef ADA_INST
+
+}  // namespace ada

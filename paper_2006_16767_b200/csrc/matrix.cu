@@ -301,6 +301,7 @@ void finish_matrix(Context& ctx, Matrix& m) {
     build_csc<V>(ctx, m);
     build_tiles(ctx, m);
     compute_features(ctx, m);
+    m.gather_spread = matrix_gather_spread(ctx, m);
 }
 
 }  // namespace
@@ -372,6 +373,7 @@ Matrix* matrix_transpose(Context& ctx, const Matrix& src) {
         copy(m->cvals, src.vals, vb * z);
         build_tiles(ctx, *m);
         compute_features(ctx, *m);
+        m->gather_spread = matrix_gather_spread(ctx, *m);
         ctx.sync();
         return m;
     } catch (...) {

@@ -54,7 +54,13 @@ void run_t(Context& ctx, const Matrix& m, Vector& x, int kernel, const adaspmv_c
                 mask = x.mask.as<uint32_t>();
             }
             V* yd = static_cast<V*>(y.dense.ensure(sizeof(V) * rows));
-            if (m.rows > 0)
+            const bool direct = kernel == 0 || kernel == 2;
+            const bool binned = direct && (cfg.row_layout == ADASPMV_ROW_LAYOUT_BINNED ||
+                                           (cfg.row_layout == ADASPMV_ROW_LAYOUT_AUTO && binned_preferred(m)));
+            if (cfg.row_layout < 0 || cfg.row_layout > 2) invalid("unknown row_layout");
+            if (binned)
+                run_row_binned<V, SR>(ctx, m, x.dense.as<V>(), mask, yd, cfg.bin_rows, cfg.bin_tile_nnz, lanes);
+            else if (m.rows > 0)
                 run_row_major<V, SR>(ctx, m, x.dense.as<V>(), mask, kernel == 1 || kernel == 3,
                                      lanes, yd);
             y.has_dense = true;

@@ -316,3 +316,64 @@ def test_matrix_market_and_binary_round_trip(ctx, tmp_path):
     q.write_text("%%MatrixMarket matrix coordinate pattern symmetric\n3 3 3\n2 1\n3 3\n2 1\n")
     s = A.load_matrix(q, ctx=ctx).download()
     assert s[0].tolist() == [0, 1, 2, 3] and s[1].tolist() == [1, 0, 2] and s[2].tolist() == [2.0, 2.0, 1.0]
+
+
+# ---- row-bin execution of K0/K2 (kernels_binned.cu) ----------------------------
+# Overrides exercise many bins (bin_rows), bins split into several tiles whose
+# partial y segments are combined with atomics (bin_tile_nnz), and empty bins.
+BIN_CFGS = [dict(), dict(bin_rows=7), dict(bin_rows=64, bin_tile_nnz=5), dict(bin_tile_nnz=1000)]
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
+@pytest.mark.parametrize("name,case", CASES, ids=[c[0] for c in CASES])
+def test_binned_row_layout_vs_oracle(ctx, port, name, case, dt):
+    rows, cols, ro, ci, vals = case
+    vals = np.asarray(vals, dt)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    for nx in sorted({0, 1, max(1, cols // 3), cols}):
+        xi, xv = synth.sparse_vector(cols, nx, seed=nx + 5, dtype=dt)
+        xd = port.sparse_to_dense(cols, xi, xv)
+        y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, xd)
+        for cfg in BIN_CFGS:
+            for k in (0, 2):
+                out = A.run_kernel(m, k, A.DenseVector(xd), A.KernelConfig(row_layout=2, **cfg))
+                what = f"binned {name} k={k} nnz_x={nx} {cfg} {np.dtype(dt).name}"
+                assert_dense_close(out.dense().values, y_ref, bound, dt, what)
+                s = out.sparse()
+                assert_sparse_match(s.indices, s.values, y_ref, bound, dt, what)
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
+def test_binned_multi_chunk_and_semirings(ctx, port, dt):
+    # > 2^17 (f32) / 2^18 (f64) columns: entries of a bin span several column
+    # chunks.  PLUS_TIMES against the oracle; OR_AND / MIN_PLUS are order-free
+    # and must equal the CSR execution bit for bit.
+    rows, cols, ro, ci, vals = synth.random_csr(3000, 600_000, 0.0001, seed=21, dtype=dt)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    for nx in (1, 3000, cols // 2, cols):
+        xi, xv = synth.sparse_vector(cols, nx, seed=nx, dtype=dt)
+        xd = port.sparse_to_dense(cols, xi, xv)
+        y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, xd)
+        for cfg in BIN_CFGS:
+            for k in (0, 2):
+                c2 = A.KernelConfig(row_layout=2, **cfg)
+                out = A.run_kernel(m, k, A.DenseVector(xd), c2)
+                assert_dense_close(out.dense().values, y_ref, bound, dt, f"multichunk k={k} {cfg}")
+                for sr in (A.OR_AND, A.MIN_PLUS):
+                    xs = A.SparseVector(cols, xi, xv)
+                    b = A.run_kernel(m, k, xs, A.KernelConfig(semiring=sr, row_layout=2, **cfg))
+                    c = A.run_kernel(m, k, xs, A.KernelConfig(semiring=sr, row_layout=1))
+                    assert b.dense().values.tobytes() == c.dense().values.tobytes(), (sr, k, cfg)
+
+
+def test_binned_auto_layout_large_uniform(ctx, port):
+    # auto picks the row bins for a scattered matrix (mean gather distance
+    # >> 64 KiB of x) with >= 2^20 nonzeros; results match the oracle
+    rows, cols, ro, ci, vals = synth.random_csr(300_000, 300_000, 12 / 300_000, seed=5, dtype=np.float32)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    assert m.gather_spread() * 4 > 65536
+    xd = np.random.default_rng(1).uniform(-1, 1, cols).astype(np.float32)
+    y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, xd)
+    for layout in (0, 1, 2):
+        out = A.run_kernel(m, 0, A.DenseVector(xd), A.KernelConfig(row_layout=layout))
+        assert_dense_close(out.dense().values, y_ref, bound, np.float32, f"layout={layout}")

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--lanes", default="0")
     ap.add_argument("--densities", default="1.0")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--layouts", default="0", help="row_layout values for K0/K2 (0 auto, 1 csr, 2 bins)")
     a = ap.parse_args()
     ctx = A.Context(0)
     ctx.set_timing(True)
@@ -51,11 +52,16 @@ def main():
                 x.set_sparse(xi, xv)
             V = vals.dtype.itemsize
             b_spmv = (rows + 1) * 8 + ro[-1] * (4 + V) + cols * V + rows * V
+            yfirst = None
             for k in [int(s) for s in a.kernels.split(",")]:
-                for lanes in [int(s) for s in a.lanes.split(",")]:
+                for lanes, lay in [(int(s), int(l)) for s in a.lanes.split(",") for l in a.layouts.split(",")]:
                     x.prepare(k)
-                    cfg = A.KernelConfig(lanes_per_row=lanes)
+                    cfg = A.KernelConfig(lanes_per_row=lanes, row_layout=lay)
                     A.run_kernel(m, k, x, cfg, out=out)
+                    y = out.dense().values.astype(np.float64)
+                    if yfirst is None:
+                        yfirst = y
+                    dev = float(np.max(np.abs(y - yfirst)) / max(np.max(np.abs(yfirst)), 1e-300))
                     ts = []
                     for _ in range(a.reps):
                         with torch.cuda.stream(stream):
@@ -64,7 +70,8 @@ def main():
                         A.run_kernel(m, k, x, cfg, out=out)
                         ts.append(out.elapsed())
                     t = float(np.median(ts))
-                    print(f"{name:7s} x={dens:<8g} k={k} lanes={lanes:2d}  {t * 1e6:9.2f} us  "
+                    print(f"{name:7s} x={dens:<8g} k={k} lanes={lanes:2d} layout={lay} {t * 1e6:9.2f} us  "
+                          f"maxdev={dev:.1e} "
                           f"B_spmv/t={b_spmv / t / 1e9:8.1f} GB/s ({100 * b_spmv / t / hbm:5.1f}% of HBM)",
                           flush=True)
 
