@@ -284,6 +284,18 @@ int adaspmv_bfs(adaspmv_ctx* ctx, const adaspmv_matrix* m, int64_t source, int s
                 const adaspmv_bundle* b, int forced_kernel, int64_t* levels, int64_t* n_levels,
                 adaspmv_iteration_report* reports, int64_t max_reports);
 
+/* Incremental (delta-propagation) PageRank: P = A with
+ * column j scaled by 1/deg_col(j) (pattern; dangling columns propagate
+ * nothing), built once per call on the device.  rank = 0,
+ * delta = 1/n; repeat { rank += delta; delta = {d*(P delta)_i : |.| >= prune,
+ * != 0} } until delta is empty or `max_iters` multiplies were done.  Kernel
+ * per iteration: `bundle`, else `forced_kernel` (0..7), else (-1) the
+ * built-in bytes model.  rank[n] (host, may be NULL) gets the ranks widened
+ * to double; reports as adaspmv_bfs. */
+int adaspmv_pagerank(adaspmv_ctx* ctx, const adaspmv_matrix* m, double damping, double prune,
+                     int64_t max_iters, const adaspmv_bundle* b, int forced_kernel, double* rank,
+                     int64_t* n_iters, adaspmv_iteration_report* reports, int64_t max_reports);
+
 #ifdef __cplusplus
 }
 #endif

@@ -402,4 +402,17 @@ inline std::vector<index_t> bfs(const DualMatrix& m, index_t source, int semirin
     return levels;
 }
 
+// ---- incremental PageRank -------------------------------------------------
+inline std::vector<double> pagerank_incremental(const DualMatrix& m, double damping = 0.85,
+                                                double prune = 1e-6, int64_t max_iters = 300,
+                                                const SelectorBundle* b = nullptr, int forced_kernel = -1,
+                                                int64_t* n_iters = nullptr) {
+    std::vector<double> rank(static_cast<size_t>(m.rows()));
+    int64_t it = 0;
+    check(adaspmv_pagerank(m.context().get(), m.get(), damping, prune, max_iters, b ? b->get() : nullptr,
+                           forced_kernel, rank.data(), &it, nullptr, 0));
+    if (n_iters) *n_iters = it;
+    return rank;
+}
+
 }  // namespace adaspmv::cuda

@@ -170,6 +170,52 @@ int64_t or_bfs_queue(int64_t n, const int64_t* co, const int64_t* ri, int64_t so
     return nlev;
 }
 
+/* SPEC.md:498-506 incremental PageRank (delta propagation with pruning),
+ * pinned only by SPEC's examples and by dense power iteration (tests).
+ * P = A with column j scaled by 1/deg_col(j) (pattern; SPEC.md:543 dangling
+ * columns propagate nothing); multiply with A as stored.
+ * rank = 0, delta = 1/n; while delta != {} and it < max_iters:
+ *   rank += delta; y = P delta; delta = {d*y_i : |d*y_i| >= prune, != 0}.
+ * Products are formed as (1/deg_j) * delta_j, like a multiply by P's values.
+ * Returns the number of multiplies. */
+int64_t or_pagerank_incremental(int64_t n, const int64_t* co, const int64_t* ri, double damping,
+                                double prune, int64_t max_iters, double* rank) {
+    double* dv = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double* y = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    int64_t* di = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    int64_t nd = n, it = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        rank[i] = 0.0;
+        di[i] = i;
+        dv[i] = 1.0 / (double)n;
+    }
+    while (nd > 0 && it < max_iters) {
+        for (int64_t k = 0; k < nd; ++k) rank[di[k]] += dv[k];
+        for (int64_t i = 0; i < n; ++i) y[i] = 0.0;
+        for (int64_t k = 0; k < nd; ++k) {
+            const int64_t j = di[k];
+            const int64_t deg = co[j + 1] - co[j];
+            if (deg == 0) continue;
+            const double w = 1.0 / (double)deg;
+            for (int64_t e = co[j]; e < co[j + 1]; ++e) y[ri[e]] += w * dv[k];
+        }
+        nd = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            const double v = damping * y[i];
+            if (v != 0.0 && fabs(v) >= prune) {
+                di[nd] = i;
+                dv[nd] = v;
+                ++nd;
+            }
+        }
+        ++it;
+    }
+    free(dv);
+    free(y);
+    free(di);
+    return it;
+}
+
 void or_vector_features_sparse(int64_t n, int64_t nnz, const int64_t* co, int64_t nnz_x,
                                const int64_t* xi, double* out4) {
     int64_t ns = or_effective_nnz(co, nnz_x, xi);

@@ -66,6 +66,9 @@ int or_tree_predict(const int32_t* feature, const double* threshold, const int32
 /* Queue BFS over the pattern of A (edge r->c for every stored (r,c) read as
  * y = A x: vertex r is reached from frontier vertex c).  levels[i] = -1
  * when unreached.  Returns the number of levels (iterations). */
+/* SPEC.md:498-506 incremental PageRank (see adaspmv_oracle.c); rank[n]. */
+int64_t or_pagerank_incremental(int64_t n, const int64_t* co, const int64_t* ri, double damping,
+                                double prune, int64_t max_iters, double* rank);
 int64_t or_bfs_queue(int64_t n, const int64_t* col_offsets, const int64_t* row_indices,
                      int64_t source, int64_t* levels);
 

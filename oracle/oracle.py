@@ -82,6 +82,9 @@ class Port:
         L.or_tree_predict.argtypes = [_i32p, _f64p, _i32p, _i32p, _i32p, _f64p]
         L.or_bfs_queue.restype = C.c_int64
         L.or_bfs_queue.argtypes = [C.c_int64, _i64p, _i64p, C.c_int64, _i64p]
+        L.or_pagerank_incremental.restype = C.c_int64
+        L.or_pagerank_incremental.argtypes = [C.c_int64, _i64p, _i64p, C.c_double, C.c_double, C.c_int64,
+                                              _f64p]
         L.or_vector_features_sparse.argtypes = [C.c_int64, C.c_int64, _i64p, C.c_int64, _i64p, _f64p]
         for sfx, rp in (("_f64", _f64p), ("_f32", _f32p)):
             nr = _nullable(np.float64 if sfx == "_f64" else np.float32)
@@ -183,6 +186,12 @@ class Port:
         lv = np.zeros(n, np.int64)
         nl = self.lib.or_bfs_queue(n, _as(col_offsets, np.int64), _as(row_indices, np.int64), int(source), lv)
         return lv, int(nl)
+
+    def pagerank_incremental(self, n, col_offsets, row_indices, damping=0.85, prune=1e-6, max_iters=300):
+        rank = np.zeros(n, np.float64)
+        it = self.lib.or_pagerank_incremental(n, _as(col_offsets, np.int64), _as(row_indices, np.int64),
+                                              float(damping), float(prune), int(max_iters), rank)
+        return rank, int(it)
 
     # --- value-typed kernels ---------------------------------------------
     def reference_multiply(self, rows, ro, ci, vals, x):

@@ -172,6 +172,7 @@ def load(path: Optional[os.PathLike] = None):
         "adaspmv_sort_reduce_pairs": [vp, i64, vp, vp, C.c_int, i64, vp, vp, P(i64)],
         "adaspmv_shard_rows": [vp, i64, C.c_int, vp],
         "adaspmv_bfs": [vp, vp, i64, C.c_int, vp, C.c_int, vp, P(i64), vp, i64],
+        "adaspmv_pagerank": [vp, vp, C.c_double, C.c_double, i64, vp, C.c_int, vp, P(i64), vp, i64],
         "adaspmv_execute_iteration": [vp, vp, vp, vp, C.c_int, vp, vp, vp],
     }
     for name, args in sigs.items():
@@ -941,3 +942,25 @@ def bfs(m: DualMatrix, source: int = 0, semiring: int = OR_AND, bundle: Optional
         out.append(dict(iteration=r.iteration, nnz_x=r.nnz_x, kernel=r.kernel, feature_s=r.feature_s,
                         predict_s=r.predict_s, convert_s=r.convert_s, kernel_s=r.kernel_s))
     return levels, out
+
+
+def _reports(reps, n, max_reports):
+    out = []
+    for i in range(min(n, max_reports)):
+        r = reps[i]
+        out.append(dict(iteration=r.iteration, nnz_x=r.nnz_x, kernel=r.kernel, feature_s=r.feature_s,
+                        predict_s=r.predict_s, convert_s=r.convert_s, kernel_s=r.kernel_s))
+    return out
+
+
+def pagerank_incremental(m: DualMatrix, damping: float = 0.85, prune: float = 1e-6, max_iters: int = 300,
+                         bundle: Optional[SelectorBundle] = None, force_kernel: int = -1,
+                         max_reports: int = 4096, download_rank: bool = True):
+    """Incremental delta-propagation PageRank -> (rank float64[n] or None, reports)."""
+    rank = np.empty(m.rows(), np.float64) if download_rank else None
+    nit = C.c_int64()
+    reps = (_IterReport * max_reports)()
+    _check(_lib.adaspmv_pagerank(m.ctx.h, m.h, float(damping), float(prune), int(max_iters),
+                                 bundle.h if bundle else None, int(force_kernel), _ptr(rank), C.byref(nit),
+                                 C.cast(reps, C.c_void_p), max_reports))
+    return rank, _reports(reps, nit.value, max_reports)

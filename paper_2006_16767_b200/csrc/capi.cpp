@@ -934,4 +934,16 @@ int adaspmv_bfs(adaspmv_ctx* ctx, const adaspmv_matrix* m, int64_t source, int s
     });
 }
 
+int adaspmv_pagerank(adaspmv_ctx* ctx, const adaspmv_matrix* m, double damping, double prune,
+                     int64_t max_iters, const adaspmv_bundle* b, int forced_kernel, double* rank,
+                     int64_t* n_iters, adaspmv_iteration_report* reports, int64_t max_reports) {
+    return guarded([&] {
+        bind(ctx);
+        need(m, "matrix");
+        need(n_iters, "n_iters");
+        ada::pagerank(*ctx, *m, damping, prune, max_iters, b, forced_kernel, rank, n_iters, reports,
+                      max_reports);
+    });
+}
+
 }  // extern "C"

@@ -278,4 +278,9 @@ void bfs(Context& ctx, const Matrix& m, int64_t source, int semiring, const Bund
          int forced, int64_t* levels, int64_t* n_levels, adaspmv_iteration_report* reports,
          int64_t max_reports);
 
+// incremental PageRank (pagerank.cu)
+void pagerank(Context& ctx, const Matrix& m, double damping, double prune, int64_t max_iters,
+              const Bundle* b, int forced, double* rank, int64_t* n_iters,
+              adaspmv_iteration_report* reports, int64_t max_reports);
+
 }  // namespace ada

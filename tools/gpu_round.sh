@@ -8,6 +8,6 @@ timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpu
 tail -2 gpurun_out/bench.err
 timeout 900 python tools/bfs_bench.py --scale 22 --reps 3 --out gpurun_out/bfs22.json 2>&1 | tail -13
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"row_direct_kernel" -c 1 -o gpurun_out/prof_c2_spmv python tools/kernel_sweep.py --inputs c2 --kernels 0 --reps 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"binned_row_kernel" -c 1 -o gpurun_out/prof_c2_spmv python tools/kernel_sweep.py --inputs c2 --kernels 0 --reps 1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"col_direct_atomic_kernel" -c 1 -o gpurun_out/prof_c2_colatomic python tools/kernel_sweep.py --inputs c2 --kernels 4 --densities 0.5 --reps 1 > /dev/null 2>&1
 ls -la gpurun_out | tail -12
