@@ -39,7 +39,7 @@ namespace ada {
 
 namespace {
 
-constexpr uint32_t kBinSmemBytes = 114688;  // 112 KiB of y segment per CTA (1 CTA / SM)
+constexpr uint32_t kBinSmemBytes = 229376;  // <= 224 KiB of y segment per CTA (1 CTA / SM)
 
 template <class V>
 struct PkVal {
