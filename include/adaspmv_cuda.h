@@ -93,6 +93,11 @@ typedef struct {
     int32_t row_layout;
     int32_t bin_rows;                    /* rows per bin override (0 = auto) */
     int64_t bin_tile_nnz;                /* entries per bin tile override (0 = auto) */
+    /* CTAs per bin tile: 1 = one CTA owns a bin tile; 2 = a thread-block
+     * cluster pair shares it (twice the rows per bin, the pair's shared-memory
+     * y segments combined over DSMEM); 0 = auto. */
+    int32_t bin_cluster;
+    int32_t reserved;
 } adaspmv_config;
 
 enum { ADASPMV_ROW_LAYOUT_AUTO = 0, ADASPMV_ROW_LAYOUT_CSR = 1, ADASPMV_ROW_LAYOUT_BINNED = 2 };

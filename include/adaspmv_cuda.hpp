@@ -172,6 +172,7 @@ struct KernelConfig {
     int row_layout = ADASPMV_ROW_LAYOUT_AUTO;  // K0/K2 execution (adaspmv_cuda.h)
     int bin_rows = 0;
     long long bin_tile_nnz = 0;
+    int bin_cluster = 0;  // CTAs per bin tile (1 single, 2 cluster pair, 0 auto)
     adaspmv_config c() const {
         adaspmv_config r{};
         r.workers = workers;
@@ -181,6 +182,7 @@ struct KernelConfig {
         r.row_layout = row_layout;
         r.bin_rows = bin_rows;
         r.bin_tile_nnz = bin_tile_nnz;
+        r.bin_cluster = bin_cluster;
         return r;
     }
 };

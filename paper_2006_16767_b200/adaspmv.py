@@ -103,7 +103,7 @@ class _Config(C.Structure):
     _fields_ = [("workers", C.c_int32), ("atomic_private_accumulators", C.c_int32),
                 ("semiring", C.c_int32), ("lanes_per_row", C.c_int32),
                 ("row_layout", C.c_int32), ("bin_rows", C.c_int32),
-                ("bin_tile_nnz", C.c_int64)]
+                ("bin_tile_nnz", C.c_int64), ("bin_cluster", C.c_int32), ("reserved", C.c_int32)]
 
 
 _lib = None
@@ -355,6 +355,7 @@ class KernelConfig:  # kernels.hpp:154-162 (+ device knobs)
     row_layout: int = 0       # K0/K2: 0 auto, 1 CSR gather, 2 row bins
     bin_rows: int = 0         # rows per bin override (0 = auto)
     bin_tile_nnz: int = 0     # entries per bin tile override (0 = auto)
+    bin_cluster: int = 0      # CTAs per bin tile: 1 single, 2 cluster pair, 0 auto
 
     def _c(self) -> _Config:
         c = _Config()
@@ -365,6 +366,7 @@ class KernelConfig:  # kernels.hpp:154-162 (+ device knobs)
         c.row_layout = int(self.row_layout)
         c.bin_rows = int(self.bin_rows)
         c.bin_tile_nnz = int(self.bin_tile_nnz)
+        c.bin_cluster = int(self.bin_cluster)
         return c
 
 

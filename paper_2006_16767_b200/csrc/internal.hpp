@@ -120,12 +120,19 @@ struct BinLayout {
     bool built = false;
     int dtype = -1;
     int64_t force_rows = 0;   // rows-per-bin override it was built with
+    int cluster_req = 0;      // bin_cluster request it was built with
+    int cluster = 1;          // CTAs per bin tile (1, or 2 = cluster pair)
     int64_t R = 0, nbins = 0, nchunks = 0;
     int rbits = 0, cw = 0;
     DevBuf pk, bv, chunk_off;
     std::vector<int64_t> bin_start;  // host: first entry of each bin, [nbins] = nnz
     int64_t tile_cap = -1, ntiles = 0;
     bool multi = false;       // some bin is split into several tiles
+    // heavy rows (degree > heavy_min) are left out of the bins (their entries
+    // would serialise on one shared-memory slot) and run from the CSR as
+    // segments of <= kHeavySeg entries: int64 (row, begin, end) triples
+    int64_t heavy_min = 0, nsegs = 0, n_light = 0;
+    DevBuf segs;
     DevBuf tiles, tile_bin, tile_multi;
 };
 

@@ -26,7 +26,10 @@
 // in column order), so results match within the floating-point tolerance of
 // SURVEY.md 8(c) and are not run-to-run bitwise reproducible, like the
 // atomic column kernels.  OR_AND and MIN_PLUS are exact.
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <array>
 #include <numeric>
 #include <vector>
 
@@ -40,6 +43,7 @@ namespace ada {
 namespace {
 
 constexpr uint32_t kBinSmemBytes = 229376;  // <= 224 KiB of y segment per CTA (1 CTA / SM)
+constexpr int kBinClusterAuto = 1;          // bin_cluster = 0 resolves to this
 
 template <class V>
 struct PkVal {
@@ -49,10 +53,13 @@ struct PkVal {
 
 // One warp per column of the CSC: key = bin of the row, payload = packed
 // entry; counts per (bin, chunk) for the chunk offsets.
+// Entries of heavy rows (degree > heavy_min) get the sentinel key nbins and
+// are not counted: they sort behind every bin and are never streamed.
 template <class V>
 __global__ void bin_expand_kernel(const int64_t* __restrict__ co, const int32_t* __restrict__ ri,
                                   const V* __restrict__ cv, int64_t cols, int64_t R, int rbits,
-                                  int cw, int64_t nchunks, uint32_t* __restrict__ keys,
+                                  int cw, int64_t nchunks, const int64_t* __restrict__ ro,
+                                  int64_t heavy_min, int64_t nbins, uint32_t* __restrict__ keys,
                                   PkVal<V>* __restrict__ pay,
                                   unsigned long long* __restrict__ counts) {
     const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
@@ -66,6 +73,11 @@ __global__ void bin_expand_kernel(const int64_t* __restrict__ co, const int32_t*
         int run = 0;
         for (int64_t k = b + lane; k < e; k += 32) {
             const int64_t row = ri[k];
+            if (heavy_min > 0 && __ldg(ro + row + 1) - __ldg(ro + row) > heavy_min) {
+                keys[k] = static_cast<uint32_t>(nbins);
+                pay[k] = PkVal<V>{0u, V(0)};
+                continue;
+            }
             const int64_t bin = row / R;
             keys[k] = static_cast<uint32_t>(bin);
             const uint32_t rl = static_cast<uint32_t>(row - bin * R);
@@ -123,7 +135,16 @@ __global__ void gather_spread_kernel(const int64_t* __restrict__ ro, const int32
 // ---------------------------------------------------------------------------
 // 1024 threads x 8 entries in flight per thread: measured best on C2 (B200):
 // 1024x8 170 us, 1024x6 174, 1024x4 197, 512x16 217, 512x12 227, 256x32 363.
-template <class V, int SR, bool MASKED, int kBinUnroll = 8, bool NOALLOC = false, int kBinThreads = 1024>
+//
+// CL = 2: the tiles come in pairs (2p, 2p+1) covering the two halves of one
+// bin tile; the pair is a thread-block cluster, each CTA accumulates its
+// half into its own shared-memory y segment, and after a cluster barrier CTA
+// r combines rows [r*nr/2, (r+1)*nr/2) of both segments (the peer's over
+// DSMEM) and writes them.  Bins twice as tall halve the number of times x is
+// streamed through L2 and double the entries per x line (fewer L1
+// wavefronts per gather instruction).
+template <class V, int SR, bool MASKED, int CL = 1, int kBinUnroll = 8, bool NOALLOC = false,
+          int kBinThreads = 1024>
 __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
     int64_t rows, int64_t R, int rbits, int cw, int64_t nchunks,
     const int64_t* __restrict__ tiles, const int32_t* __restrict__ tile_bin,
@@ -203,15 +224,115 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
             }
         }
     }
-    __syncthreads();
+    int lo = 0, hi = nr;
+    const V* peer = nullptr;
+    if constexpr (CL == 2) {
+        namespace cg = cooperative_groups;
+        cg::cluster_group cl = cg::this_cluster();
+        cl.sync();  // both halves accumulated
+        const unsigned rank = cl.block_rank();
+        peer = cl.map_shared_rank(ys, rank ^ 1u);
+        const int half = (nr + 1) >> 1;
+        lo = rank ? half : 0;
+        hi = rank ? nr : half;
+    } else {
+        __syncthreads();
+    }
     if (!tile_multi[t]) {  // the tile owns its bin's rows: plain coalesced stores
-        for (int i = threadIdx.x; i < nr; i += kBinThreads) y[r0 + i] = ys[i];
+        for (int i = lo + static_cast<int>(threadIdx.x); i < hi; i += kBinThreads)
+            y[r0 + i] = CL == 2 ? S::add(ys[i], peer[i]) : ys[i];
     } else {               // partial segment: combine into the identity-filled y
-        for (int i = threadIdx.x; i < nr; i += kBinThreads) {
-            const V v = ys[i];
+        for (int i = lo + static_cast<int>(threadIdx.x); i < hi; i += kBinThreads) {
+            const V v = CL == 2 ? S::add(ys[i], peer[i]) : ys[i];
             if (v != S::zero()) AtomicCombine<SR>::apply(y + r0 + i, v);
         }
     }
+    if constexpr (CL == 2) cooperative_groups::this_cluster().sync();  // peer reads done before exit
+}
+
+constexpr int64_t kHeavySeg = 8192;  // entries per heavy-row segment (one CTA)
+
+__global__ void heavy_rows_kernel(const int64_t* __restrict__ ro, int64_t rows, int64_t heavy_min,
+                                  int64_t* __restrict__ list, unsigned long long* __restrict__ count) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < rows; r += stride) {
+        const int64_t b = ro[r], e = ro[r + 1];
+        if (e - b > heavy_min) {
+            const unsigned long long i = atomicAdd(count, 1ull);
+            list[3 * i] = r;
+            list[3 * i + 1] = b;
+            list[3 * i + 2] = e;
+        }
+    }
+}
+
+// One CTA per heavy-row segment: strided (coalesced) pass over its CSR
+// entries, CTA reduction, one atomic combine into y[row] (which the binned
+// kernel left at the identity).
+template <class V, int SR, bool MASKED>
+__global__ void __launch_bounds__(256) heavy_seg_kernel(const int64_t* __restrict__ segs,
+                                                        const int32_t* __restrict__ ci,
+                                                        const V* __restrict__ vals,
+                                                        const V* __restrict__ x,
+                                                        const uint32_t* __restrict__ mask,
+                                                        V* __restrict__ y) {
+    using S = Semiring<SR, V>;
+    __shared__ V red[8];
+    const int64_t row = segs[3 * blockIdx.x], b = segs[3 * blockIdx.x + 1], e = segs[3 * blockIdx.x + 2];
+    V acc = S::zero();
+    for (int64_t k = b + threadIdx.x; k < e; k += 256) {
+        const int c = __ldg(ci + k);
+        if (MASKED && !((__ldg(mask + (c >> 5)) >> (c & 31)) & 1u)) continue;
+        acc = S::fma(S::kUsesValues ? __ldg(vals + k) : V(1), __ldg(x + c), acc);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc = S::add(acc, __shfl_xor_sync(kFull, acc, d));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        V t = red[0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) t = S::add(t, red[w]);
+        if (t != S::zero()) AtomicCombine<SR>::apply(y + row, t);
+    }
+}
+
+// Heavy rows of the matrix as (row, begin, end) segments of <= kHeavySeg
+// entries, sorted by row (device list; the count crosses to the host once).
+void plan_heavy(Context& ctx, const Matrix& m, BinLayout& L) {
+    L.nsegs = 0;
+    if (L.heavy_min <= 0 || m.rows == 0) return;
+    DevBuf list, cnt;
+    unsigned long long* dcount = static_cast<unsigned long long*>(cnt.ensure(sizeof(unsigned long long)));
+    ADA_CUDA(cudaMemsetAsync(dcount, 0, sizeof(unsigned long long), ctx.stream));
+    const int64_t cap = std::max<int64_t>(m.nnz / (L.heavy_min + 1) + 1, 1);
+    list.ensure(sizeof(int64_t) * 3 * static_cast<size_t>(cap));
+    const int64_t g = std::min<int64_t>((m.rows + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 16);
+    heavy_rows_kernel<<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(m.row_off.as<int64_t>(), m.rows,
+                                                                         L.heavy_min, list.as<int64_t>(), dcount);
+    ADA_LAUNCHED(ctx);
+    unsigned long long n = 0;
+    ADA_CUDA(cudaMemcpyAsync(&n, dcount, sizeof(n), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    if (n == 0) return;
+    std::vector<int64_t> h(3 * static_cast<size_t>(n));
+    ADA_CUDA(cudaMemcpyAsync(h.data(), list.p, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    std::vector<std::array<int64_t, 3>> rs(static_cast<size_t>(n));
+    for (size_t i = 0; i < rs.size(); ++i) rs[i] = {h[3 * i], h[3 * i + 1], h[3 * i + 2]};
+    std::sort(rs.begin(), rs.end());
+    std::vector<int64_t> segs;
+    for (const auto& r : rs)
+        for (int64_t b = r[1]; b < r[2]; b += kHeavySeg) {
+            segs.push_back(r[0]);
+            segs.push_back(b);
+            segs.push_back(std::min(b + kHeavySeg, r[2]));
+        }
+    L.nsegs = static_cast<int64_t>(segs.size() / 3);
+    L.segs.ensure(sizeof(int64_t) * segs.size());
+    ADA_CUDA(cudaMemcpyAsync(L.segs.p, segs.data(), sizeof(int64_t) * segs.size(), cudaMemcpyHostToDevice,
+                             ctx.stream));
+    ctx.sync();
 }
 
 template <class V>
@@ -221,12 +342,20 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
     int rbits = 0;
     while ((int64_t(1) << rbits) < rmax) ++rbits;
     int64_t nbins;
+    L.cluster = 1;
     if (L.force_rows > 0) {
         nbins = (m.rows + L.force_rows - 1) / L.force_rows;
+        L.cluster = L.cluster_req == 2 ? 2 : 1;
     } else {
         nbins = (m.rows + rmax - 1) / rmax;
         // at least one bin per SM when rows allow bins of >= 1024 rows
         nbins = std::max<int64_t>(nbins, std::min<int64_t>(ctx.sm_count, (m.rows + 1023) / 1024));
+        // cluster pairs: one bin per SM pair, twice as tall, when it still fits
+        const int64_t r1 = (m.rows + nbins - 1) / nbins;
+        if (L.cluster_req == 2 && nbins >= 2 && 2 * r1 <= rmax) {
+            nbins = (nbins + 1) / 2;
+            L.cluster = 2;
+        }
     }
     nbins = std::max<int64_t>(nbins, 1);
     const int64_t R = std::max<int64_t>((m.rows + nbins - 1) / nbins, 1);
@@ -240,6 +369,13 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
     L.cw = cw;
     L.nbins = nbins;
     L.nchunks = nchunks;
+    // heavy rows: a row whose entries would put several lanes of one warp
+    // instruction on the same shared-memory slot (degree well above the
+    // column-sorted window a warp covers) runs from the CSR instead
+    const int64_t per_bin = m.nnz / nbins + 1;
+    L.heavy_min = m.feat[3] > static_cast<double>(kHeavySeg / 2)
+                      ? std::max<int64_t>(kHeavySeg / 2, per_bin / 512) : 0;
+    plan_heavy(ctx, m, L);
     const int64_t nnz = m.nnz;
     const size_t z = static_cast<size_t>(std::max<int64_t>(nnz, 1));
     L.pk.ensure(sizeof(uint32_t) * z);
@@ -259,12 +395,13 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
         bin_expand_kernel<V><<<static_cast<unsigned>(std::max<int64_t>((warps * 32 + 255) / 256, 1)), 256, 0,
                                ctx.stream>>>(m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(),
                                              m.cvals.as<V>(), m.cols, R, rbits, cw, nchunks,
+                                             m.row_off.as<int64_t>(), L.nsegs ? L.heavy_min : 0, nbins,
                                              k0.as<uint32_t>(), p0.as<PkVal<V>>(),
                                              counts.as<unsigned long long>());
         ADA_LAUNCHED(ctx);
         const int which = radix_sort_pairs<PkVal<V>>(ctx, k0.as<uint32_t>(), p0.as<PkVal<V>>(),
                                                      k1.as<uint32_t>(), p1.as<PkVal<V>>(), nnz,
-                                                     bits_for(nbins), cnt, ctx.scratch[5]);
+                                                     bits_for(nbins + 1), cnt, ctx.scratch[5]);
         const PkVal<V>* sorted = which ? p1.as<PkVal<V>>() : p0.as<PkVal<V>>();
         const int64_t g = std::min<int64_t>((nnz + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 32);
         bin_unpack_kernel<V><<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(sorted, nnz, L.pk.as<uint32_t>(),
@@ -295,17 +432,35 @@ void plan_tiles(Context& ctx, const Matrix& m, BinLayout& L, int64_t cap_req) {
         cap = std::max<int64_t>(static_cast<int64_t>(fair * 1.25), 16384);
     }
     if (L.tile_cap == cap) return;
+    // a work unit is one CTA (cluster 1) or a CTA pair (cluster 2) of `cap`
+    // entries per CTA; units of a bin are equal column-contiguous splits
     struct T { int64_t e0, e1; int32_t bin, multi; };
     std::vector<T> ts;
     bool multi = false;
+    const int cl = L.cluster;
     for (int64_t b = 0; b < L.nbins; ++b) {
         const int64_t s = L.bin_start[static_cast<size_t>(b)], e = L.bin_start[static_cast<size_t>(b + 1)];
-        const int64_t k = std::max<int64_t>((e - s + cap - 1) / cap, 1);
-        for (int64_t i = 0; i < k; ++i)
-            ts.push_back(T{s + (e - s) * i / k, s + (e - s) * (i + 1) / k, static_cast<int32_t>(b), k > 1});
+        const int64_t k = std::max<int64_t>((e - s + cl * cap - 1) / (cl * cap), 1);
+        for (int64_t i = 0; i < k * cl; ++i)
+            ts.push_back(T{s + (e - s) * i / (k * cl), s + (e - s) * (i + 1) / (k * cl), static_cast<int32_t>(b), k > 1});
         multi = multi || k > 1;
     }
-    std::stable_sort(ts.begin(), ts.end(), [](const T& a, const T& b) { return a.e1 - a.e0 > b.e1 - b.e0; });
+    if (cl == 1) {
+        std::stable_sort(ts.begin(), ts.end(), [](const T& a, const T& b) { return a.e1 - a.e0 > b.e1 - b.e0; });
+    } else {  // heaviest pair first, pairs kept adjacent (cluster = CTAs 2p, 2p+1)
+        std::vector<size_t> pr(ts.size() / 2);
+        std::iota(pr.begin(), pr.end(), size_t(0));
+        std::stable_sort(pr.begin(), pr.end(), [&](size_t a, size_t b) {
+            return ts[2 * a + 1].e1 - ts[2 * a].e0 > ts[2 * b + 1].e1 - ts[2 * b].e0;
+        });
+        std::vector<T> o;
+        o.reserve(ts.size());
+        for (size_t p : pr) {
+            o.push_back(ts[2 * p]);
+            o.push_back(ts[2 * p + 1]);
+        }
+        ts.swap(o);
+    }
     const size_t nt = ts.size();
     std::vector<int64_t> h_t(2 * nt);
     std::vector<int32_t> h_b(nt), h_m(nt);
@@ -353,10 +508,14 @@ bool binned_preferred(const Matrix& m) {
 
 template <class V, int SR>
 void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* mask, V* y,
-                    int64_t force_rows, int64_t tile_cap, int variant) {
-    if (!m.bins->built || m.bins->force_rows != force_rows || m.bins->dtype != m.dtype) {
+                    int64_t force_rows, int64_t tile_cap, int cluster) {
+    if (cluster < 0 || cluster > 2) invalid("bin_cluster must be 0, 1 or 2");
+    const int creq = cluster == 0 ? kBinClusterAuto : cluster;
+    if (!m.bins->built || m.bins->force_rows != force_rows || m.bins->dtype != m.dtype ||
+        m.bins->cluster_req != creq) {
         m.bins.reset(new BinLayout());
         m.bins->force_rows = force_rows;
+        m.bins->cluster_req = creq;
         m.bins->dtype = m.dtype;
         build_layout<V>(ctx, m, *m.bins);
     }
@@ -366,17 +525,38 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
     if (L.multi) fill_value<V, SR>(ctx, y, m.rows);
     const size_t smem = sizeof(V) * static_cast<size_t>(L.R);
     const int nt = 1024;
-    auto launch = [&](auto kern) {
+    auto launch = [&](auto kern, int cl) {
         ADA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        kern<<<static_cast<unsigned>(L.ntiles), nt, smem, ctx.stream>>>(
-            m.rows, L.R, L.rbits, L.cw, L.nchunks, L.tiles.as<int64_t>(), L.tile_bin.as<int32_t>(),
-            L.tile_multi.as<int32_t>(), L.chunk_off.as<int64_t>(), L.pk.as<uint32_t>(), L.bv.as<V>(), x,
-            mask, y);
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(static_cast<unsigned>(L.ntiles));
+        lc.blockDim = dim3(nt);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = ctx.stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = static_cast<unsigned>(cl);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        ADA_CUDA(cudaLaunchKernelEx(&lc, kern, m.rows, L.R, L.rbits, L.cw, L.nchunks, L.tiles.as<int64_t>(),
+                                    L.tile_bin.as<int32_t>(), L.tile_multi.as<int32_t>(),
+                                    L.chunk_off.as<int64_t>(), L.pk.as<uint32_t>(), L.bv.as<V>(), x, mask, y));
         ADA_LAUNCHED(ctx);
     };
-    (void)variant;
-    if (mask) launch(binned_row_kernel<V, SR, true>);
-    else launch(binned_row_kernel<V, SR, false>);
+    if (L.cluster == 2) {
+        if (mask) launch(binned_row_kernel<V, SR, true, 2>, 2);
+        else launch(binned_row_kernel<V, SR, false, 2>, 2);
+    } else {
+        if (mask) launch(binned_row_kernel<V, SR, true, 1>, 1);
+        else launch(binned_row_kernel<V, SR, false, 1>, 1);
+    }
+    if (L.nsegs > 0) {  // heavy rows, after the bins wrote their identity
+        auto hk = mask ? heavy_seg_kernel<V, SR, true> : heavy_seg_kernel<V, SR, false>;
+        hk<<<static_cast<unsigned>(L.nsegs), 256, 0, ctx.stream>>>(L.segs.as<int64_t>(), m.col_idx.as<int32_t>(),
+                                                                  m.vals.as<V>(), x, mask, y);
+        ADA_LAUNCHED(ctx);
+    }
 }
 
 #define ADA_INST(V, SR)                                                                                \

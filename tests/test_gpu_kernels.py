@@ -321,7 +321,9 @@ def test_matrix_market_and_binary_round_trip(ctx, tmp_path):
 # ---- row-bin execution of K0/K2 (kernels_binned.cu) ----------------------------
 # Overrides exercise many bins (bin_rows), bins split into several tiles whose
 # partial y segments are combined with atomics (bin_tile_nnz), and empty bins.
-BIN_CFGS = [dict(), dict(bin_rows=7), dict(bin_rows=64, bin_tile_nnz=5), dict(bin_tile_nnz=1000)]
+BIN_CFGS = [dict(), dict(bin_rows=7), dict(bin_rows=64, bin_tile_nnz=5), dict(bin_tile_nnz=1000),
+            dict(bin_cluster=2), dict(bin_rows=64, bin_cluster=2), dict(bin_rows=9, bin_tile_nnz=7, bin_cluster=2),
+            dict(bin_cluster=1)]
 
 
 @pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
@@ -377,3 +379,32 @@ def test_binned_auto_layout_large_uniform(ctx, port):
     for layout in (0, 1, 2):
         out = A.run_kernel(m, 0, A.DenseVector(xd), A.KernelConfig(row_layout=layout))
         assert_dense_close(out.dense().values, y_ref, bound, np.float32, f"layout={layout}")
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
+def test_binned_heavy_rows(ctx, port, dt):
+    # rows far above the bin's warp window (degree > 4096) run from the CSR as
+    # segments; light rows stay in the bins.  Plus-times vs the oracle,
+    # OR_AND / MIN_PLUS bitwise vs the CSR execution, masked K2 included.
+    rng = np.random.default_rng(9)
+    rows, cols = 5000, 60000
+    deg = rng.integers(0, 8, size=rows)
+    deg[[0, 17, 2500, 4999]] = [30000, 9000, 4097, 20000]
+    ro = np.zeros(rows + 1, np.int64)
+    ro[1:] = np.cumsum(deg)
+    ci = np.concatenate([np.sort(rng.choice(cols, size=d, replace=False)) for d in deg]).astype(np.int64)
+    vals = rng.uniform(-1, 1, len(ci)).astype(dt)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    for nx in (1, 700, cols // 2, cols):
+        xi, xv = synth.sparse_vector(cols, nx, seed=nx + 1, dtype=dt)
+        xd = port.sparse_to_dense(cols, xi, xv)
+        y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, xd)
+        for cfg in (dict(), dict(bin_cluster=2), dict(bin_rows=100, bin_tile_nnz=300)):
+            for k in (0, 2):
+                out = A.run_kernel(m, k, A.DenseVector(xd), A.KernelConfig(row_layout=2, **cfg))
+                assert_dense_close(out.dense().values, y_ref, bound, dt, f"heavy k={k} nx={nx} {cfg}")
+                xs = A.SparseVector(cols, xi, xv)
+                for sr in (A.OR_AND, A.MIN_PLUS):
+                    b = A.run_kernel(m, k, xs, A.KernelConfig(semiring=sr, row_layout=2, **cfg))
+                    c = A.run_kernel(m, k, xs, A.KernelConfig(semiring=sr, row_layout=1))
+                    assert b.dense().values.tobytes() == c.dense().values.tobytes(), (sr, k, cfg)

@@ -1,5 +1,5 @@
-"""Device time of binned K0 on C2 vs rows per bin and tile cap (tuning aid).
-  python tools/bin_rows_sweep.py 0:0,57344:0,57344:300000 """
+"""Device time of binned K0 on C2 vs rows per bin, tile cap and CTAs per bin
+tile (tuning aid).   python tools/bin_rows_sweep.py 0:0:1,0:0:2,57344:0:1 """
 import sys
 import numpy as np
 import torch
@@ -17,8 +17,8 @@ stream = torch.cuda.ExternalStream(ctx.stream)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 ref = None
 for spec in (sys.argv[1] if len(sys.argv) > 1 else "0:0").split(","):
-    r, c = (int(v) for v in spec.split(":"))
-    cfg = A.KernelConfig(row_layout=2, bin_rows=r, bin_tile_nnz=c)
+    r, c, cl = (int(v) for v in spec.split(":"))
+    cfg = A.KernelConfig(row_layout=2, bin_rows=r, bin_tile_nnz=c, bin_cluster=cl)
     y = A.run_kernel(m, 0, x, cfg, out=out).dense().values.astype(np.float64)
     ref = y if ref is None else ref
     ts = []
@@ -28,5 +28,5 @@ for spec in (sys.argv[1] if len(sys.argv) > 1 else "0:0").split(","):
             torch.cuda._sleep(400_000)
         A.run_kernel(m, 0, x, cfg, out=out)
         ts.append(out.elapsed())
-    print(f"bin_rows {r:7d} tile_cap {c:8d}: {np.median(ts) * 1e6:7.1f} us  max|dy| {np.abs(y - ref).max():.2e}",
+    print(f"bin_rows {r:7d} tile_cap {c:8d} cluster {cl}: {np.median(ts) * 1e6:7.1f} us  max|dy| {np.abs(y - ref).max():.2e}",
           flush=True)

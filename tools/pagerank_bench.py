@@ -57,8 +57,14 @@ def main():
     for name, b, forced in modes:
         r, reps = A.pagerank_incremental(m, a.damping, a.prune, a.max_iters, bundle=b, force_kernel=forced)
         ok = None
+        diag = {}
         if exp is not None:
-            ok = bool(np.all(np.abs(r - exp) <= rtol * np.abs(exp) + 4 * a.prune))
+            exc = np.abs(r - exp) - (rtol * np.abs(exp) + 4 * a.prune)
+            ok = bool(np.all(exc <= 0))
+            i = int(np.argmax(exc))
+            diag = {"max_excess": float(exc[i]), "at": i, "rank": float(exp[i]), "got": float(r[i]),
+                    "violations": int(np.sum(exc > 0)), "l1_diff": float(np.abs(r - exp).sum()),
+                    "max_rel": float(np.max(np.abs(r - exp) / np.maximum(np.abs(exp), 1e-300)))}
         ts = []
         for _ in range(a.reps):
             ctx.synchronize()
@@ -69,12 +75,13 @@ def main():
         t = float(np.median(ts))
         k_ms = sum(x["kernel_s"] for x in reps) * 1e3
         res["runs"][name] = {"seconds": round(t, 6), "kernel_ms": round(k_ms, 4), "iterations": len(reps),
-                             "ranks_match": ok,
+                             "ranks_match": ok, "diag": diag,
                              "per_iter": [{"nnz_x": x["nnz_x"], "kernel": A.KernelId.from_index(x["kernel"]).name(),
                                            "kernel_ms": round(x["kernel_s"] * 1e3, 4),
                                            "select_ms": round(x["predict_s"] * 1e3, 4),
                                            "convert_ms": round(x["convert_s"] * 1e3, 4)} for x in reps]}
-        print(f"{name:10s} {t * 1e3:9.3f} ms  kernels {k_ms:8.3f} ms  iters {len(reps)}  ranks_ok={ok}", flush=True)
+        print(f"{name:10s} {t * 1e3:9.3f} ms  kernels {k_ms:8.3f} ms  iters {len(reps)}  ranks_ok={ok} {diag}",
+              flush=True)
     fixed = {k: v["seconds"] for k, v in res["runs"].items() if k.startswith("fixed_")}
     best_fixed = min(fixed, key=fixed.get)
     # per-iteration best-of-8 (deltas identical across kernels in f64; in f32
