@@ -77,6 +77,21 @@ def corpus(scale: str):
     return items
 
 
+def biased_vector(col_deg, nnz, seed, dtype):
+    """Support drawn without replacement with probability proportional to the
+    column degree (+1): the shape of BFS frontiers and PageRank deltas on
+    power-law graphs (their nonzeros sit on high-degree vertices), which
+    uniform supports never produce.  Values U[-1,1)."""
+    rng = np.random.default_rng(seed)
+    n = len(col_deg)
+    nnz = min(int(nnz), n)
+    w = col_deg.astype(np.float64) + 1.0
+    # Efraimidis-Spirakis weighted sampling without replacement: top-k of u^(1/w)
+    keys = np.log(rng.random(n)) / w
+    idx = np.sort(np.argpartition(-keys, nnz - 1)[:nnz]).astype(np.int64) if nnz < n else np.arange(n)
+    return idx, rng.uniform(-1.0, 1.0, nnz).astype(dtype)
+
+
 def densities(n, geo=16, uni=8):
     """geometric:k and uniform:k density points (nnz_x)."""
     g = np.unique(np.round(np.geomspace(1, n, geo)).astype(np.int64))
@@ -113,8 +128,16 @@ def main():
             rows, cols, ro, ci, vals = gen()
             m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
             dt = np.dtype(vals.dtype)
-            for k_idx, nx in enumerate(densities(cols)):
-                xi, xv = synth.sparse_vector(cols, nx, seed=1000 + k_idx, dtype=dt)
+            col_deg = np.bincount(ci, minlength=cols)
+            skewed = col_deg.max() > 8 * max(col_deg.mean(), 1.0)
+            pts = [(nx, False) for nx in densities(cols)]
+            if skewed:  # degree-biased supports (BFS / PageRank shapes) on skewed matrices
+                pts += [(nx, True) for nx in densities(cols, geo=10, uni=4) if nx < cols]
+            for k_idx, (nx, biased) in enumerate(pts):
+                if biased:
+                    xi, xv = biased_vector(col_deg, nx, seed=5000 + k_idx, dtype=dt)
+                else:
+                    xi, xv = synth.sparse_vector(cols, nx, seed=1000 + k_idx, dtype=dt)
                 x = A.DeviceVector(cols, dt, ctx)
                 if nx == cols:
                     d = np.zeros(cols, dt)
@@ -135,7 +158,7 @@ def main():
                         A.run_kernel(m, k, x, out=out)
                         rep.append(out.elapsed())
                     ts.append(float(np.median(rep)))
-                w.writerow([name, dt.name, nx] + [repr(float(v)) for v in f] + [repr(t) for t in ts])
+                w.writerow([name + ("/biased" if biased else ""), dt.name, nx] + [repr(float(v)) for v in f] + [repr(t) for t in ts])
                 fh.flush()
             print(f"{name}: {rows}x{cols} nnz={ro[-1]} in {time.time() - t0:.1f}s", flush=True)
             del m
