@@ -150,6 +150,7 @@ void launch_pull_e(Context& ctx, const Matrix& m, const Vector& x, const int32_t
 template <class V, int SR>
 void launch_pull(Context& ctx, const Matrix& m, const Vector& x, const int32_t* lv, Output& y) {
     V* yd = static_cast<V*>(y.dense.ensure(sizeof(V) * static_cast<size_t>(std::max<int64_t>(m.rows, 1))));
+    y.z_n = -1;  // the pull writes only unvisited rows: no sparse-reset record
     const bool early = SR == SR_OR_AND || (SR == SR_MIN_PLUS && m.pattern);
     if (early) launch_pull_e<V, SR, true>(ctx, m, x, lv, yd);
     else launch_pull_e<V, SR, false>(ctx, m, x, lv, yd);

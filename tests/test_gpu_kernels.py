@@ -408,3 +408,30 @@ def test_binned_heavy_rows(ctx, port, dt):
                     b = A.run_kernel(m, k, xs, A.KernelConfig(semiring=sr, row_layout=2, **cfg))
                     c = A.run_kernel(m, k, xs, A.KernelConfig(semiring=sr, row_layout=1))
                     assert b.dense().values.tobytes() == c.dense().values.tobytes(), (sr, k, cfg)
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
+def test_atomic_sparse_reset_reuses_output(ctx, port, dt):
+    # K4/K6 into the same MultiplyOutput re-initialise only the rows the
+    # previous small-support multiply touched; interleave supports, kernels,
+    # semirings and a second matrix and compare every result with the oracle.
+    rows, cols, ro, ci, vals = synth.random_csr(20000, 15000, 0.0004, seed=31, dtype=dt)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    r2, c2, ro2, ci2, v2 = synth.random_csr(20000, 15000, 0.0003, seed=32, dtype=dt)
+    m2 = A.DualMatrix.from_csr(r2, c2, ro2, ci2, v2, ctx=ctx)
+    out = A.MultiplyOutput(ctx)
+    seq = [(m, 4, 3), (m, 4, 5), (m, 6, 2), (m, 4, 0), (m, 6, 40), (m, 0, 15000), (m, 4, 1), (m2, 4, 7),
+           (m, 4, 9), (m, 5, 4), (m, 4, 3), (m, 6, 3000), (m, 4, 2)]
+    for i, (mat, k, nx) in enumerate(seq):
+        rr, cc, roo, cii, vv = (rows, cols, ro, ci, vals) if mat is m else (r2, c2, ro2, ci2, v2)
+        xi, xv = synth.sparse_vector(cc, nx, seed=100 + i, dtype=dt)
+        xd = port.sparse_to_dense(cc, xi, xv)
+        y_ref, bound = ref_and_bound(port, rr, roo, cii, vv, xd)
+        x = A.SparseVector(cc, xi, xv) if k >= 4 else A.DenseVector(xd)
+        y = A.run_kernel(mat, k, x, out=out)
+        assert_dense_close(y.dense().values, y_ref, bound, dt, f"step {i} k={k} nx={nx}")
+    # min-plus after plus-times into the same buffer: identity differs (+inf)
+    xi, xv = synth.sparse_vector(cols, 5, seed=7, dtype=dt)
+    a = A.run_kernel(m, 4, A.SparseVector(cols, xi, xv), A.KernelConfig(semiring=A.MIN_PLUS), out=out)
+    b = A.run_kernel(m, 4, A.SparseVector(cols, xi, xv), A.KernelConfig(semiring=A.MIN_PLUS))
+    assert a.dense().values.tobytes() == b.dense().values.tobytes()
