@@ -444,27 +444,7 @@ int adaspmv_vector_set_sparse(adaspmv_ctx* ctx, adaspmv_vector* v, int64_t nnz,
             need(indices, "indices");
             need(values, "values");
         }
-        // SparseVector::validate (sparse.hpp:120-129), narrowed into pinned staging
-        int32_t* st = static_cast<int32_t*>(ctx->stage(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(nnz, 1))));
-        ctx->sync();  // the stage may still feed a previous async copy
-        for (int64_t k = 0; k < nnz; ++k) {
-            const int64_t i = indices[k];
-            if (i < 0 || i >= v->n) ada::invalid("sparse vector: index out of range");
-            if (k > 0 && i <= indices[k - 1]) ada::invalid("sparse vector: indices not strictly increasing");
-            st[k] = static_cast<int32_t>(i);
-        }
-        v->invalidate();
-        const size_t vb = static_cast<size_t>(ada::value_bytes(v->dtype));
-        v->sp_idx.ensure(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(nnz, 1)));
-        v->sp_val.ensure(vb * static_cast<size_t>(std::max<int64_t>(nnz, 1)));
-        if (nnz > 0) {
-            ADA_CUDA(cudaMemcpyAsync(v->sp_idx.p, st, sizeof(int32_t) * static_cast<size_t>(nnz),
-                                     cudaMemcpyHostToDevice, ctx->stream));
-            ADA_CUDA(cudaMemcpyAsync(v->sp_val.p, values, vb * static_cast<size_t>(nnz),
-                                     cudaMemcpyHostToDevice, ctx->stream));
-        }
-        v->nnz = nnz;
-        v->has_sparse = true;
+        ada::vector_set_sparse_host(*ctx, *v, nnz, indices, values);
     });
 }
 

@@ -245,6 +245,9 @@ Matrix* matrix_transpose(Context& ctx, const Matrix& m);
 void vector_set_dense_device(Context& ctx, Vector& v, const void* d_vals);
 void vector_set_sparse_device(Context& ctx, Vector& v, int64_t nnz, const int32_t* d_idx,
                               const void* d_vals);
+// host int64 indices (the reference's index_t) + values: H2D, then validated
+// and narrowed on the device (one synchronisation for the verdict)
+void vector_set_sparse_host(Context& ctx, Vector& v, int64_t nnz, const int64_t* h_idx, const void* h_vals);
 // dense view; entries absent from a sparse input hold the identity of
 // `semiring` (0 for plus-times / or-and, +inf for min-plus)
 void vector_ensure_dense(Context& ctx, Vector& v, int semiring = ADASPMV_PLUS_TIMES);

@@ -105,13 +105,13 @@ int64_t next_delta(Context& ctx, Output& y, Vector& x, V* rank, V d, V prune) { 
     if (y.has_sparse) {
         const int64_t nnz = output_nnz(ctx, y);
         scan3(ctx, nnz, SparseDeltaIn<V>{y.sp_val.as<V>(), d, prune},
-              DeltaEpi<V>{y.sp_idx.as<int32_t>(), y.sp_val.as<V>(), d, rank, xi, xv}, ctx.dscal(3),
+              DeltaEpi<V>{y.sp_idx.as<int32_t>(), y.sp_val.as<V>(), d, rank, xi, xv}, ctx.dscal(5),
               ctx.scratch[4]);
     } else {
         scan3(ctx, y.n, DenseDeltaIn<V>{y.dense.as<V>(), d, prune},
-              DeltaEpi<V>{nullptr, y.dense.as<V>(), d, rank, xi, xv}, ctx.dscal(3), ctx.scratch[4]);
+              DeltaEpi<V>{nullptr, y.dense.as<V>(), d, rank, xi, xv}, ctx.dscal(5), ctx.scratch[4]);
     }
-    x.nnz = ctx.fetch_scalar(ctx.dscal(3));
+    x.nnz = ctx.fetch_scalar(ctx.dscal(5));
     x.has_sparse = true;
     return x.nnz;
 }

@@ -123,6 +123,53 @@ void vector_set_dense_device(Context& ctx, Vector& v, const void* d_vals) {
     v.has_dense = true;
 }
 
+// SparseVector::validate (sparse.hpp:120-129) on the device while narrowing
+// the caller's int64 indices: err = min over violations of (k << 1 | kind),
+// kind 0 = index out of range, 1 = not strictly increasing (the reference's
+// first failing position wins, range before order at the same position).
+__global__ void narrow_validate_kernel(int64_t nnz, int64_t n, const int64_t* __restrict__ in,
+                                       int32_t* __restrict__ out, unsigned long long* __restrict__ err) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz; k += stride) {
+        const int64_t i = in[k];
+        unsigned long long e = ~0ull;
+        if (i < 0 || i >= n) e = static_cast<unsigned long long>(k) << 1;
+        else if (k > 0 && i <= in[k - 1]) e = (static_cast<unsigned long long>(k) << 1) | 1ull;
+        if (e != ~0ull) atomicMin(err, e);
+        out[k] = static_cast<int32_t>(i);
+    }
+}
+
+void vector_set_sparse_host(Context& ctx, Vector& v, int64_t nnz, const int64_t* h_idx, const void* h_vals) {
+    if (nnz < 0) invalid("sparse vector: negative nnz");
+    v.invalidate();
+    const size_t vb = static_cast<size_t>(value_bytes(v.dtype));
+    const size_t z = static_cast<size_t>(std::max<int64_t>(nnz, 1));
+    v.sp_idx.ensure(sizeof(int32_t) * z);
+    v.sp_val.ensure(vb * z);
+    if (nnz > 0) {
+        int64_t* st = static_cast<int64_t*>(v.stage_idx.ensure(sizeof(int64_t) * z));
+        unsigned long long* err = reinterpret_cast<unsigned long long*>(ctx.dscal(6));
+        ADA_CUDA(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx.stream));
+        ADA_CUDA(cudaMemcpyAsync(st, h_idx, sizeof(int64_t) * static_cast<size_t>(nnz), cudaMemcpyHostToDevice,
+                                 ctx.stream));
+        ADA_CUDA(cudaMemcpyAsync(v.sp_val.p, h_vals, vb * static_cast<size_t>(nnz), cudaMemcpyHostToDevice,
+                                 ctx.stream));
+        const int64_t g = std::min<int64_t>((nnz + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 16);
+        narrow_validate_kernel<<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(nnz, v.n, st,
+                                                                                v.sp_idx.as<int32_t>(), err);
+        ADA_LAUNCHED(ctx);
+        const unsigned long long e = static_cast<unsigned long long>(ctx.fetch_scalar(ctx.dscal(6)));
+        if (e != ~0ull) {
+            v.invalidate();
+            if (e & 1ull) invalid("sparse vector: indices not strictly increasing");
+            invalid("sparse vector: index out of range");
+        }
+    }
+    v.nnz = nnz;
+    v.has_sparse = true;
+}
+
 void vector_set_sparse_device(Context& ctx, Vector& v, int64_t nnz, const int32_t* d_idx,
                               const void* d_vals) {
     if (nnz < 0 || nnz > v.n) invalid("sparse vector: nnz out of range");
