@@ -33,12 +33,20 @@ __global__ void widen_levels_kernel(const int32_t* __restrict__ lv, int64_t n, i
     if (i < n) out[i] = lv[i];
 }
 
+// The frontier update is one scan whose items pack (kept ? 1 : 0) << kCntShift
+// | deg_col(row): the prefix gives each kept row its frontier slot AND its
+// effective-nnz offset (kernels.hpp:400-404's eff_offsets of the next x), and
+// the total gives nnz_x and nnz_s in one device-to-host read.
+constexpr int kCntShift = 36;  // fused packing: nnz_s < 2^36 and frontier < 2^27
+
 template <class V, int SR>
 struct DenseFrontierIn {
     const V* y;
     const int32_t* lv;
+    const int64_t* co;  // null: plain 0/1 items (no packing)
     __device__ int64_t operator()(int64_t i) const {
-        return (y[i] != Semiring<SR, V>::zero() && lv[i] < 0) ? 1 : 0;
+        if (!(y[i] != Semiring<SR, V>::zero() && lv[i] < 0)) return 0;
+        return co ? (int64_t(1) << kCntShift) | (co[i + 1] - co[i]) : 1;
     }
 };
 
@@ -47,8 +55,11 @@ struct SparseFrontierIn {
     const int32_t* yi;
     const V* yv;
     const int32_t* lv;
+    const int64_t* co;
     __device__ int64_t operator()(int64_t k) const {
-        return (yv[k] != Semiring<SR, V>::zero() && lv[yi[k]] < 0) ? 1 : 0;
+        const int32_t r = yi[k];
+        if (!(yv[k] != Semiring<SR, V>::zero() && lv[r] < 0)) return 0;
+        return co ? (int64_t(1) << kCntShift) | (co[r + 1] - co[r]) : 1;
     }
 };
 
@@ -58,34 +69,53 @@ struct FrontierEpi {
     int32_t* lv;
     int32_t* xi;
     V* xv;
+    int64_t* eff;       // null: no effective-nnz offsets
     int32_t level;
     V value;
     __device__ void operator()(int64_t i, int64_t p, int64_t v) const {
         if (!v) return;
         const int32_t row = yi ? yi[i] : static_cast<int32_t>(i);
+        const int64_t slot = eff ? p >> kCntShift : p;
         lv[row] = level;
-        xi[p] = row;
-        xv[p] = value;
+        xi[slot] = row;
+        xv[slot] = value;
+        if (eff) eff[slot] = p & ((int64_t(1) << kCntShift) - 1);
     }
 };
 
+__global__ void set_i64_kernel(int64_t* p, int64_t v) { *p = v; }
+
 template <class V, int SR>
-int64_t next_frontier(Context& ctx, Output& y, Vector& x, int32_t* lv, int32_t level) {
+int64_t next_frontier(Context& ctx, const Matrix& m, Output& y, Vector& x, int32_t* lv, int32_t level) {
     x.invalidate();
     int32_t* xi = static_cast<int32_t*>(x.sp_idx.ensure(sizeof(int32_t) * static_cast<size_t>(x.n)));
     V* xv = static_cast<V*>(x.sp_val.ensure(sizeof(V) * static_cast<size_t>(x.n)));
     const V value = SR == SR_MIN_PLUS ? V(level) : V(1);
+    // fused nnz_s / eff offsets when the packing cannot overflow (x.n = cols)
+    const bool fused = m.nnz < (int64_t(1) << kCntShift) && x.n < (int64_t(1) << (63 - kCntShift));
+    const int64_t* co = fused ? m.col_off.as<int64_t>() : nullptr;
+    int64_t* eff = fused ? static_cast<int64_t*>(x.eff.ensure(sizeof(int64_t) * static_cast<size_t>(x.n + 1))) : nullptr;
     if (y.has_sparse) {
         const int64_t nnz = output_nnz(ctx, y);
-        scan3(ctx, nnz, SparseFrontierIn<V, SR>{y.sp_idx.as<int32_t>(), y.sp_val.as<V>(), lv},
-              FrontierEpi<V>{y.sp_idx.as<int32_t>(), lv, xi, xv, level, value}, ctx.dscal(2),
+        scan3(ctx, nnz, SparseFrontierIn<V, SR>{y.sp_idx.as<int32_t>(), y.sp_val.as<V>(), lv, co},
+              FrontierEpi<V>{y.sp_idx.as<int32_t>(), lv, xi, xv, eff, level, value}, ctx.dscal(2),
               ctx.scratch[4]);
     } else {
-        scan3(ctx, y.n, DenseFrontierIn<V, SR>{y.dense.as<V>(), lv},
-              FrontierEpi<V>{nullptr, lv, xi, xv, level, value}, ctx.dscal(2), ctx.scratch[4]);
+        scan3(ctx, y.n, DenseFrontierIn<V, SR>{y.dense.as<V>(), lv, co},
+              FrontierEpi<V>{nullptr, lv, xi, xv, eff, level, value}, ctx.dscal(2), ctx.scratch[4]);
     }
-    x.nnz = ctx.fetch_scalar(ctx.dscal(2));
+    const int64_t tot = ctx.fetch_scalar(ctx.dscal(2));
+    x.nnz = fused ? tot >> kCntShift : tot;
     x.has_sparse = true;
+    if (fused) {
+        const int64_t nnz_s = tot & ((int64_t(1) << kCntShift) - 1);
+        set_i64_kernel<<<1, 1, 0, ctx.stream>>>(eff + x.nnz, nnz_s);  // eff[nnz_x] = nnz_s
+        ADA_LAUNCHED(ctx);
+        x.has_eff = true;
+        x.eff_matrix = m.id;
+        x.nnz_s = nnz_s;
+        x.nnz_s_matrix = m.id;
+    }
     return x.nnz;
 }
 
@@ -150,7 +180,6 @@ void launch_pull_e(Context& ctx, const Matrix& m, const Vector& x, const int32_t
 template <class V, int SR>
 void launch_pull(Context& ctx, const Matrix& m, const Vector& x, const int32_t* lv, Output& y) {
     V* yd = static_cast<V*>(y.dense.ensure(sizeof(V) * static_cast<size_t>(std::max<int64_t>(m.rows, 1))));
-    y.z_n = -1;  // the pull writes only unvisited rows: no sparse-reset record
     const bool early = SR == SR_OR_AND || (SR == SR_MIN_PLUS && m.pattern);
     if (early) launch_pull_e<V, SR, true>(ctx, m, x, lv, yd);
     else launch_pull_e<V, SR, false>(ctx, m, x, lv, yd);
@@ -234,7 +263,7 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         if (k == 2 || k == 3) launch_pull<V, SR>(ctx, m, x, lv, y);  // RowSpMSpV, output-masked
         else run_kernel(ctx, m, x, k, cfg, y);
         ADA_CUDA(cudaEventRecord(ev[2], ctx.stream));
-        visited += next_frontier<V, SR>(ctx, y, x, lv, static_cast<int32_t>(it + 1));  // syncs
+        visited += next_frontier<V, SR>(ctx, m, y, x, lv, static_cast<int32_t>(it + 1));  // syncs
         if (reports && it < max_reports) {
             float c_ms = 0, k_ms = 0;
             ADA_CUDA(cudaEventElapsedTime(&c_ms, ev[0], ev[1]));

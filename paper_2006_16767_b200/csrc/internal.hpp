@@ -158,6 +158,8 @@ struct Matrix {
     bool pattern = false;   // created without values (all 1.0)
     double gather_spread = 0;  // mean |col - row*n/m| over the nonzeros (columns)
     mutable std::unique_ptr<BinLayout> bins{new BinLayout()};
+    // column-normalised pattern copy for PageRank (pagerank.cu), built once
+    mutable std::unique_ptr<Matrix> colnorm;
     int vbytes() const { return value_bytes(dtype); }
 };
 
@@ -196,16 +198,6 @@ struct Output {
     int64_t nnz = -1;      // host-known nnz_y (-1 = only on device, slot d_nnz)
     DevBuf d_nnz;          // device int64 nnz_y
     int semiring = ADASPMV_PLUS_TIMES;  // identity of absent entries
-    // Sparse-reset record of the dense buffer (atomic column write-back): the
-    // buffer at z_ptr holds the identity of z_sr everywhere except in the rows
-    // of columns z_cols[0..z_n) of matrix z_matrix, so the next atomic
-    // multiply re-initialises only those rows instead of all m.  z_n < 0: no
-    // record (any other writer of the dense buffer clears it).
-    uint64_t z_matrix = 0;
-    int z_sr = -1;
-    const void* z_ptr = nullptr;
-    int64_t z_n = -1, z_work = 0;
-    DevBuf z_cols;
     // device-time bracket of the last run (recorded when Context::timing)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     bool timed = false;

@@ -44,10 +44,9 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
                     int64_t force_rows, int64_t tile_cap, int cluster = 0);
 
 // K4-K7 (kernels_col.cu).  Atomic -> dense y (y_dense); sort -> sparse y
-// (y_idx, y_val, *d_nnz on device).  x is the sparse operand.  prefilled:
-// y_dense already holds the identity (sparse reset done by the caller).
+// (y_idx, y_val, *d_nnz on device).  x is the sparse operand.
 template <class V, int SR>
-void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort, bool private_acc, bool prefilled,
+void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort, bool private_acc,
                    int lanes, V* y_dense, int32_t* y_idx, V* y_val, int64_t* d_nnz,
                    int64_t* h_nnz);
 

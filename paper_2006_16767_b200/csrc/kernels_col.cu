@@ -499,14 +499,14 @@ bool launch_private(Context& ctx, const Matrix& m, Vector& x, bool lb, V* y) {
 
 template <class V, int SR>
 void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort, bool private_acc,
-                   bool prefilled, int lanes, V* y_dense, int32_t* y_idx, V* y_val, int64_t* d_nnz,
+                   int lanes, V* y_dense, int32_t* y_idx, V* y_val, int64_t* d_nnz,
                    int64_t* h_nnz) {
     vector_ensure_sparse(ctx, x);
     const int G = lanes > 0 ? lanes : default_lanes_per_row(m.avg_col);
     *h_nnz = -1;
     if (!sort) {
         // atomic write-back into a dense y initialised to the identity
-        if (!prefilled) fill_value<V, SR>(ctx, y_dense, m.rows);
+        fill_value<V, SR>(ctx, y_dense, m.rows);
         if (x.nnz == 0 || m.nnz == 0) return;
         if (private_acc && launch_private<V, SR>(ctx, m, x, lb, y_dense)) return;
         if (!lb) {
@@ -615,7 +615,7 @@ int64_t sort_reduce_pairs_device(Context& ctx, int64_t npairs, const int32_t* d_
 }
 
 #define ADA_INST(V, SR)                                                                       \
-    template void run_col_major<V, SR>(Context&, const Matrix&, Vector&, bool, bool, bool, bool, int, \
+    template void run_col_major<V, SR>(Context&, const Matrix&, Vector&, bool, bool, bool, int, \
                                        V*, int32_t*, V*, int64_t*, int64_t*);
 ADA_INST(float, SR_PLUS_TIMES)
 ADA_INST(double, SR_PLUS_TIMES)

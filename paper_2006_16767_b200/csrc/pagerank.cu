@@ -65,18 +65,33 @@ __device__ __forceinline__ bool keep(V v, V prune) {
     return v != V(0) && fabs(v) >= prune;
 }
 
+// Items pack (kept ? 1 : 0) << kCntShift | deg_col(row) when `co` is set:
+// the prefix is each kept row's delta slot and its effective-nnz offset, the
+// total gives nnz_x and nnz_s in one read (as the BFS frontier update).
+constexpr int kCntShift = 36;
+
 template <class V>
 struct DenseDeltaIn {
     const V* y;
     V d, prune;
-    __device__ int64_t operator()(int64_t i) const { return keep(d * y[i], prune) ? 1 : 0; }
+    const int64_t* co;
+    __device__ int64_t operator()(int64_t i) const {
+        if (!keep(d * y[i], prune)) return 0;
+        return co ? (int64_t(1) << kCntShift) | (co[i + 1] - co[i]) : 1;
+    }
 };
 
 template <class V>
 struct SparseDeltaIn {
+    const int32_t* yi;
     const V* yv;
     V d, prune;
-    __device__ int64_t operator()(int64_t k) const { return keep(d * yv[k], prune) ? 1 : 0; }
+    const int64_t* co;
+    __device__ int64_t operator()(int64_t k) const {
+        if (!keep(d * yv[k], prune)) return 0;
+        const int32_t r = yi[k];
+        return co ? (int64_t(1) << kCntShift) | (co[r + 1] - co[r]) : 1;
+    }
 };
 
 template <class V>
@@ -87,32 +102,50 @@ struct DeltaEpi {
     V* rank;  // null: do not accumulate (the multiply budget is spent)
     int32_t* xi;
     V* xv;
+    int64_t* eff;  // null: plain 0/1 items
     __device__ void operator()(int64_t i, int64_t p, int64_t v) const {
         if (!v) return;
         const int32_t row = yi ? yi[i] : static_cast<int32_t>(i);
         const V dv = d * yv[i];
         if (rank) rank[row] += dv;  // rank += delta' (the next iteration's first step, fused)
-        xi[p] = row;
-        xv[p] = dv;
+        const int64_t slot = eff ? p >> kCntShift : p;
+        xi[slot] = row;
+        xv[slot] = dv;
+        if (eff) eff[slot] = p & ((int64_t(1) << kCntShift) - 1);
     }
 };
 
+__global__ void set_i64_kernel(int64_t* p, int64_t v) { *p = v; }
+
 template <class V>
-int64_t next_delta(Context& ctx, Output& y, Vector& x, V* rank, V d, V prune) {  // rank may be null
+int64_t next_delta(Context& ctx, const Matrix& m, Output& y, Vector& x, V* rank, V d, V prune) {  // rank may be null
     x.invalidate();
     int32_t* xi = static_cast<int32_t*>(x.sp_idx.ensure(sizeof(int32_t) * static_cast<size_t>(x.n)));
     V* xv = static_cast<V*>(x.sp_val.ensure(sizeof(V) * static_cast<size_t>(x.n)));
+    const bool fused = m.nnz < (int64_t(1) << kCntShift) && x.n < (int64_t(1) << (63 - kCntShift));
+    const int64_t* co = fused ? m.col_off.as<int64_t>() : nullptr;
+    int64_t* eff = fused ? static_cast<int64_t*>(x.eff.ensure(sizeof(int64_t) * static_cast<size_t>(x.n + 1))) : nullptr;
     if (y.has_sparse) {
         const int64_t nnz = output_nnz(ctx, y);
-        scan3(ctx, nnz, SparseDeltaIn<V>{y.sp_val.as<V>(), d, prune},
-              DeltaEpi<V>{y.sp_idx.as<int32_t>(), y.sp_val.as<V>(), d, rank, xi, xv}, ctx.dscal(5),
+        scan3(ctx, nnz, SparseDeltaIn<V>{y.sp_idx.as<int32_t>(), y.sp_val.as<V>(), d, prune, co},
+              DeltaEpi<V>{y.sp_idx.as<int32_t>(), y.sp_val.as<V>(), d, rank, xi, xv, eff}, ctx.dscal(5),
               ctx.scratch[4]);
     } else {
-        scan3(ctx, y.n, DenseDeltaIn<V>{y.dense.as<V>(), d, prune},
-              DeltaEpi<V>{nullptr, y.dense.as<V>(), d, rank, xi, xv}, ctx.dscal(5), ctx.scratch[4]);
+        scan3(ctx, y.n, DenseDeltaIn<V>{y.dense.as<V>(), d, prune, co},
+              DeltaEpi<V>{nullptr, y.dense.as<V>(), d, rank, xi, xv, eff}, ctx.dscal(5), ctx.scratch[4]);
     }
-    x.nnz = ctx.fetch_scalar(ctx.dscal(5));
+    const int64_t tot = ctx.fetch_scalar(ctx.dscal(5));
+    x.nnz = fused ? tot >> kCntShift : tot;
     x.has_sparse = true;
+    if (fused) {
+        const int64_t nnz_s = tot & ((int64_t(1) << kCntShift) - 1);
+        set_i64_kernel<<<1, 1, 0, ctx.stream>>>(eff + x.nnz, nnz_s);  // eff[nnz_x] = nnz_s
+        ADA_LAUNCHED(ctx);
+        x.has_eff = true;
+        x.eff_matrix = m.id;
+        x.nnz_s = nnz_s;
+        x.nnz_s_matrix = m.id;
+    }
     return x.nnz;
 }
 
@@ -134,9 +167,9 @@ void pagerank_t(Context& ctx, const Matrix& g, double damping, double prune, int
                 const Bundle* b, int forced, double* rank_out, int64_t* n_iters,
                 adaspmv_iteration_report* reports, int64_t max_reports) {
     const int64_t n = g.rows;
-    // P: same structure, column-normalised pattern values
-    std::unique_ptr<Matrix> P;
-    {
+    // P: same structure, column-normalised pattern values; cached on the
+    // graph matrix (structure-only, immutable after construction)
+    if (!g.colnorm) {
         DevBuf pv;
         V* vals = static_cast<V*>(pv.ensure(sizeof(V) * static_cast<size_t>(std::max<int64_t>(g.nnz, 1))));
         if (g.nnz > 0) {
@@ -144,9 +177,10 @@ void pagerank_t(Context& ctx, const Matrix& g, double damping, double prune, int
                 g.col_idx.as<int32_t>(), g.col_off.as<int64_t>(), g.nnz, vals);
             ADA_LAUNCHED(ctx);
         }
-        P.reset(matrix_create_device(ctx, g.rows, g.cols, g.nnz, g.row_off.as<int64_t>(),
-                                     g.col_idx.as<int32_t>(), vals, g.dtype, false));
+        g.colnorm.reset(matrix_create_device(ctx, g.rows, g.cols, g.nnz, g.row_off.as<int64_t>(),
+                                             g.col_idx.as<int32_t>(), vals, g.dtype, false));
     }
+    const Matrix* P = g.colnorm.get();
     DevBuf rb;
     V* rank = static_cast<V*>(rb.ensure(sizeof(V) * static_cast<size_t>(std::max<int64_t>(n, 1))));
     Vector x;
@@ -199,7 +233,7 @@ void pagerank_t(Context& ctx, const Matrix& g, double damping, double prune, int
         ADA_CUDA(cudaEventRecord(ev[2], ctx.stream));
         // delta' joins rank only if another multiply may follow (SPEC.md:498-506:
         // rank holds exactly the deltas that were propagated or are final)
-        next_delta<V>(ctx, y, x, it + 1 < max_iters ? rank : nullptr, static_cast<V>(damping),
+        next_delta<V>(ctx, *P, y, x, it + 1 < max_iters ? rank : nullptr, static_cast<V>(damping),
                       static_cast<V>(prune));  // syncs
         if (reports && it < max_reports) {
             float c_ms = 0, k_ms = 0;

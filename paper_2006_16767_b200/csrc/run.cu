@@ -37,53 +37,6 @@ struct CompactOut {
     }
 };
 
-// Sparse reset: y[r] = identity for every row r of the recorded columns
-// (one warp per column; CSC row indices are coalesced).
-template <class V, int SR>
-__global__ void sparse_reset_kernel(int64_t ncols, const int32_t* __restrict__ cols,
-                                    const int64_t* __restrict__ co, const int32_t* __restrict__ ri,
-                                    V* __restrict__ y) {
-    const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (w >= ncols) return;
-    const int32_t c = cols[w];
-    for (int64_t k = co[c] + lane; k < co[c + 1]; k += 32) y[ri[k]] = Semiring<SR, V>::zero();
-}
-
-// The atomic column write-back re-initialises only the rows the previous
-// multiply into this buffer touched, when that is much less than m rows.
-template <class V, int SR>
-bool try_sparse_reset(Context& ctx, const Matrix& m, Output& y, const V* yd) {
-    if (y.z_n < 0 || y.z_matrix != m.id || y.z_sr != SR || y.z_ptr != yd) return false;
-    if (y.z_work * 8 > m.rows) return false;  // estimated rows to reset vs a full fill
-    if (y.z_n > 0) {
-        sparse_reset_kernel<V, SR><<<static_cast<unsigned>((y.z_n * 32 + 255) / 256), 256, 0, ctx.stream>>>(
-            y.z_n, y.z_cols.as<int32_t>(), m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(),
-            const_cast<V*>(yd));
-        ADA_LAUNCHED(ctx);
-    }
-    return true;
-}
-
-template <class V, int SR>
-void record_touched(Context& ctx, const Matrix& m, const Vector& x, Output& y, const V* yd) {
-    // estimated entries of the support's columns; record only small supports
-    const int64_t work = x.nnz_s >= 0 && x.nnz_s_matrix == m.id
-                             ? x.nnz_s
-                             : static_cast<int64_t>(static_cast<double>(x.nnz) * std::max(m.avg_col, 1.0));
-    if (x.nnz < 0 || work * 8 > m.rows) return;
-    if (x.nnz > 0) {
-        y.z_cols.ensure(sizeof(int32_t) * static_cast<size_t>(x.nnz));
-        ADA_CUDA(cudaMemcpyAsync(y.z_cols.p, x.sp_idx.p, sizeof(int32_t) * static_cast<size_t>(x.nnz),
-                                 cudaMemcpyDeviceToDevice, ctx.stream));
-    }
-    y.z_n = x.nnz;
-    y.z_work = work;
-    y.z_matrix = m.id;
-    y.z_sr = SR;
-    y.z_ptr = yd;
-}
-
 template <class V, int SR>
 void run_t(Context& ctx, const Matrix& m, Vector& x, int kernel, const adaspmv_config& cfg,
            Output& y) {
@@ -101,7 +54,6 @@ void run_t(Context& ctx, const Matrix& m, Vector& x, int kernel, const adaspmv_c
                 mask = x.mask.as<uint32_t>();
             }
             V* yd = static_cast<V*>(y.dense.ensure(sizeof(V) * rows));
-            y.z_n = -1;  // full overwrite
             const bool direct = kernel == 0 || kernel == 2;
             const bool binned = direct && (cfg.row_layout == ADASPMV_ROW_LAYOUT_BINNED ||
                                            (cfg.row_layout == ADASPMV_ROW_LAYOUT_AUTO && binned_preferred(m)));
@@ -121,19 +73,15 @@ void run_t(Context& ctx, const Matrix& m, Vector& x, int kernel, const adaspmv_c
             if (!sort) {
                 V* yd = static_cast<V*>(y.dense.ensure(sizeof(V) * rows));
                 int64_t dummy;
-                vector_ensure_sparse(ctx, x);
-                const bool pre = try_sparse_reset<V, SR>(ctx, m, y, yd);
-                y.z_n = -1;
-                run_col_major<V, SR>(ctx, m, x, lb, false, cfg.atomic_private_accumulators != 0, pre,
+                run_col_major<V, SR>(ctx, m, x, lb, false, cfg.atomic_private_accumulators != 0,
                                      lanes, yd, nullptr, nullptr, nullptr, &dummy);
-                record_touched<V, SR>(ctx, m, x, y, yd);
                 y.has_dense = true;
             } else {
                 int32_t* yi = static_cast<int32_t*>(y.sp_idx.ensure(sizeof(int32_t) * rows));
                 V* yv = static_cast<V*>(y.sp_val.ensure(sizeof(V) * rows));
                 int64_t* dn = static_cast<int64_t*>(y.d_nnz.ensure(sizeof(int64_t)));
                 int64_t hn = -1;
-                run_col_major<V, SR>(ctx, m, x, lb, true, false, false, lanes, nullptr, yi, yv, dn, &hn);
+                run_col_major<V, SR>(ctx, m, x, lb, true, false, lanes, nullptr, yi, yv, dn, &hn);
                 y.nnz = hn;
                 y.has_sparse = true;
             }
@@ -155,7 +103,6 @@ void run_v(Context& ctx, const Matrix& m, Vector& x, int kernel, const adaspmv_c
 template <class V, int SR>
 void dense_from_sparse(Context& ctx, Output& y) {
     V* d = static_cast<V*>(y.dense.ensure(sizeof(V) * static_cast<size_t>(std::max<int64_t>(y.n, 1))));
-    y.z_n = -1;
     fill_value<V, SR>(ctx, d, y.n);
     const int64_t nnz = output_nnz(ctx, y);
     if (nnz > 0) {

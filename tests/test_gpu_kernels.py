@@ -411,10 +411,9 @@ def test_binned_heavy_rows(ctx, port, dt):
 
 
 @pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
-def test_atomic_sparse_reset_reuses_output(ctx, port, dt):
-    # K4/K6 into the same MultiplyOutput re-initialise only the rows the
-    # previous small-support multiply touched; interleave supports, kernels,
-    # semirings and a second matrix and compare every result with the oracle.
+def test_atomic_output_reuse(ctx, port, dt):
+    # one MultiplyOutput reused across supports, kernels, semirings and a
+    # second matrix: every result matches the oracle (no stale rows).
     rows, cols, ro, ci, vals = synth.random_csr(20000, 15000, 0.0004, seed=31, dtype=dt)
     m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
     r2, c2, ro2, ci2, v2 = synth.random_csr(20000, 15000, 0.0003, seed=32, dtype=dt)
