@@ -485,8 +485,10 @@ def run_ours(args, rank, world):
     if prof.exists():
         try:
             pj = json.loads(prof.read_text())
+            # spmv_direct reads the whole matrix whatever x holds: its DRAM
+            # traffic per launch does not depend on the x sparsity
             if A.KernelId.from_index(k_dom).name() in pj.get("kernel", "") and \
-                    f"x = {int(SPARSITIES[dom] * 100)} %" in pj.get("kernel", ""):
+                    (k_dom == 0 or f"x = {int(SPARSITIES[dom] * 100)} %" in pj.get("kernel", "")):
                 traffic = pj.get("traffic_bytes_per_launch")
         except Exception:
             traffic = None

@@ -153,7 +153,10 @@ __global__ void __launch_bounds__(256) bfs_pull_kernel(int64_t rows, const int64
             hit[j] = c[j] >= 0 && ((__ldg(fmask + (c[j] >> 5)) >> (c[j] & 31)) & 1u);
 #pragma unroll
         for (int j = 0; j < kU; ++j)
-            if (hit[j]) acc = S::fma(S::kUsesValues ? __ldg(vals + k0 + j * G) : V(1), __ldg(x + c[j]), acc);
+            // OR_AND: a frontier hit is the whole answer (x holds 1 there), no x load
+            if (hit[j])
+                acc = SR == SR_OR_AND ? V(1)
+                                      : S::fma(S::kUsesValues ? __ldg(vals + k0 + j * G) : V(1), __ldg(x + c[j]), acc);
         if (EARLY && acc != S::zero()) break;
     }
 #pragma unroll
@@ -170,7 +173,7 @@ void launch_pull_e(Context& ctx, const Matrix& m, const Vector& x, const int32_t
     case GG:                                                                                    \
         bfs_pull_kernel<V, GG, SR, EARLY><<<blocks, 256, 0, ctx.stream>>>(                      \
             m.rows, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), m.vals.as<V>(),           \
-            x.dense.as<V>(), x.mask.as<uint32_t>(), lv, y);                                     \
+            SR == SR_OR_AND ? nullptr : x.dense.as<V>(), x.mask.as<uint32_t>(), lv, y);         \
         break;
     switch (G) { ADA_G(1) ADA_G(2) ADA_G(4) ADA_G(8) ADA_G(16) ADA_G(32) default: invalid("lanes"); }
 #undef ADA_G
@@ -252,9 +255,11 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         else k = heuristic_kernel(ctx, m, x, visited);
         const auto t1 = clk::now();
         ADA_CUDA(cudaEventRecord(ev[0], ctx.stream));
-        if (k <= 3) {
+        if (k == 2 || k == 3) {  // output-masked pull: the mask, and x values unless OR_AND
+            vector_ensure_mask(ctx, x);
+            if (SR != SR_OR_AND) vector_ensure_dense(ctx, x, SR);
+        } else if (k <= 1) {
             vector_ensure_dense(ctx, x, SR);
-            if (k >= 2) vector_ensure_mask(ctx, x);
         } else if (k == 6 || k == 7) {
             vector_ensure_eff(ctx, x, m);
         }

@@ -122,8 +122,9 @@ struct BinLayout {
     int64_t force_rows = 0;   // rows-per-bin override it was built with
     int cluster_req = 0;      // bin_cluster request it was built with
     int cluster = 1;          // CTAs per bin tile (1, or 2 = cluster pair)
-    int64_t R = 0, nbins = 0, nchunks = 0;
+    int64_t R = 0, nbins = 0, nchunks = 0;  // R = rows of the tallest bin (shared-memory segment)
     int rbits = 0, cw = 0;
+    DevBuf bin_r0;                  // int64 [nbins+1]: first row of each bin (variable-height bins)
     DevBuf pk, bv, chunk_off;
     std::vector<int64_t> bin_start;  // host: first entry of each bin, [nbins] = nnz
     int64_t tile_cap = -1, ntiles = 0;

@@ -57,8 +57,8 @@ struct PkVal {
 // are not counted: they sort behind every bin and are never streamed.
 template <class V>
 __global__ void bin_expand_kernel(const int64_t* __restrict__ co, const int32_t* __restrict__ ri,
-                                  const V* __restrict__ cv, int64_t cols, int64_t R, int rbits,
-                                  int cw, int64_t nchunks, const int64_t* __restrict__ ro,
+                                  const V* __restrict__ cv, int64_t cols, const int64_t* __restrict__ r0s,
+                                  int rbits, int cw, int64_t nchunks, const int64_t* __restrict__ ro,
                                   int64_t heavy_min, int64_t nbins, uint32_t* __restrict__ keys,
                                   PkVal<V>* __restrict__ pay,
                                   unsigned long long* __restrict__ counts) {
@@ -78,9 +78,15 @@ __global__ void bin_expand_kernel(const int64_t* __restrict__ co, const int32_t*
                 pay[k] = PkVal<V>{0u, V(0)};
                 continue;
             }
-            const int64_t bin = row / R;
+            int64_t lo = 0, hi = nbins;  // bin: largest b with r0s[b] <= row
+            while (hi - lo > 1) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (__ldg(r0s + mid) <= row) lo = mid;
+                else hi = mid;
+            }
+            const int64_t bin = lo;
             keys[k] = static_cast<uint32_t>(bin);
-            const uint32_t rl = static_cast<uint32_t>(row - bin * R);
+            const uint32_t rl = static_cast<uint32_t>(row - __ldg(r0s + bin));
             pay[k] = PkVal<V>{((static_cast<uint32_t>(j) & cmask) << rbits) | rl, cv[k]};
             // rows ascend within the column: count runs of equal bins per lane
             if (bin != prev_bin) {
@@ -146,7 +152,7 @@ __global__ void gather_spread_kernel(const int64_t* __restrict__ ro, const int32
 template <class V, int SR, bool MASKED, int CL = 1, int kBinUnroll = 8, bool NOALLOC = false,
           int kBinThreads = 1024>
 __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
-    int64_t rows, int64_t R, int rbits, int cw, int64_t nchunks,
+    const int64_t* __restrict__ bin_r0, int rbits, int cw, int64_t nchunks,
     const int64_t* __restrict__ tiles, const int32_t* __restrict__ tile_bin,
     const int32_t* __restrict__ tile_multi, const int64_t* __restrict__ chunk_off,
     const uint32_t* __restrict__ pk, const V* __restrict__ bv, const V* __restrict__ x,
@@ -157,8 +163,8 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
     const int64_t t = blockIdx.x;
     const int64_t bin = tile_bin[t];
     const int64_t e0 = tiles[2 * t], e1 = tiles[2 * t + 1];
-    const int64_t r0 = bin * R;
-    const int nr = static_cast<int>(min(R, rows - r0));
+    const int64_t r0 = bin_r0[bin];
+    const int nr = static_cast<int>(bin_r0[bin + 1] - r0);
     for (int i = threadIdx.x; i < nr; i += kBinThreads) ys[i] = S::zero();
     __syncthreads();
 
@@ -335,6 +341,55 @@ void plan_heavy(Context& ctx, const Matrix& m, BinLayout& L) {
     ctx.sync();
 }
 
+struct LightDegIn {
+    const int64_t* ro;
+    int64_t heavy_min;  // 0: every row is light
+    __device__ int64_t operator()(int64_t r) const {
+        const int64_t d = ro[r + 1] - ro[r];
+        return heavy_min > 0 && d > heavy_min ? 0 : d;
+    }
+};
+
+// cut[k] = first row r with prefix(r) >= k * total / nb (prefix = light
+// entries of rows < r), k = 1 .. nb-1
+__global__ void work_cuts_kernel(const int64_t* __restrict__ pre, int64_t rows, int64_t nb, int64_t* __restrict__ cut) {
+    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x + 1;
+    if (k >= nb) return;
+    const int64_t total = pre[rows];
+    const int64_t t = static_cast<int64_t>(static_cast<double>(total) * static_cast<double>(k) / static_cast<double>(nb));
+    int64_t lo = 0, hi = rows;  // first r in [0, rows] with pre[r] >= t
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (pre[mid] < t) lo = mid + 1;
+        else hi = mid;
+    }
+    cut[k - 1] = lo;
+}
+
+struct WritePrefix {
+    int64_t* out;
+    __device__ void operator()(int64_t i, int64_t p, int64_t) const { out[i] = p; }
+};
+
+// Row cuts of `nb` bins holding equal shares of the light entries (sorted,
+// deduplicated, starting at row 0).
+std::vector<int64_t> equal_work_cuts(Context& ctx, const Matrix& m, int64_t nb, int64_t heavy_min) {
+    std::vector<int64_t> cuts{0};
+    if (nb <= 1 || m.rows == 0) return cuts;
+    DevBuf pre, cut;
+    int64_t* p = static_cast<int64_t*>(pre.ensure(sizeof(int64_t) * static_cast<size_t>(m.rows + 1)));
+    scan3(ctx, m.rows, LightDegIn{m.row_off.as<int64_t>(), heavy_min}, WritePrefix{p}, p + m.rows, ctx.scratch[5]);
+    int64_t* c = static_cast<int64_t*>(cut.ensure(sizeof(int64_t) * static_cast<size_t>(nb)));
+    work_cuts_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, ctx.stream>>>(p, m.rows, nb, c);
+    ADA_LAUNCHED(ctx);
+    std::vector<int64_t> h(static_cast<size_t>(nb - 1));
+    ADA_CUDA(cudaMemcpyAsync(h.data(), c, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    for (int64_t v : h)
+        if (v > cuts.back() && v < m.rows) cuts.push_back(v);
+    return cuts;
+}
+
 template <class V>
 void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
     const int vb = sizeof(V);
@@ -358,10 +413,38 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
         }
     }
     nbins = std::max<int64_t>(nbins, 1);
-    const int64_t R = std::max<int64_t>((m.rows + nbins - 1) / nbins, 1);
-    if (R > rmax) invalid("binned layout: rows per bin exceed the shared-memory segment");
-    nbins = std::max<int64_t>((m.rows + R - 1) / R, 1);
+    // heavy rows: a row whose entries would put several lanes of one warp
+    // instruction on the same shared-memory slot (degree well above the
+    // column-sorted window a warp covers) runs from the CSR instead
+    const int64_t per_bin = m.nnz / nbins + 1;
+    L.heavy_min = m.feat[3] > static_cast<double>(kHeavySeg / 2)
+                      ? std::max<int64_t>(kHeavySeg / 2, per_bin / 512) : 0;
+    std::vector<int64_t> cuts;
+    if (L.force_rows > 0 || L.cluster == 2 || m.nnz == 0) {  // equal-height bins
+        const int64_t R0 = std::max<int64_t>((m.rows + nbins - 1) / nbins, 1);
+        if (R0 > rmax) invalid("binned layout: rows per bin exceed the shared-memory segment");
+        for (int64_t r = 0; r < m.rows; r += R0) cuts.push_back(r);
+    } else {  // equal-work bins (light entries), no taller than the segment
+        cuts = equal_work_cuts(ctx, m, nbins, L.heavy_min);
+        std::vector<int64_t> split;
+        for (size_t i = 0; i < cuts.size(); ++i) {
+            const int64_t a = cuts[i], b = i + 1 < cuts.size() ? cuts[i + 1] : m.rows;
+            const int64_t parts = std::max<int64_t>((b - a + rmax - 1) / rmax, 1);
+            for (int64_t p = 0; p < parts; ++p) split.push_back(a + (b - a) * p / parts);
+        }
+        cuts.swap(split);
+    }
+    if (cuts.empty()) cuts.push_back(0);
+    cuts.push_back(m.rows);
+    nbins = static_cast<int64_t>(cuts.size()) - 1;
     if (nbins >= (int64_t(1) << 31)) invalid("binned layout: too many bins");
+    int64_t R = 1;
+    for (int64_t b = 0; b < nbins; ++b) R = std::max<int64_t>(R, cuts[static_cast<size_t>(b + 1)] - cuts[static_cast<size_t>(b)]);
+    if (R > rmax) invalid("binned layout: rows per bin exceed the shared-memory segment");
+    L.bin_r0.ensure(sizeof(int64_t) * cuts.size());
+    ADA_CUDA(cudaMemcpyAsync(L.bin_r0.p, cuts.data(), sizeof(int64_t) * cuts.size(), cudaMemcpyHostToDevice,
+                             ctx.stream));
+    ctx.sync();  // host cuts go out of scope
     const int cw = 32 - rbits;
     const int64_t nchunks = std::max<int64_t>((m.cols + (int64_t(1) << cw) - 1) >> cw, 1);
     L.R = R;
@@ -369,12 +452,6 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
     L.cw = cw;
     L.nbins = nbins;
     L.nchunks = nchunks;
-    // heavy rows: a row whose entries would put several lanes of one warp
-    // instruction on the same shared-memory slot (degree well above the
-    // column-sorted window a warp covers) runs from the CSR instead
-    const int64_t per_bin = m.nnz / nbins + 1;
-    L.heavy_min = m.feat[3] > static_cast<double>(kHeavySeg / 2)
-                      ? std::max<int64_t>(kHeavySeg / 2, per_bin / 512) : 0;
     plan_heavy(ctx, m, L);
     const int64_t nnz = m.nnz;
     const size_t z = static_cast<size_t>(std::max<int64_t>(nnz, 1));
@@ -394,7 +471,7 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
         const int64_t warps = std::min<int64_t>(m.cols, static_cast<int64_t>(ctx.sm_count) * 64);
         bin_expand_kernel<V><<<static_cast<unsigned>(std::max<int64_t>((warps * 32 + 255) / 256, 1)), 256, 0,
                                ctx.stream>>>(m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(),
-                                             m.cvals.as<V>(), m.cols, R, rbits, cw, nchunks,
+                                             m.cvals.as<V>(), m.cols, L.bin_r0.as<int64_t>(), rbits, cw, nchunks,
                                              m.row_off.as<int64_t>(), L.nsegs ? L.heavy_min : 0, nbins,
                                              k0.as<uint32_t>(), p0.as<PkVal<V>>(),
                                              counts.as<unsigned long long>());
@@ -539,7 +616,8 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
         at[0].val.clusterDim.z = 1;
         lc.attrs = at;
         lc.numAttrs = 1;
-        ADA_CUDA(cudaLaunchKernelEx(&lc, kern, m.rows, L.R, L.rbits, L.cw, L.nchunks, L.tiles.as<int64_t>(),
+        ADA_CUDA(cudaLaunchKernelEx(&lc, kern, static_cast<const int64_t*>(L.bin_r0.as<int64_t>()), L.rbits,
+                                    L.cw, L.nchunks, L.tiles.as<int64_t>(),
                                     L.tile_bin.as<int32_t>(), L.tile_multi.as<int32_t>(),
                                     L.chunk_off.as<int64_t>(), L.pk.as<uint32_t>(), L.bv.as<V>(), x, mask, y));
         ADA_LAUNCHED(ctx);
