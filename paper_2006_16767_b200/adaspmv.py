@@ -675,8 +675,8 @@ class MultiplyOutput:
     def sparse(self) -> SparseVector:
         n, _, _, dt = self._info()
         k = self.nnz()
-        idx = np.zeros(max(k, 1), np.int64)
-        val = np.zeros(max(k, 1), dt)
+        idx = np.empty(max(k, 1), np.int64)
+        val = np.empty(max(k, 1), dt)
         kk = C.c_int64()
         _check(_lib.adaspmv_output_sparse(self.ctx.h, self.h, k, _ptr(idx), _ptr(val), C.byref(kk)))
         return SparseVector(n, idx[:k], val[:k])

@@ -529,9 +529,10 @@ int adaspmv_vector_get_sparse(adaspmv_ctx* ctx, adaspmv_vector* v, int64_t capac
         const int64_t n = std::min(capacity, v->nnz);
         if (n <= 0) return;
         if (indices) {
-            std::vector<int32_t> tmp(static_cast<size_t>(n));
-            ADA_CUDA(copy_sync(ctx, tmp.data(), v->sp_idx.p, sizeof(int32_t) * tmp.size(), cudaMemcpyDeviceToHost));
-            for (int64_t k = 0; k < n; ++k) indices[k] = tmp[static_cast<size_t>(k)];
+            ada::DevBuf& w = ctx->scratch[7];
+            int64_t* d64 = static_cast<int64_t*>(w.ensure(sizeof(int64_t) * static_cast<size_t>(n)));
+            ada::widen_indices(*ctx, n, v->sp_idx.as<int32_t>(), d64);
+            ADA_CUDA(copy_sync(ctx, indices, d64, sizeof(int64_t) * static_cast<size_t>(n), cudaMemcpyDeviceToHost));
         }
         if (values)
             ADA_CUDA(copy_sync(ctx, values, v->sp_val.p, static_cast<size_t>(ada::value_bytes(v->dtype)) * static_cast<size_t>(n),
@@ -788,11 +789,12 @@ int adaspmv_output_sparse(adaspmv_ctx* ctx, adaspmv_output* y, int64_t capacity,
         if (nnz_y) *nnz_y = nnz;
         const int64_t n = std::min(capacity, nnz);
         if (n <= 0) return;
-        if (indices) {
-            int32_t* st = static_cast<int32_t*>(ctx->stage(sizeof(int32_t) * static_cast<size_t>(n)));
-            ADA_CUDA(cudaMemcpyAsync(st, y->sp_idx.p, sizeof(int32_t) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, ctx->stream));
-            ctx->sync();
-            for (int64_t k = 0; k < n; ++k) indices[k] = st[k];
+        if (indices) {  // widened to the reference's int64 index_t on the device, one D2H
+            ada::DevBuf& w = ctx->scratch[7];
+            int64_t* d64 = static_cast<int64_t*>(w.ensure(sizeof(int64_t) * static_cast<size_t>(n)));
+            ada::widen_indices(*ctx, n, y->sp_idx.as<int32_t>(), d64);
+            ADA_CUDA(cudaMemcpyAsync(indices, d64, sizeof(int64_t) * static_cast<size_t>(n), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
         }
         if (values)
             ADA_CUDA(cudaMemcpyAsync(values, y->sp_val.p, static_cast<size_t>(ada::value_bytes(y->dtype)) * static_cast<size_t>(n),

@@ -249,6 +249,8 @@ void vector_ensure_mask(Context& ctx, Vector& v);
 void vector_ensure_eff(Context& ctx, Vector& v, const Matrix& m);  // also sparse
 int64_t vector_nnz(Context& ctx, Vector& v);
 int64_t vector_nnz_s(Context& ctx, Vector& v, const Matrix& m);
+// out[k] = in[k] (int32 device indices -> int64), on ctx's stream
+void widen_indices(Context& ctx, int64_t n, const int32_t* in, int64_t* out);
 
 void run_kernel(Context& ctx, const Matrix& m, Vector& x, int kernel, const adaspmv_config& cfg,
                 Output& y);

@@ -477,6 +477,7 @@ bool launch_private(Context& ctx, const Matrix& m, Vector& x, bool lb, V* y) {
     const size_t smem = sizeof(V) * static_cast<size_t>(m.rows);
     if (smem > kPrivateSmem || m.rows == 0) return false;  // y does not fit: plain atomic path
     const int64_t nnz_s = lb ? vector_nnz_s(ctx, x, m) : 0;
+    if (lb) vector_ensure_eff(ctx, x, m);  // nnz_s may be known without the offsets
     const unsigned grid = static_cast<unsigned>(2 * ctx.sm_count);
     if (lb) {
         ADA_CUDA(cudaFuncSetAttribute(col_private_kernel<V, SR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -515,6 +516,7 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
         }
         const int64_t nnz_s = vector_nnz_s(ctx, x, m);
         if (nnz_s == 0) return;
+        vector_ensure_eff(ctx, x, m);  // nnz_s may be known without the offsets
         const int64_t tiles = (nnz_s + kColTile - 1) / kColTile;
         col_lb_kernel<V, SR, false><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
             x.nnz, nnz_s, tiles, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
@@ -538,6 +540,7 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
         return;
     }
     const int64_t nnz_s = vector_nnz_s(ctx, x, m);
+    vector_ensure_eff(ctx, x, m);  // nnz_s may be known without the offsets
     DevBuf& kb0 = ctx.scratch[0];
     DevBuf& kb1 = ctx.scratch[1];
     DevBuf& vb0 = ctx.scratch[2];

@@ -36,6 +36,8 @@ void features(Context& ctx, const Matrix& m, Vector& v, uint32_t mask, double* o
     for (int i = 0; i < 9; ++i)
         if (mask & (1u << i)) out[i] = m.feat[i];
     if (mask & ((1u << 9) | (1u << 10))) {
+        // a dense-only x gets nnz_x and nnz_s from one pass (vector_nnz_s)
+        if (v.nnz < 0 && v.has_dense && !v.has_sparse && v.n == m.cols) vector_nnz_s(ctx, v, m);
         const double nx = static_cast<double>(vector_nnz(ctx, v));
         if (mask & (1u << 9)) out[9] = nx;
         if (mask & (1u << 10)) out[10] = v.n > 0 ? nx / static_cast<double>(v.n) : 0.0;

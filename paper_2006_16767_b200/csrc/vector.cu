@@ -250,8 +250,58 @@ int64_t vector_nnz(Context& ctx, Vector& v) {
     return v.nnz;
 }
 
+__global__ void widen_kernel(int64_t n, const int32_t* __restrict__ in, int64_t* __restrict__ out) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n; k += stride) out[k] = in[k];
+}
+
+void widen_indices(Context& ctx, int64_t n, const int32_t* in, int64_t* out) {
+    if (n <= 0) return;
+    const int64_t g = std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 16);
+    widen_kernel<<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(n, in, out);
+    ADA_LAUNCHED(ctx);
+}
+
+// nnz_x and nnz_s of a dense-only vector in one pass (no sparse conversion):
+// out[0] += #{i : x_i != 0}, out[1] += sum of deg_col(i) over them.
+template <class V>
+__global__ void dense_counts_kernel(int64_t n, const V* __restrict__ x, const int64_t* __restrict__ co,
+                                    unsigned long long* __restrict__ out) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    long long c = 0, s = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+        if (x[i] != V(0)) {
+            ++c;
+            s += co[i + 1] - co[i];
+        }
+    c = warp_sum(c);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0 && (c || s)) {
+        atomicAdd(out, static_cast<unsigned long long>(c));
+        atomicAdd(out + 1, static_cast<unsigned long long>(s));
+    }
+}
+
 int64_t vector_nnz_s(Context& ctx, Vector& v, const Matrix& m) {
     if (v.nnz_s >= 0 && v.nnz_s_matrix == m.id) return v.nnz_s;
+    if (v.has_dense && !v.has_sparse && v.dense_fill < 0 && v.n == m.cols) {  // user dense x: one pass
+        unsigned long long* out = reinterpret_cast<unsigned long long*>(ctx.dscal(7));
+        ADA_CUDA(cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), ctx.stream));
+        const int64_t g = std::max<int64_t>(std::min<int64_t>((v.n + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 8), 1);
+        if (v.dtype == ADASPMV_F64)
+            dense_counts_kernel<double><<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(v.n, v.dense.as<double>(),
+                                                                                         m.col_off.as<int64_t>(), out);
+        else
+            dense_counts_kernel<float><<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(v.n, v.dense.as<float>(),
+                                                                                        m.col_off.as<int64_t>(), out);
+        ADA_LAUNCHED(ctx);
+        ADA_CUDA(cudaMemcpyAsync(ctx.h_scalars, out, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        v.nnz = ctx.h_scalars[0];
+        v.nnz_s = ctx.h_scalars[1];
+        v.nnz_s_matrix = m.id;
+        return v.nnz_s;
+    }
     vector_ensure_eff(ctx, v, m);
     v.nnz_s = ctx.fetch_scalar(v.eff.as<int64_t>() + v.nnz);
     v.nnz_s_matrix = m.id;

@@ -2,6 +2,7 @@
 per point, host wall time of set_{sparse,dense} (H2D + validation), the
 adaptive select + run, and the result read (D2H), plus raw pinned copy
 bandwidth for reference.   python tools/e2e_profile.py"""
+import ctypes as C
 import sys
 import time
 from pathlib import Path
@@ -16,7 +17,7 @@ from paper_2006_16767_b200 import selector as S  # noqa: E402
 
 
 def main():
-    rows, cols, ro, ci, vals = bench.make_matrix()
+    (rows, cols, ro, ci, vals), _ = bench.make_matrix()
     ctx = A.Context(0)
     m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
     bundle = A.SelectorBundle.load(S.DEFAULT_PATH)
@@ -33,6 +34,7 @@ def main():
             pinned.append(("sparse", (torch.from_numpy(xi).pin_memory().numpy(),
                                       torch.from_numpy(xv).pin_memory().numpy())))
     ybuf = torch.zeros(rows, dtype=torch.float32).pin_memory().numpy()
+    yidx = torch.zeros(rows, dtype=torch.int64).pin_memory().numpy()
     # raw copy bandwidth
     dev = torch.empty(rows, dtype=torch.float32, device="cuda")
     hst = torch.zeros(rows, dtype=torch.float32).pin_memory()
@@ -60,7 +62,8 @@ def main():
             t2 = time.perf_counter()
             ns = A.effective_nnz(m, x)
             if k.index() in (5, 7) or 4 * ns < rows:
-                y.sparse()
+                ny = C.c_int64()
+                A._check(A._lib.adaspmv_output_sparse(ctx.h, y.h, rows, A._ptr(yidx), A._ptr(ybuf), C.byref(ny)))
             else:
                 A._check(A._lib.adaspmv_output_dense(ctx.h, y.h, A._ptr(ybuf)))
             t3 = time.perf_counter()
