@@ -97,7 +97,10 @@ typedef struct {
      * cluster pair shares it (twice the rows per bin, the pair's shared-memory
      * y segments combined over DSMEM); 0 = auto. */
     int32_t bin_cluster;
-    int32_t reserved;
+    /* x bytes per column panel of the row bins, KiB (<= 0 = one panel, the
+     * default): the bins stream x panel by panel, their y segments
+     * accumulating across panels (opt-in). */
+    int32_t bin_panel_kib;
 } adaspmv_config;
 
 enum { ADASPMV_ROW_LAYOUT_AUTO = 0, ADASPMV_ROW_LAYOUT_CSR = 1, ADASPMV_ROW_LAYOUT_BINNED = 2 };

@@ -173,6 +173,7 @@ struct KernelConfig {
     int bin_rows = 0;
     long long bin_tile_nnz = 0;
     int bin_cluster = 0;  // CTAs per bin tile (1 single, 2 cluster pair, 0 auto)
+    int bin_panel_kib = 0;  // x bytes per column panel of the row bins (<= 0: one panel)
     adaspmv_config c() const {
         adaspmv_config r{};
         r.workers = workers;
@@ -183,6 +184,7 @@ struct KernelConfig {
         r.bin_rows = bin_rows;
         r.bin_tile_nnz = bin_tile_nnz;
         r.bin_cluster = bin_cluster;
+        r.bin_panel_kib = bin_panel_kib;
         return r;
     }
 };

@@ -103,7 +103,7 @@ class _Config(C.Structure):
     _fields_ = [("workers", C.c_int32), ("atomic_private_accumulators", C.c_int32),
                 ("semiring", C.c_int32), ("lanes_per_row", C.c_int32),
                 ("row_layout", C.c_int32), ("bin_rows", C.c_int32),
-                ("bin_tile_nnz", C.c_int64), ("bin_cluster", C.c_int32), ("reserved", C.c_int32)]
+                ("bin_tile_nnz", C.c_int64), ("bin_cluster", C.c_int32), ("bin_panel_kib", C.c_int32)]
 
 
 _lib = None
@@ -356,6 +356,7 @@ class KernelConfig:  # kernels.hpp:154-162 (+ device knobs)
     bin_rows: int = 0         # rows per bin override (0 = auto)
     bin_tile_nnz: int = 0     # entries per bin tile override (0 = auto)
     bin_cluster: int = 0      # CTAs per bin tile: 1 single, 2 cluster pair, 0 auto
+    bin_panel_kib: int = 0    # x KiB per column panel of the row bins (<= 0: one panel)
 
     def _c(self) -> _Config:
         c = _Config()
@@ -367,6 +368,7 @@ class KernelConfig:  # kernels.hpp:154-162 (+ device knobs)
         c.bin_rows = int(self.bin_rows)
         c.bin_tile_nnz = int(self.bin_tile_nnz)
         c.bin_cluster = int(self.bin_cluster)
+        c.bin_panel_kib = int(self.bin_panel_kib)
         return c
 
 

@@ -127,7 +127,9 @@ struct BinLayout {
     DevBuf bin_r0;                  // int64 [nbins+1]: first row of each bin (variable-height bins)
     DevBuf pk, bv, chunk_off;
     std::vector<int64_t> bin_start;  // host: first entry of each bin, [nbins] = nnz
-    int64_t tile_cap = -1, ntiles = 0;
+    std::vector<int64_t> h_chunk_off;  // host copy of chunk_off (panel tile planning)
+    int64_t tile_cap = -1, ntiles = 0, panel_chunks = -1;
+    std::vector<int64_t> panel_tile0;  // first tile of each column panel, [npanels] = ntiles
     bool multi = false;       // some bin is split into several tiles
     // heavy rows (degree > heavy_min) are left out of the bins (their entries
     // would serialise on one shared-memory slot) and run from the CSR as

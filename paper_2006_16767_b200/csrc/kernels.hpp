@@ -41,7 +41,7 @@ void run_row_major(Context& ctx, const Matrix& m, const V* x, const uint32_t* ma
 // first use.  mask == nullptr -> SpMV.
 template <class V, int SR>
 void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* mask, V* y,
-                    int64_t force_rows, int64_t tile_cap, int cluster = 0);
+                    int64_t force_rows, int64_t tile_cap, int cluster = 0, int panel_kib = 0);
 
 // K4-K7 (kernels_col.cu).  Atomic -> dense y (y_dense); sort -> sparse y
 // (y_idx, y_val, *d_nnz on device).  x is the sparse operand.

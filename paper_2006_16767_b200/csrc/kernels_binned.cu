@@ -152,7 +152,7 @@ __global__ void gather_spread_kernel(const int64_t* __restrict__ ro, const int32
 template <class V, int SR, bool MASKED, int CL = 1, int kBinUnroll = 8, bool NOALLOC = false,
           int kBinThreads = 1024>
 __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
-    const int64_t* __restrict__ bin_r0, int rbits, int cw, int64_t nchunks,
+    int64_t tile0, const int64_t* __restrict__ bin_r0, int rbits, int cw, int64_t nchunks,
     const int64_t* __restrict__ tiles, const int32_t* __restrict__ tile_bin,
     const int32_t* __restrict__ tile_multi, const int64_t* __restrict__ chunk_off,
     const uint32_t* __restrict__ pk, const V* __restrict__ bv, const V* __restrict__ x,
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
     using S = Semiring<SR, V>;
     extern __shared__ __align__(16) unsigned char bin_smem[];
     V* ys = reinterpret_cast<V*>(bin_smem);
-    const int64_t t = blockIdx.x;
+    const int64_t t = tile0 + blockIdx.x;
     const int64_t bin = tile_bin[t];
     const int64_t e0 = tiles[2 * t], e1 = tiles[2 * t + 1];
     const int64_t r0 = bin_r0[bin];
@@ -244,9 +244,15 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
     } else {
         __syncthreads();
     }
-    if (!tile_multi[t]) {  // the tile owns its bin's rows: plain coalesced stores
+    const int mode = tile_multi[t];
+    if (mode == 0) {  // the tile owns its bin's rows: plain coalesced stores
         for (int i = lo + static_cast<int>(threadIdx.x); i < hi; i += kBinThreads)
             y[r0 + i] = CL == 2 ? S::add(ys[i], peer[i]) : ys[i];
+    } else if (mode == 2) {  // owns the rows in a later column panel: y += segment
+        for (int i = lo + static_cast<int>(threadIdx.x); i < hi; i += kBinThreads) {
+            const V v = CL == 2 ? S::add(ys[i], peer[i]) : ys[i];
+            if (v != S::zero()) y[r0 + i] = S::add(y[r0 + i], v);
+        }
     } else {               // partial segment: combine into the identity-filled y
         for (int i = lo + static_cast<int>(threadIdx.x); i < hi; i += kBinThreads) {
             const V v = CL == 2 ? S::add(ys[i], peer[i]) : ys[i];
@@ -495,6 +501,7 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
     ctx.sync();
     L.bin_start.resize(static_cast<size_t>(nbins + 1));
     for (int64_t b = 0; b <= nbins; ++b) L.bin_start[static_cast<size_t>(b)] = all[static_cast<size_t>(b * nchunks)];
+    L.h_chunk_off.swap(all);
     L.tile_cap = -1;
     L.built = true;
 }
@@ -502,42 +509,62 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
 // Tiles: every bin gets ceil(count / cap) equal column-contiguous tiles (at
 // least one, so its rows are written); heaviest first (longest-processing-
 // time order for the hardware block scheduler).
-void plan_tiles(Context& ctx, const Matrix& m, BinLayout& L, int64_t cap_req) {
+void plan_tiles(Context& ctx, const Matrix& m, BinLayout& L, int64_t cap_req, int64_t panel_chunks) {
     int64_t cap = cap_req;
     if (cap <= 0) {
         const double fair = static_cast<double>(m.nnz) / static_cast<double>(ctx.sm_count);
         cap = std::max<int64_t>(static_cast<int64_t>(fair * 1.25), 16384);
     }
-    if (L.tile_cap == cap) return;
-    // a work unit is one CTA (cluster 1) or a CTA pair (cluster 2) of `cap`
-    // entries per CTA; units of a bin are equal column-contiguous splits
-    struct T { int64_t e0, e1; int32_t bin, multi; };
+    panel_chunks = std::min<int64_t>(std::max<int64_t>(panel_chunks, 1), L.nchunks);
+    if (L.cluster == 2) panel_chunks = L.nchunks;  // pairs: one panel
+    if (L.tile_cap == cap && L.panel_chunks == panel_chunks) return;
+    // Column panels of `panel_chunks` chunks are launched one after another;
+    // within a panel a work unit is one CTA (cluster 1) or a CTA pair
+    // (cluster 2) of <= `cap` entries per CTA, a bin's units being equal
+    // column-contiguous splits.  mode: 0 store the bin's rows, 1 atomic
+    // combine (bin split in this panel), 2 load-add-store (later panel).
+    struct T { int64_t e0, e1; int32_t bin, mode; };
     std::vector<T> ts;
+    std::vector<int64_t> p0;
     bool multi = false;
     const int cl = L.cluster;
-    for (int64_t b = 0; b < L.nbins; ++b) {
-        const int64_t s = L.bin_start[static_cast<size_t>(b)], e = L.bin_start[static_cast<size_t>(b + 1)];
-        const int64_t k = std::max<int64_t>((e - s + cl * cap - 1) / (cl * cap), 1);
-        for (int64_t i = 0; i < k * cl; ++i)
-            ts.push_back(T{s + (e - s) * i / (k * cl), s + (e - s) * (i + 1) / (k * cl), static_cast<int32_t>(b), k > 1});
-        multi = multi || k > 1;
-    }
-    if (cl == 1) {
-        std::stable_sort(ts.begin(), ts.end(), [](const T& a, const T& b) { return a.e1 - a.e0 > b.e1 - b.e0; });
-    } else {  // heaviest pair first, pairs kept adjacent (cluster = CTAs 2p, 2p+1)
-        std::vector<size_t> pr(ts.size() / 2);
-        std::iota(pr.begin(), pr.end(), size_t(0));
-        std::stable_sort(pr.begin(), pr.end(), [&](size_t a, size_t b) {
-            return ts[2 * a + 1].e1 - ts[2 * a].e0 > ts[2 * b + 1].e1 - ts[2 * b].e0;
-        });
-        std::vector<T> o;
-        o.reserve(ts.size());
-        for (size_t p : pr) {
-            o.push_back(ts[2 * p]);
-            o.push_back(ts[2 * p + 1]);
+    const int64_t nc = L.nchunks;
+    for (int64_t c0 = 0; c0 < nc; c0 += panel_chunks) {
+        const int64_t c1 = std::min(c0 + panel_chunks, nc);
+        const size_t first = ts.size();
+        p0.push_back(static_cast<int64_t>(first));
+        for (int64_t b = 0; b < L.nbins; ++b) {
+            const int64_t s = L.h_chunk_off[static_cast<size_t>(b * nc + c0)];
+            const int64_t e = L.h_chunk_off[static_cast<size_t>(b * nc + c1)];
+            if (c0 > 0 && e == s) continue;  // nothing to add in a later panel
+            const int64_t k = std::max<int64_t>((e - s + cl * cap - 1) / (cl * cap), 1);
+            const int32_t mode = k > 1 ? 1 : (c0 > 0 ? 2 : 0);
+            for (int64_t i = 0; i < k * cl; ++i)
+                ts.push_back(T{s + (e - s) * i / (k * cl), s + (e - s) * (i + 1) / (k * cl), static_cast<int32_t>(b), mode});
+            multi = multi || k > 1;
         }
-        ts.swap(o);
+        if (cl == 1) {
+            std::stable_sort(ts.begin() + static_cast<std::ptrdiff_t>(first), ts.end(),
+                             [](const T& a, const T& b) { return a.e1 - a.e0 > b.e1 - b.e0; });
+        } else {  // heaviest pair first, pairs kept adjacent (cluster = CTAs 2p, 2p+1)
+            std::vector<size_t> pr((ts.size() - first) / 2);
+            std::iota(pr.begin(), pr.end(), size_t(0));
+            auto at = [&](size_t i) -> const T& { return ts[first + i]; };
+            std::stable_sort(pr.begin(), pr.end(), [&](size_t a, size_t b) {
+                return at(2 * a + 1).e1 - at(2 * a).e0 > at(2 * b + 1).e1 - at(2 * b).e0;
+            });
+            std::vector<T> o;
+            o.reserve(ts.size() - first);
+            for (size_t q : pr) {
+                o.push_back(at(2 * q));
+                o.push_back(at(2 * q + 1));
+            }
+            std::copy(o.begin(), o.end(), ts.begin() + static_cast<std::ptrdiff_t>(first));
+        }
     }
+    p0.push_back(static_cast<int64_t>(ts.size()));
+    L.panel_tile0.swap(p0);
+    L.panel_chunks = panel_chunks;
     const size_t nt = ts.size();
     std::vector<int64_t> h_t(2 * nt);
     std::vector<int32_t> h_b(nt), h_m(nt);
@@ -545,7 +572,7 @@ void plan_tiles(Context& ctx, const Matrix& m, BinLayout& L, int64_t cap_req) {
         h_t[2 * i] = ts[i].e0;
         h_t[2 * i + 1] = ts[i].e1;
         h_b[i] = ts[i].bin;
-        h_m[i] = ts[i].multi;
+        h_m[i] = ts[i].mode;
     }
     L.tiles.ensure(sizeof(int64_t) * h_t.size());
     L.tile_bin.ensure(sizeof(int32_t) * nt);
@@ -585,7 +612,7 @@ bool binned_preferred(const Matrix& m) {
 
 template <class V, int SR>
 void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* mask, V* y,
-                    int64_t force_rows, int64_t tile_cap, int cluster) {
+                    int64_t force_rows, int64_t tile_cap, int cluster, int panel_kib) {
     if (cluster < 0 || cluster > 2) invalid("bin_cluster must be 0, 1 or 2");
     const int creq = cluster == 0 ? kBinClusterAuto : cluster;
     if (!m.bins->built || m.bins->force_rows != force_rows || m.bins->dtype != m.dtype ||
@@ -597,15 +624,21 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
         build_layout<V>(ctx, m, *m.bins);
     }
     BinLayout& L = *m.bins;
-    plan_tiles(ctx, m, L, tile_cap);
+    // column panels (opt-in): x streamed in pieces of panel_kib.  Off by
+    // default: on R-MAT 26 (x = 268 MB > L2) 16-96 MiB panels measured 3-25 %
+    // slower than one pass (the gathers concentrate on hub columns that stay
+    // in L2; the bound is the L1 data pipe)
+    const int64_t chunk_bytes = (int64_t(1) << L.cw) * static_cast<int64_t>(sizeof(V));
+    const int64_t pbytes = panel_kib > 0 ? int64_t(panel_kib) * 1024 : INT64_MAX / 2;
+    plan_tiles(ctx, m, L, tile_cap, std::max<int64_t>(pbytes / chunk_bytes, 1));
     if (m.rows == 0) return;
     if (L.multi) fill_value<V, SR>(ctx, y, m.rows);
     const size_t smem = sizeof(V) * static_cast<size_t>(L.R);
     const int nt = 1024;
-    auto launch = [&](auto kern, int cl) {
+    auto launch = [&](auto kern, int cl, int64_t t0, int64_t nt_) {
         ADA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         cudaLaunchConfig_t lc{};
-        lc.gridDim = dim3(static_cast<unsigned>(L.ntiles));
+        lc.gridDim = dim3(static_cast<unsigned>(nt_));
         lc.blockDim = dim3(nt);
         lc.dynamicSmemBytes = smem;
         lc.stream = ctx.stream;
@@ -616,18 +649,22 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
         at[0].val.clusterDim.z = 1;
         lc.attrs = at;
         lc.numAttrs = 1;
-        ADA_CUDA(cudaLaunchKernelEx(&lc, kern, static_cast<const int64_t*>(L.bin_r0.as<int64_t>()), L.rbits,
+        ADA_CUDA(cudaLaunchKernelEx(&lc, kern, t0, static_cast<const int64_t*>(L.bin_r0.as<int64_t>()), L.rbits,
                                     L.cw, L.nchunks, L.tiles.as<int64_t>(),
                                     L.tile_bin.as<int32_t>(), L.tile_multi.as<int32_t>(),
                                     L.chunk_off.as<int64_t>(), L.pk.as<uint32_t>(), L.bv.as<V>(), x, mask, y));
         ADA_LAUNCHED(ctx);
     };
-    if (L.cluster == 2) {
-        if (mask) launch(binned_row_kernel<V, SR, true, 2>, 2);
-        else launch(binned_row_kernel<V, SR, false, 2>, 2);
-    } else {
-        if (mask) launch(binned_row_kernel<V, SR, true, 1>, 1);
-        else launch(binned_row_kernel<V, SR, false, 1>, 1);
+    for (size_t p = 0; p + 1 < L.panel_tile0.size(); ++p) {  // panels in column order, same stream
+        const int64_t t0 = L.panel_tile0[p], t1 = L.panel_tile0[p + 1];
+        if (t1 <= t0) continue;
+        if (L.cluster == 2) {
+            if (mask) launch(binned_row_kernel<V, SR, true, 2>, 2, t0, t1 - t0);
+            else launch(binned_row_kernel<V, SR, false, 2>, 2, t0, t1 - t0);
+        } else {
+            if (mask) launch(binned_row_kernel<V, SR, true, 1>, 1, t0, t1 - t0);
+            else launch(binned_row_kernel<V, SR, false, 1>, 1, t0, t1 - t0);
+        }
     }
     if (L.nsegs > 0) {  // heavy rows, after the bins wrote their identity
         auto hk = mask ? heavy_seg_kernel<V, SR, true> : heavy_seg_kernel<V, SR, false>;
@@ -639,7 +676,7 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
 
 #define ADA_INST(V, SR)                                                                                \
     template void run_row_binned<V, SR>(Context&, const Matrix&, const V*, const uint32_t*, V*, int64_t, \
-                                        int64_t, int);
+                                        int64_t, int, int);
 ADA_INST(float, SR_PLUS_TIMES)
 ADA_INST(double, SR_PLUS_TIMES)
 ADA_INST(float, SR_OR_AND)

@@ -60,7 +60,7 @@ void run_t(Context& ctx, const Matrix& m, Vector& x, int kernel, const adaspmv_c
             if (cfg.row_layout < 0 || cfg.row_layout > 2) invalid("unknown row_layout");
             if (binned)
                 run_row_binned<V, SR>(ctx, m, x.dense.as<V>(), mask, yd, cfg.bin_rows, cfg.bin_tile_nnz,
-                                      cfg.bin_cluster);
+                                      cfg.bin_cluster, cfg.bin_panel_kib);
             else if (m.rows > 0)
                 run_row_major<V, SR>(ctx, m, x.dense.as<V>(), mask, kernel == 1 || kernel == 3,
                                      lanes, yd);

@@ -323,7 +323,8 @@ def test_matrix_market_and_binary_round_trip(ctx, tmp_path):
 # partial y segments are combined with atomics (bin_tile_nnz), and empty bins.
 BIN_CFGS = [dict(), dict(bin_rows=7), dict(bin_rows=64, bin_tile_nnz=5), dict(bin_tile_nnz=1000),
             dict(bin_cluster=2), dict(bin_rows=64, bin_cluster=2), dict(bin_rows=9, bin_tile_nnz=7, bin_cluster=2),
-            dict(bin_cluster=1)]
+            dict(bin_cluster=1), dict(bin_panel_kib=1), dict(bin_panel_kib=1, bin_tile_nnz=500),
+            dict(bin_panel_kib=1, bin_rows=64), dict(bin_panel_kib=-1)]
 
 
 @pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])

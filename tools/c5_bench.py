@@ -70,6 +70,7 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--kernels", default="0,1,2,3,4,6")
     ap.add_argument("--densities", default="0.00001,0.001,0.1,1.0")
+    ap.add_argument("--panels", default="", help="x KiB per column panel to time spmv_direct with (dense x)")
     a = ap.parse_args()
     t0 = time.time()
     n, ro, ci = rmat_device(a.scale)
@@ -136,6 +137,27 @@ def main():
             row["kernels"][str(k)] = ent
             print(dens, k, ent, flush=True)
         res["spmv"].append(row)
+    if a.panels:  # spmv_direct (row bins) vs the column-panel width, dense x
+        xd = np.random.default_rng(7).uniform(-1, 1, n).astype(np.float32)
+        x = A.DeviceVector(n, np.float32, ctx).set_dense(xd)
+        ref = None
+        res["panels"] = []
+        for pk in [int(v) for v in a.panels.split(",")]:
+            cfg = A.KernelConfig(row_layout=2, bin_panel_kib=pk)
+            y = A.run_kernel(m, 0, x, cfg, out=out)
+            s_ = float(np.sum(y.dense().values, dtype=np.float64))
+            ref = s_ if ref is None else ref
+            ts = []
+            for _ in range(a.reps):
+                with torch.cuda.stream(stream):
+                    torch.cuda._sleep(400_000)
+                ts.append(A.run_kernel(m, 0, x, cfg, out=out).elapsed())
+            t = float(np.median(ts))
+            b_spmv = (n + 1) * 8 + nnz * 8 + n * 4 + n * 4
+            ent = {"panel_kib": pk, "t_us": round(t * 1e6, 1), "pct_hbm_spmv_bytes": round(100 * b_spmv / t / hbm, 1),
+                   "y_sum_rel_diff": abs(s_ - ref) / max(abs(ref), 1e-30)}
+            res["panels"].append(ent)
+            print("panel", ent, flush=True)
     del out
     lv_ref = None
     for name, forced in (("heuristic", -1), ("row_lb_masked_pull", 3), ("col_lb_atomic", 6)):
