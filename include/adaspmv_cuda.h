@@ -232,6 +232,48 @@ int adaspmv_run(adaspmv_ctx* ctx, const adaspmv_matrix* m, adaspmv_vector* x, in
 int adaspmv_run_adaptive(adaspmv_ctx* ctx, const adaspmv_matrix* m, adaspmv_vector* x,
                          const adaspmv_bundle* b, const adaspmv_config* cfg, adaspmv_output* y,
                          int* chosen);
+/* ---- batched multiplies from host buffers (serving path) ------------------ */
+/* One operand x in the reference's host layout: nnz < 0 = DenseVector
+ * (sparse.hpp:99-109, `values` holds n reals); else SparseVector
+ * (sparse.hpp:113-130, nnz int64 indices strictly increasing and < n). */
+typedef struct {
+    int64_t nnz;
+    const int64_t* indices;
+    const void* values;
+} adaspmv_host_operand;
+
+/* Result form of a batched multiply. */
+enum {
+    ADASPMV_RESULT_DENSE = 0,  /* MultiplyOutput::dense(): m values */
+    ADASPMV_RESULT_SPARSE = 1, /* MultiplyOutput::sparse(): int64 indices + values, zeros dropped */
+    ADASPMV_RESULT_AUTO = 2    /* the smaller of the two (sparse when the sort kernels produced it or
+                                  nnz_s bounds nnz_y below the dense size); `form` reports which */
+};
+
+/* One result in host memory.  In: form, capacity (sparse entries the
+ * indices/values buffers hold), indices (int64, may be NULL for DENSE),
+ * values (m reals for DENSE / AUTO, `capacity` reals for SPARSE).  Out: form
+ * written, kernel run (KernelId::index()), nnz_y (SPARSE; -1 for DENSE). */
+typedef struct {
+    int32_t form;
+    int32_t kernel;
+    int64_t capacity;
+    int64_t* indices;
+    void* values;
+    int64_t nnz_y;
+} adaspmv_host_result;
+
+/* `count` independent multiplies y_k = A x_k, each exactly what
+ * vector_set_* -> run_adaptive (or run with `forced_kernel` >= 0) ->
+ * output_dense/sparse does, pipelined over `lanes` (0 = 3) streams of the
+ * device: one vector's host-to-device copy, another's multiply and a third's
+ * device-to-host copy overlap.  Pinned host buffers make the copies
+ * asynchronous.  Returns after every result is in host memory; the first
+ * failure (e.g. an invalid operand) stops the batch and is reported. */
+int adaspmv_run_batch(adaspmv_ctx* ctx, const adaspmv_matrix* m, const adaspmv_bundle* b,
+                      int forced_kernel, const adaspmv_config* cfg, int64_t count,
+                      const adaspmv_host_operand* xs, adaspmv_host_result* ys, int lanes);
+
 /* MultiplyOutput (kernels.hpp:116-152). */
 int adaspmv_output_info(adaspmv_output* y, int64_t* length, int* has_dense, int* has_sparse,
                         int* dtype);

@@ -396,6 +396,76 @@ inline KernelId predict_kernel(const DualMatrix& m, const SparseVector& x, const
     return KernelId::from_index(k);
 }
 
+// ---- batched multiplies from host vectors (adaspmv_run_batch) ------------------------
+// One operand of a batch: a DenseVector or a SparseVector (the other empty).
+struct BatchOperand {
+    const DenseVector* dense = nullptr;
+    const SparseVector* sparse = nullptr;
+};
+
+// Result of one batched multiply: the dense or the sparse form of y
+// (MultiplyOutput::dense()/sparse(), kernels.hpp:136-144) and the kernel run.
+struct BatchResult {
+    KernelId kernel;
+    bool is_sparse = false;
+    DenseVector dense;
+    SparseVector sparse;
+};
+
+// y_k = A x_k for every operand, selected by `b` (or `forced_kernel` >= 0),
+// pipelined over `lanes` streams; `form` = ADASPMV_RESULT_DENSE / SPARSE / AUTO.
+inline std::vector<BatchResult> run_batch(const DualMatrix& m, const std::vector<BatchOperand>& xs,
+                                          const SelectorBundle* b, int forced_kernel = -1,
+                                          int form = ADASPMV_RESULT_AUTO, const KernelConfig& cfg = {},
+                                          int lanes = 0) {
+    const size_t n = xs.size();
+    std::vector<adaspmv_host_operand> ops(n);
+    std::vector<adaspmv_host_result> res(n);
+    std::vector<BatchResult> out(n);
+    const index_t rows = m.rows();
+    for (size_t k = 0; k < n; ++k) {
+        if (xs[k].sparse) {
+            if (xs[k].sparse->length != m.cols()) throw std::invalid_argument("run_batch: vector length != matrix columns");
+            ops[k] = {xs[k].sparse->nnz(), xs[k].sparse->indices.data(), xs[k].sparse->values.data()};
+        } else if (xs[k].dense) {
+            if (xs[k].dense->size() != m.cols()) throw std::invalid_argument("run_batch: vector length != matrix columns");
+            ops[k] = {-1, nullptr, xs[k].dense->values.data()};
+        } else {
+            throw std::invalid_argument("run_batch: empty operand");
+        }
+        // buffers for either form (AUTO decides on the device side)
+        out[k].dense.values.resize(static_cast<size_t>(rows));
+        res[k].form = form;
+        res[k].values = out[k].dense.values.data();
+        if (form != ADASPMV_RESULT_DENSE) {
+            out[k].sparse.length = rows;
+            out[k].sparse.indices.resize(static_cast<size_t>(rows));
+            out[k].sparse.values.resize(static_cast<size_t>(rows));
+            res[k].capacity = rows;
+            res[k].indices = out[k].sparse.indices.data();
+            if (form == ADASPMV_RESULT_SPARSE) res[k].values = out[k].sparse.values.data();
+        }
+    }
+    const adaspmv_config c = cfg.c();
+    check(adaspmv_run_batch(m.context().get(), m.get(), b ? b->get() : nullptr, forced_kernel, &c,
+                            static_cast<int64_t>(n), ops.data(), res.data(), lanes));
+    for (size_t k = 0; k < n; ++k) {
+        out[k].kernel = KernelId::from_index(res[k].kernel);
+        out[k].is_sparse = res[k].form == ADASPMV_RESULT_SPARSE;
+        if (out[k].is_sparse) {
+            const size_t nz = static_cast<size_t>(res[k].nnz_y);
+            if (form == ADASPMV_RESULT_AUTO)  // values landed in the dense buffer
+                out[k].sparse.values.assign(out[k].dense.values.begin(), out[k].dense.values.begin() + nz);
+            out[k].sparse.indices.resize(nz);
+            out[k].sparse.values.resize(nz);
+            out[k].dense.values.clear();
+        } else {
+            out[k].sparse = SparseVector{};
+        }
+    }
+    return out;
+}
+
 // ---- BFS driver --------------------------------------------------------
 inline std::vector<index_t> bfs(const DualMatrix& m, index_t source, int semiring = ADASPMV_OR_AND,
                                 const SelectorBundle* b = nullptr, int forced_kernel = -1) {

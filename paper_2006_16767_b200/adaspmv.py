@@ -106,6 +106,17 @@ class _Config(C.Structure):
                 ("bin_tile_nnz", C.c_int64), ("bin_cluster", C.c_int32), ("bin_panel_kib", C.c_int32)]
 
 
+class _HostOperand(C.Structure):
+    _fields_ = [("nnz", C.c_int64), ("indices", C.c_void_p), ("values", C.c_void_p)]
+
+
+class _HostResult(C.Structure):
+    _fields_ = [("form", C.c_int32), ("kernel", C.c_int32), ("capacity", C.c_int64),
+                ("indices", C.c_void_p), ("values", C.c_void_p), ("nnz_y", C.c_int64)]
+
+
+RESULT_DENSE, RESULT_SPARSE, RESULT_AUTO = 0, 1, 2
+
 _lib = None
 
 
@@ -174,6 +185,7 @@ def load(path: Optional[os.PathLike] = None):
         "adaspmv_bfs": [vp, vp, i64, C.c_int, vp, C.c_int, vp, P(i64), vp, i64],
         "adaspmv_pagerank": [vp, vp, C.c_double, C.c_double, i64, vp, C.c_int, vp, P(i64), vp, i64],
         "adaspmv_execute_iteration": [vp, vp, vp, vp, C.c_int, vp, vp, vp],
+        "adaspmv_run_batch": [vp, vp, vp, C.c_int, vp, i64, vp, vp, C.c_int],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -853,6 +865,70 @@ def run_adaptive(m: DualMatrix, x, bundle: SelectorBundle, cfg: Optional[KernelC
     _check(_lib.adaspmv_run_adaptive(m.ctx.h, m.h, v.h, bundle.h, C.byref(c), out.h, C.byref(k)))
     out._operand = v
     return out, KernelId.from_index(k.value)
+
+
+class BatchResult:
+    """One result of run_batch: `kernel` (KernelId), `is_sparse`, and
+    `dense` (DenseVector) or `sparse` (SparseVector, int64 indices)."""
+
+    def __init__(self, kernel, is_sparse, dense=None, sparse=None):
+        self.kernel, self.is_sparse, self.dense, self.sparse = kernel, is_sparse, dense, sparse
+
+
+def run_batch(m: DualMatrix, xs, bundle: Optional[SelectorBundle] = None, force_kernel: int = -1,
+              form: int = RESULT_AUTO, cfg: Optional[KernelConfig] = None, lanes: int = 0,
+              buffers=None):
+    """adaspmv_run_batch: y_k = A x_k for every host operand in `xs`
+    (DenseVector, SparseVector, or numpy arrays: 1-D values = dense, a pair
+    (indices, values) = sparse), selected by `bundle` (else `force_kernel`),
+    pipelined over `lanes` streams.  `buffers` (optional, one (indices int64,
+    values) pair of length rows per operand, ideally pinned) receive the
+    results without allocation; the returned BatchResults view them."""
+    ops = (_HostOperand * max(len(xs), 1))()
+    res = (_HostResult * max(len(xs), 1))()
+    keep = []
+    rows = m.rows()
+    vdt = m.dtype
+    bufs = []
+    for k, x in enumerate(xs):
+        if isinstance(x, DenseVector):
+            x = np.ascontiguousarray(x.values, dtype=vdt)
+        elif isinstance(x, SparseVector):
+            x = (x.indices, x.values)
+        if isinstance(x, tuple):
+            xi = np.ascontiguousarray(x[0], dtype=np.int64)
+            xv = np.ascontiguousarray(x[1], dtype=vdt)
+            keep += [xi, xv]
+            ops[k].nnz, ops[k].indices, ops[k].values = len(xi), xi.ctypes.data, xv.ctypes.data
+        else:
+            xd = np.ascontiguousarray(x, dtype=vdt)
+            if len(xd) != m.cols():
+                raise InvalidArgument("run_batch: vector length != matrix columns")
+            keep.append(xd)
+            ops[k].nnz, ops[k].indices, ops[k].values = -1, None, xd.ctypes.data
+        if buffers is not None:
+            bi, bv = buffers[k]
+        else:
+            bi = np.empty(rows if form != RESULT_DENSE else 0, np.int64)
+            bv = np.empty(rows, vdt)
+        bufs.append((bi, bv))
+        res[k].form = int(form)
+        res[k].capacity = len(bi) if form != RESULT_DENSE else 0
+        res[k].indices = bi.ctypes.data if form != RESULT_DENSE and len(bi) else None
+        res[k].values = bv.ctypes.data
+    c = (cfg or KernelConfig())._c()
+    _check(_lib.adaspmv_run_batch(m.ctx.h, m.h, bundle.h if bundle else None, int(force_kernel), C.byref(c),
+                                  len(xs), C.cast(ops, C.c_void_p), C.cast(res, C.c_void_p), int(lanes)))
+    out = []
+    for k in range(len(xs)):
+        bi, bv = bufs[k]
+        kid = KernelId.from_index(res[k].kernel)
+        if res[k].form == RESULT_SPARSE:
+            nz = int(res[k].nnz_y)
+            out.append(BatchResult(kid, True, sparse=SparseVector(rows, bi[:nz], bv[:nz], dtype=vdt)))
+        else:
+            out.append(BatchResult(kid, False, dense=DenseVector(bv[:rows])))
+    return out
 
 
 def execute_iteration(m: DualMatrix, x, bundle: Optional[SelectorBundle] = None, force_kernel: int = -1,

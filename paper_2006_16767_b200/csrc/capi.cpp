@@ -133,9 +133,56 @@ void* Context::stage(size_t bytes) {
     return h_stage;
 }
 
-int64_t Context::fetch_scalar(const int64_t* d) {
-    ADA_CUDA(cudaMemcpyAsync(h_scalars, d, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+void context_init(Context& ctx, int device, cudaStream_t stream) {
+    ctx.device = device;
+    ADA_CUDA(cudaSetDevice(device));
+    ADA_CUDA(cudaFree(nullptr));
+    if (stream) {
+        ctx.stream = stream;
+    } else {
+        ADA_CUDA(cudaStreamCreateWithFlags(&ctx.stream, cudaStreamNonBlocking));
+        ctx.own_stream = true;
+    }
+    ADA_CUDA(cudaDeviceGetAttribute(&ctx.sm_count, cudaDevAttrMultiProcessorCount, device));
+    ADA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx.h_scalars), 64 * sizeof(int64_t), cudaHostAllocMapped));
+    ADA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx.h_scalars_dev), ctx.h_scalars, 0));
+    // keep freed blocks in the device's default pool instead of returning
+    // them to the driver at every synchronisation
+    cudaMemPool_t pool;
+    ADA_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    ADA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    g_alloc_stream = ctx.stream;
+    ctx.d_scalars.ensure(64 * sizeof(int64_t));
+}
+
+void context_release(Context& ctx) {
+    ctx.lanes.clear();
+    cudaSetDevice(ctx.device);
+    g_alloc_stream = ctx.stream;
+    cudaStreamSynchronize(ctx.stream);
+    for (auto& b : ctx.scratch) b.release();
+    ctx.d_scalars.release();
+    ctx.lb_partials.release();
+    if (ctx.h_scalars) cudaFreeHost(ctx.h_scalars);
+    if (ctx.h_stage) cudaFreeHost(ctx.h_stage);
+    ctx.h_scalars = nullptr;
+    ctx.h_stage = nullptr;
+    if (ctx.own_stream) {
+        cudaStreamSynchronize(ctx.stream);  // the releases above are ordered on it
+        cudaStreamDestroy(ctx.stream);
+    }
+    ctx.stream = nullptr;
+    ctx.own_stream = false;
+}
+
+void Context::fetch_scalars(const int64_t* d, int n) {
+    copy_scalars_kernel_launch(*this, d, h_scalars_dev, n);
     ADA_CUDA(cudaStreamSynchronize(stream));
+}
+
+int64_t Context::fetch_scalar(const int64_t* d) {
+    fetch_scalars(d, 1);
     return h_scalars[0];
 }
 
@@ -150,26 +197,7 @@ int adaspmv_ctx_create(int device, void* stream, adaspmv_ctx** out) {
     return guarded([&] {
         need(out, "out");
         auto ctx = std::make_unique<adaspmv_ctx>();
-        ctx->device = device;
-        ADA_CUDA(cudaSetDevice(device));
-        ADA_CUDA(cudaFree(nullptr));
-        if (stream) {
-            ctx->stream = static_cast<cudaStream_t>(stream);
-        } else {
-            ADA_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-            ctx->own_stream = true;
-        }
-        ADA_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
-        ADA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_scalars), 64 * sizeof(int64_t),
-                               cudaHostAllocDefault));
-        // keep freed blocks in the device's default pool instead of returning
-        // them to the driver at every synchronisation
-        cudaMemPool_t pool;
-        ADA_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-        uint64_t threshold = UINT64_MAX;
-        ADA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
-        ada::g_alloc_stream = ctx->stream;
-        ctx->d_scalars.ensure(64 * sizeof(int64_t));
+        ada::context_init(*ctx, device, static_cast<cudaStream_t>(stream));
         *out = ctx.release();
     });
 }
@@ -177,13 +205,7 @@ int adaspmv_ctx_create(int device, void* stream, adaspmv_ctx** out) {
 int adaspmv_ctx_destroy(adaspmv_ctx* ctx) {
     if (!ctx) return ADASPMV_OK;
     return guarded([&] {
-        bind_quiet(ctx);
-        cudaStreamSynchronize(ctx->stream);
-        for (auto& b : ctx->scratch) b.release();
-        ctx->d_scalars.release();
-        if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
-        if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
-        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        ada::context_release(*ctx);
         delete ctx;
     });
 }
@@ -755,6 +777,26 @@ int adaspmv_execute_iteration(adaspmv_ctx* ctx, const adaspmv_matrix* m, adaspmv
             report->convert_s = conv_ms * 1e-3;
             report->kernel_s = kern_ms * 1e-3;
         }
+    });
+}
+
+int adaspmv_run_batch(adaspmv_ctx* ctx, const adaspmv_matrix* m, const adaspmv_bundle* b,
+                      int forced_kernel, const adaspmv_config* cfg, int64_t count,
+                      const adaspmv_host_operand* xs, adaspmv_host_result* ys, int lanes) {
+    return guarded([&] {
+        bind(ctx);
+        need(m, "matrix");
+        if (count < 0) ada::invalid("run_batch: negative count");
+        if (count > 0) {
+            need(xs, "operands");
+            need(ys, "results");
+        }
+        if (forced_kernel > 7) ada::invalid("kernel index out of range");
+        if (forced_kernel < 0 && !b) ada::invalid("run_batch: no bundle and no forced kernel");
+        if (lanes < 0 || lanes > 16) ada::invalid("run_batch: lanes must be in [0, 16]");
+        adaspmv_config c{};
+        if (cfg) c = *cfg;
+        ada::run_batch(*ctx, *m, b, forced_kernel, c, count, xs, ys, lanes == 0 ? 3 : lanes);
     });
 }
 

@@ -15,6 +15,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -84,6 +85,8 @@ struct DevBuf {
     T* as() const { return static_cast<T*>(p); }
 };
 
+struct BatchLane;  // batch.cpp: one pipelined stream of adaspmv_run_batch
+
 struct Context {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -95,17 +98,28 @@ struct Context {
     // [0..3] sort write-back keys/values (double buffered), [4] vector scans,
     // [5] matrix build scans, [6..9] radix counts / scan / segment sums / flags
     DevBuf scratch[10];
-    // pinned host scalars for D2H of counts (nnz_s, nnz_y, ...)
+    // pinned, device-mapped host scalars for counts (nnz_s, nnz_y, ...): a
+    // one-thread kernel stores them over PCIe (scalars_to_host) instead of a
+    // copy-engine transfer, which would queue behind other streams' large
+    // device-to-host copies (adaspmv_run_batch lanes)
     int64_t* h_scalars = nullptr;
+    int64_t* h_scalars_dev = nullptr;  // device alias of h_scalars
     DevBuf d_scalars;  // 64 int64 slots
+    // per-tile head/tail partials of the LB row kernels (kernels_row.cu):
+    // context-owned so that contexts sharing a matrix never share them
+    DevBuf lb_partials;
     // pinned staging for host vector uploads
     void* h_stage = nullptr;
     size_t h_stage_cap = 0;
+    // lanes of adaspmv_run_batch, created on first use and kept
+    std::vector<std::unique_ptr<BatchLane>> lanes;
     void* stage(size_t bytes);  // pinned host buffer of >= bytes
     void sync() { ADA_CUDA(cudaStreamSynchronize(stream)); }
     int64_t* dscal(int i) { return d_scalars.as<int64_t>() + i; }
     // D2H one device int64 (synchronises the stream)
     int64_t fetch_scalar(const int64_t* d);
+    // h_scalars[0..n) = d[0..n) (synchronises the stream)
+    void fetch_scalars(const int64_t* d, int n);
 };
 
 // LB tiles of the row-major kernels: fixed kRowTile nonzeros per warp
@@ -154,7 +168,9 @@ struct Matrix {
     DevBuf tile_head;
     DevBuf empty_rows;        // int32 ids of rows with no entries (written by the LB fix-up)
     int64_t n_empty = 0;
-    DevBuf tile_partials;   // per tile: head partial, tail partial (V) + tail row (int64)
+    // guards the lazily-built structures (row-bin layout) when several
+    // contexts (adaspmv_run_batch lanes) multiply with the same matrix
+    mutable std::mutex lazy;
     double feat[9] = {0};
     int64_t max_col_deg = 0;
     double avg_col = 0;
@@ -216,6 +232,15 @@ struct Output {
     }
 };
 
+// One lane of a batched multiply: its own stream (context), operand and
+// output, so that lanes overlap their copies and kernels.
+struct BatchLane {
+    Context c;
+    Vector v;
+    Output y;
+    ~BatchLane();
+};
+
 // One decision tree: flat node array.
 struct Tree {
     int target = 0;          // 0 pattern, 1 workload, 2 write-back
@@ -232,6 +257,15 @@ struct Bundle {
 };
 
 // ---- entry points implemented in the .cu/.cpp files ------------------------
+// context set-up / tear-down (capi.cpp): stream (own unless given), pinned
+// scalars, device pool release threshold
+void context_init(Context& ctx, int device, cudaStream_t stream);
+void context_release(Context& ctx);
+
+// adaspmv_run_batch (batch.cpp)
+void run_batch(Context& ctx, const Matrix& m, const Bundle* b, int forced, const adaspmv_config& cfg,
+               int64_t count, const adaspmv_host_operand* xs, adaspmv_host_result* ys, int lanes);
+
 Matrix* matrix_create_device(Context& ctx, int64_t rows, int64_t cols, int64_t nnz,
                              const int64_t* d_ro, const int32_t* d_ci, const void* d_vals,
                              int dtype, bool pattern);
@@ -251,6 +285,8 @@ void vector_ensure_mask(Context& ctx, Vector& v);
 void vector_ensure_eff(Context& ctx, Vector& v, const Matrix& m);  // also sparse
 int64_t vector_nnz(Context& ctx, Vector& v);
 int64_t vector_nnz_s(Context& ctx, Vector& v, const Matrix& m);
+// dst[i] = src[i], i < n <= 64, by one thread on ctx's stream (dst: mapped host)
+void copy_scalars_kernel_launch(Context& ctx, const int64_t* src, int64_t* dst, int n);
 // out[k] = in[k] (int32 device indices -> int64), on ctx's stream
 void widen_indices(Context& ctx, int64_t n, const int32_t* in, int64_t* out);
 

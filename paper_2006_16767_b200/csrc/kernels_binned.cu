@@ -615,6 +615,10 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
                     int64_t force_rows, int64_t tile_cap, int cluster, int panel_kib) {
     if (cluster < 0 || cluster > 2) invalid("bin_cluster must be 0, 1 or 2");
     const int creq = cluster == 0 ? kBinClusterAuto : cluster;
+    // the layout and tile plan are built once, under the matrix's lock, and
+    // completed on this stream before another context may launch from them
+    std::unique_lock<std::mutex> lk(m.lazy);
+    bool built_now = false;
     if (!m.bins->built || m.bins->force_rows != force_rows || m.bins->dtype != m.dtype ||
         m.bins->cluster_req != creq) {
         m.bins.reset(new BinLayout());
@@ -622,6 +626,7 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
         m.bins->cluster_req = creq;
         m.bins->dtype = m.dtype;
         build_layout<V>(ctx, m, *m.bins);
+        built_now = true;
     }
     BinLayout& L = *m.bins;
     // column panels (opt-in): x streamed in pieces of panel_kib.  Off by
@@ -630,7 +635,10 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
     // in L2; the bound is the L1 data pipe)
     const int64_t chunk_bytes = (int64_t(1) << L.cw) * static_cast<int64_t>(sizeof(V));
     const int64_t pbytes = panel_kib > 0 ? int64_t(panel_kib) * 1024 : INT64_MAX / 2;
+    const int64_t plan0[2] = {L.tile_cap, L.panel_chunks};
     plan_tiles(ctx, m, L, tile_cap, std::max<int64_t>(pbytes / chunk_bytes, 1));
+    if (built_now || plan0[0] != L.tile_cap || plan0[1] != L.panel_chunks) ctx.sync();
+    lk.unlock();
     if (m.rows == 0) return;
     if (L.multi) fill_value<V, SR>(ctx, y, m.rows);
     const size_t smem = sizeof(V) * static_cast<size_t>(L.R);

@@ -369,7 +369,8 @@ void launch_lb(Context& ctx, const Matrix& m, const V* x, const uint32_t* mask, 
         return;
     }
     const int64_t T = m.n_row_tiles;
-    V* head = reinterpret_cast<V*>(m.tile_partials.p);
+    // head partial, tail partial (V) and tail row (int64) per tile
+    V* head = static_cast<V*>(ctx.lb_partials.ensure((2 * sizeof(V) + sizeof(int64_t)) * static_cast<size_t>(T)));
     V* tail = head + T;
     int64_t* trow = reinterpret_cast<int64_t*>(tail + T);
     row_lb_kernel<V, VALIDATE, SR><<<static_cast<unsigned>((T + kWarps - 1) / kWarps), kNT, 0, ctx.stream>>>(

@@ -132,9 +132,6 @@ void build_tiles(Context& ctx, Matrix& m) {
     scan3(ctx, m.rows, EmptyRowIn{m.row_off.as<int64_t>()}, EmptyRowEpi{m.empty_rows.as<int32_t>()},
           ctx.dscal(3), ctx.scratch[5]);
     m.n_empty = ctx.fetch_scalar(ctx.dscal(3));
-    // head partial, tail partial (V) and tail row (int64) per tile
-    m.tile_partials.ensure((2 * static_cast<size_t>(m.vbytes()) + sizeof(int64_t)) *
-                           static_cast<size_t>(std::max<int64_t>(m.n_row_tiles, 1)));
 }
 
 // degree statistics: slot[0] = max, [1] = min, [2] = sum of squares (u64)

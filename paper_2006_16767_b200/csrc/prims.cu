@@ -46,4 +46,13 @@ __global__ void __launch_bounds__(kRsThreads) radix_upsweep_kernel(const uint32_
     counts[static_cast<int64_t>(threadIdx.x) * ntiles + blockIdx.x] = hist[threadIdx.x];
 }
 
+__global__ void copy_scalars_kernel(const int64_t* __restrict__ src, volatile int64_t* dst, int n) {
+    if (static_cast<int>(threadIdx.x) < n) dst[threadIdx.x] = src[threadIdx.x];
+}
+
+void copy_scalars_kernel_launch(Context& ctx, const int64_t* src, int64_t* dst, int n) {
+    copy_scalars_kernel<<<1, 64, 0, ctx.stream>>>(src, dst, n);
+    ADA_LAUNCHED(ctx);
+}
+
 }  // namespace ada

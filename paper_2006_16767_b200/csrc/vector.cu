@@ -295,8 +295,7 @@ int64_t vector_nnz_s(Context& ctx, Vector& v, const Matrix& m) {
             dense_counts_kernel<float><<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(v.n, v.dense.as<float>(),
                                                                                         m.col_off.as<int64_t>(), out);
         ADA_LAUNCHED(ctx);
-        ADA_CUDA(cudaMemcpyAsync(ctx.h_scalars, out, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
-        ctx.sync();
+        ctx.fetch_scalars(reinterpret_cast<const int64_t*>(out), 2);
         v.nnz = ctx.h_scalars[0];
         v.nnz_s = ctx.h_scalars[1];
         v.nnz_s_matrix = m.id;
