@@ -162,7 +162,11 @@ void run_batch(Context& ctx, const Matrix& m, const Bundle* b, int forced, const
         const size_t i = static_cast<size_t>(a), j = static_cast<size_t>(b);
         const bool fa = in_b[i] < out_b[i], fb = in_b[j] < out_b[j];
         if (fa != fb) return fa;
-        return fa ? in_b[i] < in_b[j] : out_b[i] > out_b[j];
+        // ties (equal keys) go to the operand that frees the other copy
+        // direction sooner: the smaller input in the second group, the
+        // larger result in the first
+        if (fa) return in_b[i] != in_b[j] ? in_b[i] < in_b[j] : out_b[i] > out_b[j];
+        return out_b[i] != out_b[j] ? out_b[i] > out_b[j] : in_b[i] < in_b[j];
     });
     std::atomic<int64_t> next{0};
     std::atomic<bool> stop{false};
