@@ -289,13 +289,13 @@ int adaspmv_matrix_from_triplets(adaspmv_ctx* ctx, int64_t rows, int64_t cols, i
         need(out, "out");
         check_dtype(dtype);
         if (count < 0) ada::invalid("negative triplet count");
-        std::vector<double> tv(static_cast<size_t>(count));
-        for (int64_t i = 0; i < count; ++i)
-            tv[static_cast<size_t>(i)] = dtype == ADASPMV_F64 ? static_cast<const double*>(t_values)[i]
-                                                              : static_cast<const float*>(t_values)[i];
-        ada::HostCsr h = ada::csr_from_triplets(rows, cols, count, t_rows, t_cols, tv.data(),
-                                                dtype == ADASPMV_F32);
-        *out = from_host(*ctx, h, dtype);
+        if (count > 0) {
+            need(t_rows, "rows");
+            need(t_cols, "cols");
+            need(t_values, "values");
+        }
+        *out = static_cast<adaspmv_matrix*>(
+            ada::matrix_from_triplets_device(*ctx, rows, cols, count, t_rows, t_cols, t_values, dtype));
     });
 }
 
@@ -305,8 +305,21 @@ int adaspmv_matrix_load(adaspmv_ctx* ctx, const char* path, int dtype, adaspmv_m
         need(out, "out");
         need(path, "path");
         check_dtype(dtype);
-        ada::HostCsr h = ada::load_matrix_file(path, dtype);
-        *out = from_host(*ctx, h, dtype);
+        ada::HostMatrixFile h = ada::load_matrix_file(path, dtype);
+        if (h.is_csr) {
+            *out = from_host(*ctx, h.csr, dtype);
+            return;
+        }
+        ada::HostTriplets& t = h.trip;
+        const int64_t n = static_cast<int64_t>(t.r.size());
+        if (dtype == ADASPMV_F64) {
+            *out = static_cast<adaspmv_matrix*>(
+                ada::matrix_from_triplets_device(*ctx, t.rows, t.cols, n, t.r.data(), t.c.data(), t.v.data(), dtype));
+        } else {  // real_t = float: the parsed double narrowed once, as the reference's float build
+            std::vector<float> v32(t.v.begin(), t.v.end());
+            *out = static_cast<adaspmv_matrix*>(
+                ada::matrix_from_triplets_device(*ctx, t.rows, t.cols, n, t.r.data(), t.c.data(), v32.data(), dtype));
+        }
     });
 }
 

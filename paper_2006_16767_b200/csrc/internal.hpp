@@ -316,9 +316,24 @@ struct HostCsr {
     std::vector<int64_t> row_offsets, col_indices;
     std::vector<double> values;  // widened; narrowed per dtype at upload
 };
-HostCsr csr_from_triplets(int64_t rows, int64_t cols, int64_t count, const int64_t* tr,
-                          const int64_t* tc, const double* tv, bool round_f32);
-HostCsr load_matrix_file(const std::string& path, int dtype);
+// Matrix Market coordinate entries in file order (symmetric entries
+// mirrored right after their source), 0-based, values as parsed (double)
+struct HostTriplets {
+    int64_t rows = 0, cols = 0;
+    std::vector<int64_t> r, c;
+    std::vector<double> v;
+};
+struct HostMatrixFile {
+    bool is_csr = false;  // ASPMVBIN: csr; Matrix Market: trip
+    HostCsr csr;
+    HostTriplets trip;
+};
+HostTriplets load_mm(const std::string& path);  // parallel, serial on any irregularity
+HostMatrixFile load_matrix_file(const std::string& path, int dtype);
+// DualMatrix::from_triplets (sparse.hpp:220-258) on the device (ingest.cu);
+// h_v holds `count` values of `dtype`
+Matrix* matrix_from_triplets_device(Context& ctx, int64_t rows, int64_t cols, int64_t count, const int64_t* h_r,
+                                    const int64_t* h_c, const void* h_v, int dtype);
 void write_matrix_market_file(const std::string& path, int64_t rows, int64_t cols,
                               const std::vector<int64_t>& ro, const std::vector<int64_t>& ci,
                               const std::vector<double>& vals);

@@ -9,6 +9,10 @@ Fixtures (npz):
   prims.npz               make_partition / segment_of / dense_to_sparse /
                           bitmask / sort_reduce_pairs examples
   mm_cases.npz            Matrix Market texts and the CSR the reference loads
+  triplets.npz            from_triplets cases (duplicates, unsorted, -0.0,
+                          empty rows) and a >1 MB Matrix Market file (text
+                          regenerated from its seed by big_mm_text) with the
+                          sha256 of the CSR the reference loads
 """
 from __future__ import annotations
 
@@ -117,6 +121,76 @@ def mm_cases(tmp: Path):
     np.savez_compressed(OUT / "mm_cases.npz", **rec)
 
 
+TRIPLET_CASES = [(5, 4, 12, 0), (40, 30, 400, 1), (1, 1, 3, 2), (300, 200, 6000, 3), (2000, 1500, 40000, 4),
+                 (7, 9, 0, 5)]
+
+
+def triplet_case(rows, cols, n, seed, dt):
+    """Triplets with many duplicates (coordinates drawn from a small pool),
+    input order random, some -0.0 and exact zeros."""
+    rng = np.random.default_rng(seed)
+    pool = max(1, n // 3)
+    pr = rng.integers(0, rows, pool)
+    pc = rng.integers(0, cols, pool)
+    pick = rng.integers(0, pool, n)
+    tr, tc = pr[pick].astype(np.int64), pc[pick].astype(np.int64)
+    tv = rng.uniform(-1, 1, n).astype(dt)
+    if n:
+        tv[rng.random(n) < 0.05] = -0.0
+        tv[rng.random(n) < 0.05] = 0.0
+    return tr, tc, tv
+
+
+def big_mm_text(seed=11, rows=20000, cols=15000, n=70000, symmetric=True):
+    """A ~1.7 MB Matrix Market file: comments and blank lines between
+    entries, CRLF line ends, duplicates, mixed number formats."""
+    rng = np.random.default_rng(seed)
+    r = rng.integers(1, rows + 1, n)
+    c = rng.integers(1, cols + 1, n)
+    if symmetric:
+        cols = rows
+        c = rng.integers(1, rows + 1, n)
+    v = rng.uniform(-10, 10, n)
+    lines = ["%%MatrixMarket matrix coordinate real " + ("symmetric" if symmetric else "general"),
+             "% generated", f"{rows} {cols} {n}"]
+    for i in range(n):
+        fmt = ("%.17g", "%.6e", "%.3f")[i % 3]
+        lines.append(f"{r[i]} {c[i]} " + fmt % v[i] + ("\r" if i % 7 == 0 else ""))
+        if i % 997 == 0:
+            lines.append("% a comment line")
+        if i % 1499 == 0:
+            lines.append("   ")
+    return "\n".join(lines) + "\n"
+
+
+def triplets(tmp: Path):
+    import hashlib
+    rec = {}
+    k = 0
+    for dt in (np.float64, np.float32):
+        ref = Ref(dt)
+        for rows, cols, n, seed in TRIPLET_CASES:
+            tr, tc, tv = triplet_case(rows, cols, n, seed, dt)
+            M = ref.from_triplets(rows, cols, tr, tc, tv)
+            ro, ci, cv, *_ = M.export()
+            p = f"t{k}_"
+            rec[p + "meta"] = np.array([rows, cols, n, seed, 64 if dt == np.float64 else 32], np.int64)
+            rec[p + "ro"], rec[p + "ci"], rec[p + "v"] = ro, ci, cv
+            k += 1
+    rec["nt"] = np.array([k])
+    for dt in (np.float64, np.float32):
+        ref = Ref(dt)
+        for sym in (True, False):
+            p = tmp / "big.mtx"
+            p.write_text(big_mm_text(symmetric=sym))
+            M = ref.load_matrix(p)
+            ro, ci, cv, *_ = M.export()
+            h = hashlib.sha256(ro.tobytes() + ci.tobytes() + cv.tobytes()).hexdigest()
+            rec[f"big_{np.dtype(dt).name}_{int(sym)}_sha"] = np.array(h)
+            rec[f"big_{np.dtype(dt).name}_{int(sym)}_nnz"] = np.array([len(ci)], np.int64)
+    np.savez_compressed(OUT / "triplets.npz", **rec)
+
+
 if __name__ == "__main__":
     import tempfile
 
@@ -125,4 +199,5 @@ if __name__ == "__main__":
     prims()
     with tempfile.TemporaryDirectory() as d:
         mm_cases(Path(d))
+        triplets(Path(d))
     print(f"golden: {n64} f64 + {n32} f32 kernel cases, prims, {len(MM_TEXTS)} MM files")
