@@ -150,7 +150,7 @@ __global__ void gather_spread_kernel(const int64_t* __restrict__ ro, const int32
 // streamed through L2 and double the entries per x line (fewer L1
 // wavefronts per gather instruction).
 template <class V, int SR, bool MASKED, int CL = 1, int kBinUnroll = 8, bool NOALLOC = false,
-          int kBinThreads = 1024>
+          int kBinThreads = 1024, bool PF = false>
 __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
     int64_t tile0, const int64_t* __restrict__ bin_r0, int rbits, int cw, int64_t nchunks,
     const int64_t* __restrict__ tiles, const int32_t* __restrict__ tile_bin,
@@ -171,39 +171,70 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
     const int64_t* __restrict__ co = chunk_off + bin * nchunks;
     const uint32_t rmask = (1u << rbits) - 1u;
     if (e0 < e1) {
+        // 32-bit entry offsets relative to the tile (a tile is < 2^32
+        // entries): the per-entry index, chunk and address arithmetic stays
+        // in 32-bit registers
+        const uint32_t n_e = static_cast<uint32_t>(e1 - e0);
+        const uint32_t* __restrict__ pkt = pk + e0;
+        const V* __restrict__ bvt = bv + e0;
         // chunk of the thread's first entry: largest c with co[c] <= e (binary search)
         const int64_t efirst = e0 + threadIdx.x;
-        int64_t lo = 0, hi = nchunks;
+        int lo = 0, hi = static_cast<int>(nchunks);
         while (hi - lo > 1) {
-            const int64_t mid = (lo + hi) >> 1;
+            const int mid = (lo + hi) >> 1;
             if (__ldg(co + mid) <= efirst) lo = mid;
             else hi = mid;
         }
-        int64_t c = lo;
-        int64_t nb = __ldg(co + c + 1);  // end of chunk c
-        for (int64_t base = e0; base < e1; base += static_cast<int64_t>(kBinThreads) * kBinUnroll) {
-            uint32_t p[kBinUnroll];
-            V a[kBinUnroll];
-            int col[kBinUnroll];
-            bool ok[kBinUnroll];
+        int c = lo;
+        auto chunk_end = [&](int cc) -> uint32_t {  // end of chunk cc, tile-relative, clamped
+            const int64_t v = __ldg(co + cc + 1) - e0;
+            return v < static_cast<int64_t>(n_e) ? static_cast<uint32_t>(v) : n_e;
+        };
+        uint32_t nb = chunk_end(c);
+        uint32_t cbase = static_cast<uint32_t>(c) << cw;
+        constexpr uint32_t kStep = static_cast<uint32_t>(kBinThreads) * kBinUnroll;
+        // PF: the next batch's entry words and values are loaded before this
+        // batch's gathers and shared-memory updates
+        uint32_t pn[kBinUnroll];
+        V an[kBinUnroll];
+        auto load_batch = [&](uint32_t b, uint32_t* pp, V* aa) {
 #pragma unroll
             for (int j = 0; j < kBinUnroll; ++j) {
-                const int64_t e = base + j * kBinThreads + threadIdx.x;
-                ok[j] = e < e1;
-                p[j] = ok[j] ? ld_stream(reinterpret_cast<const int*>(pk) + e) : 0;
-                if (S::kUsesValues) a[j] = ok[j] ? ld_stream(bv + e) : V(0);
-                else a[j] = V(1);
+                const uint32_t e = b + j * kBinThreads;
+                pp[j] = e < n_e ? static_cast<uint32_t>(ld_stream(reinterpret_cast<const int*>(pkt) + e)) : 0u;
+                if (S::kUsesValues) aa[j] = e < n_e ? ld_stream(bvt + e) : V(0);
+                else aa[j] = V(1);
+            }
+        };
+        if (PF) load_batch(threadIdx.x, pn, an);
+        for (uint32_t base = threadIdx.x; base < n_e; base += kStep) {
+            uint32_t p[kBinUnroll];
+            V a[kBinUnroll];
+            uint32_t col[kBinUnroll];
+            bool ok[kBinUnroll];
+#pragma unroll
+            for (int j = 0; j < kBinUnroll; ++j) ok[j] = base + j * kBinThreads < n_e;
+            if (PF) {
+#pragma unroll
+                for (int j = 0; j < kBinUnroll; ++j) {
+                    p[j] = pn[j];
+                    a[j] = an[j];
+                }
+                if (base + kStep < n_e) load_batch(base + kStep, pn, an);
+            } else {
+                load_batch(base, p, a);
             }
 #pragma unroll
             for (int j = 0; j < kBinUnroll; ++j) {
-                const int64_t e = base + j * kBinThreads + threadIdx.x;
-                if (ok[j]) {
-                    while (e >= nb) {
+                const uint32_t e = base + j * kBinThreads;
+                if (ok[j] && e >= nb) {
+                    do {
                         ++c;
-                        nb = __ldg(co + c + 1);
-                    }
+                        nb = chunk_end(c);
+                    } while (e >= nb);
+                    cbase = static_cast<uint32_t>(c) << cw;
                 }
-                col[j] = static_cast<int>((static_cast<uint32_t>(c) << cw) + (p[j] >> rbits));
+                col[j] = cbase + (p[j] >> rbits);
             }
             if (MASKED) {
 #pragma unroll
@@ -212,7 +243,8 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
             }
             V xv[kBinUnroll];
 #pragma unroll
-            for (int j = 0; j < kBinUnroll; ++j) xv[j] = ok[j] ? (NOALLOC ? ld_stream(x + col[j]) : __ldg(x + col[j])) : S::zero();
+            for (int j = 0; j < kBinUnroll; ++j)
+                xv[j] = ok[j] ? (NOALLOC ? ld_stream(x + col[j]) : __ldg(x + col[j])) : S::zero();
 #pragma unroll
             for (int j = 0; j < kBinUnroll; ++j) {
                 if (!ok[j]) continue;
