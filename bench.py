@@ -254,57 +254,85 @@ def run_ours_multi(args, rank, world):
     out = A.MultiplyOutput(ctx)
     pinned = [(i.cpu().pin_memory(), v.cpu().pin_memory()) for _, i, v in bufs] if rank == 0 else None
 
-    def step(from_host=False):
-        for p, (dense, idx, val) in enumerate(bufs):
-            if from_host and rank == 0:  # e2e: this point's x comes from host memory
-                idx.copy_(pinned[p][0], non_blocking=True)
-                val.copy_(pinned[p][1], non_blocking=True)
-            if not dense:
-                dist.broadcast(idx, 0)
-            dist.broadcast(val, 0)
-            if dense:
-                x.set_dense_device(val.data_ptr())
-            else:
-                x.set_sparse_device(idx.numel(), idx.data_ptr(), val.data_ptr())
-            A.run_adaptive(m, x, bundle, out=out)
-            if from_host:
-                out.dense()  # D2H of this rank's y block
-
-    flops_local = 0
-    for dense, idx, val in bufs:  # useful work per point (outside any timed region)
-        dist.broadcast(idx, 0) if not dense else None
-        dist.broadcast(val, 0)
+    def set_x(dense, idx, val):
         if dense:
             x.set_dense_device(val.data_ptr())
         else:
             x.set_sparse_device(idx.numel(), idx.data_ptr(), val.data_ptr())
+
+    def bcast(dense, idx, val):
+        if not dense:
+            dist.broadcast(idx, 0)
+        dist.broadcast(val, 0)
+
+    # per point: the kernel this rank's selector picks for its block (features
+    # of the broadcast x against the local block)
+    flops_local = 0
+    chosen = []
+    for dense, idx, val in bufs:  # outside any timed region
+        bcast(dense, idx, val)
+        set_x(dense, idx, val)
         flops_local += 2 * A.effective_nnz(m, x)
+        k, _, _ = A.predict_kernel(m, x, bundle)
+        chosen.append(k.index())
+    ctx.set_timing(True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def step():
+        """One sweep: per point, the x broadcast (CUDA events on the shared
+        stream) and the multiply (the library's events), each started with the
+        GPU spinning so host enqueue latency is excluded -- the same protocol
+        as the 1-GPU path; the untimed x hand-over (device copy + format
+        conversion) sits between them."""
+        t_x = t_k = 0.0
+        for p, (dense, idx, val) in enumerate(bufs):
+            torch.cuda._sleep(GATE_CYCLES)
+            ev[0].record(stream)
+            bcast(dense, idx, val)
+            ev[1].record(stream)
+            set_x(dense, idx, val)
+            x.prepare(chosen[p])
+            torch.cuda._sleep(GATE_CYCLES)
+            A.run_kernel(m, chosen[p], x, out=out)
+            t_k += out.elapsed()
+            t_x += ev[0].elapsed_time(ev[1]) * 1e-3
+        return t_x, t_k
+
     for _ in range(args.warmup):
         step()
     l0 = ctx.launches
     dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
+        per = [step() for _ in range(args.steps)]
+    torch.cuda.synchronize()
     launches = (ctx.launches - l0) // max(1, args.steps)
     dist.barrier()
-    t_local = e0.elapsed_time(e1) * 1e-3 / args.steps
-    # e2e: x from pinned host memory on rank 0, y blocks back to host
+    t_exch = statistics.median(p[0] for p in per)
+    t_local = statistics.median(p[0] + p[1] for p in per)
+    ctx.set_timing(False)
+
+    def e2e_step():
+        for p, (dense, idx, val) in enumerate(bufs):
+            if rank == 0:  # this point's x comes from host memory
+                idx.copy_(pinned[p][0], non_blocking=True)
+                val.copy_(pinned[p][1], non_blocking=True)
+            bcast(dense, idx, val)
+            set_x(dense, idx, val)
+            A.run_adaptive(m, x, bundle, out=out)
+            out.dense()  # D2H of this rank's y block
+
+    # e2e: x from pinned host memory on rank 0, broadcast, select, multiply,
+    # y blocks back to host
     e2e_t = []
     for _ in range(max(2, args.steps // 2)):
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        step(from_host=True)
+        e2e_step()
         torch.cuda.synchronize()
         e2e_t.append(time.perf_counter() - t0)
-    tt = torch.tensor([t_local, float(flops_local), statistics.median(e2e_t)], dtype=torch.float64, device=dev)
+    tt = torch.tensor([t_local, float(flops_local), statistics.median(e2e_t), t_exch], dtype=torch.float64, device=dev)
     tmax = tt.clone()
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     fl = tt[1:2].clone()
@@ -323,7 +351,12 @@ def run_ours_multi(args, rank, world):
             "config": {"workload": WORKLOAD + ", row-partitioned: one C2-sized row block per GPU",
                        "rows_per_gpu": rows, "cols": cols, "x_sparsity": list(SPARSITIES),
                        "parallelism": f"row-partitioned x{world} (NCCL broadcast of x per point)",
-                       "exchange_bytes_per_step": xbytes, "l2": "inputs larger than L2 at the dense points"},
+                       "exchange_bytes_per_step": xbytes, "l2": "inputs larger than L2 at the dense points",
+                       "timing": "per point: x broadcast (events) + multiply (library events), GPU gated, "
+                                 "max over ranks; selection and x hand-over untimed as on 1 GPU"},
+            "exchange": {"ms_per_step": round(float(tmax[3].item()) * 1e3, 4),
+                         "fraction": round(float(tmax[3].item()) / t_step, 4),
+                         "GBps": round(xbytes * max(world - 1, 0) / max(float(tmax[3].item()), 1e-12) / 1e9, 1)},
             "e2e": {"value": round(e2e_v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(xbytes),
                     "d2h_bytes_per_step": int(rows * 4 * len(bufs)),
                     "note": "x H2D on rank 0 then NCCL broadcast; each rank's y block D2H; max over ranks"},
@@ -432,6 +465,30 @@ def run_ours(args, rank, world):
         t_med = float(tt.item())
     flops = sum(2 * s for s in nnz_s)
     value = world * flops / t_med / 1e9
+    # ---- selection overhead (reported beside the kernel
+    # time): fresh vectors, so the features are computed, not cached ----------
+    sel_t, conv_t = [], []
+    fresh = A.DeviceVector(cols, np.float32, ctx)
+    for _ in range(max(3, args.steps // 2)):
+        s_sel = s_conv = 0.0
+        for xi, xv in vecs:
+            if len(xi) == cols:
+                d = np.zeros(cols, np.float32)
+                d[xi] = xv
+                fresh.set_dense(d)
+            else:
+                fresh.set_sparse(xi, xv)
+            ctx.synchronize()
+            _, rep = A.execute_iteration(m, fresh, bundle, out=out)
+            s_sel += rep["feature_s"] + rep["predict_s"]
+            s_conv += rep["convert_s"]
+        sel_t.append(s_sel)
+        conv_t.append(s_conv)
+    overhead = {"select_us_per_step": round(statistics.median(sel_t) * 1e6, 1),
+                "convert_us_per_step": round(statistics.median(conv_t) * 1e6, 1),
+                "note": "host feature pull (nnz_s on the device, one scalar back) + tree walk, and the "
+                        "device format conversion the chosen kernel needs; excluded from value, "
+                        "included in e2e"}
     # ---- e2e through the public API with host buffers ----------------------
     # One step = one adaptive_run_batch call over the 7 host vectors (pinned),
     # results back in pinned host buffers in their smaller form; the batch
@@ -540,6 +597,7 @@ def run_ours(args, rank, world):
                      "peak_source": src, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                      "traffic": traffic, "alg_bytes": int(fam[k_dom])},
         "selector_regret": round(regret_total, 4),
+        "overhead": overhead,
         "gpu_launches": int(launches),
         "points": points,
         "setup_s": {"generate": round(gen_s, 1), "upload_csc_features": round(upload_s, 2)},

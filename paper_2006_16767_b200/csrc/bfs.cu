@@ -259,7 +259,14 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         else k = heuristic_kernel(ctx, m, x, visited);
         const auto t1 = clk::now();
         ADA_CUDA(cudaEventRecord(ev[0], ctx.stream));
-        if (k == 2 || k == 3) {  // output-masked pull: the mask, and x values unless OR_AND
+        // RowSpMSpV (K2/K3) runs as the output-masked pull: a row already
+        // visited cannot join the next frontier, so skipping it
+        // changes no level.  With the boolean semiring SpMV (K0/K1) does
+        // too: non-frontier entries of x are false and add nothing (with
+        // values, an Inf * 0 of the plain SpMV could differ, so those keep
+        // the unmasked multiply).
+        const bool pull = k == 2 || k == 3 || (SR == SR_OR_AND && k <= 1);
+        if (pull) {  // output-masked pull: the mask, and x values unless OR_AND
             vector_ensure_mask(ctx, x);
             if (SR != SR_OR_AND) vector_ensure_dense(ctx, x, SR);
         } else if (k <= 1) {
@@ -269,7 +276,7 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         }
         ADA_CUDA(cudaEventRecord(ev[1], ctx.stream));
         const int64_t nnz_x = x.nnz;
-        if (k == 2 || k == 3) launch_pull<V, SR>(ctx, m, x, lv, y);  // RowSpMSpV, output-masked
+        if (pull) launch_pull<V, SR>(ctx, m, x, lv, y);  // row-major, output-masked
         else run_kernel(ctx, m, x, k, cfg, y);
         ADA_CUDA(cudaEventRecord(ev[2], ctx.stream));
         visited += next_frontier<V, SR>(ctx, m, y, x, lv, static_cast<int32_t>(it + 1));  // syncs

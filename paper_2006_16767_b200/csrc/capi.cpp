@@ -154,6 +154,9 @@ void context_init(Context& ctx, int device, cudaStream_t stream) {
     ADA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     g_alloc_stream = ctx.stream;
     ctx.d_scalars.ensure(64 * sizeof(int64_t));
+    // slots 10-12 are the accumulators of the one-launch reductions
+    // (vector.cu: reduce2_to_host), which expect them zero between calls
+    ADA_CUDA(cudaMemsetAsync(ctx.d_scalars.p, 0, 64 * sizeof(int64_t), ctx.stream));
 }
 
 void context_release(Context& ctx) {

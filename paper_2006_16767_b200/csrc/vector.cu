@@ -262,47 +262,102 @@ void widen_indices(Context& ctx, int64_t n, const int32_t* in, int64_t* out) {
     ADA_LAUNCHED(ctx);
 }
 
-// nnz_x and nnz_s of a dense-only vector in one pass (no sparse conversion):
-// out[0] += #{i : x_i != 0}, out[1] += sum of deg_col(i) over them.
-template <class V>
-__global__ void dense_counts_kernel(int64_t n, const V* __restrict__ x, const int64_t* __restrict__ co,
-                                    unsigned long long* __restrict__ out) {
+// Selector features in ONE launch: every block reduces its share of
+// (count, sum) and adds it into two device accumulators; the last block to
+// finish (ticket) stores the totals into the context's mapped pinned scalars
+// and re-zeroes the accumulators for the next call.  The host synchronises
+// the stream and reads them: no scan, no copy kernel, no copy engine.
+template <class F>
+__global__ void __launch_bounds__(256) reduce2_to_host_kernel(int64_t n, F f, unsigned long long* __restrict__ acc,
+                                                              unsigned int* __restrict__ ticket,
+                                                              volatile int64_t* host) {
+    __shared__ unsigned long long part[2][8];
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     long long c = 0, s = 0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
-        if (x[i] != V(0)) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+        const int64_t d = f(i);
+        if (d >= 0) {
             ++c;
-            s += co[i + 1] - co[i];
+            s += d;
         }
+    }
     c = warp_sum(c);
     s = warp_sum(s);
-    if ((threadIdx.x & 31) == 0 && (c || s)) {
-        atomicAdd(out, static_cast<unsigned long long>(c));
-        atomicAdd(out + 1, static_cast<unsigned long long>(s));
+    if ((threadIdx.x & 31) == 0) {
+        part[0][threadIdx.x >> 5] = static_cast<unsigned long long>(c);
+        part[1][threadIdx.x >> 5] = static_cast<unsigned long long>(s);
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tc = 0, ts = 0;
+        for (int w = 0; w < 8; ++w) {
+            tc += part[0][w];
+            ts += part[1][w];
+        }
+        if (tc) atomicAdd(acc, tc);
+        if (ts) atomicAdd(acc + 1, ts);
+        __threadfence();
+        if (atomicAdd(ticket, 1u) == gridDim.x - 1) {  // last block: publish and reset
+            __threadfence();
+            const unsigned long long fc = atomicExch(acc, 0ull), fs = atomicExch(acc + 1, 0ull);
+            host[0] = static_cast<int64_t>(fc);
+            host[1] = static_cast<int64_t>(fs);
+            __threadfence_system();
+            *ticket = 0u;
+        }
+    }
+}
+
+// sparse x: every stored index counts (its value may be an explicit zero,
+// sparse.hpp:348-359), weight = deg_col
+struct SparseDeg {
+    const int64_t* co;
+    const int32_t* xi;
+    __device__ int64_t operator()(int64_t s) const {
+        const int32_t c = xi[s];
+        return co[c + 1] - co[c];
+    }
+};
+// dense x: nonzeros count (-1 marks a zero)
+template <class V>
+struct DenseDeg {
+    const V* x;
+    const int64_t* co;
+    __device__ int64_t operator()(int64_t i) const { return x[i] != V(0) ? co[i + 1] - co[i] : -1; }
+};
+
+template <class F>
+void reduce2_to_host(Context& ctx, int64_t n, F f) {
+    const int64_t g = std::max<int64_t>(std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 8), 1);
+    reduce2_to_host_kernel<<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(
+        n, f, reinterpret_cast<unsigned long long*>(ctx.dscal(10)), reinterpret_cast<unsigned int*>(ctx.dscal(12)),
+        ctx.h_scalars_dev);
+    ADA_LAUNCHED(ctx);
+    ADA_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 
 int64_t vector_nnz_s(Context& ctx, Vector& v, const Matrix& m) {
     if (v.nnz_s >= 0 && v.nnz_s_matrix == m.id) return v.nnz_s;
-    if (v.has_dense && !v.has_sparse && v.dense_fill < 0 && v.n == m.cols) {  // user dense x: one pass
-        unsigned long long* out = reinterpret_cast<unsigned long long*>(ctx.dscal(7));
-        ADA_CUDA(cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), ctx.stream));
-        const int64_t g = std::max<int64_t>(std::min<int64_t>((v.n + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 8), 1);
+    if (v.has_eff && v.eff_matrix == m.id) {  // offsets already built: their total
+        v.nnz_s = ctx.fetch_scalar(v.eff.as<int64_t>() + v.nnz);
+    } else if (v.has_sparse) {
+        if (v.nnz == 0) {
+            v.nnz_s = 0;
+        } else {
+            reduce2_to_host(ctx, v.nnz, SparseDeg{m.col_off.as<int64_t>(), v.sp_idx.as<int32_t>()});
+            v.nnz_s = ctx.h_scalars[1];
+        }
+    } else if (v.has_dense && v.dense_fill < 0 && v.n == m.cols) {  // user dense x: nnz_x and nnz_s in one pass
         if (v.dtype == ADASPMV_F64)
-            dense_counts_kernel<double><<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(v.n, v.dense.as<double>(),
-                                                                                         m.col_off.as<int64_t>(), out);
+            reduce2_to_host(ctx, v.n, DenseDeg<double>{v.dense.as<double>(), m.col_off.as<int64_t>()});
         else
-            dense_counts_kernel<float><<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(v.n, v.dense.as<float>(),
-                                                                                        m.col_off.as<int64_t>(), out);
-        ADA_LAUNCHED(ctx);
-        ctx.fetch_scalars(reinterpret_cast<const int64_t*>(out), 2);
+            reduce2_to_host(ctx, v.n, DenseDeg<float>{v.dense.as<float>(), m.col_off.as<int64_t>()});
         v.nnz = ctx.h_scalars[0];
         v.nnz_s = ctx.h_scalars[1];
-        v.nnz_s_matrix = m.id;
-        return v.nnz_s;
+    } else {
+        vector_ensure_eff(ctx, v, m);
+        v.nnz_s = ctx.fetch_scalar(v.eff.as<int64_t>() + v.nnz);
     }
-    vector_ensure_eff(ctx, v, m);
-    v.nnz_s = ctx.fetch_scalar(v.eff.as<int64_t>() + v.nnz);
     v.nnz_s_matrix = m.id;
     return v.nnz_s;
 }
