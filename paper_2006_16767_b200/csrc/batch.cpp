@@ -158,8 +158,14 @@ void run_batch(Context& ctx, const Matrix& m, const Bundle* b, int forced, const
         out_b[i] = ys[k].form == ADASPMV_RESULT_DENSE ? dense_out
                    : ys[k].form == ADASPMV_RESULT_SPARSE ? sp_out : std::min(sp_out, dense_out);
     }
+    // Operands whose copies are small (< 2 MB both ways) are cheap for the
+    // copy engines but still hold a lane for a few synchronisations: they go
+    // after the large ones so the large transfers start at once.
+    constexpr double kSmall = 2.0 * (1 << 20);
     std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
         const size_t i = static_cast<size_t>(a), j = static_cast<size_t>(b);
+        const bool sa = in_b[i] + out_b[i] < kSmall, sb = in_b[j] + out_b[j] < kSmall;
+        if (sa != sb) return sb;
         const bool fa = in_b[i] < out_b[i], fb = in_b[j] < out_b[j];
         if (fa != fb) return fa;
         // ties (equal keys) go to the operand that frees the other copy
