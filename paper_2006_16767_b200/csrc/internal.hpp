@@ -142,7 +142,7 @@ struct BinLayout {
     DevBuf pk, bv, chunk_off;
     std::vector<int64_t> bin_start;  // host: first entry of each bin, [nbins] = nnz
     std::vector<int64_t> h_chunk_off;  // host copy of chunk_off (panel tile planning)
-    int64_t tile_cap = -1, ntiles = 0, panel_chunks = -1;
+    int64_t tile_cap = -1, tile_cap_req = -1, ntiles = 0, panel_chunks = -1;
     std::vector<int64_t> panel_tile0;  // first tile of each column panel, [npanels] = ntiles
     bool multi = false;       // some bin is split into several tiles
     // heavy rows (degree > heavy_min) are left out of the bins (their entries

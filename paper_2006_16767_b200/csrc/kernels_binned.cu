@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <array>
+#include <functional>
 #include <numeric>
 #include <vector>
 
@@ -457,6 +458,12 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
     const int64_t per_bin = m.nnz / nbins + 1;
     L.heavy_min = m.feat[3] > static_cast<double>(kHeavySeg / 2)
                       ? std::max<int64_t>(kHeavySeg / 2, per_bin / 512) : 0;
+    // Skewed (power-law) matrices: hub rows meet hub columns, so in the low
+    // columns of a bin the same rows recur inside one warp's 32-entry window
+    // and serialise on their shared-memory slots even at modest degree.
+    // Measured on B200 (row degree cut 4096/2048/1024/512/256): R-MAT 20
+    // 269/186/142/142/138 us, R-MAT 22 654/566/566/548/585 us.
+    if (m.feat[8] > 0.5 && m.feat[3] > 512.0) L.heavy_min = 512;
     std::vector<int64_t> cuts;
     if (L.force_rows > 0 || L.cluster == 2 || m.nnz == 0) {  // equal-height bins
         const int64_t R0 = std::max<int64_t>((m.rows + nbins - 1) / nbins, 1);
@@ -541,15 +548,58 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
 // Tiles: every bin gets ceil(count / cap) equal column-contiguous tiles (at
 // least one, so its rows are written); heaviest first (longest-processing-
 // time order for the hardware block scheduler).
+// Tile cap (entries per CTA) for the single-panel plan: the one-wave
+// makespan of heaviest-first list scheduling of the bins' tiles over the SMs
+// (the order the tiles are launched in), over caps of 0.5-1.5x the fair share.
+// A tile costs its entries plus its y segment: zeroing and a coalesced store
+// for a whole bin, an atomic combine (~4x) for a split one.  Uniform matrices
+// keep one tile per bin; skewed ones (R-MAT) trade splits against the second
+// partial wave that a 1.25x cap leaves.
+int64_t choose_cap(const BinLayout& L, int sms, int64_t nnz) {
+    const double fair = static_cast<double>(nnz) / static_cast<double>(sms);
+    const double seg = static_cast<double>(L.R);
+    int64_t best_cap = std::max<int64_t>(static_cast<int64_t>(fair * 1.25), 16384);
+    double best = 1e300;
+    std::vector<double> cost;
+    for (int f = 50; f <= 150; f += 5) {
+        const int64_t cap = std::max<int64_t>(static_cast<int64_t>(fair * f / 100.0), 16384);
+        cost.clear();
+        for (int64_t b = 0; b < L.nbins; ++b) {
+            const int64_t n = L.bin_start[static_cast<size_t>(b + 1)] - L.bin_start[static_cast<size_t>(b)];
+            const int64_t k = std::max<int64_t>((n + cap - 1) / cap, 1);
+            for (int64_t i = 0; i < k; ++i)
+                cost.push_back(static_cast<double>(n) / static_cast<double>(k) + (k > 1 ? 4.0 : 1.0) * seg);
+        }
+        std::sort(cost.begin(), cost.end(), std::greater<double>());
+        std::vector<double> sm(static_cast<size_t>(sms), 0.0);  // min-heap of SM finish times
+        std::make_heap(sm.begin(), sm.end(), std::greater<double>());
+        double span = 0;
+        for (double c : cost) {
+            std::pop_heap(sm.begin(), sm.end(), std::greater<double>());
+            sm.back() += c;
+            span = std::max(span, sm.back());
+            std::push_heap(sm.begin(), sm.end(), std::greater<double>());
+        }
+        if (span < best * 0.999) {
+            best = span;
+            best_cap = cap;
+        }
+    }
+    return best_cap;
+}
+
 void plan_tiles(Context& ctx, const Matrix& m, BinLayout& L, int64_t cap_req, int64_t panel_chunks) {
+    panel_chunks = std::min<int64_t>(std::max<int64_t>(panel_chunks, 1), L.nchunks);
+    if (L.cluster == 2) panel_chunks = L.nchunks;  // pairs: one panel
+    if (L.tile_cap_req == cap_req && L.panel_chunks == panel_chunks && L.tile_cap >= 0) return;
     int64_t cap = cap_req;
     if (cap <= 0) {
         const double fair = static_cast<double>(m.nnz) / static_cast<double>(ctx.sm_count);
-        cap = std::max<int64_t>(static_cast<int64_t>(fair * 1.25), 16384);
+        cap = L.cluster == 1 && panel_chunks == L.nchunks
+                  ? choose_cap(L, ctx.sm_count, m.nnz)
+                  : std::max<int64_t>(static_cast<int64_t>(fair * 1.25), 16384);
     }
-    panel_chunks = std::min<int64_t>(std::max<int64_t>(panel_chunks, 1), L.nchunks);
-    if (L.cluster == 2) panel_chunks = L.nchunks;  // pairs: one panel
-    if (L.tile_cap == cap && L.panel_chunks == panel_chunks) return;
+    L.tile_cap_req = cap_req;
     // Column panels of `panel_chunks` chunks are launched one after another;
     // within a panel a work unit is one CTA (cluster 1) or a CTA pair
     // (cluster 2) of <= `cap` entries per CTA, a bin's units being equal
@@ -667,9 +717,9 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
     // in L2; the bound is the L1 data pipe)
     const int64_t chunk_bytes = (int64_t(1) << L.cw) * static_cast<int64_t>(sizeof(V));
     const int64_t pbytes = panel_kib > 0 ? int64_t(panel_kib) * 1024 : INT64_MAX / 2;
-    const int64_t plan0[2] = {L.tile_cap, L.panel_chunks};
+    const int64_t plan0[2] = {L.ntiles, L.panel_chunks};
     plan_tiles(ctx, m, L, tile_cap, std::max<int64_t>(pbytes / chunk_bytes, 1));
-    if (built_now || plan0[0] != L.tile_cap || plan0[1] != L.panel_chunks) ctx.sync();
+    if (built_now || plan0[0] != L.ntiles || plan0[1] != L.panel_chunks) ctx.sync();
     lk.unlock();
     if (m.rows == 0) return;
     if (L.multi) fill_value<V, SR>(ctx, y, m.rows);

@@ -94,6 +94,30 @@ def A_abs(m, c2):
     return _ABS["m"]
 
 
+def test_c2_batch_sweep_vs_oracle(c2, port):
+    """The e2e path of bench.py: one adaptive_run_batch over the C2 sweep's host
+    vectors (int64-indexed sparse points, a dense 100 % point), results in
+    their smaller form, each checked against the oracle."""
+    rows, cols, ro, ci, vals, m = c2
+    bundle = A.SelectorBundle.load(S.DEFAULT_PATH)
+    xs, dense = [], []
+    for i, sp in enumerate((1e-5, 1e-3, 0.1, 0.5, 1.0)):
+        nx = max(1, int(round(sp * cols)))
+        xi, xv = synth.sparse_vector(cols, nx, seed=77 + i, dtype=np.float32)
+        d = np.zeros(cols, np.float32)
+        d[xi] = xv
+        dense.append(d)
+        xs.append(d if nx == cols else (xi, xv))
+    res = A.run_batch(m, xs, bundle=bundle, form=A.RESULT_AUTO, lanes=3)
+    for i, (r, d) in enumerate(zip(res, dense)):
+        y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, d)
+        what = f"batch op {i} kernel {r.kernel.name()}"
+        if r.is_sparse:
+            assert_sparse_match(r.sparse.indices, r.sparse.values, y_ref, bound, np.float32, what)
+        else:
+            assert_dense_close(r.dense.values, y_ref, bound, np.float32, what)
+
+
 def test_c3_class_bfs_levels(ctx, port):
     n, _, ro, ci, _ = synth.rmat(20, 16, seed=2)
     m = A.DualMatrix.from_csr(n, n, ro, ci, None, dtype=np.float32, ctx=ctx)

@@ -1,3 +1,2 @@
 #!/bin/bash
-ADASPMV_BENCH_FORCE_MULTI=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29541 bench.py --gpus 1 --steps 5 --warmup 3 > gpurun_out/bench_multi1.json; echo "rc=$?"
-ls -la gpurun_out/
+python tools/kernel_sweep.py --inputs c1 --kernels 0,1 --lanes 0,1,2 --densities 1.0 --reps 15 2>&1 | tail -6
