@@ -141,9 +141,17 @@ def triplet_case(rows, cols, n, seed, dt):
     return tr, tc, tv
 
 
-def big_mm_text(seed=11, rows=20000, cols=15000, n=70000, symmetric=True):
+def big_mm_text(seed=11, rows=20000, cols=15000, n=70000, symmetric=True, pattern=False):
     """A ~1.7 MB Matrix Market file: comments and blank lines between
     entries, CRLF line ends, duplicates, mixed number formats."""
+    if pattern:  # ~1.4 MB pattern file
+        rng = np.random.default_rng(seed + 1)
+        n = 2 * n
+        r = rng.integers(1, rows + 1, n)
+        c = rng.integers(1, cols + 1, n)
+        lines = ["%%MatrixMarket matrix coordinate pattern general", f"{rows} {cols} {n}"]
+        lines += [f"{r[i]} {c[i]}" + ("\r" if i % 5 == 0 else "") for i in range(n)]
+        return "\n".join(lines) + "\n"
     rng = np.random.default_rng(seed)
     r = rng.integers(1, rows + 1, n)
     c = rng.integers(1, cols + 1, n)
@@ -188,6 +196,14 @@ def triplets(tmp: Path):
             h = hashlib.sha256(ro.tobytes() + ci.tobytes() + cv.tobytes()).hexdigest()
             rec[f"big_{np.dtype(dt).name}_{int(sym)}_sha"] = np.array(h)
             rec[f"big_{np.dtype(dt).name}_{int(sym)}_nnz"] = np.array([len(ci)], np.int64)
+    for dt in (np.float64, np.float32):
+        p = tmp / "bigp.mtx"
+        p.write_text(big_mm_text(pattern=True))
+        M = Ref(dt).load_matrix(p)
+        ro, ci, cv, *_ = M.export()
+        rec[f"bigp_{np.dtype(dt).name}_sha"] = np.array(
+            hashlib.sha256(ro.tobytes() + ci.tobytes() + cv.tobytes()).hexdigest())
+        rec[f"bigp_{np.dtype(dt).name}_nnz"] = np.array([len(ci)], np.int64)
     np.savez_compressed(OUT / "triplets.npz", **rec)
 
 

@@ -106,3 +106,21 @@ def test_batch_invalid_operand_raises(ctx):
     # the context stays usable
     r = A.run_batch(m, [good], force_kernel=4)
     assert r[0].kernel.index() == 4
+
+
+def test_batch_many_operands_more_lanes_than_needed(ctx, port):
+    """A long batch (60 operands, more lanes than the default) and a batch
+    shorter than the lane count both return every result in order."""
+    dt = np.float32
+    rows, cols, ro, ci, vals = synth.random_csr(4000, 3000, 0.002, seed=8, dtype=dt)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    xs, dense = _batch(cols, dt, seeds=range(100, 160))
+    for lanes, sub in ((8, slice(None)), (16, slice(0, 3))):
+        res = A.run_batch(m, xs[sub], force_kernel=6, lanes=lanes)
+        assert len(res) == len(dense[sub])
+        for r, d in zip(res, dense[sub]):
+            y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, d)
+            if r.is_sparse:
+                assert_sparse_match(r.sparse.indices, r.sparse.values, y_ref, bound, dt)
+            else:
+                assert_dense_close(r.dense.values, y_ref, bound, dt)

@@ -81,6 +81,19 @@ def test_large_mm_parallel_parser_matches_reference(ctx, tmp_path, dt, sym):
     assert h == str(z[key + "_sha"])
 
 
+@pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
+def test_large_pattern_mm_matches_reference(ctx, tmp_path, dt):
+    z = np.load(GOLD / "triplets.npz")
+    p = tmp_path / "bigp.mtx"
+    p.write_text(big_mm_text(pattern=True))
+    assert p.stat().st_size > (1 << 20)
+    ro, ci, v = A.load_matrix(p, dtype=dt, ctx=ctx).download()[:3]
+    key = f"bigp_{np.dtype(dt).name}"
+    assert len(ci) == int(z[key + "_nnz"][0])
+    h = hashlib.sha256(ro.tobytes() + ci.tobytes() + v.astype(dt).tobytes()).hexdigest()
+    assert h == str(z[key + "_sha"])
+
+
 def test_large_mm_errors_report_reference_line(ctx, tmp_path):
     text = big_mm_text(symmetric=False)
     lines = text.split("\n")
