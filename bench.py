@@ -222,12 +222,19 @@ def run_ours_multi(args, rank, world):
     from paper_2006_16767_b200 import synth
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: ADASPMV_BENCH_BACKEND=gloo runs several ranks on one GPU
+    # (NCCL needs one GPU per rank) to exercise the N > 1 logic end to end
+    backend = os.environ.get("ADASPMV_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend != "nccl" else local
     dev = torch.device("cuda", local)
     torch.cuda.set_device(local)
     # stdout carries exactly one JSON line: keep NCCL's version banner off it
     if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
         os.environ["NCCL_DEBUG"] = "WARN"
-    dist.init_process_group("nccl", device_id=dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)  # collectives order against it; the library launches on it
     ctx = A.Context(local, stream=stream.cuda_stream)
