@@ -151,7 +151,7 @@ __global__ void gather_spread_kernel(const int64_t* __restrict__ ro, const int32
 // streamed through L2 and double the entries per x line (fewer L1
 // wavefronts per gather instruction).
 template <class V, int SR, bool MASKED, int CL = 1, int kBinUnroll = 8, bool NOALLOC = false,
-          int kBinThreads = 1024, bool PF = false>
+          int kBinThreads = 1024>
 __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
     int64_t tile0, const int64_t* __restrict__ bin_r0, int rbits, int cw, int64_t nchunks,
     const int64_t* __restrict__ tiles, const int32_t* __restrict__ tile_bin,
@@ -194,10 +194,6 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
         uint32_t nb = chunk_end(c);
         uint32_t cbase = static_cast<uint32_t>(c) << cw;
         constexpr uint32_t kStep = static_cast<uint32_t>(kBinThreads) * kBinUnroll;
-        // PF: the next batch's entry words and values are loaded before this
-        // batch's gathers and shared-memory updates
-        uint32_t pn[kBinUnroll];
-        V an[kBinUnroll];
         auto load_batch = [&](uint32_t b, uint32_t* pp, V* aa) {
 #pragma unroll
             for (int j = 0; j < kBinUnroll; ++j) {
@@ -207,7 +203,6 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
                 else aa[j] = V(1);
             }
         };
-        if (PF) load_batch(threadIdx.x, pn, an);
         for (uint32_t base = threadIdx.x; base < n_e; base += kStep) {
             uint32_t p[kBinUnroll];
             V a[kBinUnroll];
@@ -215,16 +210,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
             bool ok[kBinUnroll];
 #pragma unroll
             for (int j = 0; j < kBinUnroll; ++j) ok[j] = base + j * kBinThreads < n_e;
-            if (PF) {
-#pragma unroll
-                for (int j = 0; j < kBinUnroll; ++j) {
-                    p[j] = pn[j];
-                    a[j] = an[j];
-                }
-                if (base + kStep < n_e) load_batch(base + kStep, pn, an);
-            } else {
-                load_batch(base, p, a);
-            }
+            load_batch(base, p, a);
 #pragma unroll
             for (int j = 0; j < kBinUnroll; ++j) {
                 const uint32_t e = base + j * kBinThreads;
