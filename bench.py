@@ -16,9 +16,13 @@ Every point is also timed with all 8 kernels (best-of-8, regret).
 
 Timing: CUDA events on the library's stream around each multiply, medians
 over K steps after W warm-up steps; an L2 flush (256 MiB write) precedes every
-timed multiply whose working set fits in L2.  e2e repeats the step through
-the public API with host buffers (pinned), H2D of x and D2H of y inside the
-timed region, wall clock with a synchronize at the end of each point.
+timed multiply whose working set fits in L2.  Selection overhead (feature
+pulls + tree walks, format conversions) is measured on fresh vectors and
+reported beside the value ("overhead").  e2e repeats the step through the
+public API with host buffers (pinned): one adaspmv_run_batch call over the 7
+vectors (H2D of x, select, multiply, D2H of y in its smaller form, pipelined
+over 3 streams), wall clock; "sequential_value" is the same through single
+calls.  N > 1 (torchrun): the row-partitioned mode, see run_ours_multi.
 """
 from __future__ import annotations
 
