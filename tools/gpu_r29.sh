@@ -1,2 +1,3 @@
 #!/bin/bash
-python tools/kernel_sweep.py --inputs c2 --kernels 4,6 --lanes 0,1,2,8,16,32 --densities 0.00001,0.001,0.01,0.1,0.5 --reps 7 2>&1 | grep c2
+timeout 600 ncu --set full --clock-control none -k regex:"row_direct_kernel" -c 1 -o gpurun_out/prof_c1 python tools/kernel_sweep.py --inputs c1 --kernels 0 --reps 1 > /dev/null 2>&1
+ls gpurun_out/
