@@ -447,9 +447,12 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
     // Skewed (power-law) matrices: hub rows meet hub columns, so in the low
     // columns of a bin the same rows recur inside one warp's 32-entry window
     // and serialise on their shared-memory slots even at modest degree.
-    // Measured on B200 (row degree cut 4096/2048/1024/512/256): R-MAT 20
-    // 269/186/142/142/138 us, R-MAT 22 654/566/566/548/585 us.
-    if (m.feat[8] > 0.5 && m.feat[3] > 512.0) L.heavy_min = 512;
+    // The CSR-segment path does not profit from zeros in x as the bins do,
+    // so the cut trades dense-x against half-dense-x time.  Measured on B200
+    // (K0, x density 0.3 / 0.6 / 1.0; cut 4096 / 2048 / 1024 / 512):
+    //   R-MAT 22  501 550 654 / 486 509 566 / 486 507 566 / 509 521 548 us
+    //   R-MAT 20  105 157 269 / 142 159 183 / 116 126 143 / 116 126 144 us
+    if (m.feat[8] > 0.5 && m.feat[3] > 1024.0) L.heavy_min = 1024;
     std::vector<int64_t> cuts;
     if (L.force_rows > 0 || L.cluster == 2 || m.nnz == 0) {  // equal-height bins
         const int64_t R0 = std::max<int64_t>((m.rows + nbins - 1) / nbins, 1);
