@@ -435,3 +435,26 @@ def test_atomic_output_reuse(ctx, port, dt):
     a = A.run_kernel(m, 4, A.SparseVector(cols, xi, xv), A.KernelConfig(semiring=A.MIN_PLUS), out=out)
     b = A.run_kernel(m, 4, A.SparseVector(cols, xi, xv), A.KernelConfig(semiring=A.MIN_PLUS))
     assert a.dense().values.tobytes() == b.dense().values.tobytes()
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
+def test_binned_skewed_rows_cut_to_csr_segments(ctx, port, dt):
+    """A power-law matrix (Gini > 0.5, rows above the 1024 cut): its heavy
+    rows run as CSR segments after the bins (kernels_binned.cu) -- every
+    density, K0 and K2, against the oracle; OR_AND bit-equal to the CSR run."""
+    rows, cols, ro, ci, vals = synth.rmat(15, 32, seed=5, values="uniform")
+    vals = np.asarray(vals, dt)
+    assert np.diff(ro).max() > 1024
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    assert m.features()[8] > 0.5
+    for nx in (1, cols // 50, cols // 2, cols):
+        xi, xv = synth.sparse_vector(cols, nx, seed=nx + 9, dtype=dt)
+        xd = port.sparse_to_dense(cols, xi, xv)
+        y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, xd)
+        for k in (0, 2):
+            out = A.run_kernel(m, k, A.DenseVector(xd), A.KernelConfig(row_layout=2))
+            assert_dense_close(out.dense().values, y_ref, bound, dt, f"rmat binned k={k} nnz_x={nx}")
+            xs = A.SparseVector(cols, xi, xv)
+            b = A.run_kernel(m, k, xs, A.KernelConfig(semiring=A.OR_AND, row_layout=2))
+            c = A.run_kernel(m, k, xs, A.KernelConfig(semiring=A.OR_AND, row_layout=1))
+            assert b.dense().values.tobytes() == c.dense().values.tobytes(), (k, nx)
