@@ -54,7 +54,7 @@ void set_operand(Context& c, Vector& v, const adaspmv_host_operand& x) {
         v.has_dense = true;
     } else {
         if (x.nnz > 0 && (!x.indices || !x.values)) invalid("run_batch: sparse operand without indices/values");
-        vector_set_sparse_host(c, v, x.nnz, x.indices, x.values);
+        vector_set_sparse_host_deferred(c, v, x.nnz, x.indices, x.values);
     }
 }
 
@@ -194,6 +194,9 @@ void run_batch(Context& ctx, const Matrix& m, const Bundle* b, int forced, const
                     set_operand(ln.c, ln.v, xs[k]);
                     const double t1 = trace ? now() : 0;
                     const int kern = forced >= 0 ? forced : predict(ln.c, m, ln.v, *b, nullptr, nullptr);
+                    // the operand's validation verdict (usually already here:
+                    // the selector's nnz_s read synchronised the stream)
+                    if (xs[k].nnz >= 0) vector_check_deferred(ln.c, ln.v);
                     const double t2 = trace ? now() : 0;
                     run_kernel(ln.c, m, ln.v, kern, cfg, ln.y);
                     fetch_result(ln.c, m, ln.v, ln.y, kern, ys[k]);

@@ -277,6 +277,14 @@ void vector_set_sparse_device(Context& ctx, Vector& v, int64_t nnz, const int32_
 // host int64 indices (the reference's index_t) + values: H2D, then validated
 // and narrowed on the device (one synchronisation for the verdict)
 void vector_set_sparse_host(Context& ctx, Vector& v, int64_t nnz, const int64_t* h_idx, const void* h_vals);
+// the same without waiting for the verdict: indices out of range are stored
+// as 0 meanwhile; vector_check_deferred (synchronises) throws the reference's
+// error.  Used by the batch lanes, whose next synchronisation (nnz_s for the
+// selector) then carries the verdict too.
+constexpr int kVerdictSlot = 16;  // in Context::h_scalars
+void vector_set_sparse_host_deferred(Context& ctx, Vector& v, int64_t nnz, const int64_t* h_idx,
+                                     const void* h_vals);
+void vector_check_deferred(Context& ctx, Vector& v);
 // dense view; entries absent from a sparse input hold the identity of
 // `semiring` (0 for plus-times / or-and, +inf for min-plus)
 void vector_ensure_dense(Context& ctx, Vector& v, int semiring = ADASPMV_PLUS_TIMES);

@@ -136,8 +136,52 @@ __global__ void narrow_validate_kernel(int64_t nnz, int64_t n, const int64_t* __
         if (i < 0 || i >= n) e = static_cast<unsigned long long>(k) << 1;
         else if (k > 0 && i <= in[k - 1]) e = (static_cast<unsigned long long>(k) << 1) | 1ull;
         if (e != ~0ull) atomicMin(err, e);
-        out[k] = static_cast<int32_t>(i);
+        // an out-of-range index is stored as 0, so that kernels launched before
+        // the verdict is read (deferred validation) stay in bounds
+        out[k] = (i < 0 || i >= n) ? 0 : static_cast<int32_t>(i);
     }
+}
+
+namespace {
+void throw_verdict(Vector& v, unsigned long long e) {
+    if (e == ~0ull) return;
+    v.invalidate();
+    if (e & 1ull) invalid("sparse vector: indices not strictly increasing");
+    invalid("sparse vector: index out of range");
+}
+}  // namespace
+
+void vector_set_sparse_host_deferred(Context& ctx, Vector& v, int64_t nnz, const int64_t* h_idx,
+                                     const void* h_vals) {
+    if (nnz < 0) invalid("sparse vector: negative nnz");
+    v.invalidate();
+    const size_t vb = static_cast<size_t>(value_bytes(v.dtype));
+    const size_t z = static_cast<size_t>(std::max<int64_t>(nnz, 1));
+    v.sp_idx.ensure(sizeof(int32_t) * z);
+    v.sp_val.ensure(vb * z);
+    unsigned long long* err = reinterpret_cast<unsigned long long*>(ctx.dscal(6));
+    ADA_CUDA(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx.stream));
+    if (nnz > 0) {
+        int64_t* st = static_cast<int64_t*>(v.stage_idx.ensure(sizeof(int64_t) * z));
+        ADA_CUDA(cudaMemcpyAsync(st, h_idx, sizeof(int64_t) * static_cast<size_t>(nnz), cudaMemcpyHostToDevice,
+                                 ctx.stream));
+        ADA_CUDA(cudaMemcpyAsync(v.sp_val.p, h_vals, vb * static_cast<size_t>(nnz), cudaMemcpyHostToDevice,
+                                 ctx.stream));
+        const int64_t g = std::min<int64_t>((nnz + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 16);
+        narrow_validate_kernel<<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(nnz, v.n, st,
+                                                                                v.sp_idx.as<int32_t>(), err);
+        ADA_LAUNCHED(ctx);
+    }
+    // the verdict lands in the mapped scalars (slot kVerdictSlot) with the
+    // stream's next synchronisation; vector_check_deferred reads it
+    copy_scalars_kernel_launch(ctx, ctx.dscal(6), ctx.h_scalars_dev + kVerdictSlot, 1);
+    v.nnz = nnz;
+    v.has_sparse = true;
+}
+
+void vector_check_deferred(Context& ctx, Vector& v) {
+    ctx.sync();
+    throw_verdict(v, static_cast<unsigned long long>(ctx.h_scalars[kVerdictSlot]));
 }
 
 void vector_set_sparse_host(Context& ctx, Vector& v, int64_t nnz, const int64_t* h_idx, const void* h_vals) {
