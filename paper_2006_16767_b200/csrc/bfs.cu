@@ -99,13 +99,15 @@ int64_t next_frontier(Context& ctx, const Matrix& m, Output& y, Vector& x, int32
     if (y.has_sparse) {
         const int64_t nnz = output_nnz(ctx, y);
         scan3(ctx, nnz, SparseFrontierIn<V, SR>{y.sp_idx.as<int32_t>(), y.sp_val.as<V>(), lv, co},
-              FrontierEpi<V>{y.sp_idx.as<int32_t>(), lv, xi, xv, eff, level, value}, ctx.dscal(2),
+              FrontierEpi<V>{y.sp_idx.as<int32_t>(), lv, xi, xv, eff, level, value}, ctx.h_scalars_dev + kScanTotalSlot,
               ctx.scratch[4]);
     } else {
         scan3(ctx, y.n, DenseFrontierIn<V, SR>{y.dense.as<V>(), lv, co},
-              FrontierEpi<V>{nullptr, lv, xi, xv, eff, level, value}, ctx.dscal(2), ctx.scratch[4]);
+              FrontierEpi<V>{nullptr, lv, xi, xv, eff, level, value}, ctx.h_scalars_dev + kScanTotalSlot, ctx.scratch[4]);
     }
-    const int64_t tot = ctx.fetch_scalar(ctx.dscal(2));
+    // the scan's total was stored straight into the mapped scalars
+    ctx.sync();
+    const int64_t tot = ctx.h_scalars[kScanTotalSlot];
     x.nnz = fused ? tot >> kCntShift : tot;
     x.has_sparse = true;
     if (fused) {

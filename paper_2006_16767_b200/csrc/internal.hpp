@@ -282,6 +282,9 @@ void vector_set_sparse_host(Context& ctx, Vector& v, int64_t nnz, const int64_t*
 // error.  Used by the batch lanes, whose next synchronisation (nnz_s for the
 // selector) then carries the verdict too.
 constexpr int kVerdictSlot = 16;  // in Context::h_scalars
+// the per-iteration frontier / delta scans of BFS and PageRank store their
+// total directly into this mapped slot (no copy kernel before the read)
+constexpr int kScanTotalSlot = 20;
 void vector_set_sparse_host_deferred(Context& ctx, Vector& v, int64_t nnz, const int64_t* h_idx,
                                      const void* h_vals);
 void vector_check_deferred(Context& ctx, Vector& v);

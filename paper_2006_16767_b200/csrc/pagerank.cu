@@ -128,13 +128,15 @@ int64_t next_delta(Context& ctx, const Matrix& m, Output& y, Vector& x, V* rank,
     if (y.has_sparse) {
         const int64_t nnz = output_nnz(ctx, y);
         scan3(ctx, nnz, SparseDeltaIn<V>{y.sp_idx.as<int32_t>(), y.sp_val.as<V>(), d, prune, co},
-              DeltaEpi<V>{y.sp_idx.as<int32_t>(), y.sp_val.as<V>(), d, rank, xi, xv, eff}, ctx.dscal(5),
+              DeltaEpi<V>{y.sp_idx.as<int32_t>(), y.sp_val.as<V>(), d, rank, xi, xv, eff}, ctx.h_scalars_dev + kScanTotalSlot,
               ctx.scratch[4]);
     } else {
         scan3(ctx, y.n, DenseDeltaIn<V>{y.dense.as<V>(), d, prune, co},
-              DeltaEpi<V>{nullptr, y.dense.as<V>(), d, rank, xi, xv, eff}, ctx.dscal(5), ctx.scratch[4]);
+              DeltaEpi<V>{nullptr, y.dense.as<V>(), d, rank, xi, xv, eff}, ctx.h_scalars_dev + kScanTotalSlot, ctx.scratch[4]);
     }
-    const int64_t tot = ctx.fetch_scalar(ctx.dscal(5));
+    // the scan's total was stored straight into the mapped scalars
+    ctx.sync();
+    const int64_t tot = ctx.h_scalars[kScanTotalSlot];
     x.nnz = fused ? tot >> kCntShift : tot;
     x.has_sparse = true;
     if (fused) {

@@ -46,6 +46,8 @@ __global__ void __launch_bounds__(kRsThreads) radix_upsweep_kernel(const uint32_
     counts[static_cast<int64_t>(threadIdx.x) * ntiles + blockIdx.x] = hist[threadIdx.x];
 }
 
+__global__ void scan_zero_kernel(int64_t* p) { *reinterpret_cast<volatile int64_t*>(p) = 0; }
+
 __global__ void copy_scalars_kernel(const int64_t* __restrict__ src, volatile int64_t* dst, int n) {
     if (static_cast<int>(threadIdx.x) < n) dst[threadIdx.x] = src[threadIdx.x];
 }

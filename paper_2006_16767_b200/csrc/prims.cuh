@@ -72,11 +72,17 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(int64_t n, In 
     if (single && threadIdx.x == 0 && d_total) *d_total = total;
 }
 
-// Host driver.  `tmp` must hold max(1, ceil(n/kScanTile)) int64.
+__global__ void scan_zero_kernel(int64_t* p);
+
+// Host driver.  `tmp` must hold max(1, ceil(n/kScanTile)) int64.  d_total
+// (device int64, or the device alias of mapped host memory) gets the total.
 template <class In, class Epi>
 void scan3(Context& ctx, int64_t n, In in, Epi epi, int64_t* d_total, DevBuf& tmp) {
-    if (n <= 0) {
-        if (d_total) ADA_CUDA(cudaMemsetAsync(d_total, 0, sizeof(int64_t), ctx.stream));
+    if (n <= 0) {  // d_total may be mapped host memory: a store, not a memset
+        if (d_total) {
+            scan_zero_kernel<<<1, 1, 0, ctx.stream>>>(d_total);
+            ADA_LAUNCHED(ctx);
+        }
         return;
     }
     const int64_t nt = (n + kScanTile - 1) / kScanTile;

@@ -1,0 +1,4 @@
+#!/bin/bash
+timeout 900 python -m pytest tests/ -m gpu -q -p no:cacheprovider -x 2>&1 | grep -E "^E |passed|failed" | head
+timeout 900 python tools/bfs_bench.py --scale 22 --reps 5 --out gpurun_out/bfs22.json 2>&1 | grep -E "selector|heuristic|best"
+timeout 900 python tools/pagerank_bench.py --scale 22 --prune 1e-8 --out gpurun_out/pr22.json 2>&1 | grep -E "best"
