@@ -306,6 +306,24 @@ int adaspmv_sort_reduce_pairs(adaspmv_ctx* ctx, int64_t npairs, const int64_t* r
  * snapped so no row is split (partition.hpp:30-33 search). */
 int adaspmv_shard_rows(const int64_t* row_offsets, int64_t rows, int nshards, int64_t* cuts);
 
+/* ---- row-partitioned multi-GPU mode, one process ---- */
+/* The matrix (host CSR, as adaspmv_matrix_create_csr) is cut into `ngpu`
+ * contiguous row blocks of ~nnz/ngpu nonzeros (adaspmv_shard_rows); block g
+ * lives on devices[g] (NULL: device g) as its own DualMatrix.  A run sends x
+ * (nnz_x < 0: dense, `values` = n reals; else int64-indexed sparse) to every
+ * block, each block selects (bundle, or `forced_kernel` >= 0) and multiplies,
+ * and y (m reals, host) receives every block at its row offset; `kernels`
+ * (optional, ngpu ints) gets each block's KernelId::index(). */
+typedef struct adaspmv_multi adaspmv_multi;
+int adaspmv_multi_create(int ngpu, const int* devices, int64_t rows, int64_t cols,
+                         const int64_t* row_offsets, const int64_t* col_indices, const void* values,
+                         int dtype, adaspmv_multi** out);
+int adaspmv_multi_cuts(const adaspmv_multi* mm, int64_t* cuts); /* ngpu + 1 row cuts */
+int adaspmv_multi_run(adaspmv_multi* mm, const adaspmv_bundle* b, int forced_kernel,
+                      const adaspmv_config* cfg, int64_t nnz_x, const int64_t* indices,
+                      const void* values, void* y, int* kernels);
+int adaspmv_multi_destroy(adaspmv_multi* mm);
+
 /* ---- BFS driver ------------------------------------------ */
 typedef struct {
     int64_t iteration;

@@ -466,6 +466,44 @@ inline std::vector<BatchResult> run_batch(const DualMatrix& m, const std::vector
     return out;
 }
 
+// ---- row-partitioned mode in one process (adaspmv_multi_*) ------------------------------
+class MultiMatrix {
+public:
+    // rows of the host CSR cut into devices.size() blocks of ~nnz/G nonzeros
+    MultiMatrix(const std::vector<int>& devices, index_t rows, index_t cols, const std::vector<index_t>& row_offsets,
+                const std::vector<index_t>& col_indices, const std::vector<real_t>& values)
+        : rows_(rows), g_(static_cast<int>(devices.size())) {
+        adaspmv_multi* h = nullptr;
+        check(adaspmv_multi_create(g_, devices.data(), rows, cols, row_offsets.data(), col_indices.data(),
+                                   values.empty() ? nullptr : values.data(), kDtype, &h));
+        h_.reset(h, adaspmv_multi_destroy);
+    }
+    // y = A x (dense x); the per-block kernel choices go to `kernels` if given
+    DenseVector multiply(const DenseVector& x, const SelectorBundle* b, int forced_kernel = -1,
+                         std::vector<int>* kernels = nullptr) const {
+        DenseVector y(rows_);
+        std::vector<int> ks(static_cast<size_t>(g_));
+        check(adaspmv_multi_run(h_.get(), b ? b->get() : nullptr, forced_kernel, nullptr, -1, nullptr,
+                                x.values.data(), y.values.data(), ks.data()));
+        if (kernels) *kernels = ks;
+        return y;
+    }
+    DenseVector multiply(const SparseVector& x, const SelectorBundle* b, int forced_kernel = -1,
+                         std::vector<int>* kernels = nullptr) const {
+        DenseVector y(rows_);
+        std::vector<int> ks(static_cast<size_t>(g_));
+        check(adaspmv_multi_run(h_.get(), b ? b->get() : nullptr, forced_kernel, nullptr, x.nnz(), x.indices.data(),
+                                x.values.data(), y.values.data(), ks.data()));
+        if (kernels) *kernels = ks;
+        return y;
+    }
+
+private:
+    index_t rows_;
+    int g_;
+    std::shared_ptr<adaspmv_multi> h_;
+};
+
 // ---- BFS driver --------------------------------------------------------
 inline std::vector<index_t> bfs(const DualMatrix& m, index_t source, int semiring = ADASPMV_OR_AND,
                                 const SelectorBundle* b = nullptr, int forced_kernel = -1) {

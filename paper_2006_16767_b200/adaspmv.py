@@ -186,6 +186,10 @@ def load(path: Optional[os.PathLike] = None):
         "adaspmv_pagerank": [vp, vp, C.c_double, C.c_double, i64, vp, C.c_int, vp, P(i64), vp, i64],
         "adaspmv_execute_iteration": [vp, vp, vp, vp, C.c_int, vp, vp, vp],
         "adaspmv_run_batch": [vp, vp, vp, C.c_int, vp, i64, vp, vp, C.c_int],
+        "adaspmv_multi_create": [C.c_int, vp, i64, i64, vp, vp, vp, C.c_int, P(vp)],
+        "adaspmv_multi_cuts": [vp, vp],
+        "adaspmv_multi_run": [vp, vp, C.c_int, vp, i64, vp, vp, vp, vp],
+        "adaspmv_multi_destroy": [vp],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -929,6 +933,57 @@ def run_batch(m: DualMatrix, xs, bundle: Optional[SelectorBundle] = None, force_
         else:
             out.append(BatchResult(kid, False, dense=DenseVector(bv[:rows])))
     return out
+
+
+class MultiMatrix:
+    """adaspmv_multi: the row-partitioned mode in one process -- G row blocks
+    of ~nnz/G nonzeros, block g on devices[g]."""
+
+    def __init__(self, rows, cols, row_offsets, col_indices, values=None, devices=(0,), dtype=None):
+        load()
+        ro = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        ci = np.ascontiguousarray(col_indices, dtype=np.int64)
+        if dtype is None:
+            dtype = np.float64 if values is None else np.asarray(values).dtype
+        self.dtype = np.dtype(dtype)
+        vals = None if values is None else np.ascontiguousarray(values, dtype=self.dtype)
+        dev = np.ascontiguousarray(devices, dtype=np.int32)
+        self.rows, self.cols, self.ngpu = int(rows), int(cols), len(dev)
+        self.h = C.c_void_p()
+        _check(_lib.adaspmv_multi_create(self.ngpu, _ptr(dev), self.rows, self.cols, _ptr(ro), _ptr(ci),
+                                         _ptr(vals), _dtype_code(self.dtype), C.byref(self.h)))
+
+    def cuts(self) -> np.ndarray:
+        c = np.zeros(self.ngpu + 1, np.int64)
+        _check(_lib.adaspmv_multi_cuts(self.h, _ptr(c)))
+        return c
+
+    def multiply(self, x, bundle: Optional["SelectorBundle"] = None, force_kernel: int = -1,
+                 cfg: Optional[KernelConfig] = None):
+        """y = A x (x: dense values, or an (indices, values) pair) -> (y, per-block KernelIds)."""
+        y = np.empty(self.rows, self.dtype)
+        ks = np.zeros(self.ngpu, np.int32)
+        c = (cfg or KernelConfig())._c()
+        if isinstance(x, tuple):
+            xi = np.ascontiguousarray(x[0], dtype=np.int64)
+            xv = np.ascontiguousarray(x[1], dtype=self.dtype)
+            nnz = len(xi)
+        else:
+            xi, xv, nnz = None, np.ascontiguousarray(x, dtype=self.dtype), -1
+        _check(_lib.adaspmv_multi_run(self.h, bundle.h if bundle else None, int(force_kernel), C.byref(c), nnz,
+                                      _ptr(xi), _ptr(xv), _ptr(y), _ptr(ks)))
+        return y, [KernelId.from_index(int(k)) for k in ks]
+
+    def close(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.adaspmv_multi_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def execute_iteration(m: DualMatrix, x, bundle: Optional[SelectorBundle] = None, force_kernel: int = -1,

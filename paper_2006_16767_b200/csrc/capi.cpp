@@ -22,6 +22,7 @@ struct adaspmv_matrix : ada::Matrix {};
 struct adaspmv_vector : ada::Vector {};
 struct adaspmv_output : ada::Output {};
 struct adaspmv_bundle : ada::Bundle {};
+struct adaspmv_multi : ada::Multi {};
 
 namespace {
 
@@ -950,17 +951,50 @@ int adaspmv_shard_rows(const int64_t* row_offsets, int64_t rows, int nshards, in
         need(cuts, "cuts");
         if (nshards <= 0) ada::invalid("shard_rows: nshards must be positive");
         if (rows < 0) ada::invalid("shard_rows: negative rows");
-        const int64_t nnz = row_offsets[rows];
-        cuts[0] = 0;
-        for (int g = 1; g < nshards; ++g) {
-            const int64_t pos = nnz * g / nshards;
-            // first row starting at or after pos: rows never split
-            int64_t r = static_cast<int64_t>(std::lower_bound(row_offsets, row_offsets + rows + 1, pos) - row_offsets);
-            if (r > rows) r = rows;
-            cuts[g] = std::max(r, cuts[g - 1]);
-        }
-        cuts[nshards] = rows;
+        ada::shard_cuts(row_offsets, rows, nshards, cuts);
     });
+}
+
+int adaspmv_multi_create(int ngpu, const int* devices, int64_t rows, int64_t cols, const int64_t* row_offsets,
+                         const int64_t* col_indices, const void* values, int dtype, adaspmv_multi** out) {
+    return guarded([&] {
+        need(out, "out");
+        need(row_offsets, "row_offsets");
+        check_dtype(dtype);
+        if (ngpu <= 0 || ngpu > 64) ada::invalid("multi: ngpu must be in [1, 64]");
+        if (rows < 0 || cols < 0) ada::invalid("negative matrix dimension");
+        if (row_offsets[rows] > 0) need(col_indices, "col_indices");
+        validate_host_csr(rows, cols, row_offsets, col_indices);
+        *out = static_cast<adaspmv_multi*>(
+            ada::multi_create(ngpu, devices, rows, cols, row_offsets, col_indices, values, dtype));
+    });
+}
+
+int adaspmv_multi_cuts(const adaspmv_multi* mm, int64_t* cuts) {
+    return guarded([&] {
+        need(mm, "multi");
+        need(cuts, "cuts");
+        std::copy(mm->cuts.begin(), mm->cuts.end(), cuts);
+    });
+}
+
+int adaspmv_multi_run(adaspmv_multi* mm, const adaspmv_bundle* b, int forced_kernel, const adaspmv_config* cfg,
+                      int64_t nnz_x, const int64_t* indices, const void* values, void* y, int* kernels) {
+    return guarded([&] {
+        need(mm, "multi");
+        if (forced_kernel > 7) ada::invalid("kernel index out of range");
+        if (forced_kernel < 0 && !b) ada::invalid("multi_run: no bundle and no forced kernel");
+        if (nnz_x > 0 || (nnz_x < 0 && mm->cols > 0)) need(values, "values");
+        if (nnz_x > 0) need(indices, "indices");
+        adaspmv_config c{};
+        if (cfg) c = *cfg;
+        ada::multi_run(*mm, b, forced_kernel, c, nnz_x, indices, values, y, kernels);
+    });
+}
+
+int adaspmv_multi_destroy(adaspmv_multi* mm) {
+    if (!mm) return ADASPMV_OK;
+    return guarded([&] { delete static_cast<ada::Multi*>(mm); });
 }
 
 int adaspmv_bfs(adaspmv_ctx* ctx, const adaspmv_matrix* m, int64_t source, int semiring,

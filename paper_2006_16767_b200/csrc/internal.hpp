@@ -241,6 +241,22 @@ struct BatchLane {
     ~BatchLane();
 };
 
+// One shard of the single-process row-partitioned mode (multi.cpp): its
+// device context, its row block as a matrix, an operand and an output.
+struct MultiShard {
+    Context ctx;
+    Matrix* m = nullptr;
+    Vector v;
+    Output y;
+    ~MultiShard();
+};
+struct Multi {
+    int64_t rows = 0, cols = 0;
+    int dtype = ADASPMV_F64;
+    std::vector<int64_t> cuts;  // [G+1] row cuts
+    std::vector<std::unique_ptr<MultiShard>> shards;
+};
+
 // One decision tree: flat node array.
 struct Tree {
     int target = 0;          // 0 pattern, 1 workload, 2 write-back
@@ -261,6 +277,13 @@ struct Bundle {
 // scalars, device pool release threshold
 void context_init(Context& ctx, int device, cudaStream_t stream);
 void context_release(Context& ctx);
+
+// row-partitioned multi-GPU mode (multi.cpp)
+void shard_cuts(const int64_t* ro, int64_t rows, int g, int64_t* cuts);
+Multi* multi_create(int ngpu, const int* devices, int64_t rows, int64_t cols, const int64_t* ro,
+                    const int64_t* ci, const void* vals, int dtype);
+void multi_run(Multi& mm, const Bundle* b, int forced, const adaspmv_config& cfg, int64_t nnz_x,
+               const int64_t* idx, const void* vals, void* y_host, int* kernels);
 
 // adaspmv_run_batch (batch.cpp)
 void run_batch(Context& ctx, const Matrix& m, const Bundle* b, int forced, const adaspmv_config& cfg,
