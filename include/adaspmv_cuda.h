@@ -284,6 +284,12 @@ int adaspmv_output_dense(adaspmv_ctx* ctx, adaspmv_output* y, void* values);
  * Writes nnz_y; copies up to `capacity` entries when indices/values != NULL. */
 int adaspmv_output_sparse(adaspmv_ctx* ctx, adaspmv_output* y, int64_t capacity,
                           int64_t* indices, void* values, int64_t* nnz_y);
+/* KernelCounters (kernels.hpp:106-111; the reference's ADASPMV_ENABLE_COUNTERS
+ * build): while enabled on a context, every run records out3[0] values_read
+ * (matrix entries consumed -- a product formed), out3[1] pairs_emitted (sort
+ * write-back) and out3[2] cas_retries (always 0: hardware atomics). */
+int adaspmv_ctx_set_counters(adaspmv_ctx* ctx, int enable);
+int adaspmv_output_counters(adaspmv_ctx* ctx, adaspmv_output* y, uint64_t out3[3]);
 /* Seconds between the events of the last timed run of `y` (synchronises). */
 int adaspmv_output_elapsed(adaspmv_ctx* ctx, adaspmv_output* y, double* seconds);
 /* Device pointers of the views (materialised on demand). */

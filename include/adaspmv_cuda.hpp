@@ -139,6 +139,13 @@ inline WorkPartition make_partition(std::span<const index_t> offsets, index_t to
     return p;
 }
 
+// KernelCounters (kernels.hpp:106-111)
+struct KernelCounters {
+    std::uint64_t values_read = 0;    // matrix entries consumed
+    std::uint64_t pairs_emitted = 0;  // (row, product) pairs on the sort path
+    std::uint64_t cas_retries = 0;    // 0 on the device: hardware atomics
+};
+
 // ---- host value types (sparse.hpp:99-151) ---------------------------------------
 struct DenseVector {
     std::vector<real_t> values;
@@ -206,6 +213,7 @@ public:
     Context& operator=(const Context&) = delete;
     adaspmv_ctx* get() const { return h_; }
     void synchronize() { check(adaspmv_ctx_synchronize(h_)); }
+    void set_counters(bool enable) { check(adaspmv_ctx_set_counters(h_, enable ? 1 : 0)); }
 
 private:
     adaspmv_ctx* h_ = nullptr;
@@ -294,6 +302,13 @@ public:
         return *sparse_;
     }
     adaspmv_output* get() const { return h_.get(); }
+    // KernelCounters (kernels.hpp:106-111) of the run, when the context counts
+    // (Context::set_counters); std::invalid_argument otherwise
+    KernelCounters counters() const {
+        std::uint64_t c[3] = {0, 0, 0};
+        check(adaspmv_output_counters(ctx_->get(), h_.get(), c));
+        return KernelCounters{c[0], c[1], c[2]};
+    }
 
 private:
     bool info(int which) const {

@@ -140,6 +140,8 @@ def load(path: Optional[os.PathLike] = None):
         "adaspmv_ctx_launch_count": [vp],
         "adaspmv_ctx_set_timing": [vp, C.c_int],
         "adaspmv_output_elapsed": [vp, vp, P(C.c_double)],
+        "adaspmv_ctx_set_counters": [vp, C.c_int],
+        "adaspmv_output_counters": [vp, vp, vp],
         "adaspmv_matrix_create_csr": [vp, i64, i64, vp, vp, vp, C.c_int, P(vp)],
         "adaspmv_matrix_create_csr_device": [vp, i64, i64, i64, vp, vp, vp, C.c_int, P(vp)],
         "adaspmv_matrix_from_triplets": [vp, i64, i64, i64, vp, vp, vp, C.c_int, P(vp)],
@@ -418,6 +420,10 @@ class Context:
     @property
     def launches(self) -> int:
         return int(_lib.adaspmv_ctx_launch_count(self.h))
+
+    def set_counters(self, enable: bool = True):
+        """KernelCounters for every following run (kernels.hpp:106-111)."""
+        _check(_lib.adaspmv_ctx_set_counters(self.h, 1 if enable else 0))
 
     def set_timing(self, enable: bool = True):
         """Bracket every multiply with CUDA events (MultiplyOutput.elapsed())."""
@@ -698,6 +704,13 @@ class MultiplyOutput:
         kk = C.c_int64()
         _check(_lib.adaspmv_output_sparse(self.ctx.h, self.h, k, _ptr(idx), _ptr(val), C.byref(kk)))
         return SparseVector(n, idx[:k], val[:k])
+
+    def counters(self) -> dict:
+        """KernelCounters of the run that produced this output (the context
+        must count): values_read, pairs_emitted, cas_retries."""
+        c = np.zeros(3, np.uint64)
+        _check(_lib.adaspmv_output_counters(self.ctx.h, self.h, _ptr(c)))
+        return dict(values_read=int(c[0]), pairs_emitted=int(c[1]), cas_retries=int(c[2]))
 
     def elapsed(self) -> float:
         """Device seconds of the last timed run (Context.set_timing)."""

@@ -232,6 +232,27 @@ int adaspmv_ctx_set_timing(adaspmv_ctx* ctx, int enable) {
     });
 }
 
+int adaspmv_ctx_set_counters(adaspmv_ctx* ctx, int enable) {
+    return guarded([&] {
+        need(ctx, "context");
+        ctx->counters = enable != 0;
+    });
+}
+
+int adaspmv_output_counters(adaspmv_ctx* ctx, adaspmv_output* y, uint64_t out3[3]) {
+    return guarded([&] {
+        bind(ctx);
+        need(y, "output");
+        need(out3, "out");
+        if (!y->has_ctr) ada::invalid("output_counters: the run was not counted (adaspmv_ctx_set_counters)");
+        unsigned long long h[2] = {0, 0};
+        ADA_CUDA(copy_sync(ctx, h, y->d_ctr.p, sizeof(h), cudaMemcpyDeviceToHost));
+        out3[0] = h[0];
+        out3[1] = h[1];
+        out3[2] = 0;  // hardware atomics: no counted CAS retries
+    });
+}
+
 int adaspmv_output_elapsed(adaspmv_ctx* ctx, adaspmv_output* y, double* seconds) {
     return guarded([&] {
         bind(ctx);

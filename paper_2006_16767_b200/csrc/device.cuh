@@ -50,6 +50,15 @@ __device__ __forceinline__ double ld_stream(const double* p) {
     return r;
 }
 
+// KernelCounters (kernels.hpp:106-111) on the device, when the context asks
+// for them (adaspmv_ctx_set_counters): ctr[0] values_read = matrix entries
+// consumed (a product formed: under PLUS_TIMES / MIN_PLUS one value load),
+// ctr[1] pairs_emitted on the sort write-back.  cas_retries stays 0: the
+// atomic write-backs use hardware atomics, not a counted CAS loop.
+__device__ __forceinline__ void count_add(unsigned long long* ctr, int slot, unsigned long long v) {
+    if (ctr && v) atomicAdd(ctr + slot, v);
+}
+
 // ---- semirings ---------------------------------------------------------------
 // PlusTimes: the reference algebra (kernels.hpp:236).  MinPlus: y_i =
 // min_j (a_ij + x_j), identity +inf.  OrAnd: y_i = OR_j (a_ij != 0 && x_j != 0)

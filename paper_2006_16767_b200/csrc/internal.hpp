@@ -94,6 +94,8 @@ struct Context {
     int sm_count = 148;
     int64_t launches = 0;
     bool timing = false;  // bracket every run with CUDA events (adaspmv_output_elapsed)
+    bool counters = false;  // KernelCounters per run (adaspmv_ctx_set_counters)
+    unsigned long long* ctr = nullptr;  // the running output's device counters (kernels' last argument)
     // general scratch (reused by every call; calls on a context are serialised)
     // [0..3] sort write-back keys/values (double buffered), [4] vector scans,
     // [5] matrix build scans, [6..9] radix counts / scan / segment sums / flags
@@ -217,6 +219,10 @@ struct Output {
     int64_t nnz = -1;      // host-known nnz_y (-1 = only on device, slot d_nnz)
     DevBuf d_nnz;          // device int64 nnz_y
     int semiring = ADASPMV_PLUS_TIMES;  // identity of absent entries
+    // KernelCounters of the last run (kernels.hpp:106-111), when the context
+    // counts: [0] values_read, [1] pairs_emitted
+    DevBuf d_ctr;
+    bool has_ctr = false;
     // device-time bracket of the last run (recorded when Context::timing)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     bool timed = false;

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
     const int64_t* __restrict__ tiles, const int32_t* __restrict__ tile_bin,
     const int32_t* __restrict__ tile_multi, const int64_t* __restrict__ chunk_off,
     const uint32_t* __restrict__ pk, const V* __restrict__ bv, const V* __restrict__ x,
-    const uint32_t* __restrict__ mask, V* __restrict__ y) {
+    const uint32_t* __restrict__ mask, V* __restrict__ y, unsigned long long* __restrict__ ctr) {
     using S = Semiring<SR, V>;
     extern __shared__ __align__(16) unsigned char bin_smem[];
     V* ys = reinterpret_cast<V*>(bin_smem);
@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
         // entries): the per-entry index, chunk and address arithmetic stays
         // in 32-bit registers
         const uint32_t n_e = static_cast<uint32_t>(e1 - e0);
+        if (!MASKED && threadIdx.x == 0) count_add(ctr, 0, n_e);  // every entry of the tile is consumed
         const uint32_t* __restrict__ pkt = pk + e0;
         const V* __restrict__ bvt = bv + e0;
         // chunk of the thread's first entry: largest c with co[c] <= e (binary search)
@@ -227,6 +228,12 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
 #pragma unroll
                 for (int j = 0; j < kBinUnroll; ++j)
                     if (ok[j]) ok[j] = (__ldg(mask + (col[j] >> 5)) >> (col[j] & 31)) & 1u;
+                if (ctr) {
+                    unsigned n = 0;
+#pragma unroll
+                    for (int j = 0; j < kBinUnroll; ++j) n += ok[j];
+                    count_add(ctr, 0, n);
+                }
             }
             V xv[kBinUnroll];
 #pragma unroll
@@ -306,16 +313,20 @@ __global__ void __launch_bounds__(256) heavy_seg_kernel(const int64_t* __restric
                                                         const V* __restrict__ vals,
                                                         const V* __restrict__ x,
                                                         const uint32_t* __restrict__ mask,
-                                                        V* __restrict__ y) {
+                                                        V* __restrict__ y,
+                                                        unsigned long long* __restrict__ ctr) {
     using S = Semiring<SR, V>;
     __shared__ V red[8];
+    unsigned cnt = 0;
     const int64_t row = segs[3 * blockIdx.x], b = segs[3 * blockIdx.x + 1], e = segs[3 * blockIdx.x + 2];
     V acc = S::zero();
     for (int64_t k = b + threadIdx.x; k < e; k += 256) {
         const int c = __ldg(ci + k);
         if (MASKED && !((__ldg(mask + (c >> 5)) >> (c & 31)) & 1u)) continue;
         acc = S::fma(S::kUsesValues ? __ldg(vals + k) : V(1), __ldg(x + c), acc);
+        ++cnt;
     }
+    count_add(ctr, 0, cnt);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) acc = S::add(acc, __shfl_xor_sync(kFull, acc, d));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
@@ -731,7 +742,8 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
         ADA_CUDA(cudaLaunchKernelEx(&lc, kern, t0, static_cast<const int64_t*>(L.bin_r0.as<int64_t>()), L.rbits,
                                     L.cw, L.nchunks, L.tiles.as<int64_t>(),
                                     L.tile_bin.as<int32_t>(), L.tile_multi.as<int32_t>(),
-                                    L.chunk_off.as<int64_t>(), L.pk.as<uint32_t>(), L.bv.as<V>(), x, mask, y));
+                                    L.chunk_off.as<int64_t>(), L.pk.as<uint32_t>(), L.bv.as<V>(), x, mask, y,
+                                    ctx.ctr));
         ADA_LAUNCHED(ctx);
     };
     for (size_t p = 0; p + 1 < L.panel_tile0.size(); ++p) {  // panels in column order, same stream
@@ -748,7 +760,7 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
     if (L.nsegs > 0) {  // heavy rows, after the bins wrote their identity
         auto hk = mask ? heavy_seg_kernel<V, SR, true> : heavy_seg_kernel<V, SR, false>;
         hk<<<static_cast<unsigned>(L.nsegs), 256, 0, ctx.stream>>>(L.segs.as<int64_t>(), m.col_idx.as<int32_t>(),
-                                                                  m.vals.as<V>(), x, mask, y);
+                                                                  m.vals.as<V>(), x, mask, y, ctx.ctr);
         ADA_LAUNCHED(ctx);
     }
 }

@@ -45,7 +45,7 @@ template <class V, int G, int SR>
 __global__ void __launch_bounds__(kNT) col_direct_atomic_kernel(
     int64_t nnz_x, const int32_t* __restrict__ xi, const V* __restrict__ xv,
     const int64_t* __restrict__ co, const int32_t* __restrict__ ri, const V* __restrict__ cv,
-    V* __restrict__ y) {
+    V* __restrict__ y, unsigned long long* __restrict__ ctr) {
     using S = Semiring<SR, V>;
     const int64_t gid = static_cast<int64_t>(blockIdx.x) * kNT + threadIdx.x;
     const int64_t s = gid / G;
@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kNT) col_direct_atomic_kernel(
     const int32_t col = __ldg(xi + s);
     const V xval = __ldg(xv + s);
     const int64_t b = __ldg(co + col), e = __ldg(co + col + 1);
+    if (ctr && lg == 0) count_add(ctr, 0, static_cast<unsigned long long>(e - b));  // the column's entries
     for (int64_t k0 = b + lg; k0 < e; k0 += G * kU) {
         int r[kU];
         V a[kU];
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(kNT) col_lb_kernel(
     int64_t nnz_x, int64_t nnz_s, int64_t ntiles, const int64_t* __restrict__ eff,
     const int32_t* __restrict__ xi, const V* __restrict__ xv, const int64_t* __restrict__ co,
     const int32_t* __restrict__ ri, const V* __restrict__ cv, V* __restrict__ y,
-    uint32_t* __restrict__ keys, V* __restrict__ pvals) {
+    uint32_t* __restrict__ keys, V* __restrict__ pvals, unsigned long long* __restrict__ ctr) {
     using S = Semiring<SR, V>;
     constexpr int kW = kNT / 32;
     constexpr int kJ = kColTile / 32;  // entries per lane
@@ -121,6 +122,10 @@ __global__ void __launch_bounds__(kNT) col_lb_kernel(
     if (t >= ntiles) return;
     const int64_t tb = t * kColTile;
     const int ten = static_cast<int>(min(static_cast<int64_t>(kColTile), nnz_s - tb));
+    if (lane == 0) {  // the tile's effective entries, each consumed (and emitted) once
+        count_add(ctr, 0, static_cast<unsigned long long>(ten));
+        if (EMIT) count_add(ctr, 1, static_cast<unsigned long long>(ten));
+    }
     const int64_t s_lo = warp_segment_of(eff, 0, nnz_x + 1, tb, lane);
     const int64_t s_hi = warp_segment_of(eff, s_lo, nnz_x + 1, tb + ten - 1, lane);  // inclusive
     const int64_t span = s_hi - s_lo + 1;
@@ -198,7 +203,8 @@ template <class V, int G, int SR>
 __global__ void __launch_bounds__(kNT) col_direct_emit_kernel(
     int64_t nnz_x, const int64_t* __restrict__ eff, const int32_t* __restrict__ xi,
     const V* __restrict__ xv, const int64_t* __restrict__ co, const int32_t* __restrict__ ri,
-    const V* __restrict__ cv, uint32_t* __restrict__ keys, V* __restrict__ pvals) {
+    const V* __restrict__ cv, uint32_t* __restrict__ keys, V* __restrict__ pvals,
+    unsigned long long* __restrict__ ctr) {
     using S = Semiring<SR, V>;
     const int64_t gid = static_cast<int64_t>(blockIdx.x) * kNT + threadIdx.x;
     const int64_t s = gid / G;
@@ -207,6 +213,10 @@ __global__ void __launch_bounds__(kNT) col_direct_emit_kernel(
     const int32_t col = __ldg(xi + s);
     const V xval = __ldg(xv + s);
     const int64_t b = __ldg(co + col), e = __ldg(co + col + 1);
+    if (ctr && lg == 0) {
+        count_add(ctr, 0, static_cast<unsigned long long>(e - b));
+        count_add(ctr, 1, static_cast<unsigned long long>(e - b));
+    }
     const int64_t out = __ldg(eff + s) - b;
     for (int64_t k = b + lg; k < e; k += G) {
         keys[out + k] = static_cast<uint32_t>(__ldg(ri + k));
@@ -262,7 +272,8 @@ template <class V, int SR>
 __global__ void __launch_bounds__(kSmallNT) col_sort_small_kernel(
     int64_t nnz_x, const int32_t* __restrict__ xi, const V* __restrict__ xv,
     const int64_t* __restrict__ co, const int32_t* __restrict__ ri, const V* __restrict__ cv,
-    int32_t* __restrict__ out_idx, V* __restrict__ out_val, int64_t* __restrict__ d_nnz) {
+    int32_t* __restrict__ out_idx, V* __restrict__ out_val, int64_t* __restrict__ d_nnz,
+    unsigned long long* __restrict__ ctr) {
     using S = Semiring<SR, V>;
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* skey = reinterpret_cast<uint64_t*>(smem);                  // kSmallPairs
@@ -311,6 +322,10 @@ __global__ void __launch_bounds__(kSmallNT) col_sort_small_kernel(
         __syncthreads();
     }
     const int n = static_cast<int>(base);
+    if (threadIdx.x == 0) {  // every emitted pair consumed one matrix entry
+        count_add(ctr, 0, static_cast<unsigned long long>(n));
+        count_add(ctr, 1, static_cast<unsigned long long>(n));
+    }
     int np2 = 1;
     while (np2 < n) np2 <<= 1;
     for (int i = n + threadIdx.x; i < np2; i += kSmallNT) skey[i] = ~0ull;
@@ -380,7 +395,7 @@ void launch_small_sort(Context& ctx, const Matrix& m, Vector& x, int32_t* y_idx,
                                   static_cast<int>(smem)));
     col_sort_small_kernel<V, SR><<<1, kSmallNT, smem, ctx.stream>>>(
         x.nnz, x.sp_idx.as<int32_t>(), x.sp_val.as<V>(), m.col_off.as<int64_t>(),
-        m.row_idx.as<int32_t>(), m.cvals.as<V>(), y_idx, y_val, d_nnz);
+        m.row_idx.as<int32_t>(), m.cvals.as<V>(), y_idx, y_val, d_nnz, ctx.ctr);
     ADA_LAUNCHED(ctx);
 }
 
@@ -391,7 +406,7 @@ void launch_direct_atomic(Context& ctx, const Matrix& m, Vector& x, int G, V* y)
     case GG:                                                                                 \
         col_direct_atomic_kernel<V, GG, SR><<<blocks, kNT, 0, ctx.stream>>>(                 \
             x.nnz, x.sp_idx.as<int32_t>(), x.sp_val.as<V>(), m.col_off.as<int64_t>(),        \
-            m.row_idx.as<int32_t>(), m.cvals.as<V>(), y);                                    \
+            m.row_idx.as<int32_t>(), m.cvals.as<V>(), y, ctx.ctr);                           \
         break;
     switch (G) {
         ADA_G(1) ADA_G(2) ADA_G(4) ADA_G(8) ADA_G(16) ADA_G(32)
@@ -408,7 +423,8 @@ void launch_direct_emit(Context& ctx, const Matrix& m, Vector& x, int G, uint32_
     case GG:                                                                                 \
         col_direct_emit_kernel<V, GG, SR><<<blocks, kNT, 0, ctx.stream>>>(                   \
             x.nnz, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),            \
-            m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), keys, pv);    \
+            m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), keys, pv,     \
+            ctx.ctr);                                                                        \
         break;
     switch (G) {
         ADA_G(1) ADA_G(2) ADA_G(4) ADA_G(8) ADA_G(16) ADA_G(32)
@@ -429,7 +445,8 @@ template <class V, int SR, bool LB>
 __global__ void __launch_bounds__(kNT) col_private_kernel(
     int64_t nnz_x, int64_t nnz_s, int64_t rows, const int64_t* __restrict__ eff,
     const int32_t* __restrict__ xi, const V* __restrict__ xv, const int64_t* __restrict__ co,
-    const int32_t* __restrict__ ri, const V* __restrict__ cv, V* __restrict__ y) {
+    const int32_t* __restrict__ ri, const V* __restrict__ cv, V* __restrict__ y,
+    unsigned long long* __restrict__ ctr) {
     using S = Semiring<SR, V>;
     extern __shared__ __align__(16) unsigned char priv_smem[];
     V* acc = reinterpret_cast<V*>(priv_smem);
@@ -439,6 +456,7 @@ __global__ void __launch_bounds__(kNT) col_private_kernel(
     if (LB) {
         const int64_t ib = nnz_s * c / W, ie = nnz_s * (c + 1) / W;
         const int64_t len = ie - ib;
+        if (threadIdx.x == 0) count_add(ctr, 0, static_cast<unsigned long long>(len));
         const int64_t p0 = ib + len * threadIdx.x / kNT, p1 = ib + len * (threadIdx.x + 1) / kNT;
         if (p0 < p1) {
             int64_t s = segment_search(eff, 0, nnz_x + 1, p0);
@@ -461,6 +479,7 @@ __global__ void __launch_bounds__(kNT) col_private_kernel(
         for (int64_t s = sb + threadIdx.x; s < se; s += kNT) {
             const int32_t col = __ldg(xi + s);
             const V xval = __ldg(xv + s);
+            count_add(ctr, 0, static_cast<unsigned long long>(__ldg(co + col + 1) - __ldg(co + col)));
             for (int64_t k = __ldg(co + col); k < __ldg(co + col + 1); ++k)
                 AtomicCombine<SR>::apply(acc + __ldg(ri + k), S::mul(S::kUsesValues ? __ldg(cv + k) : V(1), xval));
         }
@@ -484,13 +503,13 @@ bool launch_private(Context& ctx, const Matrix& m, Vector& x, bool lb, V* y) {
                                       static_cast<int>(kPrivateSmem)));
         col_private_kernel<V, SR, true><<<grid, kNT, smem, ctx.stream>>>(
             x.nnz, nnz_s, m.rows, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
-            m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), y);
+            m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), y, ctx.ctr);
     } else {
         ADA_CUDA(cudaFuncSetAttribute(col_private_kernel<V, SR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kPrivateSmem)));
         col_private_kernel<V, SR, false><<<grid, kNT, smem, ctx.stream>>>(
             x.nnz, 0, m.rows, nullptr, x.sp_idx.as<int32_t>(), x.sp_val.as<V>(), m.col_off.as<int64_t>(),
-            m.row_idx.as<int32_t>(), m.cvals.as<V>(), y);
+            m.row_idx.as<int32_t>(), m.cvals.as<V>(), y, ctx.ctr);
     }
     ADA_LAUNCHED(ctx);
     return true;
@@ -521,7 +540,7 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
         col_lb_kernel<V, SR, false><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
             x.nnz, nnz_s, tiles, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
             m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), y_dense, nullptr,
-            nullptr);
+            nullptr, ctx.ctr);
         ADA_LAUNCHED(ctx);
         return;
     }
@@ -556,7 +575,7 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
         const int64_t tiles = (nnz_s + kColTile - 1) / kColTile;
         col_lb_kernel<V, SR, true><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
             x.nnz, nnz_s, tiles, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
-            m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), nullptr, k0, v0);
+            m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), nullptr, k0, v0, ctx.ctr);
         ADA_LAUNCHED(ctx);
     }
     DevBuf& counts = ctx.scratch[6];

@@ -39,9 +39,11 @@ __global__ void __launch_bounds__(kNT) row_direct_kernel(int64_t rows,
                                                          const V* __restrict__ vals,
                                                          const V* __restrict__ x,
                                                          const uint32_t* __restrict__ mask,
-                                                         V* __restrict__ y) {
+                                                         V* __restrict__ y,
+                                                         unsigned long long* __restrict__ ctr) {
     using S = Semiring<SR, V>;
     constexpr int kU = unroll_for<G>();
+    unsigned cnt = 0;
     const int64_t gid = static_cast<int64_t>(blockIdx.x) * kNT + threadIdx.x;
     const int64_t row = gid / G;
     const int lg = threadIdx.x & (G - 1);
@@ -72,11 +74,15 @@ __global__ void __launch_bounds__(kNT) row_direct_kernel(int64_t rows,
         }
 #pragma unroll
         for (int j = 0; j < kU; ++j)
-            if (ok[j]) acc = S::fma(a[j], xv[j], acc);
+            if (ok[j]) {
+                acc = S::fma(a[j], xv[j], acc);
+                ++cnt;
+            }
     }
 #pragma unroll
     for (int d = G / 2; d > 0; d >>= 1) acc = S::add(acc, __shfl_xor_sync(kFull, acc, d, G));
     if (valid && lg == 0) y[row] = acc;
+    count_add(ctr, 0, cnt);
 }
 
 // ---------------------------------------------------------------------------
@@ -236,7 +242,8 @@ __global__ void __launch_bounds__(kNT, sizeof(V) == 8 ? 3 : 4) row_lb_kernel(
     int64_t rows, int64_t nnz, int64_t ntiles, const int64_t* __restrict__ ro,
     const int32_t* __restrict__ ci, const V* __restrict__ vals, const V* __restrict__ x,
     const uint32_t* __restrict__ mask, const int64_t* __restrict__ tile_head, V* __restrict__ y,
-    V* __restrict__ head_part, V* __restrict__ tail_part, int64_t* __restrict__ tail_row) {
+    V* __restrict__ head_part, V* __restrict__ tail_part, int64_t* __restrict__ tail_row,
+    unsigned long long* __restrict__ ctr) {
     using S = Semiring<SR, V>;
     __shared__ int swin[kWarps][kWin];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -278,6 +285,7 @@ __global__ void __launch_bounds__(kNT, sizeof(V) == 8 ? 3 : 4) row_lb_kernel(
             if (VALIDATE && ok) ok = (__ldg(mask + (c[r][j] >> 5)) >> (c[r][j] & 31)) & 1u;
             xv[r][j] = ok ? __ldg(x + c[r][j]) : V(0);
             if (!ok) c[r][j] = -1;  // marks "no contribution"
+            else if (ctr) count_add(ctr, 0, 1);
         }
     }
 
@@ -352,7 +360,7 @@ void launch_direct(Context& ctx, const Matrix& m, const V* x, const uint32_t* ma
     case GG:                                                                                   \
         row_direct_kernel<V, GG, VALIDATE, SR><<<blocks, kNT, 0, ctx.stream>>>(                \
             m.rows, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), m.vals.as<V>(), x, mask, \
-            y);                                                                                \
+            y, ctx.ctr);                                                                       \
         break;
     switch (G) {
         ADA_G(1) ADA_G(2) ADA_G(4) ADA_G(8) ADA_G(16) ADA_G(32)
@@ -375,7 +383,7 @@ void launch_lb(Context& ctx, const Matrix& m, const V* x, const uint32_t* mask, 
     int64_t* trow = reinterpret_cast<int64_t*>(tail + T);
     row_lb_kernel<V, VALIDATE, SR><<<static_cast<unsigned>((T + kWarps - 1) / kWarps), kNT, 0, ctx.stream>>>(
         m.rows, m.nnz, T, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), m.vals.as<V>(), x, mask,
-        m.tile_head.as<int64_t>(), y, head, tail, trow);
+        m.tile_head.as<int64_t>(), y, head, tail, trow, ctx.ctr);
     ADA_LAUNCHED(ctx);
     if (T > 1 || m.n_empty > 0) {
         const int64_t work = std::max<int64_t>(T, std::min<int64_t>(m.n_empty, 256LL * ctx.sm_count * 8));

@@ -140,6 +140,15 @@ void run_kernel(Context& ctx, const Matrix& m, Vector& x, int kernel, const adas
             if (!e) ADA_CUDA(cudaEventCreate(&e));
         ADA_CUDA(cudaEventRecord(y.ev[0], ctx.stream));
     }
+    y.has_ctr = ctx.counters;
+    if (ctx.counters) {
+        ctx.ctr = static_cast<unsigned long long*>(y.d_ctr.ensure(2 * sizeof(unsigned long long)));
+        ADA_CUDA(cudaMemsetAsync(ctx.ctr, 0, 2 * sizeof(unsigned long long), ctx.stream));
+    }
+    struct CtrReset {
+        Context& c;
+        ~CtrReset() { c.ctr = nullptr; }
+    } ctr_reset{ctx};
     if (m.dtype == ADASPMV_F64) run_v<double>(ctx, m, x, kernel, cfg, y);
     else run_v<float>(ctx, m, x, kernel, cfg, y);
     if (y.timed) ADA_CUDA(cudaEventRecord(y.ev[1], ctx.stream));

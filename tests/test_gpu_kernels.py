@@ -458,3 +458,38 @@ def test_binned_skewed_rows_cut_to_csr_segments(ctx, port, dt):
             b = A.run_kernel(m, k, xs, A.KernelConfig(semiring=A.OR_AND, row_layout=2))
             c = A.run_kernel(m, k, xs, A.KernelConfig(semiring=A.OR_AND, row_layout=1))
             assert b.dense().values.tobytes() == c.dense().values.tobytes(), (k, nx)
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
+def test_kernel_counters(port, dt):
+    """KernelCounters (kernels.hpp:106-111) as the reference's counter build
+    records them (kernels.hpp:281-283, 447-511): values_read = nnz on the SpMV
+    path, nnz_s on the row-SpMSpV and column paths (every entry consumed once
+    -- no kernel reads a value twice or skips one); pairs_emitted = nnz_s on
+    the sort write-back; cas_retries 0.  CSR and row-bin executions, the
+    private-accumulator variant, the small and the radix sort paths."""
+    ctx = A.Context(0)
+    ctx.set_counters(True)
+    for rows, cols, dens, seed in ((700, 500, 0.02, 4), (6000, 5000, 0.004, 5)):
+        r_, c_, ro, ci, vals = synth.random_csr(rows, cols, dens, seed=seed, dtype=dt)
+        m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+        nnz = int(ro[-1])
+        co = np.bincount(ci, minlength=cols)
+        for nx in (1, 30, cols // 3, cols):
+            xi, xv = synth.sparse_vector(cols, nx, seed=nx, dtype=dt)
+            nnz_s = int(co[xi].sum())
+            xd = port.sparse_to_dense(cols, xi, xv)
+            cfgs = [A.KernelConfig(), A.KernelConfig(row_layout=2), A.KernelConfig(atomic_private_accumulators=1)]
+            for cfg in cfgs:
+                for k in range(8):
+                    x = A.SparseVector(cols, xi, xv) if k >= 4 else A.DenseVector(xd)
+                    out = A.run_kernel(m, k, x, cfg, out=A.MultiplyOutput(ctx))
+                    c = out.counters()
+                    want = nnz if k <= 1 else nnz_s
+                    assert c["values_read"] == want, (k, nx, cfg._c().row_layout, c)
+                    assert c["pairs_emitted"] == (nnz_s if k in (5, 7) else 0), (k, nx, c)
+                    assert c["cas_retries"] == 0
+    ctx.set_counters(False)
+    out = A.run_kernel(m, 0, A.DenseVector(xd), out=A.MultiplyOutput(ctx))
+    with pytest.raises(A.InvalidArgument):
+        out.counters()
