@@ -128,3 +128,25 @@ def test_c3_class_bfs_levels(ctx, port):
             lv, reps = A.bfs(m, 0, sr, force_kernel=forced)
             assert np.array_equal(lv, exp), (sr, forced)
             assert len(reps) == nl
+
+
+@pytest.mark.parametrize("sparsity", [0.01, 1.0])
+def test_c1_laplacian_fp64_all_kernels_vs_oracle(ctx, port, sparsity):
+    """configs[0]: the 2-D 5-point Laplacian on a 1000 x 1000 grid (10^6 rows,
+    4,996,000 nnz, fp64) at x = 100 % (SpMV) and 1 % (SpMSpV), every kernel
+    against the oracle at the fp64 tolerance (1e-12 of |A||x|).  x is random
+    (an all-ones x would cancel exactly on the interior rows)."""
+    rows, cols, ro, ci, vals = synth.laplacian_2d(1000, dtype=np.float64)
+    assert rows == 10 ** 6 and int(ro[-1]) == 4_996_000
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    nx = int(round(sparsity * cols))
+    xi, xv = synth.sparse_vector(cols, nx, seed=7, dtype=np.float64)
+    xd = port.sparse_to_dense(cols, xi, xv)
+    y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, xd)
+    for k in range(8):
+        x = A.SparseVector(cols, xi, xv) if k >= 4 else A.DenseVector(xd)
+        out = A.run_kernel(m, k, x)
+        assert_dense_close(out.dense().values, y_ref, bound, np.float64, f"C1 x={sparsity} k={k}")
+        if k in (5, 7):
+            s = out.sparse()
+            assert_sparse_match(s.indices, s.values, y_ref, bound, np.float64, f"C1 sparse k={k}")
