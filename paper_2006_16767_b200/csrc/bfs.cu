@@ -197,6 +197,37 @@ void launch_pull(Context& ctx, const Matrix& m, const Vector& x, const int32_t* 
     y.has_dense = true;
 }
 
+// One fused push level (boolean semiring): the column-major choices (K4-K7)
+// run K6's load-balanced tiles, and instead of an atomic write into a dense y
+// each unvisited row is claimed once (atomicCAS on its level) and appended
+// to the next frontier with its column degree -- no dense y to clear, no scan
+// over all n rows.  x becomes the next frontier; returns its size.
+template <class V>
+int64_t push_level(Context& ctx, const Matrix& m, Vector& x, int32_t* lv, int32_t level, DevBuf& nidx,
+                   DevBuf& nval, cudaEvent_t done) {
+    const size_t n = static_cast<size_t>(std::max<int64_t>(x.n, 1));
+    int32_t* ni = static_cast<int32_t*>(nidx.ensure(sizeof(int32_t) * n));
+    V* nv = static_cast<V*>(nval.ensure(sizeof(V) * n));
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(ctx.dscal(13));
+    ADA_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), ctx.stream));
+    bfs_push_lb<V>(ctx, m, x, lv, level, ni, nv, cnt);
+    ADA_CUDA(cudaEventRecord(done, ctx.stream));
+    ctx.fetch_scalars(reinterpret_cast<const int64_t*>(cnt), 2);
+    const int64_t nx = ctx.h_scalars[0], ns = ctx.h_scalars[1];
+    x.invalidate();
+    std::swap(x.sp_idx.p, nidx.p);
+    std::swap(x.sp_idx.cap, nidx.cap);
+    std::swap(x.sp_idx.s, nidx.s);
+    std::swap(x.sp_val.p, nval.p);
+    std::swap(x.sp_val.cap, nval.cap);
+    std::swap(x.sp_val.s, nval.s);
+    x.nnz = nx;
+    x.has_sparse = true;
+    x.nnz_s = ns;
+    x.nnz_s_matrix = m.id;
+    return nx;
+}
+
 // Push vs pull by the algorithmic-bytes model of SURVEY.md section 8(d):
 // column-major reads ~ nnz_s entries, row-major (validated) reads every index.
 // The pull is output-masked (bfs_pull_kernel): only the ~unvisited share of
@@ -239,6 +270,7 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
     }
     Output y;
     y.ctx = &ctx;
+    DevBuf next_idx, next_val;  // the fused push's next frontier (swapped into x)
     adaspmv_config cfg{};
     cfg.semiring = SR;
     int64_t it = 0;
@@ -268,20 +300,26 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         // values, an Inf * 0 of the plain SpMV could differ, so those keep
         // the unmasked multiply).
         const bool pull = k == 2 || k == 3 || (SR == SR_OR_AND && k <= 1);
+        // the column choices under the boolean semiring: the fused push
+        const bool push = SR == SR_OR_AND && k >= 4;
         if (pull) {  // output-masked pull: the mask, and x values unless OR_AND
             vector_ensure_mask(ctx, x);
             if (SR != SR_OR_AND) vector_ensure_dense(ctx, x, SR);
         } else if (k <= 1) {
             vector_ensure_dense(ctx, x, SR);
-        } else if (k == 6 || k == 7) {
+        } else if (k == 6 || k == 7 || push) {
             vector_ensure_eff(ctx, x, m);
         }
         ADA_CUDA(cudaEventRecord(ev[1], ctx.stream));
         const int64_t nnz_x = x.nnz;
-        if (pull) launch_pull<V, SR>(ctx, m, x, lv, y);  // row-major, output-masked
-        else run_kernel(ctx, m, x, k, cfg, y);
-        ADA_CUDA(cudaEventRecord(ev[2], ctx.stream));
-        visited += next_frontier<V, SR>(ctx, m, y, x, lv, static_cast<int32_t>(it + 1));  // syncs
+        if (push) {  // multiply + frontier update in one pass (syncs)
+            visited += push_level<V>(ctx, m, x, lv, static_cast<int32_t>(it + 1), next_idx, next_val, ev[2]);
+        } else {
+            if (pull) launch_pull<V, SR>(ctx, m, x, lv, y);  // row-major, output-masked
+            else run_kernel(ctx, m, x, k, cfg, y);
+            ADA_CUDA(cudaEventRecord(ev[2], ctx.stream));
+            visited += next_frontier<V, SR>(ctx, m, y, x, lv, static_cast<int32_t>(it + 1));  // syncs
+        }
         if (reports && it < max_reports) {
             float c_ms = 0, k_ms = 0;
             ADA_CUDA(cudaEventElapsedTime(&c_ms, ev[0], ev[1]));

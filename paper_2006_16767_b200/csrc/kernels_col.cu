@@ -105,13 +105,19 @@ __device__ __forceinline__ int64_t warp_segment_of(const int64_t* __restrict__ e
     return lo + (31 - __clz(b));
 }
 
-template <class V, int SR, bool EMIT>
+// MODE 0: atomic write-back into y (K6); 1: pair emission (K7); 2: the BFS
+// push -- each row not yet visited (lv < 0) is claimed once (atomicCAS on
+// its level) and appended to the next frontier (keys/pvals = its indices and
+// values, bfs_cnt[0] its size, bfs_cnt[1] its effective nnz).
+template <class V, int SR, int MODE>
 __global__ void __launch_bounds__(kNT) col_lb_kernel(
     int64_t nnz_x, int64_t nnz_s, int64_t ntiles, const int64_t* __restrict__ eff,
     const int32_t* __restrict__ xi, const V* __restrict__ xv, const int64_t* __restrict__ co,
     const int32_t* __restrict__ ri, const V* __restrict__ cv, V* __restrict__ y,
-    uint32_t* __restrict__ keys, V* __restrict__ pvals, unsigned long long* __restrict__ ctr) {
+    uint32_t* __restrict__ keys, V* __restrict__ pvals, unsigned long long* __restrict__ ctr,
+    int32_t* __restrict__ lv = nullptr, int32_t level = 0, unsigned long long* __restrict__ bfs_cnt = nullptr) {
     using S = Semiring<SR, V>;
+    constexpr bool EMIT = MODE == 1;
     constexpr int kW = kNT / 32;
     constexpr int kJ = kColTile / 32;  // entries per lane
     __shared__ int64_t s_base[kW][kColWin];  // co[xi[s]] - eff[s]
@@ -184,6 +190,31 @@ __global__ void __launch_bounds__(kNT) col_lb_kernel(
             r[j] = ld_stream(ri + kidx[j]);
             a[j] = S::kUsesValues ? ld_stream(cv + kidx[j]) : V(1);
         }
+    }
+    if constexpr (MODE == 2) {
+        // claims are appended warp-aggregated: one counter update per warp
+        // instruction, slots by the claiming lanes' rank
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+            const int32_t row = kidx[j] >= 0 ? r[j] : 0;
+            const bool claim = kidx[j] >= 0 && lv[row] < 0 && atomicCAS(lv + row, -1, level) == -1;
+            const unsigned ballot = __ballot_sync(kFull, claim);
+            if (ballot == 0u) continue;  // warp-uniform
+            const long long deg = warp_sum(claim ? static_cast<long long>(__ldg(co + row + 1) - __ldg(co + row)) : 0ll);
+            const int leader = __ffs(ballot) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) {
+                base = atomicAdd(bfs_cnt, static_cast<unsigned long long>(__popc(ballot)));
+                atomicAdd(bfs_cnt + 1, static_cast<unsigned long long>(deg));
+            }
+            base = __shfl_sync(kFull, base, leader);
+            if (claim) {
+                const unsigned long long slot = base + __popc(ballot & lanemask_lt());
+                reinterpret_cast<int32_t*>(keys)[slot] = row;
+                pvals[slot] = V(1);
+            }
+        }
+        return;
     }
 #pragma unroll
     for (int j = 0; j < kJ; ++j) {
@@ -517,6 +548,26 @@ bool launch_private(Context& ctx, const Matrix& m, Vector& x, bool lb, V* y) {
 
 }  // namespace
 
+// BFS push (OR_AND) over the LB tiles of K6: x needs its eff offsets;
+// next_idx / next_val receive the next frontier, cnt[0..1] its size and nnz_s.
+template <class V>
+void bfs_push_lb(Context& ctx, const Matrix& m, Vector& x, int32_t* lv, int32_t level, int32_t* next_idx,
+                 V* next_val, unsigned long long* cnt) {
+    const int64_t nnz_s = vector_nnz_s(ctx, x, m);
+    if (nnz_s == 0) return;
+    vector_ensure_eff(ctx, x, m);
+    const int64_t tiles = (nnz_s + kColTile - 1) / kColTile;
+    col_lb_kernel<V, SR_OR_AND, 2><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
+        x.nnz, nnz_s, tiles, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(), m.col_off.as<int64_t>(),
+        m.row_idx.as<int32_t>(), m.cvals.as<V>(), nullptr, reinterpret_cast<uint32_t*>(next_idx), next_val, ctx.ctr,
+        lv, level, cnt);
+    ADA_LAUNCHED(ctx);
+}
+template void bfs_push_lb<float>(Context&, const Matrix&, Vector&, int32_t*, int32_t, int32_t*, float*,
+                                 unsigned long long*);
+template void bfs_push_lb<double>(Context&, const Matrix&, Vector&, int32_t*, int32_t, int32_t*, double*,
+                                  unsigned long long*);
+
 template <class V, int SR>
 void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort, bool private_acc,
                    int lanes, V* y_dense, int32_t* y_idx, V* y_val, int64_t* d_nnz,
@@ -537,7 +588,7 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
         if (nnz_s == 0) return;
         vector_ensure_eff(ctx, x, m);  // nnz_s may be known without the offsets
         const int64_t tiles = (nnz_s + kColTile - 1) / kColTile;
-        col_lb_kernel<V, SR, false><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
+        col_lb_kernel<V, SR, 0><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
             x.nnz, nnz_s, tiles, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
             m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), y_dense, nullptr,
             nullptr, ctx.ctr);
@@ -573,7 +624,7 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
         launch_direct_emit<V, SR>(ctx, m, x, G, k0, v0);
     } else {
         const int64_t tiles = (nnz_s + kColTile - 1) / kColTile;
-        col_lb_kernel<V, SR, true><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
+        col_lb_kernel<V, SR, 1><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
             x.nnz, nnz_s, tiles, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
             m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), nullptr, k0, v0, ctx.ctr);
         ADA_LAUNCHED(ctx);
