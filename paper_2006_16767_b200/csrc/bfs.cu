@@ -124,8 +124,8 @@ int64_t next_frontier(Context& ctx, const Matrix& m, Output& y, Vector& x, int32
 
 // Output-masked pull: the fused BFS extension of K2/K3.
 // Rows already visited are skipped before any index is loaded; with the
-// boolean semiring (or min-plus on a pattern matrix, where every frontier
-// value is the current level) a lane stops at its first frontier neighbour.
+// boolean semiring, or any semiring on a pattern matrix (only membership of
+// the next frontier is used), a lane stops at its first frontier neighbour.
 // Only unvisited rows are written; the frontier update reads y only there.
 template <class V, int G, int SR, bool EARLY>
 __global__ void __launch_bounds__(256) bfs_pull_kernel(int64_t rows, const int64_t* __restrict__ ro,
@@ -189,7 +189,9 @@ void launch_pull_e(Context& ctx, const Matrix& m, const Vector& x, const int32_t
 template <class V, int SR>
 void launch_pull(Context& ctx, const Matrix& m, const Vector& x, const int32_t* lv, Output& y) {
     V* yd = static_cast<V*>(y.dense.ensure(sizeof(V) * static_cast<size_t>(std::max<int64_t>(m.rows, 1))));
-    const bool early = SR == SR_OR_AND || (SR == SR_MIN_PLUS && m.pattern);
+    // membership only: on a pattern matrix any frontier neighbour decides
+    // (plus-times sums of 1s, min-plus of 1 + level), as with the boolean one
+    const bool early = SR == SR_OR_AND || m.pattern;
     if (early) launch_pull_e<V, SR, true>(ctx, m, x, lv, yd);
     else launch_pull_e<V, SR, false>(ctx, m, x, lv, yd);
     y.reset(m.rows, m.dtype);
@@ -203,14 +205,14 @@ void launch_pull(Context& ctx, const Matrix& m, const Vector& x, const int32_t* 
 // to the next frontier with its column degree -- no dense y to clear, no scan
 // over all n rows.  x becomes the next frontier; returns its size.
 template <class V>
-int64_t push_level(Context& ctx, const Matrix& m, Vector& x, int32_t* lv, int32_t level, DevBuf& nidx,
+int64_t push_level(Context& ctx, const Matrix& m, Vector& x, int32_t* lv, int32_t level, V value, DevBuf& nidx,
                    DevBuf& nval, cudaEvent_t done) {
     const size_t n = static_cast<size_t>(std::max<int64_t>(x.n, 1));
     int32_t* ni = static_cast<int32_t*>(nidx.ensure(sizeof(int32_t) * n));
     V* nv = static_cast<V*>(nval.ensure(sizeof(V) * n));
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(ctx.dscal(13));
     ADA_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), ctx.stream));
-    bfs_push_lb<V>(ctx, m, x, lv, level, ni, nv, cnt);
+    bfs_push_lb<V>(ctx, m, x, lv, level, ni, nv, value, cnt);
     ADA_CUDA(cudaEventRecord(done, ctx.stream));
     ctx.fetch_scalars(reinterpret_cast<const int64_t*>(cnt), 2);
     const int64_t nx = ctx.h_scalars[0], ns = ctx.h_scalars[1];
@@ -300,8 +302,11 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         // values, an Inf * 0 of the plain SpMV could differ, so those keep
         // the unmasked multiply).
         const bool pull = k == 2 || k == 3 || (SR == SR_OR_AND && k <= 1);
-        // the column choices under the boolean semiring: the fused push
-        const bool push = SR == SR_OR_AND && k >= 4;
+        // the column choices run as the fused push when membership of the
+        // next frontier does not depend on values: the boolean semiring, or a
+        // pattern matrix (plus-times sums of 1s are >= 1; min-plus of 1 +
+        // level is finite)
+        const bool push = k >= 4 && (SR == SR_OR_AND || m.pattern);
         if (pull) {  // output-masked pull: the mask, and x values unless OR_AND
             vector_ensure_mask(ctx, x);
             if (SR != SR_OR_AND) vector_ensure_dense(ctx, x, SR);
@@ -313,7 +318,8 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         ADA_CUDA(cudaEventRecord(ev[1], ctx.stream));
         const int64_t nnz_x = x.nnz;
         if (push) {  // multiply + frontier update in one pass (syncs)
-            visited += push_level<V>(ctx, m, x, lv, static_cast<int32_t>(it + 1), next_idx, next_val, ev[2]);
+            const V value = SR == SR_MIN_PLUS ? V(it + 1) : V(1);  // as next_frontier writes
+            visited += push_level<V>(ctx, m, x, lv, static_cast<int32_t>(it + 1), value, next_idx, next_val, ev[2]);
         } else {
             if (pull) launch_pull<V, SR>(ctx, m, x, lv, y);  // row-major, output-masked
             else run_kernel(ctx, m, x, k, cfg, y);

@@ -287,7 +287,7 @@ void context_release(Context& ctx);
 // BFS push over K6's LB tiles (kernels_col.cu), boolean semiring
 template <class V>
 void bfs_push_lb(Context& ctx, const Matrix& m, Vector& x, int32_t* lv, int32_t level, int32_t* next_idx,
-                 V* next_val, unsigned long long* cnt);
+                 V* next_val, V value, unsigned long long* cnt);
 
 // row-partitioned multi-GPU mode (multi.cpp)
 void shard_cuts(const int64_t* ro, int64_t rows, int g, int64_t* cuts);

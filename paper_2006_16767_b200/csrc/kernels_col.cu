@@ -115,7 +115,8 @@ __global__ void __launch_bounds__(kNT) col_lb_kernel(
     const int32_t* __restrict__ xi, const V* __restrict__ xv, const int64_t* __restrict__ co,
     const int32_t* __restrict__ ri, const V* __restrict__ cv, V* __restrict__ y,
     uint32_t* __restrict__ keys, V* __restrict__ pvals, unsigned long long* __restrict__ ctr,
-    int32_t* __restrict__ lv = nullptr, int32_t level = 0, unsigned long long* __restrict__ bfs_cnt = nullptr) {
+    int32_t* __restrict__ lv = nullptr, int32_t level = 0, unsigned long long* __restrict__ bfs_cnt = nullptr,
+    V bfs_value = V(1)) {
     using S = Semiring<SR, V>;
     constexpr bool EMIT = MODE == 1;
     constexpr int kW = kNT / 32;
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(kNT) col_lb_kernel(
             if (claim) {
                 const unsigned long long slot = base + __popc(ballot & lanemask_lt());
                 reinterpret_cast<int32_t*>(keys)[slot] = row;
-                pvals[slot] = V(1);
+                pvals[slot] = bfs_value;
             }
         }
         return;
@@ -552,7 +553,7 @@ bool launch_private(Context& ctx, const Matrix& m, Vector& x, bool lb, V* y) {
 // next_idx / next_val receive the next frontier, cnt[0..1] its size and nnz_s.
 template <class V>
 void bfs_push_lb(Context& ctx, const Matrix& m, Vector& x, int32_t* lv, int32_t level, int32_t* next_idx,
-                 V* next_val, unsigned long long* cnt) {
+                 V* next_val, V value, unsigned long long* cnt) {
     const int64_t nnz_s = vector_nnz_s(ctx, x, m);
     if (nnz_s == 0) return;
     vector_ensure_eff(ctx, x, m);
@@ -560,12 +561,12 @@ void bfs_push_lb(Context& ctx, const Matrix& m, Vector& x, int32_t* lv, int32_t 
     col_lb_kernel<V, SR_OR_AND, 2><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
         x.nnz, nnz_s, tiles, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(), m.col_off.as<int64_t>(),
         m.row_idx.as<int32_t>(), m.cvals.as<V>(), nullptr, reinterpret_cast<uint32_t*>(next_idx), next_val, ctx.ctr,
-        lv, level, cnt);
+        lv, level, cnt, value);
     ADA_LAUNCHED(ctx);
 }
-template void bfs_push_lb<float>(Context&, const Matrix&, Vector&, int32_t*, int32_t, int32_t*, float*,
+template void bfs_push_lb<float>(Context&, const Matrix&, Vector&, int32_t*, int32_t, int32_t*, float*, float,
                                  unsigned long long*);
-template void bfs_push_lb<double>(Context&, const Matrix&, Vector&, int32_t*, int32_t, int32_t*, double*,
+template void bfs_push_lb<double>(Context&, const Matrix&, Vector&, int32_t*, int32_t, int32_t*, double*, double,
                                   unsigned long long*);
 
 template <class V, int SR>
