@@ -306,7 +306,10 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         // next frontier does not depend on values: the boolean semiring, or a
         // pattern matrix (plus-times sums of 1s are >= 1; min-plus of 1 +
         // level is finite)
-        const bool push = k >= 4 && (SR == SR_OR_AND || m.pattern);
+        // (a frontier reaching more entries than there are rows -- forced
+        // column kernels on a fat level -- keeps the atomic multiply + scan,
+        // which is faster there than claiming row by row)
+        const bool push = k >= 4 && (SR == SR_OR_AND || m.pattern) && vector_nnz_s(ctx, x, m) <= m.rows;
         if (pull) {  // output-masked pull: the mask, and x values unless OR_AND
             vector_ensure_mask(ctx, x);
             if (SR != SR_OR_AND) vector_ensure_dense(ctx, x, SR);
