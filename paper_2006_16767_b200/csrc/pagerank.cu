@@ -152,16 +152,21 @@ int64_t next_delta(Context& ctx, const Matrix& m, Output& y, Vector& x, V* rank,
 }
 
 // Default policy without a bundle: the algorithmic-bytes model of SURVEY.md
-// 8(d) -- column scatter (K6/K7 family) against a full row pass (K0/K1).
+// 8(d) -- column scatter (K6/K7 family) against a full row pass (K0/K1) --
+// with each scattered entry priced at 4x its bytes: an L2 atomic per entry
+// (measured on B200: C2 K6 84 us for 6.7 M entries vs K0 ~165 us for 67 M).
 int heuristic_kernel(Context& ctx, const Matrix& m, Vector& x) {
     const int64_t nnz_s = vector_nnz_s(ctx, x, m);
     const double vb = m.vbytes();
-    const double col = static_cast<double>(x.nnz) * (20.0 + vb) + static_cast<double>(nnz_s) * (4.0 + vb) +
+    constexpr double kAtomic = 4.0;
+    const double col = static_cast<double>(x.nnz) * (20.0 + vb) + kAtomic * static_cast<double>(nnz_s) * (4.0 + vb) +
                        (nnz_s <= 4096 ? 0.0 : static_cast<double>(m.rows) * vb);
     const double row = static_cast<double>(m.rows + 1) * 8.0 + static_cast<double>(m.nnz) * (4.0 + vb) +
                        static_cast<double>(m.cols + m.rows) * vb;
     if (col <= row) return nnz_s <= 4096 ? 7 : 6;
-    return m.feat[8] > 0.5 ? 1 : 0;  // skewed rows (Gini) -> load-balanced
+    // skewed rows (Gini) -> load-balanced, unless the row-bin layout (which
+    // splits the heavy rows out) runs the direct kernel
+    return m.feat[8] > 0.5 && !binned_preferred(m) ? 1 : 0;
 }
 
 template <class V>
