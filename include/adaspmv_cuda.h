@@ -132,7 +132,9 @@ const char* adaspmv_version(void);
 int adaspmv_matrix_create_csr(adaspmv_ctx* ctx, int64_t rows, int64_t cols,
                               const int64_t* row_offsets, const int64_t* col_indices,
                               const void* values, int dtype, adaspmv_matrix** out);
-/* Same from device-resident CSR (int64 offsets, int32 indices); copied. */
+/* Same from device-resident CSR (int64 offsets, int32 indices); validated on
+ * the device like the host path (CsrMatrix::validate, one synchronisation),
+ * then copied. */
 int adaspmv_matrix_create_csr_device(adaspmv_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
                                      const int64_t* d_row_offsets, const int32_t* d_col_indices,
                                      const void* d_values, int dtype, adaspmv_matrix** out);
@@ -173,7 +175,9 @@ int adaspmv_vector_set_sparse(adaspmv_ctx* ctx, adaspmv_vector* v, int64_t nnz,
                               const int64_t* indices, const void* values);
 /* DenseVector (sparse.hpp:99-109): n values. */
 int adaspmv_vector_set_dense(adaspmv_ctx* ctx, adaspmv_vector* v, const void* values);
-/* Device-resident inputs (e.g. a previous y or a BFS frontier): copied. */
+/* Device-resident inputs (e.g. a previous y or a BFS frontier): copied.  The
+ * sparse form's int32 indices are validated on the device first
+ * (SparseVector::validate, one synchronisation). */
 int adaspmv_vector_set_sparse_device(adaspmv_ctx* ctx, adaspmv_vector* v, int64_t nnz,
                                      const int32_t* d_indices, const void* d_values);
 int adaspmv_vector_set_dense_device(adaspmv_ctx* ctx, adaspmv_vector* v, const void* d_values);
@@ -334,10 +338,20 @@ int adaspmv_multi_destroy(adaspmv_multi* mm);
 typedef struct {
     int64_t iteration;
     int64_t nnz_x;      /* frontier size */
-    int32_t kernel;     /* KernelId::index() used */
-    int32_t pad;
+    int32_t kernel;     /* KernelId::index() selected (or forced) */
+    int32_t exec_mode;  /* how it ran: ADASPMV_EXEC_* (BFS fuses some choices) */
     double feature_s, predict_s, convert_s, kernel_s; /* IterationReport */
 } adaspmv_iteration_report;
+
+/* adaspmv_iteration_report::exec_mode.  BFS runs a row-major choice as the
+ * output-masked pull (K2/K3, and K0/K1 under OR_AND) and, when frontier
+ * membership does not depend on values, a column-major choice as the fused
+ * top-down push over K6's load-balanced tiles (claims rows, appends the next
+ * frontier; no dense y): `kernel` then names the selection, `exec_mode` what
+ * actually ran. */
+#define ADASPMV_EXEC_AS_SELECTED 0
+#define ADASPMV_EXEC_MASKED_PULL 1
+#define ADASPMV_EXEC_FUSED_PUSH_LB 2
 
 /* execute_iteration: lazy features -> predict_kernel (or
  * `forced_kernel` >= 0) -> convert x iff the kernel needs another format ->
@@ -358,9 +372,11 @@ int adaspmv_bfs(adaspmv_ctx* ctx, const adaspmv_matrix* m, int64_t source, int s
                 const adaspmv_bundle* b, int forced_kernel, int64_t* levels, int64_t* n_levels,
                 adaspmv_iteration_report* reports, int64_t max_reports);
 
-/* Incremental (delta-propagation) PageRank: P = A with
- * column j scaled by 1/deg_col(j) (pattern; dangling columns propagate
- * nothing), built once per call on the device.  rank = 0,
+/* Incremental (delta-propagation) PageRank: P = A^T with
+ * column j scaled by 1/outdeg(j), outdeg(j) = stored entries of row j of A
+ * (SPEC.md:500 delta' = damping * A^T_colnorm * delta: edge i -> j moves
+ * mass from i to j; pattern; dangling vertices propagate nothing,
+ * SPEC.md:543), built once per matrix on the device.  rank = 0,
  * delta = 1/n; repeat { rank += delta; delta = {d*(P delta)_i : |.| >= prune,
  * != 0} } until delta is empty or `max_iters` multiplies were done.  Kernel
  * per iteration: `bundle`, else `forced_kernel` (0..7), else (-1) the

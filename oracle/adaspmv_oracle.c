@@ -172,8 +172,10 @@ int64_t or_bfs_queue(int64_t n, const int64_t* co, const int64_t* ri, int64_t so
 
 /* SPEC.md:498-506 incremental PageRank (delta propagation with pruning),
  * pinned only by SPEC's examples and by dense power iteration (tests).
- * P = A with column j scaled by 1/deg_col(j) (pattern; SPEC.md:543 dangling
- * columns propagate nothing); multiply with A as stored.
+ * delta' = d * A^T_colnorm * delta, i.e. P = A^T with column j
+ * scaled by 1/outdeg(j).  The caller passes A's CSR as (co, ri): entry e of
+ * "column" j below is an edge j -> ri[e] of A and outdeg(j) = co[j+1]-co[j]
+ * (dangling vertices propagate nothing).
  * rank = 0, delta = 1/n; while delta != {} and it < max_iters:
  *   rank += delta; y = P delta; delta = {d*y_i : |d*y_i| >= prune, != 0}.
  * Products are formed as (1/deg_j) * delta_j, like a multiply by P's values.

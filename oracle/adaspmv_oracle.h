@@ -76,6 +76,9 @@ int64_t or_bfs_queue(int64_t n, const int64_t* col_offsets, const int64_t* row_i
     /* kernels.hpp:197-209 */                                                                  \
     void or_reference_multiply##SFX(int64_t rows, const int64_t* ro, const int64_t* ci,        \
                                     const REAL* vals, const REAL* x, REAL* y);                 \
+    /* semirings of SPEC.md:489-497 (0 plus-times, 1 or-and, 2 min-plus) */                   \
+    void or_semiring_multiply##SFX(int64_t rows, const int64_t* ro, const int64_t* ci,         \
+                                   const REAL* vals, const REAL* x, int sr, REAL* y);          \
     /* kernels.hpp:219-286 (validate = RowSpMSpV with mask, else SpMV) */                     \
     void or_row_major_multiply##SFX(int64_t rows, const int64_t* ro, const int64_t* ci,        \
                                     const REAL* vals, const REAL* x, const uint64_t* mask,     \

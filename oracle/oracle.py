@@ -90,6 +90,8 @@ class Port:
             nr = _nullable(np.float64 if sfx == "_f64" else np.float32)
             f = getattr(L, "or_reference_multiply" + sfx)
             f.argtypes = [C.c_int64, _i64p, _i64p, rp, rp, rp]
+            f = getattr(L, "or_semiring_multiply" + sfx)
+            f.argtypes = [C.c_int64, _i64p, _i64p, rp, rp, C.c_int, rp]
             f = getattr(L, "or_row_major_multiply" + sfx)
             f.argtypes = [C.c_int64, _i64p, _i64p, rp, rp, _nullable(np.uint64), C.c_int, C.c_int, rp]
             f = getattr(L, "or_spmspv_col" + sfx)
@@ -188,6 +190,7 @@ class Port:
         return lv, int(nl)
 
     def pagerank_incremental(self, n, col_offsets, row_indices, damping=0.85, prune=1e-6, max_iters=300):
+        """SPEC.md:498-506; pass A's CSR (row_offsets, col_indices): out-edges per source."""
         rank = np.zeros(n, np.float64)
         it = self.lib.or_pagerank_incremental(n, _as(col_offsets, np.int64), _as(row_indices, np.int64),
                                               float(damping), float(prune), int(max_iters), rank)
@@ -200,6 +203,16 @@ class Port:
         y = np.zeros(rows, dt)
         getattr(self.lib, "or_reference_multiply" + self._sfx(dt))(
             rows, _as(ro, np.int64), _as(ci, np.int64), vals, _as(x, dt), y)
+        return y
+
+    def semiring_multiply(self, rows, ro, ci, vals, x, sr):
+        """y = A x under semiring sr (0 plus-times, 1 or-and, 2 min-plus); dense x,
+        absent entries 0 (or-and) / +inf (min-plus)."""
+        vals = np.ascontiguousarray(vals)
+        dt = vals.dtype
+        y = np.zeros(rows, dt)
+        getattr(self.lib, "or_semiring_multiply" + self._sfx(dt))(
+            rows, _as(ro, np.int64), _as(ci, np.int64), vals, _as(x, dt), int(sr), y)
         return y
 
     def row_major_multiply(self, rows, ro, ci, vals, x, mask=None, load_balanced=False, workers=1):

@@ -45,6 +45,8 @@ LIB_PATH = PKG / "libadaspmv_cuda.so"
 
 F64, F32 = 0, 1
 PLUS_TIMES, OR_AND, MIN_PLUS = 0, 1, 2
+# adaspmv_iteration_report::exec_mode: how BFS ran the selected kernel
+EXEC_AS_SELECTED, EXEC_MASKED_PULL, EXEC_FUSED_PUSH_LB = 0, 1, 2
 FEATURE_NAMES = ("m", "n", "nnz", "max_row", "min_row", "avg_row", "relative_range",
                  "var_nnz_row", "gc", "nnz_x", "x_sparsity", "nnz_s", "m_sparsity")
 
@@ -95,7 +97,7 @@ _ERRORS = {1: InvalidArgument, 2: OutOfRange, 3: ParseError, 4: FormatError, 5: 
 
 class _IterReport(C.Structure):
     _fields_ = [("iteration", C.c_int64), ("nnz_x", C.c_int64), ("kernel", C.c_int32),
-                ("pad", C.c_int32), ("feature_s", C.c_double), ("predict_s", C.c_double),
+                ("exec_mode", C.c_int32), ("feature_s", C.c_double), ("predict_s", C.c_double),
                 ("convert_s", C.c_double), ("kernel_s", C.c_double)]
 
 
@@ -1087,8 +1089,9 @@ def bfs(m: DualMatrix, source: int = 0, semiring: int = OR_AND, bundle: Optional
     out = []
     for i in range(min(nl.value, max_reports)):
         r = reps[i]
-        out.append(dict(iteration=r.iteration, nnz_x=r.nnz_x, kernel=r.kernel, feature_s=r.feature_s,
-                        predict_s=r.predict_s, convert_s=r.convert_s, kernel_s=r.kernel_s))
+        out.append(dict(iteration=r.iteration, nnz_x=r.nnz_x, kernel=r.kernel, exec_mode=r.exec_mode,
+                        feature_s=r.feature_s, predict_s=r.predict_s, convert_s=r.convert_s,
+                        kernel_s=r.kernel_s))
     return levels, out
 
 
@@ -1096,8 +1099,9 @@ def _reports(reps, n, max_reports):
     out = []
     for i in range(min(n, max_reports)):
         r = reps[i]
-        out.append(dict(iteration=r.iteration, nnz_x=r.nnz_x, kernel=r.kernel, feature_s=r.feature_s,
-                        predict_s=r.predict_s, convert_s=r.convert_s, kernel_s=r.kernel_s))
+        out.append(dict(iteration=r.iteration, nnz_x=r.nnz_x, kernel=r.kernel, exec_mode=r.exec_mode,
+                        feature_s=r.feature_s, predict_s=r.predict_s, convert_s=r.convert_s,
+                        kernel_s=r.kernel_s))
     return out
 
 

@@ -311,12 +311,12 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         // which is faster there than claiming row by row)
         const bool push = k >= 4 && (SR == SR_OR_AND || m.pattern) && vector_nnz_s(ctx, x, m) <= m.rows;
         if (pull) {  // output-masked pull: the mask, and x values unless OR_AND
-            vector_ensure_mask(ctx, x);
+            vector_ensure_mask(ctx, x, SR);
             if (SR != SR_OR_AND) vector_ensure_dense(ctx, x, SR);
         } else if (k <= 1) {
             vector_ensure_dense(ctx, x, SR);
         } else if (k == 6 || k == 7 || push) {
-            vector_ensure_eff(ctx, x, m);
+            vector_ensure_eff(ctx, x, m, SR);
         }
         ADA_CUDA(cudaEventRecord(ev[1], ctx.stream));
         const int64_t nnz_x = x.nnz;
@@ -337,7 +337,7 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
             r.iteration = it;
             r.nnz_x = nnz_x;
             r.kernel = k;
-            r.pad = 0;
+            r.exec_mode = push ? ADASPMV_EXEC_FUSED_PUSH_LB : (pull ? ADASPMV_EXEC_MASKED_PULL : ADASPMV_EXEC_AS_SELECTED);
             r.predict_s = secs(t0, t1);  // host: tree walk + lazy features (nnz_s fetch)
             r.feature_s = 0;             // folded into predict_s (features pulled lazily)
             r.convert_s = c_ms * 1e-3;

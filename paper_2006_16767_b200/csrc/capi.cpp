@@ -292,6 +292,7 @@ int adaspmv_matrix_create_csr_device(adaspmv_ctx* ctx, int64_t rows, int64_t col
         need(d_row_offsets, "row_offsets");
         check_dtype(dtype);
         if (nnz < 0) ada::invalid("negative nnz");
+        ada::validate_device_csr(*ctx, rows, cols, nnz, d_row_offsets, d_col_indices);
         *out = static_cast<adaspmv_matrix*>(ada::matrix_create_device(
             *ctx, rows, cols, nnz, d_row_offsets, d_col_indices, d_values, dtype, d_values == nullptr));
     });
@@ -526,7 +527,7 @@ int adaspmv_vector_set_sparse_device(adaspmv_ctx* ctx, adaspmv_vector* v, int64_
     return guarded([&] {
         bind(ctx);
         need(v, "vector");
-        ada::vector_set_sparse_device(*ctx, *v, nnz, d_indices, d_values);
+        ada::vector_set_sparse_device(*ctx, *v, nnz, d_indices, d_values, true);
     });
 }
 
@@ -793,10 +794,10 @@ int adaspmv_execute_iteration(adaspmv_ctx* ctx, const adaspmv_matrix* m, adaspmv
         // convert iff the kernel needs another representation
         if (k <= 3) {
             ada::vector_ensure_dense(*ctx, *x, c.semiring);
-            if (k >= 2) ada::vector_ensure_mask(*ctx, *x);
+            if (k >= 2) ada::vector_ensure_mask(*ctx, *x, c.semiring);
         } else {
-            ada::vector_ensure_sparse(*ctx, *x);
-            if (k == 6 || k == 7) ada::vector_ensure_eff(*ctx, *x, *m);
+            ada::vector_ensure_sparse(*ctx, *x, c.semiring);
+            if (k == 6 || k == 7) ada::vector_ensure_eff(*ctx, *x, *m, c.semiring);
         }
         ADA_CUDA(cudaEventRecord(ev[1], ctx->stream));
         ada::run_kernel(*ctx, *m, *x, k, c, *y);
@@ -809,7 +810,7 @@ int adaspmv_execute_iteration(adaspmv_ctx* ctx, const adaspmv_matrix* m, adaspmv
             report->iteration = 0;
             report->nnz_x = x->nnz;
             report->kernel = k;
-            report->pad = 0;
+            report->exec_mode = ADASPMV_EXEC_AS_SELECTED;
             report->feature_s = feature_s;
             report->predict_s = select_s - feature_s;
             report->convert_s = conv_ms * 1e-3;

@@ -51,10 +51,12 @@ __device__ __forceinline__ double ld_stream(const double* p) {
 }
 
 // KernelCounters (kernels.hpp:106-111) on the device, when the context asks
-// for them (adaspmv_ctx_set_counters): ctr[0] values_read = matrix entries
-// consumed (a product formed: under PLUS_TIMES / MIN_PLUS one value load),
-// ctr[1] pairs_emitted on the sort write-back.  cas_retries stays 0: the
-// atomic write-backs use hardware atomics, not a counted CAS loop.
+// for them (adaspmv_ctx_set_counters): ctr[0] values_read = loads from the
+// matrix value array (kernels.hpp:108; every kernel loads a value exactly
+// when it forms a product -- the row SpMSpV kernels test the mask first,
+// kernels.hpp:229-240; under OR_AND, which loads no values, the entries
+// consumed), ctr[1] pairs_emitted on the sort write-back.  cas_retries stays
+// 0: the atomic write-backs use hardware atomics, not a counted CAS loop.
 __device__ __forceinline__ void count_add(unsigned long long* ctr, int slot, unsigned long long v) {
     if (ctr && v) atomicAdd(ctr + slot, v);
 }

@@ -195,6 +195,11 @@ struct Vector {
     DevBuf sp_idx;  DevBuf sp_val; bool has_sparse = false;
     int64_t nnz = -1;  // |supp x| when known on host (sparse input, or counted)
     DevBuf mask;    bool has_mask = false;   // (n+31)/32 u32 words == (n+63)/64 u64 LSB-first
+    // For a user-dense x the sparse and mask views depend on what "absent"
+    // means under the multiply's semiring: 0 (plus-times, or-and) or +inf
+    // (min-plus, where 0 is a real value).  absent_of(semiring) they were
+    // derived with; -1 = not derived from the dense values (user sparse x).
+    int sparse_absent = -1, mask_absent = -1;
     // effective-nnz prefix (eff_offsets, kernels.hpp:400-404) for one matrix
     DevBuf eff;     uint64_t eff_matrix = 0; bool has_eff = false;
     int64_t nnz_s = -1; uint64_t nnz_s_matrix = 0;
@@ -202,6 +207,7 @@ struct Vector {
     void invalidate() {
         has_dense = has_sparse = has_mask = has_eff = false;
         dense_fill = -1;
+        sparse_absent = mask_absent = -1;
         nnz = -1;
         nnz_s = -1;
         nnz_s_matrix = 0;
@@ -306,8 +312,13 @@ Matrix* matrix_create_device(Context& ctx, int64_t rows, int64_t cols, int64_t n
 Matrix* matrix_transpose(Context& ctx, const Matrix& m);
 
 void vector_set_dense_device(Context& ctx, Vector& v, const void* d_vals);
+// validate: check the indices on the device first (one synchronisation;
+// the C-ABI entry validates caller arrays, internal producers skip it)
 void vector_set_sparse_device(Context& ctx, Vector& v, int64_t nnz, const int32_t* d_idx,
-                              const void* d_vals);
+                              const void* d_vals, bool validate = false);
+// CsrMatrix::validate on caller device arrays (one synchronisation)
+void validate_device_csr(Context& ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* d_ro,
+                         const int32_t* d_ci);
 // host int64 indices (the reference's index_t) + values: H2D, then validated
 // and narrowed on the device (one synchronisation for the verdict)
 void vector_set_sparse_host(Context& ctx, Vector& v, int64_t nnz, const int64_t* h_idx, const void* h_vals);
@@ -325,9 +336,13 @@ void vector_check_deferred(Context& ctx, Vector& v);
 // dense view; entries absent from a sparse input hold the identity of
 // `semiring` (0 for plus-times / or-and, +inf for min-plus)
 void vector_ensure_dense(Context& ctx, Vector& v, int semiring = ADASPMV_PLUS_TIMES);
-void vector_ensure_sparse(Context& ctx, Vector& v);
-void vector_ensure_mask(Context& ctx, Vector& v);
-void vector_ensure_eff(Context& ctx, Vector& v, const Matrix& m);  // also sparse
+// what an absent entry of x holds under a semiring: 0 = zero, 1 = +inf
+inline int absent_of(int semiring) { return semiring == ADASPMV_MIN_PLUS ? 1 : 0; }
+// sparse / bitmask views; for a user-dense x, entries equal to the
+// semiring's identity are absent (semiring-keyed cache)
+void vector_ensure_sparse(Context& ctx, Vector& v, int semiring = ADASPMV_PLUS_TIMES);
+void vector_ensure_mask(Context& ctx, Vector& v, int semiring = ADASPMV_PLUS_TIMES);
+void vector_ensure_eff(Context& ctx, Vector& v, const Matrix& m, int semiring = ADASPMV_PLUS_TIMES);  // also sparse
 int64_t vector_nnz(Context& ctx, Vector& v);
 int64_t vector_nnz_s(Context& ctx, Vector& v, const Matrix& m);
 // dst[i] = src[i], i < n <= 64, by one thread on ctx's stream (dst: mapped host)

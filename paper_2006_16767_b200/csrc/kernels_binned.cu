@@ -200,7 +200,8 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
             for (int j = 0; j < kBinUnroll; ++j) {
                 const uint32_t e = b + j * kBinThreads;
                 pp[j] = e < n_e ? static_cast<uint32_t>(ld_stream(reinterpret_cast<const int*>(pkt) + e)) : 0u;
-                if (S::kUsesValues) aa[j] = e < n_e ? ld_stream(bvt + e) : V(0);
+                // K2 loads a value only after its mask test (kernels.hpp:229-240)
+                if (S::kUsesValues && !MASKED) aa[j] = e < n_e ? ld_stream(bvt + e) : V(0);
                 else aa[j] = V(1);
             }
         };
@@ -228,7 +229,12 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
 #pragma unroll
                 for (int j = 0; j < kBinUnroll; ++j)
                     if (ok[j]) ok[j] = (__ldg(mask + (col[j] >> 5)) >> (col[j] & 31)) & 1u;
-                if (ctr) {
+                if (S::kUsesValues) {
+#pragma unroll
+                    for (int j = 0; j < kBinUnroll; ++j)
+                        if (ok[j]) a[j] = ld_stream(bvt + base + j * kBinThreads);
+                }
+                if (ctr) {  // values_read: value loads (kernels.hpp:108)
                     unsigned n = 0;
 #pragma unroll
                     for (int j = 0; j < kBinUnroll; ++j) n += ok[j];

@@ -528,7 +528,7 @@ bool launch_private(Context& ctx, const Matrix& m, Vector& x, bool lb, V* y) {
     const size_t smem = sizeof(V) * static_cast<size_t>(m.rows);
     if (smem > kPrivateSmem || m.rows == 0) return false;  // y does not fit: plain atomic path
     const int64_t nnz_s = lb ? vector_nnz_s(ctx, x, m) : 0;
-    if (lb) vector_ensure_eff(ctx, x, m);  // nnz_s may be known without the offsets
+    if (lb) vector_ensure_eff(ctx, x, m, SR);  // nnz_s may be known without the offsets
     const unsigned grid = static_cast<unsigned>(2 * ctx.sm_count);
     if (lb) {
         ADA_CUDA(cudaFuncSetAttribute(col_private_kernel<V, SR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -556,7 +556,7 @@ void bfs_push_lb(Context& ctx, const Matrix& m, Vector& x, int32_t* lv, int32_t 
                  V* next_val, V value, unsigned long long* cnt) {
     const int64_t nnz_s = vector_nnz_s(ctx, x, m);
     if (nnz_s == 0) return;
-    vector_ensure_eff(ctx, x, m);
+    vector_ensure_eff(ctx, x, m, SR_OR_AND);
     const int64_t tiles = (nnz_s + kColTile - 1) / kColTile;
     col_lb_kernel<V, SR_OR_AND, 2><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
         x.nnz, nnz_s, tiles, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(), m.col_off.as<int64_t>(),
@@ -573,7 +573,7 @@ template <class V, int SR>
 void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort, bool private_acc,
                    int lanes, V* y_dense, int32_t* y_idx, V* y_val, int64_t* d_nnz,
                    int64_t* h_nnz) {
-    vector_ensure_sparse(ctx, x);
+    vector_ensure_sparse(ctx, x, SR);
     const int G = lanes > 0 ? lanes : default_lanes_per_row(m.avg_col);
     *h_nnz = -1;
     if (!sort) {
@@ -587,7 +587,7 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
         }
         const int64_t nnz_s = vector_nnz_s(ctx, x, m);
         if (nnz_s == 0) return;
-        vector_ensure_eff(ctx, x, m);  // nnz_s may be known without the offsets
+        vector_ensure_eff(ctx, x, m, SR);  // nnz_s may be known without the offsets
         const int64_t tiles = (nnz_s + kColTile - 1) / kColTile;
         col_lb_kernel<V, SR, 0><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
             x.nnz, nnz_s, tiles, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
@@ -611,7 +611,12 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
         return;
     }
     const int64_t nnz_s = vector_nnz_s(ctx, x, m);
-    vector_ensure_eff(ctx, x, m);  // nnz_s may be known without the offsets
+    if (nnz_s == 0) {  // every support column is empty: no pairs, empty y
+        ADA_CUDA(cudaMemsetAsync(d_nnz, 0, sizeof(int64_t), ctx.stream));
+        *h_nnz = 0;
+        return;
+    }
+    vector_ensure_eff(ctx, x, m, SR);  // nnz_s may be known without the offsets
     DevBuf& kb0 = ctx.scratch[0];
     DevBuf& kb1 = ctx.scratch[1];
     DevBuf& vb0 = ctx.scratch[2];

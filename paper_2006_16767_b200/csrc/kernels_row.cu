@@ -259,16 +259,19 @@ __global__ void __launch_bounds__(kNT, sizeof(V) == 8 ? 3 : 4) row_lb_kernel(
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
         const int p0 = r * kRound + lane * kIPT;
+        // K3 consults the bitmask before loading a value (kernels.hpp:229-240):
+        // its values are loaded below, only for entries whose x is set
+        constexpr bool kStreamVals = S::kUsesValues && !VALIDATE;
         if (p0 + kIPT <= ten) {
             int4 cc = ld_stream(reinterpret_cast<const int4*>(ci + tb + p0));
             c[r][0] = cc.x; c[r][1] = cc.y; c[r][2] = cc.z; c[r][3] = cc.w;
-            if (S::kUsesValues) Vec4<V>::load(vals + tb + p0, a[r]);
+            if (kStreamVals) Vec4<V>::load(vals + tb + p0, a[r]);
         } else {
 #pragma unroll
             for (int j = 0; j < kIPT; ++j) {
                 const bool in = p0 + j < ten;
                 c[r][j] = in ? ld_stream(ci + tb + p0 + j) : 0;
-                if (S::kUsesValues) a[r][j] = in ? ld_stream(vals + tb + p0 + j) : V(0);
+                if (kStreamVals) a[r][j] = in ? ld_stream(vals + tb + p0 + j) : V(0);
             }
         }
         if (!S::kUsesValues) {
@@ -279,13 +282,26 @@ __global__ void __launch_bounds__(kNT, sizeof(V) == 8 ? 3 : 4) row_lb_kernel(
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
         const int p0 = r * kRound + lane * kIPT;
+        bool okv[kIPT];
 #pragma unroll
         for (int j = 0; j < kIPT; ++j) {
             bool ok = p0 + j < ten;
             if (VALIDATE && ok) ok = (__ldg(mask + (c[r][j] >> 5)) >> (c[r][j] & 31)) & 1u;
-            xv[r][j] = ok ? __ldg(x + c[r][j]) : V(0);
-            if (!ok) c[r][j] = -1;  // marks "no contribution"
-            else if (ctr) count_add(ctr, 0, 1);
+            okv[j] = ok;
+        }
+        if (VALIDATE && S::kUsesValues) {  // value loads of the validated entries only
+            if (okv[0] && okv[1] && okv[2] && okv[3]) {
+                Vec4<V>::load(vals + tb + p0, a[r]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < kIPT; ++j) a[r][j] = okv[j] ? ld_stream(vals + tb + p0 + j) : V(0);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kIPT; ++j) {
+            xv[r][j] = okv[j] ? __ldg(x + c[r][j]) : V(0);
+            if (!okv[j]) c[r][j] = -1;  // marks "no contribution"
+            else if (ctr) count_add(ctr, 0, 1);  // values_read: one value load (kernels.hpp:108)
         }
     }
 

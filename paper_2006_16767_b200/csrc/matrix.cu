@@ -7,6 +7,7 @@
 // features and the LB tile heads (partition.hpp:30-33) are
 // computed once here ("computed only once at the beginning").
 #include <algorithm>
+#include <string>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -302,6 +303,57 @@ void finish_matrix(Context& ctx, Matrix& m) {
 }
 
 }  // namespace
+
+namespace {
+// CsrMatrix::validate (sparse.hpp:44-63) on caller-owned device arrays, one
+// thread per row (grid-stride).  err = min over violations of (kind << 56 |
+// row): the lowest failing kind, then the lowest row, as one verdict.
+//   kind 0 row_offsets[0] != 0 / row_offsets[rows] != nnz
+//   kind 1 row_offsets decreasing at row r
+//   kind 2 column index out of range in row r
+//   kind 3 columns not strictly increasing in row r
+__global__ void csr_validate_kernel(int64_t rows, int64_t cols, int64_t nnz, const int64_t* __restrict__ ro,
+                                    const int32_t* __restrict__ ci, unsigned long long* __restrict__ err) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t0 == 0 && (ro[0] != 0 || ro[rows] != nnz)) atomicMin(err, 0ull);
+    for (int64_t r = t0; r < rows; r += stride) {
+        const int64_t b = ro[r], e = ro[r + 1];
+        unsigned long long v = ~0ull;
+        if (e < b || b < 0 || e > nnz) {
+            v = (1ull << 56) | static_cast<unsigned long long>(r);
+        } else {
+            int32_t prev = -1;
+            for (int64_t k = b; k < e; ++k) {
+                const int32_t c = ci[k];
+                if (c < 0 || c >= cols) { v = (2ull << 56) | static_cast<unsigned long long>(r); break; }
+                if (c <= prev) { v = (3ull << 56) | static_cast<unsigned long long>(r); break; }
+                prev = c;
+            }
+        }
+        if (v != ~0ull) atomicMin(err, v);
+    }
+}
+}  // namespace
+
+void validate_device_csr(Context& ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* d_ro,
+                         const int32_t* d_ci) {
+    if (rows < 0 || cols < 0) invalid("negative matrix dimension");
+    if (nnz > 0 && !d_ci) invalid("csr: null column indices");
+    unsigned long long* err = reinterpret_cast<unsigned long long*>(ctx.dscal(6));
+    ADA_CUDA(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx.stream));
+    const int64_t g = std::min<int64_t>((rows + 255) / 256 + 1, static_cast<int64_t>(ctx.sm_count) * 16);
+    csr_validate_kernel<<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(rows, cols, nnz, d_ro, d_ci, err);
+    ADA_LAUNCHED(ctx);
+    const unsigned long long e = static_cast<unsigned long long>(ctx.fetch_scalar(ctx.dscal(6)));
+    if (e == ~0ull) return;
+    const int kind = static_cast<int>(e >> 56);
+    const std::string row = std::to_string(e & ((1ull << 56) - 1));
+    if (kind == 0) invalid("csr: row_offsets[0] != 0 or row_offsets[rows] != nnz");
+    if (kind == 1) invalid("csr: row_offsets not nondecreasing");
+    if (kind == 2) invalid("csr: column index out of range");
+    invalid("csr: columns not strictly increasing in row " + row);
+}
 
 Matrix* matrix_create_device(Context& ctx, int64_t rows, int64_t cols, int64_t nnz,
                              const int64_t* d_ro, const int32_t* d_ci, const void* d_vals,

@@ -1,11 +1,13 @@
 // pagerank.cu -- incremental (delta-propagation) PageRank driver over the
-// adaptive multiply: the paper's second
+// adaspmv multiply: the paper's second
 // varied-sparsity workload.
 //
-//   P        = A with column j scaled by 1 / deg_col(j) (stored entries of
-//              column j; values ignored, "graph" semantics), built once on
-//              the device; y = P x is multiplied with A as stored, like BFS
-//              (SPEC.md:540); dangling columns (deg 0) propagate nothing
+//   P        = A^T with column j scaled by 1 / outdeg(j), outdeg(j) = the
+//              stored entries of row j of A (values ignored, "graph"
+//              semantics): SPEC.md:500's delta' = damping * A^T_colnorm *
+//              delta, so an edge i -> j (A_ij stored) moves i's mass to j.
+//              P's CSR is A's CSC (already on the device), built once; rows
+//              with no entries (dangling vertices) propagate nothing
 //              (SPEC.md:543).
 //   rank     = 0, delta = 1/n everywhere
 //   repeat   rank += delta;  y = P delta (adaptive kernel);
@@ -37,14 +39,15 @@ using clk = std::chrono::steady_clock;
 
 double secs(clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); }
 
-// vals[k] = 1 / deg_col(col[k])
+// vals[k] = 1 / outdeg(ri[k]): entry k of A's CSC (row ri[k]) becomes entry
+// k of P's CSR, scaled by the out-degree (row length in A) of its source
 template <class V>
-__global__ void colnorm_values_kernel(const int32_t* __restrict__ ci, const int64_t* __restrict__ co,
-                                      int64_t nnz, V* __restrict__ vals) {
+__global__ void outdeg_values_kernel(const int32_t* __restrict__ ri, const int64_t* __restrict__ ro,
+                                     int64_t nnz, V* __restrict__ vals) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz; k += stride) {
-        const int32_t c = ci[k];
-        vals[k] = V(1) / static_cast<V>(co[c + 1] - co[c]);
+        const int32_t r = ri[k];
+        vals[k] = V(1) / static_cast<V>(ro[r + 1] - ro[r]);
     }
 }
 
@@ -174,18 +177,18 @@ void pagerank_t(Context& ctx, const Matrix& g, double damping, double prune, int
                 const Bundle* b, int forced, double* rank_out, int64_t* n_iters,
                 adaspmv_iteration_report* reports, int64_t max_reports) {
     const int64_t n = g.rows;
-    // P: same structure, column-normalised pattern values; cached on the
-    // graph matrix (structure-only, immutable after construction)
+    // P = A^T, column-normalised by out-degree (pattern values): its CSR is
+    // A's CSC; cached on the graph matrix (structure-only, immutable)
     if (!g.colnorm) {
         DevBuf pv;
         V* vals = static_cast<V*>(pv.ensure(sizeof(V) * static_cast<size_t>(std::max<int64_t>(g.nnz, 1))));
         if (g.nnz > 0) {
-            colnorm_values_kernel<V><<<grid_for(ctx, g.nnz, 256), 256, 0, ctx.stream>>>(
-                g.col_idx.as<int32_t>(), g.col_off.as<int64_t>(), g.nnz, vals);
+            outdeg_values_kernel<V><<<grid_for(ctx, g.nnz, 256), 256, 0, ctx.stream>>>(
+                g.row_idx.as<int32_t>(), g.row_off.as<int64_t>(), g.nnz, vals);
             ADA_LAUNCHED(ctx);
         }
-        g.colnorm.reset(matrix_create_device(ctx, g.rows, g.cols, g.nnz, g.row_off.as<int64_t>(),
-                                             g.col_idx.as<int32_t>(), vals, g.dtype, false));
+        g.colnorm.reset(matrix_create_device(ctx, g.cols, g.rows, g.nnz, g.col_off.as<int64_t>(),
+                                             g.row_idx.as<int32_t>(), vals, g.dtype, false));
     }
     const Matrix* P = g.colnorm.get();
     DevBuf rb;
@@ -250,7 +253,7 @@ void pagerank_t(Context& ctx, const Matrix& g, double damping, double prune, int
             r.iteration = it;
             r.nnz_x = nnz_x;
             r.kernel = k;
-            r.pad = 0;
+            r.exec_mode = ADASPMV_EXEC_AS_SELECTED;
             r.predict_s = secs(t0, t1);
             r.feature_s = 0;
             r.convert_s = c_ms * 1e-3;

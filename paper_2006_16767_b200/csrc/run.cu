@@ -50,7 +50,7 @@ void run_t(Context& ctx, const Matrix& m, Vector& x, int kernel, const adaspmv_c
             vector_ensure_dense(ctx, x, SR);
             const uint32_t* mask = nullptr;
             if (kernel >= 2) {
-                vector_ensure_mask(ctx, x);
+                vector_ensure_mask(ctx, x, SR);
                 mask = x.mask.as<uint32_t>();
             }
             V* yd = static_cast<V*>(y.dense.ensure(sizeof(V) * rows));

@@ -35,7 +35,7 @@ __global__ void mask_from_indices_kernel(int64_t nnz, const int32_t* __restrict_
 
 // one u32 word per warp-iteration from 32 consecutive values (LSB-first)
 template <class V>
-__global__ void mask_from_dense_kernel(int64_t n, const V* __restrict__ x,
+__global__ void mask_from_dense_kernel(int64_t n, const V* __restrict__ x, V absent,
                                        uint32_t* __restrict__ words) {
     const int64_t nw = (n + 31) / 32;
     const int64_t warp0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
@@ -43,7 +43,7 @@ __global__ void mask_from_dense_kernel(int64_t n, const V* __restrict__ x,
     const int lane = threadIdx.x & 31;
     for (int64_t w = warp0; w < nw; w += nwarps) {
         const int64_t i = w * 32 + lane;
-        const bool nz = i < n && x[i] != V(0);
+        const bool nz = i < n && x[i] != absent;
         const unsigned b = __ballot_sync(kFull, nz);
         if (lane == 0) words[w] = b;
     }
@@ -52,8 +52,12 @@ __global__ void mask_from_dense_kernel(int64_t n, const V* __restrict__ x,
 template <class V>
 struct NonzeroIn {
     const V* x;
-    __device__ int64_t operator()(int64_t i) const { return x[i] != V(0) ? 1 : 0; }
+    V absent;  // 0, or +inf under min-plus
+    __device__ int64_t operator()(int64_t i) const { return x[i] != absent ? 1 : 0; }
 };
+
+template <class V>
+V absent_value(int ab) { return ab ? V(INFINITY) : V(0); }
 
 template <class V>
 struct CompactEpi {
@@ -96,19 +100,19 @@ void ensure_dense_t(Context& ctx, Vector& v, int semiring) {
 }
 
 template <class V>
-void ensure_sparse_t(Context& ctx, Vector& v) {
+void ensure_sparse_t(Context& ctx, Vector& v, int ab) {
     const size_t cap = static_cast<size_t>(std::max<int64_t>(v.n, 1));
     v.sp_idx.ensure(sizeof(int32_t) * cap);
     v.sp_val.ensure(sizeof(V) * cap);
     const V* x = v.dense.as<V>();
-    scan3(ctx, v.n, NonzeroIn<V>{x}, CompactEpi<V>{x, v.sp_idx.as<int32_t>(), v.sp_val.as<V>()},
+    scan3(ctx, v.n, NonzeroIn<V>{x, absent_value<V>(ab)}, CompactEpi<V>{x, v.sp_idx.as<int32_t>(), v.sp_val.as<V>()},
           ctx.dscal(0), ctx.scratch[4]);
     v.nnz = ctx.fetch_scalar(ctx.dscal(0));
 }
 
 template <class V>
 int64_t count_nonzero_t(Context& ctx, const Vector& v) {
-    scan3(ctx, v.n, NonzeroIn<V>{v.dense.as<V>()}, NoEpi{}, ctx.dscal(0), ctx.scratch[4]);
+    scan3(ctx, v.n, NonzeroIn<V>{v.dense.as<V>(), V(0)}, NoEpi{}, ctx.dscal(0), ctx.scratch[4]);
     return ctx.fetch_scalar(ctx.dscal(0));
 }
 
@@ -214,9 +218,36 @@ void vector_set_sparse_host(Context& ctx, Vector& v, int64_t nnz, const int64_t*
     v.has_sparse = true;
 }
 
+// SparseVector::validate (sparse.hpp:120-129) on caller-owned int32 device
+// indices: err = min over violations of (k << 1 | kind) as in
+// narrow_validate_kernel.
+__global__ void sparse_validate_kernel(int64_t nnz, int64_t n, const int32_t* __restrict__ idx,
+                                       unsigned long long* __restrict__ err) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz; k += stride) {
+        const int32_t i = idx[k];
+        unsigned long long e = ~0ull;
+        if (i < 0 || i >= n) e = static_cast<unsigned long long>(k) << 1;
+        else if (k > 0 && i <= idx[k - 1]) e = (static_cast<unsigned long long>(k) << 1) | 1ull;
+        if (e != ~0ull) atomicMin(err, e);
+    }
+}
+
 void vector_set_sparse_device(Context& ctx, Vector& v, int64_t nnz, const int32_t* d_idx,
-                              const void* d_vals) {
+                              const void* d_vals, bool validate) {
     if (nnz < 0 || nnz > v.n) invalid("sparse vector: nnz out of range");
+    if (validate && nnz > 0) {
+        unsigned long long* err = reinterpret_cast<unsigned long long*>(ctx.dscal(6));
+        ADA_CUDA(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx.stream));
+        const int64_t g = std::min<int64_t>((nnz + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 16);
+        sparse_validate_kernel<<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(nnz, v.n, d_idx, err);
+        ADA_LAUNCHED(ctx);
+        const unsigned long long e = static_cast<unsigned long long>(ctx.fetch_scalar(ctx.dscal(6)));
+        if (e != ~0ull) {
+            if (e & 1ull) invalid("sparse vector: indices not strictly increasing");
+            invalid("sparse vector: index out of range");
+        }
+    }
     v.invalidate();
     const size_t vb = static_cast<size_t>(value_bytes(v.dtype));
     v.sp_idx.ensure(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(nnz, 1)));
@@ -241,45 +272,60 @@ void vector_ensure_dense(Context& ctx, Vector& v, int semiring) {
     v.dense_fill = fill;
 }
 
-void vector_ensure_sparse(Context& ctx, Vector& v) {
-    if (v.has_sparse) return;
-    if (!v.has_dense) invalid("vector has no value set");
-    if (v.dtype == ADASPMV_F64) ensure_sparse_t<double>(ctx, v);
-    else ensure_sparse_t<float>(ctx, v);
+void vector_ensure_sparse(Context& ctx, Vector& v, int semiring) {
+    const int ab = absent_of(semiring);
+    if (v.has_sparse && (v.sparse_absent < 0 || v.sparse_absent == ab)) return;
+    if (!v.has_dense || v.dense_fill >= 0) invalid("vector has no value set");
+    // derived from the user's dense values: entries equal to the semiring's
+    // identity are absent (dense_to_sparse, sparse.hpp:283-321, drops exact
+    // zeros under plus-times; under min-plus 0 is a value and +inf absent)
+    if (v.dtype == ADASPMV_F64) ensure_sparse_t<double>(ctx, v, ab);
+    else ensure_sparse_t<float>(ctx, v, ab);
     v.has_sparse = true;
+    v.sparse_absent = ab;
+    // the effective-nnz caches belong to the previous support
+    v.has_eff = false;
+    v.eff_matrix = 0;
+    v.nnz_s = -1;
+    v.nnz_s_matrix = 0;
 }
 
-void vector_ensure_mask(Context& ctx, Vector& v) {
-    if (v.has_mask) return;
+void vector_ensure_mask(Context& ctx, Vector& v, int semiring) {
+    const bool user_sparse = v.has_sparse && v.sparse_absent < 0;
+    const int ab = user_sparse ? -1 : absent_of(semiring);
+    if (v.has_mask && v.mask_absent == ab) return;
     const int64_t nw = (v.n + 31) / 32;
     // u64-granular allocation so host reads of (n+63)/64 words stay in bounds
     uint32_t* w = static_cast<uint32_t*>(v.mask.ensure(sizeof(uint64_t) * static_cast<size_t>(std::max<int64_t>((v.n + 63) / 64, 1))));
-    if (v.has_sparse) {
+    if (user_sparse) {
         ADA_CUDA(cudaMemsetAsync(w, 0, sizeof(uint64_t) * static_cast<size_t>((v.n + 63) / 64), ctx.stream));
         if (v.nnz > 0) {
             mask_from_indices_kernel<<<blocks_for(v.nnz, 256), 256, 0, ctx.stream>>>(
                 v.nnz, v.sp_idx.as<int32_t>(), w);
             ADA_LAUNCHED(ctx);
         }
-    } else if (v.has_dense) {
+    } else if (v.has_dense && v.dense_fill < 0) {
         ADA_CUDA(cudaMemsetAsync(w, 0, sizeof(uint64_t) * static_cast<size_t>((v.n + 63) / 64), ctx.stream));
         if (nw > 0) {
             const int blocks = static_cast<int>(std::min<int64_t>(blocks_for(nw * 32, 256), ctx.sm_count * 16));
             if (v.dtype == ADASPMV_F64)
-                mask_from_dense_kernel<double><<<blocks, 256, 0, ctx.stream>>>(v.n, v.dense.as<double>(), w);
+                mask_from_dense_kernel<double><<<blocks, 256, 0, ctx.stream>>>(v.n, v.dense.as<double>(),
+                                                                               absent_value<double>(ab), w);
             else
-                mask_from_dense_kernel<float><<<blocks, 256, 0, ctx.stream>>>(v.n, v.dense.as<float>(), w);
+                mask_from_dense_kernel<float><<<blocks, 256, 0, ctx.stream>>>(v.n, v.dense.as<float>(),
+                                                                             absent_value<float>(ab), w);
             ADA_LAUNCHED(ctx);
         }
     } else {
         invalid("vector has no value set");
     }
     v.has_mask = true;
+    v.mask_absent = ab;
 }
 
-void vector_ensure_eff(Context& ctx, Vector& v, const Matrix& m) {
+void vector_ensure_eff(Context& ctx, Vector& v, const Matrix& m, int semiring) {
+    vector_ensure_sparse(ctx, v, semiring);  // may reset the offsets (another support)
     if (v.has_eff && v.eff_matrix == m.id) return;
-    vector_ensure_sparse(ctx, v);
     int64_t* eff = static_cast<int64_t*>(v.eff.ensure(sizeof(int64_t) * static_cast<size_t>(v.nnz + 1)));
     scan3(ctx, v.nnz, DegreeIn{m.col_off.as<int64_t>(), v.sp_idx.as<int32_t>()},
           WriteExclusive{eff}, eff + v.nnz, ctx.scratch[4]);

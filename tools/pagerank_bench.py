@@ -43,9 +43,8 @@ def main():
     if not a.no_oracle:
         from oracle.oracle import Port
         port = Port()
-        co, ri, _ = port.csr_to_csc(n, n, ro, ci, np.ones(len(ci)))
         t1 = time.perf_counter()
-        exp, it_exp = port.pagerank_incremental(n, co, ri, a.damping, a.prune, a.max_iters)
+        exp, it_exp = port.pagerank_incremental(n, ro, ci, a.damping, a.prune, a.max_iters)
         t_oracle = time.perf_counter() - t1
     bundle = A.SelectorBundle.load(S.DEFAULT_PATH)
     res = {"scale": a.scale, "n": n, "nnz": int(ro[-1]), "damping": a.damping, "prune": a.prune,
