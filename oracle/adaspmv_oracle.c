@@ -170,6 +170,31 @@ int64_t or_bfs_queue(int64_t n, const int64_t* co, const int64_t* ri, int64_t so
     return nlev;
 }
 
+/* or_bfs_queue over int32 row indices (the device layout): the same queue
+ * BFS for graphs whose int64 index copy would not fit host memory (C5). */
+int64_t or_bfs_queue_i32(int64_t n, const int64_t* co, const int32_t* ri, int64_t source,
+                         int64_t* levels) {
+    for (int64_t i = 0; i < n; ++i) levels[i] = -1;
+    if (source < 0 || source >= n) return 0;
+    int32_t* q = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+    int64_t head = 0, tail = 0, nlev = 0;
+    levels[source] = 0;
+    q[tail++] = (int32_t)source;
+    while (head < tail) {
+        int64_t c = q[head++];
+        if (levels[c] + 1 > nlev) nlev = levels[c] + 1;
+        for (int64_t k = co[c]; k < co[c + 1]; ++k) {
+            int64_t r = ri[k];
+            if (levels[r] < 0) {
+                levels[r] = levels[c] + 1;
+                q[tail++] = (int32_t)r;
+            }
+        }
+    }
+    free(q);
+    return nlev;
+}
+
 /* SPEC.md:498-506 incremental PageRank (delta propagation with pruning),
  * pinned only by SPEC's examples and by dense power iteration (tests).
  * delta' = d * A^T_colnorm * delta, i.e. P = A^T with column j

@@ -71,6 +71,8 @@ int64_t or_pagerank_incremental(int64_t n, const int64_t* co, const int64_t* ri,
                                 double prune, int64_t max_iters, double* rank);
 int64_t or_bfs_queue(int64_t n, const int64_t* col_offsets, const int64_t* row_indices,
                      int64_t source, int64_t* levels);
+int64_t or_bfs_queue_i32(int64_t n, const int64_t* col_offsets, const int32_t* row_indices,
+                         int64_t source, int64_t* levels);
 
 #define OR_DECLARE(REAL, SFX)                                                                  \
     /* kernels.hpp:197-209 */                                                                  \

@@ -82,6 +82,8 @@ class Port:
         L.or_tree_predict.argtypes = [_i32p, _f64p, _i32p, _i32p, _i32p, _f64p]
         L.or_bfs_queue.restype = C.c_int64
         L.or_bfs_queue.argtypes = [C.c_int64, _i64p, _i64p, C.c_int64, _i64p]
+        L.or_bfs_queue_i32.restype = C.c_int64
+        L.or_bfs_queue_i32.argtypes = [C.c_int64, _i64p, _i32p, C.c_int64, _i64p]
         L.or_pagerank_incremental.restype = C.c_int64
         L.or_pagerank_incremental.argtypes = [C.c_int64, _i64p, _i64p, C.c_double, C.c_double, C.c_int64,
                                               _f64p]
@@ -183,6 +185,11 @@ class Port:
         return int(self.lib.or_tree_predict(_as(feature, np.int32), _as(threshold, np.float64),
                                             _as(left, np.int32), _as(right, np.int32),
                                             _as(leaf, np.int32), _as(f13, np.float64)))
+
+    def bfs_queue_i32(self, n, col_offsets, row_indices, source):
+        lv = np.zeros(n, np.int64)
+        nl = self.lib.or_bfs_queue_i32(n, _as(col_offsets, np.int64), _as(row_indices, np.int32), int(source), lv)
+        return lv, int(nl)
 
     def bfs_queue(self, n, col_offsets, row_indices, source):
         lv = np.zeros(n, np.int64)
@@ -316,13 +323,38 @@ class RefError(RuntimeError):
         self.code = code
 
 
-class Ref:
-    """oracle/_ref/libadaspmv_ref_{f64,f32}[_cnt].so."""
+def host_isa() -> str:
+    """x86-64 ISA level of this host for the timed reference build: v4 when the
+    CPU has AVX-512 (avx512f/bw/dq/vl), else v3."""
+    try:
+        flags = Path("/proc/cpuinfo").read_text().split("flags", 2)[1].split("\n", 1)[0].split()
+    except Exception:
+        return "v3"
+    return "v4" if all(f in flags for f in ("avx512f", "avx512bw", "avx512dq", "avx512vl")) else "v3"
 
-    def __init__(self, dtype=np.float64, counters=False, path: Path | None = None):
+
+def host_cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+class Ref:
+    """oracle/_ref/libadaspmv_ref_{f64,f32}[_cnt].so (checker build: -ffp-contract=off)
+    or, bench=True, libadaspmv_ref_bench_{f64,f32}_{v3,v4}.so: the reference's
+    own ref_bench flags (-O3, contraction allowed) at this host's ISA level."""
+
+    def __init__(self, dtype=np.float64, counters=False, path: Path | None = None, bench: bool = False):
         self.dtype = np.dtype(dtype)
         sfx = "f64" if self.dtype == np.float64 else "f32"
         name = f"libadaspmv_ref_{'cnt_' if counters else ''}{sfx}.so"
+        if bench:
+            name = f"libadaspmv_ref_bench_{sfx}_{host_isa()}.so"
+        self.variant = name
         path = path or HERE / "_ref" / name
         if not path.exists():
             raise OracleMissing(f"{path} not built (run `make -C oracle ref` where the reference is mounted)")
@@ -357,6 +389,7 @@ class Ref:
         L.ref_write_matrix_market.argtypes = [vp, C.c_char_p]
         L.ref_save_binary.argtypes = [vp, C.c_char_p]
         L.ref_from_triplets.argtypes = [C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p, rp, C.POINTER(vp)]
+        L.ref_bfs.argtypes = [vp, C.c_int64, C.c_int, _i64p, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
 
     def _check(self, rc):
         if rc != 0:
@@ -485,6 +518,15 @@ class RefMatrix:
         self.ref._check(self.ref.lib.ref_run_kernel(self.h, int(kernel_index), *args, int(workers),
                                                     int(private_acc), yd, yi, yv, C.byref(k), cnt))
         return yd, (yi[:k.value].copy(), yv[:k.value].copy()), cnt
+
+    def bfs(self, source=0, kernel=-1):
+        """SPEC.md:489-497 plus-times BFS with the reference's run_kernel
+        (ref_capi.cpp ref_bfs) -> (levels int64[n], n_levels, wall seconds)."""
+        n = self.rows
+        lv = np.empty(n, np.int64)
+        nl, sec = C.c_int64(), C.c_double()
+        self.ref._check(self.ref.lib.ref_bfs(self.h, int(source), int(kernel), lv, C.byref(nl), C.byref(sec)))
+        return lv, int(nl.value), float(sec.value)
 
     def bench_kernel(self, kernel_index, x_dense=None, x_sparse=None, warmup=1, repeats=10):
         dt = self.ref.dtype

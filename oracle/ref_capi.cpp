@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cstring>
 #include <exception>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -185,6 +186,63 @@ int ref_bench_kernel(void* h, int kernel_index, const real_t* x_dense, int64_t n
             times[i] = std::chrono::duration<double>(t1 - t0).count();
             (void)out;
         }
+    });
+}
+
+// SPEC.md:489-497 BFS with the reference's own run_kernel (the reference
+// ships the kernels but no driver): x = frontier (SparseVector, values 1.0),
+// y = A x as stored, next = {i : y_i != 0 and level unset}.  `kernel` >= 0
+// runs that KernelId every level; -1 picks per level by the bytes model of
+// SURVEY.md 8(d) (column kernels while the frontier's effective nnz is below
+// the row kernels' index stream, col_lb_atomic / row_lb -- the reference's
+// fastest fixed kernels on R-MAT).  Operand preparation is part
+// of each level (the executor's conversions).  Wall seconds
+// of the traversal in *seconds; levels[n] gets level or -1.
+int ref_bfs(void* h, int64_t source, int kernel, int64_t* levels, int64_t* n_levels, double* seconds) {
+    return guarded([&] {
+        auto* m = static_cast<DualMatrix*>(h);
+        const int64_t n = m->rows();
+        if (m->cols() != n) throw std::invalid_argument("bfs: matrix must be square");
+        if (source < 0 || source >= n) throw std::invalid_argument("bfs: source out of range");
+        std::fill(levels, levels + n, int64_t{-1});
+        const auto t0 = std::chrono::steady_clock::now();
+        levels[source] = 0;
+        SparseVector x;
+        x.length = n;
+        x.indices.push_back(source);
+        x.values.push_back(real_t{1});
+        int64_t it = 0;
+        while (x.nnz() > 0) {
+            int k = kernel;
+            if (k < 0) {
+                const int64_t nnz_s = effective_nnz(m->csc, x);
+                const double col = static_cast<double>(x.nnz()) * 24.0 + static_cast<double>(nnz_s) * (8.0 + sizeof(real_t)) * 2.0;
+                const double row = static_cast<double>(m->nnz()) * 8.0 + static_cast<double>(n) * 16.0;
+                k = col <= row ? 6 : 3;
+            }
+            std::optional<DenseVector> d;
+            std::optional<BitMask> mk;
+            const KernelId id = KernelId::from_index(k);
+            if (id.pattern != Pattern::ColSpMSpV) {
+                d = sparse_to_dense(x);
+                mk = build_bitmask(x);
+            }
+            OperandViews views{d ? &*d : nullptr, &x, mk ? &*mk : nullptr};
+            MultiplyOutput out = run_kernel(*m, id, views);
+            const DenseVector& y = out.dense();
+            SparseVector nx;
+            nx.length = n;
+            for (int64_t i = 0; i < n; ++i)
+                if (y.values[static_cast<size_t>(i)] != real_t{0} && levels[i] < 0) {
+                    levels[i] = it + 1;
+                    nx.indices.push_back(i);
+                    nx.values.push_back(real_t{1});
+                }
+            x = std::move(nx);
+            ++it;
+        }
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *n_levels = it;
     });
 }
 
