@@ -1,28 +1,38 @@
 #!/usr/bin/env python3
-"""bench.py -- BASELINE.json metric on its 1-GPU configuration (configs[1]):
+"""bench.py -- BASELINE.json's metric on its configurations.
 
   "GFLOP/s and HBM GB/s (% of roofline) vs x sparsity; selector regret vs best"
-  workload C2: uniform random 4M x 4M, 2^26 iid draws (~64M nnz), fp32,
-  x-sparsity sweep 0.001 % .. 100 % across all 8 kernels + the selector.
 
-A *step* is one adaptive pass over the sweep: for each of the 7 x-sparsity
-points, select a kernel (C++ decision-tree hook) and run it, inputs resident
-in HBM.  value = total useful GFLOP/s of the step = sum(2 nnz_s) / sum(t).
-Every point is also timed with all 8 kernels (best-of-8, regret).
+Headline (value, e2e, roofline): configs[1] = C2, uniform random 4M x 4M,
+2^26 iid draws (~64M nnz), fp32, x-sparsity sweep 0.001 % .. 100 % across all
+8 kernels + the selector.  A *step* is one adaptive pass over the sweep: for
+each of the 7 points select a kernel (C++ decision-tree hook) and run it,
+inputs resident in HBM.  value = sum(2 nnz_s) / sum(t).  Every point is also
+timed with all 8 kernels (best-of-8, regret).
+
+The other single-GPU configurations ride in the same JSON line under
+"configs" (C1 Laplacian fp64 at x = 100 % / 1 %, C3 R-MAT 22 BFS, C4 SVM at
+nnz_x 200 / 2,000 / 20,000), each with the selected kernel, the best of 8,
+regret, the SURVEY.md 8(d) B_alg roofline fraction and the reference CPU
+implementation timed on this box's host cores.
 
   --impl ours       (default) the CUDA library through its C-ABI
   --impl reference  the reference's own CPU implementation (oracle/_ref: the
-                    unmodified reference headers) on the host cores
+                    unmodified reference headers, built with the reference's
+                    ref_bench flags at this host's ISA level) on the host cores
 
 Timing: CUDA events on the library's stream around each multiply, medians
 over K steps after W warm-up steps; an L2 flush (256 MiB write) precedes every
-timed multiply whose working set fits in L2.  Selection overhead (feature
-pulls + tree walks, format conversions) is measured on fresh vectors and
-reported beside the value ("overhead").  e2e repeats the step through the
-public API with host buffers (pinned): one adaspmv_run_batch call over the 7
-vectors (H2D of x, select, multiply, D2H of y in its smaller form, pipelined
-over 3 streams), wall clock; "sequential_value" is the same through single
-calls.  N > 1 (torchrun): the row-partitioned mode, see run_ours_multi.
+timed multiply whose working set fits in L2.  C1 (< 50 us) is timed by CUDA
+graph replay: N x (flush + multiply) minus N x flush.  CPU
+timings follow SPEC.md:437-446 benchmark_kernel: operands prepared once, one
+warm-up call, median of >= 3 timed calls.  Selection overhead (feature pulls +
+tree walks, format conversions) is measured on fresh vectors and reported
+beside the value.  e2e repeats the step through the public API with host
+buffers (pinned): one adaspmv_run_batch call over the 7 vectors (H2D of x,
+select, multiply, D2H of y in its smaller form, pipelined over 3 streams),
+wall clock.  N > 1 (torchrun): the row-partitioned mode over ONE C2 matrix
+(strong scaling), see run_ours_multi.
 """
 from __future__ import annotations
 
@@ -46,6 +56,7 @@ SPARSITIES = (0.00001, 0.0001, 0.001, 0.01, 0.1, 0.5, 1.0)
 N = 1 << int(os.environ.get("ADASPMV_BENCH_LOG2N", "22"))  # override only for dry runs
 DRAWS = 16 * N
 GATE_CYCLES = 400_000  # ~0.2 ms at 1.9 GHz
+L2_NOTE = "256 MiB flush before timed multiplies with working set < 64 MB; larger inputs exceed L2"
 METRIC = "GFLOP/s and HBM GB/s (% of roofline) vs x sparsity; selector regret vs best"
 WORKLOAD = "C2 uniform random 4M x 4M, 2^26 draws (~64M nnz) fp32, x-sparsity sweep 0.001%-100%"
 I_B, O_B = 4, 8  # device index / offset bytes (SURVEY.md section 8 symbols)
@@ -132,98 +143,279 @@ def make_vectors(n):
     return out
 
 
-# ---------------------------------------------------------------------------
-# reference CPU arm
-# ---------------------------------------------------------------------------
-def ref_sweep_times(ref_m, vecs, kernels_per_point, repeats=1, warmup=0):
-    """Times the given kernel per point with the reference's run_kernel."""
-    ts = []
-    for (xi, xv), k in zip(vecs, kernels_per_point):
-        dense = None
-        if len(xi) == ref_m.cols:
-            dense = np.zeros(ref_m.cols, np.float32)
-            dense[xi] = xv
-        t = ref_m.bench_kernel(k, x_dense=dense, x_sparse=None if dense is not None else (xi, xv),
-                               warmup=warmup, repeats=repeats)
-        ts.append(float(np.median(t)))
-    return ts
+def c2_config(rows, cols, nnz, world):
+    """The workload description both arms print (same keys and values)."""
+    return {"workload": WORKLOAD, "rows": rows, "cols": cols, "nnz": nnz, "x_sparsity": list(SPARSITIES),
+            "l2": L2_NOTE,
+            "parallelism": f"row-partitioned x{world} (one C2 matrix, strong scaling)" if world > 1 else "single device"}
 
 
-def cpu_choose(ref_m, vecs):
-    """Best reference kernel per point (1 warm-up + 1 run each); the sort
-    write-back is skipped where nnz_x >= 1 % (seconds per call on CPU)."""
+# ---------------------------------------------------------------------------
+# the reference CPU implementation (oracle/_ref, bench build): shared by the
+# reference arm and our cpu_baseline leg, so both report the same number
+# ---------------------------------------------------------------------------
+def _ref_operand(M, xi, xv, dt):
+    if len(xi) == M.cols:
+        d = np.zeros(M.cols, dt)
+        d[xi] = xv
+        return dict(x_dense=d)
+    return dict(x_sparse=(xi, xv))
+
+
+def ref_time(M, k, op, repeats=3):
+    """SPEC.md:437-446 benchmark_kernel: 1 warm-up, median of `repeats`."""
+    return float(np.median(M.bench_kernel(k, warmup=1, repeats=repeats, **op)))
+
+
+def ref_choose(M, ops, nnz_s, kernels=range(8), sort_cap=20_000_000):
+    """Best reference kernel per operand: one warm-up + one timed call each;
+    the sort write-back is skipped above `sort_cap` effective entries (its
+    serial merge takes seconds there)."""
     best = []
-    for (xi, xv) in vecs:
-        dense = None
-        if len(xi) == ref_m.cols:
-            dense = np.zeros(ref_m.cols, np.float32)
-            dense[xi] = xv
-        cand = range(8) if len(xi) < 0.01 * ref_m.cols else (0, 1, 2, 3, 4, 6)
+    for op, ns in zip(ops, nnz_s):
         tk = {}
-        for k in cand:
-            t = ref_m.bench_kernel(k, x_dense=dense, x_sparse=None if dense is not None else (xi, xv),
-                                   warmup=1, repeats=1)
-            tk[k] = float(t[0])
+        for k in kernels:
+            if k in (5, 7) and ns > sort_cap:
+                continue
+            tk[k] = float(M.bench_kernel(k, warmup=1, repeats=1, **op)[0])
         best.append(min(tk, key=tk.get))
     return best
 
 
-def run_reference(args, rank, world):
+def ref_c2_prepare(rows, cols, ro, ci, vals, vecs):
     from oracle.oracle import Ref
+    ref = Ref(np.float32, bench=True)
+    threads = os.cpu_count() or 1
+    ref.set_threads(threads)
+    M = ref.matrix(rows, cols, ro, ci, vals)
+    col_off = M.export()[3]
+    nnz_s = [int(np.sum(col_off[xi + 1] - col_off[xi])) for xi, _ in vecs]
+    ops = [_ref_operand(M, xi, xv, np.float32) for xi, xv in vecs]
+    best = ref_choose(M, ops, nnz_s, sort_cap=400_000)
+    return ref, M, ops, nnz_s, best, threads
 
+
+def ref_c2_step(M, ops, best, repeats=3):
+    return [ref_time(M, k, op, repeats) for op, k in zip(ops, best)]
+
+
+def _cpu_meta(ref, threads, sample):
+    from oracle.oracle import host_cpu_model
+    return {"cores": threads, "kind": "reference", "sample": sample, "cpu": host_cpu_model(),
+            "build": ref.variant}
+
+
+def cpu_c1(c1):
+    """C1 on the reference: best of its 8 kernels per point (benchmark_kernel)."""
+    from oracle.oracle import Ref
+    rows, cols, ro, ci, vals, pts = c1
+    ref = Ref(np.float64, bench=True)
+    threads = os.cpu_count() or 1
+    ref.set_threads(threads)
+    M = ref.matrix(rows, cols, ro, ci, vals)
+    col_off = M.export()[3]
+    out = []
+    for name, xi, xv in pts:
+        op = _ref_operand(M, xi, xv, np.float64)
+        ns = int(np.sum(col_off[xi + 1] - col_off[xi]))
+        k = ref_choose(M, [op], [ns])[0]
+        t = ref_time(M, k, op, repeats=5)
+        out.append({"point": name, "kernel": A_name(k), "ms": round(t * 1e3, 4),
+                    "gflops": round(2 * ns / t / 1e9, 3)})
+    flops = sum(2 * int(np.sum(col_off[xi + 1] - col_off[xi])) for _, xi, _ in pts)
+    tot = sum(p["ms"] for p in out) * 1e-3
+    res = {"value": round(flops / tot / 1e9, 3), "unit": "GFLOP/s", "points": out}
+    res.update(_cpu_meta(ref, threads, "both C1 points, best reference kernel each, median of 5"))
+    return res
+
+
+def cpu_c3(n, ro_h, ci_h, q, edges):
+    """C3 on the reference: SPEC.md:489-497 BFS (plus-times, frontier 1.0)
+    with the reference's run_kernel per level (ref_capi.cpp ref_bfs)."""
+    from oracle.oracle import Ref
+    ref = Ref(np.float32, bench=True)
+    threads = os.cpu_count() or 1
+    ref.set_threads(threads)
+    M = ref.matrix(n, n, ro_h, ci_h, None)
+    lv, nl, _ = M.bfs(0, -1)  # warm-up + levels check
+    ts = [M.bfs(0, -1)[2] for _ in range(3)]
+    t = float(np.median(ts))
+    res = {"value": round(edges / t / 1e9, 4), "unit": "GTEPS", "ms": round(t * 1e3, 2),
+           "levels_match_queue_bfs": bool(np.array_equal(lv, q)), "policy": "per level: col_lb_atomic / row_lb "
+           "by the SURVEY.md 8(d) bytes model (the reference's fastest fixed kernels on R-MAT)"}
+    res.update(_cpu_meta(ref, threads, "full C3 traversal from vertex 0, median of 3 after one warm-up"))
+    return res
+
+
+def cpu_c4(c4h, pts):
+    """C4 on the reference: best of its kernels per sample row (benchmark_kernel)."""
+    from oracle.oracle import Ref
+    mr, nc, ro, ci, vals = c4h
+    ref = Ref(np.float32, bench=True)
+    threads = os.cpu_count() or 1
+    ref.set_threads(threads)
+    M = ref.matrix(mr, nc, ro, ci, vals)
+    col_off = M.export()[3]
+    out = []
+    flops = 0
+    tot = 0.0
+    for i, (xi, xv) in enumerate(pts):
+        op = _ref_operand(M, xi, xv, np.float32)
+        ns = int(np.sum(col_off[xi + 1] - col_off[xi]))
+        kern = range(8) if i == 0 else (4, 5, 6, 7)  # row kernels read all 2e8 entries: measured once
+        k = ref_choose(M, [op], [ns], kernels=kern)[0]
+        t = ref_time(M, k, op, repeats=3)
+        flops += 2 * ns
+        tot += t
+        out.append({"nnz_x": len(xi), "kernel": A_name(k), "ms": round(t * 1e3, 3), "gflops": round(2 * ns / t / 1e9, 3)})
+    res = {"value": round(flops / tot / 1e9, 3), "unit": "GFLOP/s", "points": out}
+    res.update(_cpu_meta(ref, threads, "the three C4 sample rows, best reference kernel each, median of 3"))
+    return res
+
+
+def A_name(k):
+    from paper_2006_16767_b200 import adaspmv as A
+    return A.KernelId.from_index(int(k)).name()
+
+
+# ---------------------------------------------------------------------------
+# configuration inputs (identical bytes for both arms)
+# ---------------------------------------------------------------------------
+def c1_inputs():
+    """C1: 2-D 5-point Laplacian 1000 x 1000 (10^6 rows) fp64; x dense
+    U[-1,1) (seed 7) and 1 % (10,000 entries uniform w/o replacement)."""
+    from paper_2006_16767_b200 import synth
+    rows, cols, ro, ci, vals = synth.laplacian_2d(1000, dtype=np.float64)
+    rng = np.random.default_rng(7)
+    xd = rng.uniform(-1, 1, cols)
+    xi1 = np.sort(rng.choice(cols, 10_000, replace=False)).astype(np.int64)
+    xv1 = rng.uniform(-1, 1, 10_000)
+    pts = [("x=100%", np.arange(cols, dtype=np.int64), xd), ("x=1%", xi1, xv1)]
+    return rows, cols, ro, ci, vals, pts
+
+
+def c3_inputs():
+    """C3: R-MAT scale 22 (device generator) -> device (ro, ci) + host copies."""
+    from paper_2006_16767_b200 import synth_device as SD
+    t0 = time.time()
+    n, ro, ci = SD.rmat_device(22)
+    return n, ro, ci, time.time() - t0
+
+
+def c3_levels(port, n, ro_h, ci_h):
+    q, nq = port.bfs_queue_i32(n, ro_h, ci_h, 0)
+    deg = np.diff(ro_h)
+    edges = int(deg[q >= 0].sum())
+    # SURVEY.md 8(d) BFS B_alg: per level min(push, pull), I = 4, O = 8
+    b_alg = 0.0
+    lvl_rows = []
+    for L in range(nq):
+        f = q == L
+        nnz_x = int(f.sum())
+        nnz_s = int(deg[f].sum())
+        new = int((q == L + 1).sum())
+        unv = int(deg[(q > L) | (q < 0)].sum())
+        push = nnz_x * 4 + 2 * nnz_x * 8 + nnz_s * 4 + n / 8 + new * 8
+        pull = (n + 1) * 8 + unv * 4 + 2 * n / 8 + new * 8
+        b_alg += min(push, pull)
+        lvl_rows.append({"level": L, "nnz_x": nnz_x, "nnz_s": nnz_s, "new": new,
+                         "push_MB": round(push / 1e6, 2), "pull_MB": round(pull / 1e6, 2)})
+    return q, nq, edges, b_alg, lvl_rows
+
+
+C4_NNZ_X = (200, 2000, 20000)
+
+
+def c4_inputs():
+    from paper_2006_16767_b200 import synth_device as SD
+    t0 = time.time()
+    mr, nc = 10_000_000, 2_000_000
+    ro, ci, vals, draw = SD.svm_device(mr, nc, 20, 1.0, 3)
+    pts = [SD.svm_vector(draw, nc, nx, seed=nx) for nx in C4_NNZ_X]
+    return mr, nc, ro, ci, vals, pts, time.time() - t0
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
     if rank != 0:
         return None
     (rows, cols, ro, ci, vals), gen_s = make_matrix()
     nnz = int(ro[-1])
     vecs = make_vectors(cols)
-    ref = Ref(np.float32)
-    threads = os.cpu_count() or 1
-    ref.set_threads(threads)
-    M = ref.matrix(rows, cols, ro, ci, vals)
+    ref, M, ops, nnz_s, best, threads = ref_c2_prepare(rows, cols, ro, ci, vals, vecs)
     del ci
-    col_off = M.export()[3]
-    nnz_s = [int(np.sum(col_off[xi + 1] - col_off[xi])) for xi, _ in vecs]
-    best = cpu_choose(M, vecs)
     for _ in range(args.warmup):
-        ref_sweep_times(M, vecs, best)
-    steps = [ref_sweep_times(M, vecs, best) for _ in range(args.steps)]
+        ref_c2_step(M, ops, best, repeats=1)
+    steps = [ref_c2_step(M, ops, best) for _ in range(args.steps)]
     t_step = [sum(s) for s in steps]
     flops = sum(2 * s for s in nnz_s)
     v = flops / statistics.median(t_step) / 1e9
+    meta = _cpu_meta(ref, threads, "full C2 sweep per step: each point's best reference kernel, "
+                                   "benchmark_kernel (1 warm-up, median of 3)")
     line = {
         "metric": METRIC, "value": round(v, 4), "unit": "GFLOP/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(statistics.median(t_step) * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "rows": rows, "cols": cols, "nnz": nnz,
-                   "x_sparsity": list(SPARSITIES), "kernel_per_point": best},
-        "cpu_baseline": {"value": round(v, 4), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
-                         "sample": "full C2 sweep, best reference kernel per point (chosen by one timed "
-                                   "pass; sort write-back skipped at >=1 % density)"},
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded numpy generator, SURVEY.md 8(d) C2)",
+        "config": c2_config(rows, cols, nnz, world),
+        "kernel_per_point": [A_name(k) for k in best],
+        "cpu_baseline": dict(value=round(v, 4), unit="GFLOP/s", **meta),
         "e2e": {"value": round(v, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "per_point_ms": [round(statistics.median([s[i] for s in steps]) * 1e3, 4) for i in range(len(vecs))],
         "generation_s": round(gen_s, 1),
     }
+    del M, ref
+    if args.configs:
+        line["configs"] = reference_configs(args)
     return line
+
+
+def reference_configs(args):
+    """The reference's numbers for the other single-GPU configurations."""
+    from oracle.oracle import Port
+    out = {}
+    want = set(args.configs.split(","))
+    if "C1" in want:
+        out["C1"] = cpu_c1(c1_inputs())
+    if "C3" in want:
+        import torch
+        n, ro, ci, _ = c3_inputs()
+        ro_h, ci_h = ro.cpu().numpy(), ci.cpu().numpy()
+        del ro, ci
+        torch.cuda.empty_cache()
+        q, nq, edges, _, _ = c3_levels(Port(), n, ro_h, ci_h)
+        out["C3"] = cpu_c3(n, ro_h, ci_h.astype(np.int64), q, edges)
+    if "C4" in want:
+        import torch
+        mr, nc, ro, ci, vals, pts, _ = c4_inputs()
+        c4h = (mr, nc, ro.cpu().numpy(), ci.cpu().numpy().astype(np.int64), vals.cpu().numpy())
+        del ro, ci, vals
+        torch.cuda.empty_cache()
+        out["C4"] = cpu_c4(c4h, pts)
+    return out
 
 
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 def run_ours_multi(args, rank, world):
-    """N > 1: the row-partitioned mode (north_star), weak
-    scaling.  Rank g owns a C2-sized row block (4M rows x 4M columns, 2^26
-    draws, seed 1+g) of a (N*4M) x 4M matrix; every step broadcasts each sweep
-    point's x from rank 0 over NCCL straight into device buffers handed to the
-    library, then every rank runs its own selector + kernel on its block.
-    Step time = max over ranks (CUDA events on the shared stream, barrier on
-    both sides); value = all ranks' useful flops / step time."""
+    """N > 1: the row-partitioned mode (north_star), STRONG
+    scaling over ONE C2 matrix.  Every rank draws the same C2 matrix (seed 1)
+    and keeps its nnz-balanced row block (adaspmv_shard_rows, the segment_of
+    cut of partition.hpp:30-33 snapped to row starts); every step broadcasts
+    each sweep point's x from rank 0 over NCCL straight into device buffers
+    handed to the library, then every rank runs its own selector + kernel on
+    its block (nnz_s differs per block).  Step time = max over ranks (CUDA
+    events on the shared stream, barrier on both sides); value = the whole
+    matrix's useful flops / step time, the same numerator as N = 1."""
     import torch
     import torch.distributed as dist
 
     from paper_2006_16767_b200 import adaspmv as A
     from paper_2006_16767_b200 import selector as S
-    from paper_2006_16767_b200 import synth
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # test hook: ADASPMV_BENCH_BACKEND=gloo runs several ranks on one GPU
@@ -242,9 +434,15 @@ def run_ours_multi(args, rank, world):
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)  # collectives order against it; the library launches on it
     ctx = A.Context(local, stream=stream.cuda_stream)
-    rows, cols, ro, ci, vals = synth.uniform_random(N, DRAWS, seed=1 + rank, dtype=np.float32)
-    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
-    del ci
+    (rows_all, cols, ro_all, ci_all, vals_all), gen_s = make_matrix()
+    nnz_all = int(ro_all[-1])
+    cuts = A.shard_rows(ro_all, world)
+    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    b0, b1 = int(ro_all[r0]), int(ro_all[r1])
+    rows = r1 - r0
+    ro = ro_all[r0:r1 + 1] - b0
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci_all[b0:b1], vals_all[b0:b1], ctx=ctx)
+    del ci_all, vals_all
     bundle = A.SelectorBundle.load(Path(args.bundle) if args.bundle else S.DEFAULT_PATH)
     vecs = make_vectors(cols) if rank == 0 else None
     sizes = torch.tensor([len(v[0]) for v in vecs] if rank == 0 else [0] * len(SPARSITIES), device=dev)
@@ -290,6 +488,8 @@ def run_ours_multi(args, rank, world):
         flops_local += 2 * nnz_s_local[-1]
         k, _, _ = A.predict_kernel(m, x, bundle)
         chosen.append(k.index())
+        x.prepare(k.index())
+        A.run_kernel(m, k.index(), x, out=out)  # builds the row bins before any timing
     ctx.set_timing(True)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 
@@ -327,8 +527,8 @@ def run_ours_multi(args, rank, world):
     t_local = statistics.median(p[0] + p[1] for p in per)
     ctx.set_timing(False)
 
-    ybuf = torch.zeros(rows, dtype=torch.float32).pin_memory().numpy()
-    yidx = torch.zeros(rows, dtype=torch.int64).pin_memory().numpy()
+    ybuf = torch.zeros(max(rows, 1), dtype=torch.float32).pin_memory().numpy()
+    yidx = torch.zeros(max(rows, 1), dtype=torch.int64).pin_memory().numpy()
     d2h_bytes = [0]
 
     def e2e_step():
@@ -359,6 +559,8 @@ def run_ours_multi(args, rank, world):
         e2e_step()
         torch.cuda.synchronize()
         e2e_t.append(time.perf_counter() - t0)
+    d2h = torch.tensor([float(d2h_bytes[0])], dtype=torch.float64, device=dev)
+    dist.all_reduce(d2h, op=dist.ReduceOp.SUM)
     tt = torch.tensor([t_local, float(flops_local), statistics.median(e2e_t), t_exch], dtype=torch.float64, device=dev)
     tmax = tt.clone()
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -370,29 +572,253 @@ def run_ours_multi(args, rank, world):
     line = None
     if rank == 0:
         xbytes = sum((int(v.numel()) * 4 + int(i.numel()) * 4) for _, i, v in bufs)
+        hbm, src = peaks()
+        alg = alg_bytes(rows_all, cols, nnz_all, cols, nnz_all, cols)[0]  # x = 100 %: B_spmv
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded numpy generator, SURVEY.md 8(d) C2 per rank)",
-            "config": {"workload": WORKLOAD + ", row-partitioned: one C2-sized row block per GPU",
-                       "rows_per_gpu": rows, "cols": cols, "x_sparsity": list(SPARSITIES),
-                       "parallelism": f"row-partitioned x{world} (NCCL broadcast of x per point)",
-                       "exchange_bytes_per_step": xbytes, "l2": "inputs larger than L2 at the dense points",
-                       "timing": "per point: x broadcast (events) + multiply (library events), GPU gated, "
-                                 "max over ranks; selection and x hand-over untimed as on 1 GPU"},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded numpy generator, SURVEY.md 8(d) C2, one matrix cut into row blocks)",
+            "config": c2_config(rows_all, cols, nnz_all, world),
+            "shard_rows": [int(c) for c in cuts],
+            "timing": "per point: x broadcast (events) + multiply (library events), GPU gated, max over ranks; "
+                      "selection and x hand-over untimed as on 1 GPU",
             "exchange": {"ms_per_step": round(float(tmax[3].item()) * 1e3, 4),
                          "fraction": round(float(tmax[3].item()) / t_step, 4),
+                         "bytes_per_step": int(xbytes),
                          "GBps": round(xbytes * max(world - 1, 0) / max(float(tmax[3].item()), 1e-12) / 1e9, 1)},
             "e2e": {"value": round(e2e_v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(xbytes),
-                    "d2h_bytes_per_step": int(d2h_bytes[0]),
+                    "d2h_bytes_per_step": int(d2h.item()),
                     "note": "x H2D on rank 0 then NCCL broadcast; each rank selects, multiplies and copies its "
                             "y block to pinned host memory in its smaller form; max over ranks"},
+            "roofline_aggregate": {"bound": "hbm", "x_sparsity": 1.0, "alg_bytes": int(alg),
+                                   "peak": hbm * world, "unit": "GB/s", "peak_source": src},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
+            "setup_s": {"generate": round(gen_s, 1)},
         }
     dist.destroy_process_group()
     return line
+
+
+def _timed_factory(stream, flush):
+    import torch
+
+    def timed(fn, n_rep, need_flush):
+        ts = []
+        for _ in range(n_rep):
+            with torch.cuda.stream(stream):
+                if need_flush:
+                    flush.add_(1)
+                # the GPU spins while the host enqueues the multiply, so the
+                # library's events see device time, not host launch latency
+                torch.cuda._sleep(GATE_CYCLES)
+            y = fn()
+            if isinstance(y, tuple):
+                y = y[0]
+            ts.append(y.elapsed())
+        return ts
+    return timed
+
+
+def graph_replay_time(call, gstream, flush, n=20, reps=5):
+    """Device seconds per call by CUDA graph replay (inputs
+    under ~50 us): a graph of n x (L2 flush + call) minus a graph of n x
+    flush, each replayed `reps` times (median), / n.  `call` launches on
+    `gstream` (a library context bound to it)."""
+    import torch
+    with torch.cuda.stream(gstream):
+        call()
+    torch.cuda.synchronize()
+
+    def capture(with_call):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=gstream, capture_error_mode="relaxed"):
+            for _ in range(n):
+                flush.add_(1)
+                if with_call:
+                    call()
+        return g
+
+    g1, g0 = capture(True), capture(False)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def run(g):
+        g.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            with torch.cuda.stream(gstream):
+                e[0].record()
+                g.replay()
+                e[1].record()
+            torch.cuda.synchronize()
+            ts.append(e[0].elapsed_time(e[1]) * 1e-3)
+        return statistics.median(ts)
+
+    t1, t0 = run(g1), run(g0)
+    del g1, g0
+    return max(t1 - t0, 0.0) / n
+
+
+def ours_c1(local, bundle, hbm, flush, cpu):
+    """C1 (configs[0]): fp64 Laplacian, x = 100 % and 1 %: every kernel by
+    graph replay, the selector's choice, regret, B_alg roofline."""
+    import torch
+
+    from paper_2006_16767_b200 import adaspmv as A
+    rows, cols, ro, ci, vals, pts = c1_inputs()
+    nnz = int(ro[-1])
+    gstream = torch.cuda.Stream(device=f"cuda:{local}")
+    gctx = A.Context(local, stream=gstream.cuda_stream)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=gctx)
+    co = np.bincount(ci, minlength=cols)
+    out = A.MultiplyOutput(gctx)
+    res = {"workload": "C1 2-D 5-point Laplacian 1000x1000 (10^6 rows, 4,996,000 nnz) fp64, x = 100 % and 1 %",
+           "timing": "CUDA graph replay of 20 x (256 MiB L2 flush + multiply) minus 20 x flush, median of 5",
+           "points": []}
+    flops = tot = 0.0
+    for name, xi, xv in pts:
+        x = A.DeviceVector(cols, np.float64, gctx)
+        if len(xi) == cols:
+            x.set_dense(xv)
+        else:
+            x.set_sparse(xi, xv)
+        nnz_s = int(co[xi].sum())
+        k_sel = A.predict_kernel(m, x, bundle)[0].index()
+        c = A.KernelConfig()._c()
+        ts = []
+        for k in range(8):
+            x.prepare(k)
+
+            def call(k=k):
+                A._check(A._lib.adaspmv_run(gctx.h, m.h, x.h, k, C.byref(c), out.h))
+            ts.append(graph_replay_time(call, gstream, flush))
+        b_alg, fam = alg_bytes(rows, cols, nnz, len(xi), nnz_s, nnz_s, V=8)
+        t_sel = ts[k_sel]
+        flops += 2 * nnz_s
+        tot += t_sel
+        res["points"].append({
+            "point": name, "nnz_x": len(xi), "nnz_s": nnz_s, "selected": A_name(k_sel),
+            "t_sel_us": round(t_sel * 1e6, 2), "best": A_name(int(np.argmin(ts))),
+            "t_best_us": round(min(ts) * 1e6, 2), "regret": round(t_sel / min(ts), 3),
+            "gflops_sel": round(2 * nnz_s / t_sel / 1e9, 2), "alg_bytes": int(b_alg),
+            "roofline_frac": round(b_alg / t_sel / 1e9 / hbm, 4),
+            "t_kernels_us": [round(t * 1e6, 2) for t in ts]})
+    res["value"] = round(flops / tot / 1e9, 3)
+    res["unit"] = "GFLOP/s"
+    if cpu:
+        res["cpu_reference"] = cpu_c1((rows, cols, ro, ci, vals, pts))
+    del m, out, gctx
+    return res
+
+
+def ours_c3(local, bundle, hbm, cpu, reps=5):
+    """C3 (configs[2]): R-MAT 22 BFS from vertex 0 (OR_AND), levels checked
+    against the queue BFS; traversal wall time per policy (levels stay on the
+    device), GTEPS, kernel share (overhead), SURVEY.md 8(d) BFS B_alg."""
+    import torch
+
+    from oracle.oracle import Port
+    from paper_2006_16767_b200 import adaspmv as A
+    n, ro, ci, gen_s = c3_inputs()
+    nnz = int(ro[-1].item())
+    ctx = A.Context(local)
+    t0 = time.time()
+    m = A.DualMatrix.from_device(n, n, nnz, ro.data_ptr(), ci.data_ptr(), None, np.float32, ctx)
+    build_s = time.time() - t0
+    ro_h, ci_h = ro.cpu().numpy(), ci.cpu().numpy()
+    del ro, ci
+    torch.cuda.empty_cache()
+    q, nq, edges, b_alg, lvl_rows = c3_levels(Port(), n, ro_h, ci_h)
+    policies = [("selector", dict(bundle=bundle)), ("heuristic", {})] + \
+               [(f"fixed_{A_name(k)}", dict(force_kernel=k)) for k in range(8)]
+    runs = {}
+    for name, kw in policies:
+        lv, _ = A.bfs(m, 0, A.OR_AND, **kw)
+        ok = bool(np.array_equal(lv, q))
+        walls, ksum = [], []
+        for _ in range(reps):
+            ctx.synchronize()
+            t1 = time.perf_counter()
+            _, rep = A.bfs(m, 0, A.OR_AND, download_levels=False, **kw)
+            walls.append(time.perf_counter() - t1)
+            ksum.append(sum(r["kernel_s"] + r["convert_s"] for r in rep))
+        w = statistics.median(walls)
+        runs[name] = {"ms": round(w * 1e3, 4), "gteps": round(edges / w / 1e9, 2),
+                      "device_ms": round(statistics.median(ksum) * 1e3, 4),
+                      "overhead_fraction": round(1 - statistics.median(ksum) / w, 4), "levels_ok": ok,
+                      "kernels": [r["kernel"] for r in rep], "exec_mode": [r["exec_mode"] for r in rep]}
+    fixed = {k: v for k, v in runs.items() if k.startswith("fixed_")}
+    best = min(fixed, key=lambda k: fixed[k]["ms"])
+    sel = runs["selector"]
+    res = {"workload": f"C3 R-MAT scale 22 (device generator), {nnz:,} stored entries, BFS from vertex 0, OR_AND",
+           "n": n, "nnz": nnz, "levels": nq, "reached": int((q >= 0).sum()), "edges_traversed": edges,
+           "value": sel["gteps"], "unit": "GTEPS", "selected_ms": sel["ms"], "best_fixed": best,
+           "best_fixed_ms": fixed[best]["ms"], "regret_vs_best_fixed": round(sel["ms"] / fixed[best]["ms"], 3),
+           "overhead_fraction": sel["overhead_fraction"],
+           "alg_bytes": int(b_alg), "roofline_frac": round(b_alg / (sel["ms"] * 1e-3) / 1e9 / hbm, 4),
+           "roofline_note": "sum over levels of min(push, pull) bytes (SURVEY.md 8(d)) / selector wall time",
+           "per_level": lvl_rows, "runs": runs, "setup_s": {"generate": round(gen_s, 2), "build": round(build_s, 2)}}
+    del m, ctx
+    torch.cuda.empty_cache()
+    if cpu:
+        res["cpu_reference"] = cpu_c3(n, ro_h, ci_h.astype(np.int64), q, edges)
+    return res
+
+
+def ours_c4(local, bundle, hbm, flush, cpu, reps=3):
+    """C4 (configs[3]): SVM 10M x 2M, sparse sample rows (nnz_x 200 / 2,000 /
+    20,000): all 8 kernels (events + L2 flush), the selector, regret, B_alg."""
+    import torch
+
+    from paper_2006_16767_b200 import adaspmv as A
+    mr, nc, ro, ci, vals, pts, gen_s = c4_inputs()
+    nnz = int(ro[-1].item())
+    ctx = A.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    m = A.DualMatrix.from_device(mr, nc, nnz, ro.data_ptr(), ci.data_ptr(), vals.data_ptr(), np.float32, ctx)
+    c4h = (mr, nc, ro.cpu().numpy(), ci.cpu().numpy().astype(np.int64), vals.cpu().numpy()) if cpu else None
+    del ro, ci, vals
+    torch.cuda.empty_cache()
+    ctx.set_timing(True)
+    timed = _timed_factory(stream, flush)
+    out = A.MultiplyOutput(ctx)
+    res = {"workload": f"C4 SVM-like 10M x 2M, {nnz:,} nnz, Zipf(1.0) feature popularity, fp32; "
+                       "sparse sample rows nnz_x = 200 / 2,000 / 20,000", "points": []}
+    flops = tot = 0.0
+    for xi, xv in pts:
+        x = A.DeviceVector(nc, np.float32, ctx).set_sparse(xi, xv)
+        nnz_s = A.effective_nnz(m, x)
+        ts = []
+        nnz_y = 0
+        for k in range(8):
+            x.prepare(k)
+            run = lambda k=k: A.run_kernel(m, k, x, out=out)  # noqa: E731
+            ts.append(statistics.median(timed(run, reps + 1, True)[1:]))
+            if k == 5:
+                nnz_y = out.nnz()
+        k_sel = A.predict_kernel(m, x, bundle)[0].index()
+        t_sel = ts[k_sel]
+        b_alg, _ = alg_bytes(mr, nc, nnz, len(xi), nnz_s, nnz_y)
+        flops += 2 * nnz_s
+        tot += t_sel
+        res["points"].append({
+            "nnz_x": len(xi), "nnz_s": nnz_s, "nnz_y": nnz_y, "selected": A_name(k_sel),
+            "t_sel_us": round(t_sel * 1e6, 2), "best": A_name(int(np.argmin(ts))),
+            "t_best_us": round(min(ts) * 1e6, 2), "regret": round(t_sel / min(ts), 3),
+            "gflops_sel": round(2 * nnz_s / t_sel / 1e9, 2), "alg_bytes": int(b_alg),
+            "roofline_frac": round(b_alg / t_sel / 1e9 / hbm, 4),
+            "t_kernels_us": [round(t * 1e6, 2) for t in ts]})
+    res["value"] = round(flops / tot / 1e9, 3)
+    res["unit"] = "GFLOP/s"
+    res["setup_s"] = {"generate": round(gen_s, 2)}
+    ctx.set_timing(False)
+    del m, out, ctx
+    torch.cuda.empty_cache()
+    if cpu:
+        res["cpu_reference"] = cpu_c4(c4h, pts)
+    return res
 
 
 def run_ours(args, rank, world):
@@ -403,10 +829,6 @@ def run_ours(args, rank, world):
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = A.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
     (rows, cols, ro, ci, vals), gen_s = make_matrix()
@@ -432,23 +854,18 @@ def run_ours(args, rank, world):
     nnz_x = [len(xi) for xi, _ in vecs]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     out = A.MultiplyOutput(ctx)
+    # the row-bin layout of K0/K2 (a third resident copy, nnz * (4 + V)
+    # bytes) is built by the first binned call: timed here as setup, outside
+    # every timed multiply
+    dvs[-1].prepare(0)
+    ctx.synchronize()
+    t0 = time.time()
+    A.run_kernel(m, 0, dvs[-1], out=out)
+    ctx.synchronize()
+    bins_s = time.time() - t0
 
     ctx.set_timing(True)  # CUDA events recorded by the library around each multiply
-
-    def timed(fn, n_rep, need_flush):
-        ts = []
-        for _ in range(n_rep):
-            with torch.cuda.stream(stream):
-                if need_flush:
-                    flush.add_(1)
-                # the GPU spins while the host enqueues the multiply, so the
-                # library's events see device time, not host launch latency
-                torch.cuda._sleep(GATE_CYCLES)
-            y = fn()
-            if isinstance(y, tuple):
-                y = y[0]
-            ts.append(y.elapsed())
-        return ts
+    timed = _timed_factory(stream, flush)
 
     # ---- per point: every kernel (best-of-8, regret) -------------------------
     small = [alg_bytes(rows, cols, nnz, nx, ns, 0)[0] < 64e6 for nx, ns in zip(nnz_x, nnz_s)]
@@ -478,8 +895,6 @@ def run_ours(args, rank, world):
 
     for _ in range(args.warmup):
         step_times()
-    if dist:
-        dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         steps = [step_times() for _ in range(args.steps)]
@@ -487,12 +902,8 @@ def run_ours(args, rank, world):
     launches = (ctx.launches - l0) // max(1, args.steps + args.warmup)
     t_step = [sum(s) for s in steps]
     t_med = statistics.median(t_step)
-    if dist:
-        tt = torch.tensor([t_med], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_med = float(tt.item())
     flops = sum(2 * s for s in nnz_s)
-    value = world * flops / t_med / 1e9
+    value = flops / t_med / 1e9
     # ---- selection overhead (reported beside the kernel
     # time): fresh vectors, so the features are computed, not cached ----------
     sel_t, conv_t = [], []
@@ -512,11 +923,13 @@ def run_ours(args, rank, world):
             s_conv += rep["convert_s"]
         sel_t.append(s_sel)
         conv_t.append(s_conv)
-    overhead = {"select_us_per_step": round(statistics.median(sel_t) * 1e6, 1),
-                "convert_us_per_step": round(statistics.median(conv_t) * 1e6, 1),
+    o_sel, o_conv = statistics.median(sel_t), statistics.median(conv_t)
+    overhead = {"select_us_per_step": round(o_sel * 1e6, 1),
+                "convert_us_per_step": round(o_conv * 1e6, 1),
+                "overhead_fraction": round((o_sel + o_conv) / (o_sel + o_conv + t_med), 4),
                 "note": "host feature pull (nnz_s on the device, one scalar back) + tree walk, and the "
-                        "device format conversion the chosen kernel needs; excluded from value, "
-                        "included in e2e"}
+                        "device format conversion the chosen kernel needs, per sweep; excluded from value, "
+                        "included in e2e; fraction = overhead / (overhead + kernel time), SPEC.md:561 bound 0.20"}
     # ---- e2e through the public API with host buffers ----------------------
     # One step = one adaptive_run_batch call over the 7 host vectors (pinned),
     # results back in pinned host buffers in their smaller form; the batch
@@ -567,37 +980,36 @@ def run_ours(args, rank, world):
                 A._check(A._lib.adaspmv_output_dense(ctx.h, y.h, A._ptr(ybuf)))
         if it >= args.warmup:
             seq_times.append(time.perf_counter() - t0)
-    e2e_v = world * flops / statistics.median(e2e_times) / 1e9
-    # ---- roofline of the dominant kernel (the largest share of the step) ----
+    e2e_v = flops / statistics.median(e2e_times) / 1e9
+    # ---- roofline: the SpMV end (x = 100 %), SURVEY.md 8(d) B_alg ----------
     per_point = [statistics.median([s[i] for s in steps]) for i in range(len(dvs))]
-    dom = int(np.argmax(per_point))
-    k_dom = chosen[dom]
-    out_nnz = nnz_x[dom]
-    _, fam = alg_bytes(rows, cols, nnz, nnz_x[dom], nnz_s[dom], out_nnz)
+    top = len(dvs) - 1
+    k_top = chosen[top]
+    b_alg_top, _ = alg_bytes(rows, cols, nnz, nnz_x[top], nnz_s[top], nnz_x[top])
     hbm, src = peaks()
-    achieved = fam[k_dom] / per_point[dom] / 1e9
-    # DRAM bytes of the same kernel + input from the committed ncu --set full
-    # capture (only when it is the kernel that dominates this run)
-    prof = ROOT / "profiles" / "r01_roofline_traffic.json"
+    achieved = b_alg_top / per_point[top] / 1e9
+    # DRAM bytes per launch of the same kernel + input from the committed ncu
+    # --set full capture (profiles/r02_roofline_traffic.json)
     traffic = None
-    if prof.exists():
-        try:
-            pj = json.loads(prof.read_text())
-            # spmv_direct reads the whole matrix whatever x holds: its DRAM
-            # traffic per launch does not depend on the x sparsity
-            if A.KernelId.from_index(k_dom).name() in pj.get("kernel", "") and \
-                    (k_dom == 0 or f"x = {int(SPARSITIES[dom] * 100)} %" in pj.get("kernel", "")):
-                traffic = pj.get("traffic_bytes_per_launch")
-        except Exception:
-            traffic = None
+    for pf in ("r02_roofline_traffic.json", "r01_roofline_traffic.json"):
+        prof = ROOT / "profiles" / pf
+        if prof.exists():
+            try:
+                pj = json.loads(prof.read_text())
+                if A_name(k_top) in pj.get("kernel", "") and "x = 100 %" in pj.get("kernel", ""):
+                    traffic = pj.get("traffic_bytes_per_launch")
+                    break
+            except Exception:
+                traffic = None
+    dom = int(np.argmax(per_point))
     points = []
     for i in range(len(dvs)):
         b_alg, fam_i = alg_bytes(rows, cols, nnz, nnz_x[i], nnz_s[i], 0)
         tb = min(kernel_t[i])
         points.append({
             "x_sparsity": SPARSITIES[i], "nnz_x": nnz_x[i], "nnz_s": nnz_s[i],
-            "selected": A.KernelId.from_index(chosen[i]).name(), "t_sel_us": round(per_point[i] * 1e6, 2),
-            "best": A.KernelId.from_index(int(np.argmin(kernel_t[i]))).name(), "t_best_us": round(tb * 1e6, 2),
+            "selected": A_name(chosen[i]), "t_sel_us": round(per_point[i] * 1e6, 2),
+            "best": A_name(int(np.argmin(kernel_t[i]))), "t_best_us": round(tb * 1e6, 2),
             "regret": round(per_point[i] / tb, 3),
             "gflops_sel": round(2 * nnz_s[i] / per_point[i] / 1e9, 2),
             "alg_GBps_sel": round(b_alg / per_point[i] / 1e9, 1),
@@ -610,55 +1022,65 @@ def run_ours(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_med * 1e3, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded numpy generator, SURVEY.md 8(d) C2)",
-        "config": {"workload": WORKLOAD, "rows": rows, "cols": cols, "nnz": nnz,
-                   "x_sparsity": list(SPARSITIES), "l2": "256 MiB flush before timed multiplies with "
-                   "working set < 64 MB; larger inputs exceed L2", "selector": str(bundle_path.name),
-                   "parallelism": f"row-replicated x{world}" if world > 1 else "1 GPU"},
+        "config": c2_config(rows, cols, nnz, world),
+        "selector": str(bundle_path.name),
         "e2e": {"value": round(e2e_v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "api": f"adaspmv_run_batch (pinned host buffers, {args.lanes} lanes)",
                 "ms_per_step": round(statistics.median(e2e_times) * 1e3, 3),
-                "sequential_value": round(world * flops / statistics.median(seq_times) / 1e9, 3),
+                "sequential_value": round(flops / statistics.median(seq_times) / 1e9, 3),
                 "sequential_api": "per vector: vector_set -> run_adaptive -> output copy",
                 "kernels": e2e_kernels},
-        "roofline": {"bound": "hbm", "kernel": A.KernelId.from_index(k_dom).name(),
-                     "x_sparsity": SPARSITIES[dom], "achieved": round(achieved, 1), "peak": hbm,
-                     "peak_source": src, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                     "traffic": traffic, "alg_bytes": int(fam[k_dom])},
+        "roofline": {"bound": "hbm", "kernel": A_name(k_top), "x_sparsity": SPARSITIES[top],
+                     "achieved": round(achieved, 1), "peak": hbm, "peak_source": src, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": traffic, "alg_bytes": int(b_alg_top),
+                     "alg_bytes_formula": "B_alg = min(B_spmv, B_row, B_col_atomic, B_col_sort) = B_spmv at x = 100 %",
+                     "step_share": round(per_point[top] / sum(per_point), 4),
+                     "dominant_point": SPARSITIES[dom]},
         "selector_regret": round(regret_total, 4),
         "overhead": overhead,
         "gpu_launches": int(launches),
         "points": points,
-        "setup_s": {"generate": round(gen_s, 1), "upload_csc_features": round(upload_s, 2)},
+        "setup_s": {"generate": round(gen_s, 1), "upload_csc_features": round(upload_s, 2),
+                    "row_bins": round(bins_s, 3)},
+        "clocks": clk.summary(),
     }
-    line["clocks"] = clk.summary()
-    if rank == 0 and not args.no_cpu_baseline:
+    ctx.set_timing(False)
+    cpu = rank == 0 and not args.no_cpu_baseline
+    if cpu:
         line["cpu_baseline"] = cpu_baseline(rows, cols, ro, ci, vals, vecs)
-    if dist:
-        dist.destroy_process_group()
-    return line if rank == 0 else None
+    del m, dvs, out, fresh, e2e_x
+    torch.cuda.empty_cache()
+    if args.configs:
+        hbm_peak = hbm
+        want = set(args.configs.split(","))
+        cfgs = {}
+        if "C1" in want:
+            cfgs["C1"] = ours_c1(local, bundle, hbm_peak, flush, cpu)
+        if "C3" in want:
+            cfgs["C3"] = ours_c3(local, bundle, hbm_peak, cpu)
+        if "C4" in want:
+            cfgs["C4"] = ours_c4(local, bundle, hbm_peak, flush, cpu)
+        line["configs"] = cfgs
+    return line
 
 
 def cpu_baseline(rows, cols, ro, ci, vals, vecs):
-    """The reference CPU implementation (oracle/_ref) on a bounded sample:
-    one pass over the sweep, every point with its best reference kernel."""
+    """The reference CPU implementation (oracle/_ref, bench build) on a
+    bounded sample: one pass over the sweep, every point with its best
+    reference kernel, benchmark_kernel timing -- the reference arm's step."""
     try:
-        from oracle.oracle import Ref, have_ref
+        from oracle.oracle import have_ref
         if not have_ref(np.float32):
             return {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference",
                     "sample": "oracle/_ref not built"}
-        ref = Ref(np.float32)
-        threads = os.cpu_count() or 1
-        ref.set_threads(threads)
-        M = ref.matrix(rows, cols, ro, ci, vals)
-        col_off = M.export()[3]
-        nnz_s = [int(np.sum(col_off[xi + 1] - col_off[xi])) for xi, _ in vecs]
-        best = cpu_choose(M, vecs)
-        ts = ref_sweep_times(M, vecs, best, repeats=3, warmup=1)
+        ref, M, ops, nnz_s, best, threads = ref_c2_prepare(rows, cols, ro, ci, vals, vecs)
+        ts = ref_c2_step(M, ops, best)
         v = sum(2 * s for s in nnz_s) / sum(ts) / 1e9
-        return {"value": round(v, 4), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
-                "sample": "one C2 sweep (7 points), best reference kernel per point, median of 3",
-                "per_point_ms": [round(t * 1e3, 3) for t in ts],
-                "kernel_per_point": best}
+        res = {"value": round(v, 4), "unit": "GFLOP/s", "per_point_ms": [round(t * 1e3, 3) for t in ts],
+               "kernel_per_point": [A_name(k) for k in best]}
+        res.update(_cpu_meta(ref, threads, "one C2 sweep (7 points), best reference kernel per point, "
+                                           "benchmark_kernel (1 warm-up, median of 3)"))
+        return res
     except Exception as e:  # never fail the GPU line on the baseline
         return {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
@@ -672,9 +1094,13 @@ def main():
     ap.add_argument("--bundle", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lanes", type=int, default=3, help="streams of the e2e batch pipeline")
+    ap.add_argument("--configs", default="C1,C3,C4",
+                    help="other single-GPU configurations carried in the line ('' = none); N = 1 only")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if world > 1:
+        args.configs = ""
     if args.impl == "reference":
         line = run_reference(args, rank, world)
     else:
