@@ -141,6 +141,7 @@ def load(path: Optional[os.PathLike] = None):
         "adaspmv_ctx_stream": [vp],
         "adaspmv_ctx_launch_count": [vp],
         "adaspmv_ctx_set_timing": [vp, C.c_int],
+        "adaspmv_ctx_set_bfs_loop": [vp, C.c_int],
         "adaspmv_output_elapsed": [vp, vp, P(C.c_double)],
         "adaspmv_ctx_set_counters": [vp, C.c_int],
         "adaspmv_output_counters": [vp, vp, vp],
@@ -426,6 +427,10 @@ class Context:
     def set_counters(self, enable: bool = True):
         """KernelCounters for every following run (kernels.hpp:106-111)."""
         _check(_lib.adaspmv_ctx_set_counters(self.h, 1 if enable else 0))
+
+    def set_bfs_loop(self, host_loop: bool = False):
+        """adaspmv_ctx_set_bfs_loop: False = device-resident BFS where it applies."""
+        _check(_lib.adaspmv_ctx_set_bfs_loop(self.h, int(bool(host_loop))))
 
     def set_timing(self, enable: bool = True):
         """Bracket every multiply with CUDA events (MultiplyOutput.elapsed())."""

@@ -359,12 +359,23 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
 
 }  // namespace
 
+void widen_levels(Context& ctx, const int32_t* lv, int64_t n, int64_t* out) {
+    if (n <= 0) return;
+    widen_levels_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx.stream>>>(lv, n, out);
+    ADA_LAUNCHED(ctx);
+}
+
 void bfs(Context& ctx, const Matrix& m, int64_t source, int semiring, const Bundle* b, int forced,
          int64_t* levels, int64_t* n_levels, adaspmv_iteration_report* reports,
          int64_t max_reports) {
     if (m.rows != m.cols) invalid("bfs: matrix must be square");
     if (source < 0 || source >= m.rows) invalid("bfs: source out of range");
     if (forced < -1 || forced > 7) invalid("bfs: forced kernel out of range");
+    if (semiring < ADASPMV_PLUS_TIMES || semiring > ADASPMV_MIN_PLUS) invalid("unknown semiring");
+    if (!ctx.bfs_host_loop && bfs_graph_applicable(m, semiring, forced)) {
+        bfs_graph(ctx, m, source, b, levels, n_levels, reports, max_reports);
+        return;
+    }
     const bool f64 = m.dtype == ADASPMV_F64;
     switch (semiring) {
         case ADASPMV_PLUS_TIMES:

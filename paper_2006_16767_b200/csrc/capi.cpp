@@ -232,6 +232,13 @@ int adaspmv_ctx_set_timing(adaspmv_ctx* ctx, int enable) {
     });
 }
 
+int adaspmv_ctx_set_bfs_loop(adaspmv_ctx* ctx, int host_loop) {
+    return guarded([&] {
+        need(ctx, "context");
+        ctx->bfs_host_loop = host_loop != 0;
+    });
+}
+
 int adaspmv_ctx_set_counters(adaspmv_ctx* ctx, int enable) {
     return guarded([&] {
         need(ctx, "context");

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <atomic>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -86,6 +87,10 @@ struct DevBuf {
 };
 
 struct BatchLane;  // batch.cpp: one pipelined stream of adaspmv_run_batch
+struct BfsPlan;    // bfs_graph.cu: a captured device-resident BFS level loop
+struct BfsPlanDeleter {
+    void operator()(BfsPlan* p) const;
+};
 
 struct Context {
     int device = 0;
@@ -95,6 +100,7 @@ struct Context {
     int64_t launches = 0;
     bool timing = false;  // bracket every run with CUDA events (adaspmv_output_elapsed)
     bool counters = false;  // KernelCounters per run (adaspmv_ctx_set_counters)
+    bool bfs_host_loop = false;  // adaspmv_ctx_set_bfs_loop: force the host-driven BFS level loop
     unsigned long long* ctr = nullptr;  // the running output's device counters (kernels' last argument)
     // general scratch (reused by every call; calls on a context are serialised)
     // [0..3] sort write-back keys/values (double buffered), [4] vector scans,
@@ -181,6 +187,8 @@ struct Matrix {
     mutable std::unique_ptr<BinLayout> bins{new BinLayout()};
     // column-normalised pattern copy for PageRank (pagerank.cu), built once
     mutable std::unique_ptr<Matrix> colnorm;
+    // captured device-resident BFS loop (bfs_graph.cu), built on first use
+    mutable std::unique_ptr<BfsPlan, BfsPlanDeleter> bfs_plan;
     int vbytes() const { return value_bytes(dtype); }
 };
 
@@ -277,7 +285,13 @@ struct Tree {
     std::vector<double> threshold;
 };
 
+inline uint64_t next_object_id() {
+    static std::atomic<uint64_t> n{1};
+    return n.fetch_add(1);
+}
+
 struct Bundle {
+    uint64_t id = next_object_id();  // identity for device-side caches (immutable after creation)
     int schema_version = 1;
     std::string hardware_tag;
     std::string feature_order_hash;
@@ -405,6 +419,14 @@ void save_binary_file(const std::string& path, int64_t rows, int64_t cols,
 void bfs(Context& ctx, const Matrix& m, int64_t source, int semiring, const Bundle* b,
          int forced, int64_t* levels, int64_t* n_levels, adaspmv_iteration_report* reports,
          int64_t max_reports);
+
+// device-resident BFS (bfs_graph.cu): membership-only levels, heuristic or
+// selector policy; levels / reports as bfs()
+bool bfs_graph_applicable(const Matrix& m, int semiring, int forced);
+void bfs_graph(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int64_t* levels, int64_t* n_levels,
+               adaspmv_iteration_report* reports, int64_t max_reports);
+// out[i] = lv[i] (int32 levels -> int64), on ctx's stream
+void widen_levels(Context& ctx, const int32_t* lv, int64_t n, int64_t* out);
 
 // incremental PageRank (pagerank.cu)
 void pagerank(Context& ctx, const Matrix& m, double damping, double prune, int64_t max_iters,

@@ -1,0 +1,90 @@
+"""The device-resident BFS level loop (csrc/bfs_graph.cu): levels bit exact
+against the queue BFS and the host-driven loop (adaspmv_ctx_set_bfs_loop),
+for every semiring on pattern matrices and OR_AND on valued ones, under the
+built-in policy and the trained selector (whose trees are walked on the
+device: its per-level choices must equal the host selector's on the same
+frontiers), on graphs deeper than one graph replay (kUnroll = 8 levels),
+disconnected graphs and isolated sources."""
+import numpy as np
+import pytest
+
+from paper_2006_16767_b200 import adaspmv as A
+from paper_2006_16767_b200 import selector as S
+from paper_2006_16767_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _sym(n, edges):
+    a = np.zeros((n, n), bool)
+    for u, v in edges:
+        a[u, v] = a[v, u] = True
+    r, c = np.nonzero(a)
+    ro = np.zeros(n + 1, np.int64)
+    np.add.at(ro, r + 1, 1)
+    return np.cumsum(ro), c.astype(np.int64)
+
+
+def _graphs():
+    out = []
+    # path of 40 vertices: 40 levels = 5 graph replays
+    out.append(("path40", 40, *_sym(40, [(i, i + 1) for i in range(39)])))
+    # two components + an isolated vertex
+    out.append(("disconnected", 12, *_sym(12, [(0, 1), (1, 2), (2, 0), (4, 5), (5, 6)])))
+    for seed, scale in ((1, 10), (2, 13)):
+        n, _, ro, ci, _ = synth.rmat(scale, 8, seed=seed)
+        out.append((f"rmat{scale}", n, ro, ci))
+    rows, cols, ro, ci, _ = synth.random_csr(3000, 3000, 0.002, seed=4)
+    a = np.zeros((3000, 3000), bool)
+    r = np.repeat(np.arange(3000), np.diff(ro))
+    a[r, ci] = True
+    a = a | a.T
+    np.fill_diagonal(a, False)
+    rr, cc = np.nonzero(a)
+    ro2 = np.zeros(3001, np.int64)
+    np.add.at(ro2, rr + 1, 1)
+    out.append(("random3000", 3000, np.cumsum(ro2), cc.astype(np.int64)))
+    return out
+
+
+GRAPHS = _graphs()
+
+
+@pytest.mark.parametrize("name,n,ro,ci", GRAPHS, ids=[g[0] for g in GRAPHS])
+@pytest.mark.parametrize("sr", [A.OR_AND, A.MIN_PLUS, A.PLUS_TIMES], ids=["or_and", "min_plus", "plus_times"])
+def test_device_loop_levels(ctx, port, name, n, ro, ci, sr):
+    m = A.DualMatrix.from_csr(n, n, ro, ci, None, dtype=np.float32, ctx=ctx)
+    co, ri, _ = port.csr_to_csc(n, n, ro, ci, np.ones(len(ci)))
+    bundle = A.SelectorBundle.load(S.DEFAULT_PATH)
+    for src in sorted({0, n - 1, 3 % n}):
+        exp, nl = port.bfs_queue(n, co, ri, src)
+        for kw in (dict(), dict(bundle=bundle)):
+            ctx.set_bfs_loop(False)
+            lv, reps = A.bfs(m, src, sr, **kw)
+            assert np.array_equal(lv, exp), (name, src, kw.keys())
+            assert len(reps) == nl
+            # the frontier sizes the device logged are the level sizes
+            assert [r["nnz_x"] for r in reps] == [int((exp == L).sum()) for L in range(nl)]
+            for r in reps:
+                assert r["exec_mode"] == (A.EXEC_FUSED_PUSH_LB if r["kernel"] >= 4 else A.EXEC_MASKED_PULL)
+            ctx.set_bfs_loop(True)
+            lv_h, reps_h = A.bfs(m, src, sr, **kw)
+            ctx.set_bfs_loop(False)
+            assert np.array_equal(lv_h, exp)
+            if "bundle" in kw:
+                # device tree walk == host tree walk on the same frontiers
+                assert [r["kernel"] for r in reps] == [r["kernel"] for r in reps_h], name
+
+
+def test_device_loop_valued_or_and_and_levels_download_optional(ctx, port):
+    n, _, ro, ci, vals = synth.rmat(12, 8, seed=5, values="uniform")
+    m = A.DualMatrix.from_csr(n, n, ro, ci, vals, dtype=np.float64, ctx=ctx)
+    co, ri, _ = port.csr_to_csc(n, n, ro, ci, np.ones(len(ci)))
+    exp, nl = port.bfs_queue(n, co, ri, 0)
+    lv, reps = A.bfs(m, 0, A.OR_AND)
+    assert np.array_equal(lv, exp) and len(reps) == nl
+    none, reps2 = A.bfs(m, 0, A.OR_AND, download_levels=False)
+    assert none is None and len(reps2) == nl
+    # valued matrix under plus-times: values decide y_i != 0, so the host loop runs
+    lv, reps = A.bfs(m, 0, A.PLUS_TIMES)
+    assert all(r["exec_mode"] != A.EXEC_FUSED_PUSH_LB or r["kernel"] >= 4 for r in reps)
