@@ -22,7 +22,7 @@ implementation timed on this box's host cores.
                     ref_bench flags at this host's ISA level) on the host cores
 
 Timing: CUDA events on the library's stream around each multiply, medians
-over K steps after W warm-up steps; an L2 flush (256 MiB write) precedes every
+over K steps after W warm-up steps; an L2 flush (256 MiB write, then a 256 MiB clean read) precedes every
 timed multiply whose working set fits in L2.  C1 (< 50 us) is timed by CUDA
 graph replay: N x (flush + multiply) minus N x flush.  CPU
 timings follow SPEC.md:437-446 benchmark_kernel: operands prepared once, one
@@ -56,7 +56,7 @@ SPARSITIES = (0.00001, 0.0001, 0.001, 0.01, 0.1, 0.5, 1.0)
 N = 1 << int(os.environ.get("ADASPMV_BENCH_LOG2N", "22"))  # override only for dry runs
 DRAWS = 16 * N
 GATE_CYCLES = 400_000  # ~0.2 ms at 1.9 GHz
-L2_NOTE = "256 MiB flush before timed multiplies with working set < 64 MB; larger inputs exceed L2"
+L2_NOTE = "L2 flush (256 MiB write, then 256 MiB clean read) before timed multiplies with working set < 64 MB; larger inputs exceed L2"
 METRIC = "GFLOP/s and HBM GB/s (% of roofline) vs x sparsity; selector regret vs best"
 WORKLOAD = "C2 uniform random 4M x 4M, 2^26 draws (~64M nnz) fp32, x-sparsity sweep 0.001%-100%"
 I_B, O_B = 4, 8  # device index / offset bytes (SURVEY.md section 8 symbols)
@@ -601,6 +601,23 @@ def run_ours_multi(args, rank, world):
     return line
 
 
+class L2Flush:
+    """L2 flush between timed multiplies: write a 256 MiB buffer (2x the
+    126 MB L2), then read a second 256 MiB buffer, so the dirty lines of the
+    write are written back inside the flush and the multiply starts on an L2
+    holding only clean, unrelated lines (otherwise the multiply's first reads
+    pay the DRAM write-back of the flush's dirty lines)."""
+
+    def __init__(self, device):
+        import torch
+        self.w = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+        self.r = torch.zeros(64 << 20, dtype=torch.int32, device=device)
+
+    def __call__(self):
+        self.w.add_(1)
+        self.r.amax()
+
+
 def _timed_factory(stream, flush):
     import torch
 
@@ -609,7 +626,7 @@ def _timed_factory(stream, flush):
         for _ in range(n_rep):
             with torch.cuda.stream(stream):
                 if need_flush:
-                    flush.add_(1)
+                    flush()
                 # the GPU spins while the host enqueues the multiply, so the
                 # library's events see device time, not host launch latency
                 torch.cuda._sleep(GATE_CYCLES)
@@ -635,7 +652,7 @@ def graph_replay_time(call, gstream, flush, n=20, reps=5):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=gstream, capture_error_mode="relaxed"):
             for _ in range(n):
-                flush.add_(1)
+                flush()
                 if with_call:
                     call()
         return g
@@ -675,7 +692,7 @@ def ours_c1(local, bundle, hbm, flush, cpu):
     co = np.bincount(ci, minlength=cols)
     out = A.MultiplyOutput(gctx)
     res = {"workload": "C1 2-D 5-point Laplacian 1000x1000 (10^6 rows, 4,996,000 nnz) fp64, x = 100 % and 1 %",
-           "timing": "CUDA graph replay of 20 x (256 MiB L2 flush + multiply) minus 20 x flush, median of 5",
+           "timing": "CUDA graph replay of 20 x (L2 flush: 256 MiB write + 256 MiB read; multiply) minus 20 x flush, median of 5",
            "points": []}
     flops = tot = 0.0
     for name, xi, xv in pts:
@@ -856,7 +873,7 @@ def run_ours(args, rank, world):
         dvs.append(dv)
     nnz_s = [A.effective_nnz(m, dv) for dv in dvs]
     nnz_x = [len(xi) for xi, _ in vecs]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    flush = L2Flush(f"cuda:{local}")
     out = A.MultiplyOutput(ctx)
     # the row-bin layout of K0/K2 (a third resident copy, nnz * (4 + V)
     # bytes) is built by the first binned call: timed here as setup, outside

@@ -85,6 +85,59 @@ __global__ void __launch_bounds__(kNT) row_direct_kernel(int64_t rows,
     count_add(ctr, 0, cnt);
 }
 
+// Short-row Direct kernel: one thread per row, the row's U loads issued as
+// one unrolled step, registers capped so that 8 CTAs (2048 threads) share an
+// SM.  Measured on C1 fp64 (tools/microbench/c1_mb.cu, CUDA-graph replay
+// after a clean L2 flush): the lane-group kernel above with G = 1 (U = 8,
+// 64 registers, half the warps resident) 17.5 us; this one (U = 5, 32
+// registers) 14.4 us = 89 % of HBM; staging the CTA's products in shared
+// memory 20.9 us; a warp per 32 rows with a shuffle scan 27.4 us.
+template <class V, bool VALIDATE, int SR, int U>
+__global__ void __launch_bounds__(kNT, U <= 5 ? 8 : 6) row_thread_kernel(int64_t rows,
+                                                            const int64_t* __restrict__ ro,
+                                                            const int32_t* __restrict__ ci,
+                                                            const V* __restrict__ vals,
+                                                            const V* __restrict__ x,
+                                                            const uint32_t* __restrict__ mask,
+                                                            V* __restrict__ y,
+                                                            unsigned long long* __restrict__ ctr) {
+    using S = Semiring<SR, V>;
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * kNT + threadIdx.x;
+    if (r >= rows) return;
+    const int64_t b = __ldg(ro + r), e = __ldg(ro + r + 1);
+    V acc = S::zero();
+    unsigned cnt = 0;
+    for (int64_t k0 = b; k0 < e; k0 += U) {
+        int c[U];
+        bool ok[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            ok[j] = k0 + j < e;
+            c[j] = ok[j] ? __ldg(ci + k0 + j) : 0;
+        }
+        if (VALIDATE) {
+#pragma unroll
+            for (int j = 0; j < U; ++j)
+                if (ok[j]) ok[j] = (__ldg(mask + (c[j] >> 5)) >> (c[j] & 31)) & 1u;
+        }
+        V a[U], xv[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            a[j] = ok[j] && S::kUsesValues ? __ldg(vals + k0 + j) : V(1);
+            xv[j] = ok[j] ? __ldg(x + c[j]) : S::zero();
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+            if (ok[j]) acc = S::fma(a[j], xv[j], acc);
+        if (ctr) {
+#pragma unroll
+            for (int j = 0; j < U; ++j) cnt += ok[j];
+        }
+    }
+    y[r] = acc;
+    count_add(ctr, 0, cnt);
+}
+
 // ---------------------------------------------------------------------------
 // LB warp-tile kernel.  Warp w of the grid owns items [w*T, (w+1)*T), T =
 // kRowTile = 256: two rounds of 128 items, lane l holding the 4 consecutive
@@ -378,6 +431,16 @@ void launch_direct(Context& ctx, const Matrix& m, const V* x, const uint32_t* ma
             m.rows, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), m.vals.as<V>(), x, mask, \
             y, ctx.ctr);                                                                       \
         break;
+    if (G == 1 && m.feat[3] <= 8.0) {  // short rows: one unrolled step per row
+        if (m.feat[3] <= 5.0)
+            row_thread_kernel<V, VALIDATE, SR, 5><<<blocks, kNT, 0, ctx.stream>>>(
+                m.rows, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), m.vals.as<V>(), x, mask, y, ctx.ctr);
+        else
+            row_thread_kernel<V, VALIDATE, SR, 8><<<blocks, kNT, 0, ctx.stream>>>(
+                m.rows, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), m.vals.as<V>(), x, mask, y, ctx.ctr);
+        ADA_LAUNCHED(ctx);
+        return;
+    }
     switch (G) {
         ADA_G(1) ADA_G(2) ADA_G(4) ADA_G(8) ADA_G(16) ADA_G(32)
         default: invalid("lanes_per_row must be a power of two <= 32");
