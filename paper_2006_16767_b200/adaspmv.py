@@ -428,8 +428,9 @@ class Context:
         """KernelCounters for every following run (kernels.hpp:106-111)."""
         _check(_lib.adaspmv_ctx_set_counters(self.h, 1 if enable else 0))
 
-    def set_bfs_loop(self, host_loop: bool = False):
-        """adaspmv_ctx_set_bfs_loop: False = device-resident BFS where it applies."""
+    def set_bfs_loop(self, host_loop: bool = True):
+        """adaspmv_ctx_set_bfs_loop: True (default) = host-driven level loop,
+        False = device-resident (captured) BFS where it applies."""
         _check(_lib.adaspmv_ctx_set_bfs_loop(self.h, int(bool(host_loop))))
 
     def set_timing(self, enable: bool = True):

@@ -318,17 +318,31 @@ __global__ void __launch_bounds__(256) bfs_push_kernel(BfsState* st, int p, cons
     }
 }
 
+// Frontier bitmap of a pull level (n/8 bytes, L2-resident) from the frontier
+// list; cleared again by the same list after the pull, so it is all zero
+// between pull levels.
+__global__ void __launch_bounds__(256) bfs_fmask_kernel(const BfsState* st, int p, const int32_t* __restrict__ f,
+                                                        uint32_t* __restrict__ fm, int set) {
+    if (st->mode != kModePull) return;
+    const long long n = static_cast<long long>(st->nf[p]);
+    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += static_cast<long long>(gridDim.x) * 256) {
+        const int32_t c = f[i];
+        if (set) atomicOr(fm + (c >> 5), 1u << (c & 31));
+        else fm[c >> 5] = 0u;
+    }
+}
+
 // Output-masked pull with early exit (bfs.cu bfs_pull_kernel), G lanes per
-// row, grid-stride; a column is in the frontier iff its level is level - 1.
+// row, grid-stride; frontier membership from the level's bitmap.
 template <int G>
 __global__ void __launch_bounds__(256) bfs_pull_dev_kernel(BfsState* st, int p, int64_t rows,
                                                            const int64_t* __restrict__ ro,
                                                            const int32_t* __restrict__ ci,
                                                            const int64_t* __restrict__ co,
+                                                           const uint32_t* __restrict__ fm,
                                                            int32_t* __restrict__ lv, int32_t* __restrict__ nf_out) {
     if (st->mode != kModePull) return;
     const int level = st->level;
-    const int prev = level - 1;
     const int q = p ^ 1;
     const int lane = threadIdx.x & 31;
     const int lg = threadIdx.x & (G - 1);
@@ -344,7 +358,7 @@ __global__ void __launch_bounds__(256) bfs_pull_dev_kernel(BfsState* st, int p, 
 #pragma unroll
                 for (int j = 0; j < 4; ++j) c[j] = k0 + j * G < e ? __ldg(ci + k0 + j * G) : -1;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) hit = hit || (c[j] >= 0 && lv[c[j]] == prev);
+                for (int j = 0; j < 4; ++j) hit = hit || (c[j] >= 0 && ((__ldg(fm + (c[j] >> 5)) >> (c[j] & 31)) & 1u));
             }
         }
         // OR over the row's G lanes; the group leader appends
@@ -381,7 +395,7 @@ __global__ void bfs_init_kernel(BfsState* st, int32_t* lv, int64_t n, int64_t so
 struct BfsPlan {
     cudaStream_t stream = nullptr;
     uint64_t bundle_id = 0;  // 0 = heuristic
-    DevBuf state, log, f[2], eff, part, lv, trees_i, trees_d, mfeat;
+    DevBuf state, log, f[2], eff, part, lv, fm, trees_i, trees_d, mfeat;
     DevTrees dt{};
     cudaGraphExec_t exec = nullptr;
     ~BfsPlan() {
@@ -434,9 +448,10 @@ void upload_trees(Context& ctx, const Bundle& b, BfsPlan& P) {
 }
 
 template <int G>
-void launch_pull_g(cudaStream_t s, unsigned grid, BfsState* st, int p, const Matrix& m, int32_t* lv, int32_t* out) {
+void launch_pull_g(cudaStream_t s, unsigned grid, BfsState* st, int p, const Matrix& m, const uint32_t* fm,
+                   int32_t* lv, int32_t* out) {
     bfs_pull_dev_kernel<G><<<grid, 256, 0, s>>>(st, p, m.rows, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(),
-                                                m.col_off.as<int64_t>(), lv, out);
+                                                m.col_off.as<int64_t>(), fm, lv, out);
 }
 
 // Captures kUnroll levels (parity 0, 1, 0, ...) into a graph.
@@ -450,6 +465,9 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     P.eff.ensure(sizeof(int64_t) * static_cast<size_t>(n + 1));
     P.part.ensure(sizeof(long long) * kScanBlocks);
     P.lv.ensure(sizeof(int32_t) * static_cast<size_t>(n));
+    uint32_t* fm = static_cast<uint32_t*>(P.fm.ensure(sizeof(uint32_t) * static_cast<size_t>((n + 31) / 32)));
+    ADA_CUDA(cudaMemsetAsync(fm, 0, sizeof(uint32_t) * static_cast<size_t>((n + 31) / 32), ctx.stream));
+    const unsigned fm_grid = static_cast<unsigned>(ctx.sm_count) * 4;
     double* mf = static_cast<double*>(P.mfeat.ensure(sizeof(double) * 9));
     ADA_CUDA(cudaMemcpyAsync(mf, m.feat, sizeof(double) * 9, cudaMemcpyHostToDevice, ctx.stream));
     if (b) upload_trees(ctx, *b, P);
@@ -460,10 +478,12 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     const int64_t* co = m.col_off.as<int64_t>();
     const unsigned push_grid = static_cast<unsigned>(ctx.sm_count) * 8;
     // pull: G lanes per row (early exit: a row usually stops within its first
-    // entries), grid of 8 CTAs per SM, grid-stride over the rows
+    // entries)
     const int G = std::max(1, default_lanes_per_row(m.feat[5]) / 8);
-    const unsigned pull_grid = static_cast<unsigned>(std::min<int64_t>(
-        static_cast<int64_t>(ctx.sm_count) * 8, std::max<int64_t>((n * G + 255) / 256, 1)));
+    // one group per row (a full grid, as the host loop's pull): the block
+    // scheduler balances rows that run long (no frontier neighbour, no early
+    // exit) -- a capped grid-stride grid measured 6-7x slower on C3's pull levels
+    const unsigned pull_grid = static_cast<unsigned>(std::max<int64_t>((n * G + 255) / 256, 1));
     cudaGraph_t graph = nullptr;
     ADA_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
     try {
@@ -478,12 +498,14 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
             bfs_push_kernel<<<push_grid, 256, 0, ctx.stream>>>(st, p, P.f[p].as<int32_t>(), P.eff.as<int64_t>(), co,
                                                                m.row_idx.as<int32_t>(), lv, P.f[p ^ 1].as<int32_t>());
             int32_t* out = P.f[p ^ 1].as<int32_t>();
+            bfs_fmask_kernel<<<fm_grid, 256, 0, ctx.stream>>>(st, p, P.f[p].as<int32_t>(), fm, 1);
             switch (G) {
-                case 1: launch_pull_g<1>(ctx.stream, pull_grid, st, p, m, lv, out); break;
-                case 2: launch_pull_g<2>(ctx.stream, pull_grid, st, p, m, lv, out); break;
-                case 4: launch_pull_g<4>(ctx.stream, pull_grid, st, p, m, lv, out); break;
-                default: launch_pull_g<8>(ctx.stream, pull_grid, st, p, m, lv, out); break;
+                case 1: launch_pull_g<1>(ctx.stream, pull_grid, st, p, m, fm, lv, out); break;
+                case 2: launch_pull_g<2>(ctx.stream, pull_grid, st, p, m, fm, lv, out); break;
+                case 4: launch_pull_g<4>(ctx.stream, pull_grid, st, p, m, fm, lv, out); break;
+                default: launch_pull_g<8>(ctx.stream, pull_grid, st, p, m, fm, lv, out); break;
             }
+            bfs_fmask_kernel<<<fm_grid, 256, 0, ctx.stream>>>(st, p, P.f[p].as<int32_t>(), fm, 0);
             bfs_account_kernel<<<1, 32, 0, ctx.stream>>>(st, p);
         }
         ADA_CUDA(cudaGetLastError());
@@ -521,7 +543,7 @@ void bfs_graph(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, i
     int64_t replays = 0;
     for (;;) {
         ADA_CUDA(cudaGraphLaunch(P.exec, ctx.stream));
-        ctx.launches += kUnroll * 7;
+        ctx.launches += kUnroll * 9;
         ++replays;
         copy_scalars_kernel_launch(ctx, reinterpret_cast<const int64_t*>(st), ctx.h_scalars_dev,
                                    static_cast<int>(sizeof(BfsState) / sizeof(int64_t)));

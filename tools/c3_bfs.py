@@ -1,5 +1,5 @@
-"""C3 BFS timing (bench.py's configs.C3 without the CPU reference), device
-loop vs host loop:   python tools/c3_bfs.py [--host-loop]"""
+"""C3 BFS timing (bench.py's configs.C3 without the CPU reference), host
+loop (default) vs the captured device loop:   python tools/c3_bfs.py [--device-loop]"""
 import json
 import sys
 from pathlib import Path
@@ -9,12 +9,12 @@ import bench  # noqa: E402
 from paper_2006_16767_b200 import adaspmv as A  # noqa: E402
 from paper_2006_16767_b200 import selector as S  # noqa: E402
 
-if "--host-loop" in sys.argv:
+if "--device-loop" in sys.argv:
     _orig = A.Context.__init__
 
     def _init(self, *a, **k):
         _orig(self, *a, **k)
-        self.set_bfs_loop(True)
+        self.set_bfs_loop(False)
     A.Context.__init__ = _init
 hbm, _ = bench.peaks()
 r = bench.ours_c3(0, A.SelectorBundle.load(S.DEFAULT_PATH), hbm, cpu=False)
