@@ -396,6 +396,44 @@ int adaspmv_pagerank(adaspmv_ctx* ctx, const adaspmv_matrix* m, double damping, 
                      int64_t max_iters, const adaspmv_bundle* b, int forced_kernel, double* rank,
                      int64_t* n_iters, adaspmv_iteration_report* reports, int64_t max_reports);
 
+/* ---- row-partitioned mode, one process per GPU ----------- */
+/* Rank g of `world` holds the row block [cuts[g], cuts[g+1]) of the matrix
+ * (adaspmv_shard_rows) as its own adaspmv_matrix on its context's device
+ * (all n columns, so every kernel runs locally and each rank selects its own
+ * kernel: nnz_s differs per block).  The library performs the exchanges on
+ * the context's stream, device to device:
+ *   x broadcast from a root rank (adaspmv_dist_bcast_vector),
+ *   the y blocks into a full y on every rank (adaspmv_dist_allgather_output),
+ *   the BFS frontier lists all-gathered every level (adaspmv_dist_bfs).
+ * Transport: NCCL (adaspmv_dist_create_nccl; rank 0 makes the id with
+ * adaspmv_dist_unique_id and the caller hands it to every rank, e.g. over
+ * torch.distributed; NVLink / NVSwitch between B200s), or the caller's host
+ * all-gather (adaspmv_dist_create_host: tests, ranks sharing a GPU).
+ * Collective: every rank makes the same sequence of dist calls. */
+typedef struct adaspmv_dist adaspmv_dist;
+/* Host all-gather: every rank contributes `nbytes` (the same on all ranks);
+ * recv gets world * nbytes in rank order.  Returns 0 on success. */
+typedef int (*adaspmv_allgather_fn)(void* user, const void* send, int64_t nbytes, void* recv);
+int adaspmv_dist_unique_id(void* id128);  /* ncclUniqueId, 128 bytes */
+int adaspmv_dist_create_nccl(adaspmv_ctx* ctx, int rank, int world, const void* id128, adaspmv_dist** out);
+int adaspmv_dist_create_host(adaspmv_ctx* ctx, int rank, int world, adaspmv_allgather_fn fn, void* user,
+                             adaspmv_dist** out);
+int adaspmv_dist_destroy(adaspmv_dist* d);
+/* x of rank `root` (set sparse or dense) into x of every rank (same length). */
+int adaspmv_dist_bcast_vector(adaspmv_dist* d, adaspmv_vector* x, int root);
+/* Every rank's dense y block, in rank order, into y_full (device, sum of the
+ * blocks' rows values); *total gets that sum. */
+int adaspmv_dist_allgather_output(adaspmv_dist* d, adaspmv_output* y, void* y_full_device, int64_t* total);
+/* BFS (as adaspmv_bfs) over the square matrix whose rows row0 .. row0 +
+ * rows(block) - 1 this rank holds; every level each rank multiplies its block
+ * with its own kernel choice (bundle / forced / heuristic, decided on its
+ * block), forms the next frontier among its rows and the frontier lists are
+ * all-gathered.  levels (optional) gets this rank's rows' levels; n_levels
+ * and reports (this rank's levels) as adaspmv_bfs. */
+int adaspmv_dist_bfs(adaspmv_dist* d, const adaspmv_matrix* block, int64_t row0, int64_t source, int semiring,
+                     const adaspmv_bundle* b, int forced_kernel, int64_t* levels, int64_t* n_levels,
+                     adaspmv_iteration_report* reports, int64_t max_reports);
+
 #ifdef __cplusplus
 }
 #endif

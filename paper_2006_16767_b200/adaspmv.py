@@ -120,6 +120,8 @@ class _HostResult(C.Structure):
 RESULT_DENSE, RESULT_SPARSE, RESULT_AUTO = 0, 1, 2
 
 _lib = None
+# adaspmv_allgather_fn (host transport of the dist mode)
+_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 
 
 def load(path: Optional[os.PathLike] = None):
@@ -195,6 +197,13 @@ def load(path: Optional[os.PathLike] = None):
         "adaspmv_multi_cuts": [vp, vp],
         "adaspmv_multi_run": [vp, vp, C.c_int, vp, i64, vp, vp, vp, vp],
         "adaspmv_multi_destroy": [vp],
+        "adaspmv_dist_unique_id": [vp],
+        "adaspmv_dist_create_nccl": [vp, C.c_int, C.c_int, vp, P(vp)],
+        "adaspmv_dist_create_host": [vp, C.c_int, C.c_int, _ALLGATHER_FN, vp, P(vp)],
+        "adaspmv_dist_destroy": [vp],
+        "adaspmv_dist_bcast_vector": [vp, vp, C.c_int],
+        "adaspmv_dist_allgather_output": [vp, vp, vp, P(i64)],
+        "adaspmv_dist_bfs": [vp, vp, i64, i64, C.c_int, vp, C.c_int, vp, P(i64), vp, i64],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -998,6 +1007,87 @@ class MultiMatrix:
     def close(self):
         if getattr(self, "h", None) and _lib is not None:
             _lib.adaspmv_multi_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dist_unique_id() -> bytes:
+    """adaspmv_dist_unique_id: a fresh ncclUniqueId (128 bytes) for rank 0 to share."""
+    load()
+    buf = (C.c_char * 128)()
+    _check(_lib.adaspmv_dist_unique_id(buf))
+    return bytes(buf)
+
+
+class Dist:
+    """adaspmv_dist: the exchange of the row-partitioned mode with one process
+    per GPU.  `Dist.nccl(ctx, rank, world, uid)` is the
+    product transport (NCCL over NVLink); `Dist.host(ctx, rank, world,
+    allgather)` routes the exchange through a host callable
+    `allgather(bytes) -> list[bytes]` (every rank's contribution, rank order),
+    e.g. torch.distributed over gloo -- tests, and ranks sharing one GPU."""
+
+    def __init__(self, ctx: Context, rank: int, world: int, h, keep=None):
+        self.ctx, self.rank, self.world, self.h, self._keep = ctx, int(rank), int(world), h, keep
+
+    @classmethod
+    def nccl(cls, ctx: Context, rank: int, world: int, uid: bytes) -> "Dist":
+        if len(uid) != 128:
+            raise InvalidArgument("dist: the NCCL unique id is 128 bytes")
+        buf = (C.c_char * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(_lib.adaspmv_dist_create_nccl(ctx.h, int(rank), int(world), buf, C.byref(h)))
+        return cls(ctx, rank, world, h)
+
+    @classmethod
+    def host(cls, ctx: Context, rank: int, world: int, allgather) -> "Dist":
+        def cb(_user, send, nbytes, recv):
+            try:
+                mine = C.string_at(send, nbytes) if nbytes > 0 else b""
+                parts = allgather(mine)
+                blob = b"".join(parts)
+                if len(blob) != nbytes * world:
+                    return 1
+                if nbytes > 0:
+                    C.memmove(recv, blob, len(blob))
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to the library as a failed exchange
+                return 1
+        fn = _ALLGATHER_FN(cb)
+        h = C.c_void_p()
+        _check(_lib.adaspmv_dist_create_host(ctx.h, int(rank), int(world), fn, None, C.byref(h)))
+        return cls(ctx, rank, world, h, keep=fn)
+
+    def bcast_vector(self, x: "DeviceVector", root: int = 0):
+        _check(_lib.adaspmv_dist_bcast_vector(self.h, x.h, int(root)))
+        return x
+
+    def allgather_output(self, y: "MultiplyOutput", y_full_ptr: int) -> int:
+        """Every rank's dense y block into the device buffer at y_full_ptr."""
+        tot = C.c_int64()
+        _check(_lib.adaspmv_dist_allgather_output(self.h, y.h, C.c_void_p(y_full_ptr), C.byref(tot)))
+        return tot.value
+
+    def bfs(self, block: DualMatrix, row0: int, source: int = 0, semiring: int = OR_AND,
+            bundle: Optional["SelectorBundle"] = None, force_kernel: int = -1, max_reports: int = 4096,
+            download_levels: bool = True):
+        """-> (levels of this rank's rows or None, this rank's per-level reports)."""
+        levels = np.empty(block.rows(), np.int64) if download_levels else None
+        nl = C.c_int64()
+        reps = (_IterReport * max_reports)()
+        _check(_lib.adaspmv_dist_bfs(self.h, block.h, int(row0), int(source), int(semiring),
+                                     bundle.h if bundle else None, int(force_kernel), _ptr(levels),
+                                     C.byref(nl), C.cast(reps, C.c_void_p), max_reports))
+        return levels, _reports(reps, nl.value, max_reports)
+
+    def close(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.adaspmv_dist_destroy(self.h)
             self.h = None
 
     def __del__(self):

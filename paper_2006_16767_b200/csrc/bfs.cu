@@ -24,11 +24,6 @@ using clk = std::chrono::steady_clock;
 
 double secs(clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); }
 
-__global__ void init_levels_kernel(int32_t* lv, int64_t n, int64_t source) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i < n) lv[i] = i == source ? 0 : -1;
-}
-
 __global__ void widen_levels_kernel(const int32_t* __restrict__ lv, int64_t n, int64_t* __restrict__ out) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i < n) out[i] = lv[i];
@@ -86,14 +81,33 @@ struct FrontierEpi {
 
 __global__ void set_i64_kernel(int64_t* p, int64_t v) { *p = v; }
 
+// row block -> global vertex ids (dist BFS: the block's rows start at row0)
+__global__ void add_offset_kernel(int32_t* __restrict__ ids, int64_t n, int64_t off) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) ids[i] = static_cast<int32_t>(ids[i] + off);
+}
+
+template <class V>
+__global__ void fill_kernel(V* __restrict__ p, int64_t n, V v) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void init_block_levels_kernel(int32_t* lv, int64_t nr, int64_t src_local) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < nr) lv[i] = i == src_local ? 0 : -1;
+}
+
 template <class V, int SR>
-int64_t next_frontier(Context& ctx, const Matrix& m, Output& y, Vector& x, int32_t* lv, int32_t level) {
+int64_t next_frontier(Context& ctx, const Matrix& m, Output& y, Vector& x, int32_t* lv, int32_t level,
+                      bool local_ids = false) {
     x.invalidate();
     int32_t* xi = static_cast<int32_t*>(x.sp_idx.ensure(sizeof(int32_t) * static_cast<size_t>(x.n)));
     V* xv = static_cast<V*>(x.sp_val.ensure(sizeof(V) * static_cast<size_t>(x.n)));
     const V value = SR == SR_MIN_PLUS ? V(level) : V(1);
     // fused nnz_s / eff offsets when the packing cannot overflow (x.n = cols)
-    const bool fused = m.nnz < (int64_t(1) << kCntShift) && x.n < (int64_t(1) << (63 - kCntShift));
+    // and the row ids are the column ids (not on a row block: local_ids)
+    const bool fused = !local_ids && m.nnz < (int64_t(1) << kCntShift) && x.n < (int64_t(1) << (63 - kCntShift));
     const int64_t* co = fused ? m.col_off.as<int64_t>() : nullptr;
     int64_t* eff = fused ? static_cast<int64_t*>(x.eff.ensure(sizeof(int64_t) * static_cast<size_t>(x.n + 1))) : nullptr;
     if (y.has_sparse) {
@@ -246,15 +260,51 @@ int heuristic_kernel(Context& ctx, const Matrix& m, Vector& x, int64_t visited) 
     return 2;
 }
 
+// The frontier this rank formed among its rows (block-local ids in
+// x.sp_idx[0 .. x.nnz)) -> the global frontier: ids shifted to vertex ids,
+// every rank's list all-gathered in rank order (= ascending vertex order:
+// blocks are contiguous), values refilled.  Returns the global size.
+template <class V>
+int64_t gather_frontier(Context& ctx, Dist& d, Vector& x, int64_t row0, V value, DevBuf& gathered) {
+    const int64_t cnt = std::max<int64_t>(x.nnz, 0);
+    if (cnt > 0 && row0 != 0) {
+        add_offset_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, ctx.stream>>>(x.sp_idx.as<int32_t>(),
+                                                                                           cnt, row0);
+        ADA_LAUNCHED(ctx);
+    }
+    gathered.ensure(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(x.n, 1)));
+    const int64_t total = d.allgatherv(x.sp_idx.p, cnt, sizeof(int32_t), gathered.p);
+    x.invalidate();
+    std::swap(x.sp_idx.p, gathered.p);
+    std::swap(x.sp_idx.cap, gathered.cap);
+    std::swap(x.sp_idx.s, gathered.s);
+    V* xv = static_cast<V*>(x.sp_val.ensure(sizeof(V) * static_cast<size_t>(std::max<int64_t>(x.n, 1))));
+    if (total > 0) {
+        fill_kernel<V><<<static_cast<unsigned>((total + 255) / 256), 256, 0, ctx.stream>>>(xv, total, value);
+        ADA_LAUNCHED(ctx);
+    }
+    x.nnz = total;
+    x.has_sparse = true;
+    return total;
+}
+
+// Level-synchronous BFS.  dist == nullptr: the whole
+// square matrix on this device.  dist != nullptr: m is the row block
+// [row0, row0 + m.rows) of an m.cols-vertex graph; levels
+// and the kernel decisions are per block, the frontier is exchanged.
 template <class V, int SR>
 void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int forced,
            int64_t* levels, int64_t* n_levels, adaspmv_iteration_report* reports,
-           int64_t max_reports) {
-    const int64_t n = m.rows;
-    DevBuf lvb;
-    int32_t* lv = static_cast<int32_t*>(lvb.ensure(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(n, 1))));
-    init_levels_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx.stream>>>(lv, n, source);
-    ADA_LAUNCHED(ctx);
+           int64_t max_reports, Dist* dist = nullptr, int64_t row0 = 0) {
+    const int64_t n = m.cols;   // vertices (= rows of the whole matrix)
+    const int64_t nr = m.rows;  // rows held here
+    DevBuf lvb, gathered;
+    int32_t* lv = static_cast<int32_t*>(lvb.ensure(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(nr, 1))));
+    const int64_t src_local = source - row0;  // outside [0, nr): another rank's row
+    if (nr > 0) {
+        init_block_levels_kernel<<<static_cast<unsigned>((nr + 255) / 256), 256, 0, ctx.stream>>>(lv, nr, src_local);
+        ADA_LAUNCHED(ctx);
+    }
     Vector x;
     x.ctx = &ctx;
     x.n = n;
@@ -276,7 +326,7 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
     adaspmv_config cfg{};
     cfg.semiring = SR;
     int64_t it = 0;
-    int64_t visited = 1;
+    int64_t visited = src_local >= 0 && src_local < nr ? 1 : 0;  // of this block's rows
     // device-side phase timing without extra synchronisation: events around
     // the conversion and the multiply, read after the frontier-size fetch
     cudaEvent_t ev[3];
@@ -320,15 +370,16 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
         }
         ADA_CUDA(cudaEventRecord(ev[1], ctx.stream));
         const int64_t nnz_x = x.nnz;
+        const V value = SR == SR_MIN_PLUS ? V(it + 1) : V(1);  // as next_frontier writes
         if (push) {  // multiply + frontier update in one pass (syncs)
-            const V value = SR == SR_MIN_PLUS ? V(it + 1) : V(1);  // as next_frontier writes
             visited += push_level<V>(ctx, m, x, lv, static_cast<int32_t>(it + 1), value, next_idx, next_val, ev[2]);
         } else {
             if (pull) launch_pull<V, SR>(ctx, m, x, lv, y);  // row-major, output-masked
             else run_kernel(ctx, m, x, k, cfg, y);
             ADA_CUDA(cudaEventRecord(ev[2], ctx.stream));
-            visited += next_frontier<V, SR>(ctx, m, y, x, lv, static_cast<int32_t>(it + 1));  // syncs
+            visited += next_frontier<V, SR>(ctx, m, y, x, lv, static_cast<int32_t>(it + 1), dist != nullptr);
         }
+        if (dist) gather_frontier<V>(ctx, *dist, x, row0, value, gathered);  // the next x on every rank
         if (reports && it < max_reports) {
             float c_ms = 0, k_ms = 0;
             ADA_CUDA(cudaEventElapsedTime(&c_ms, ev[0], ev[1]));
@@ -349,10 +400,11 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
     if (!levels) return;  // traversal only (levels stay on the device)
     // widen on the device, one D2H of the caller's int64 array
     DevBuf l64;
-    int64_t* d64 = static_cast<int64_t*>(l64.ensure(sizeof(int64_t) * static_cast<size_t>(std::max<int64_t>(n, 1))));
-    widen_levels_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx.stream>>>(lv, n, d64);
+    if (nr <= 0) return;
+    int64_t* d64 = static_cast<int64_t*>(l64.ensure(sizeof(int64_t) * static_cast<size_t>(nr)));
+    widen_levels_kernel<<<static_cast<unsigned>((nr + 255) / 256), 256, 0, ctx.stream>>>(lv, nr, d64);
     ADA_LAUNCHED(ctx);
-    ADA_CUDA(cudaMemcpyAsync(levels, d64, sizeof(int64_t) * static_cast<size_t>(n), cudaMemcpyDeviceToHost,
+    ADA_CUDA(cudaMemcpyAsync(levels, d64, sizeof(int64_t) * static_cast<size_t>(nr), cudaMemcpyDeviceToHost,
                              ctx.stream));
     ctx.sync();
 }
@@ -389,6 +441,30 @@ void bfs(Context& ctx, const Matrix& m, int64_t source, int semiring, const Bund
         case ADASPMV_MIN_PLUS:
             f64 ? bfs_t<double, SR_MIN_PLUS>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports)
                 : bfs_t<float, SR_MIN_PLUS>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports);
+            break;
+        default: invalid("unknown semiring");
+    }
+}
+
+void bfs_dist(Context& ctx, const Matrix& m, Dist& d, int64_t row0, int64_t source, int semiring, const Bundle* b,
+              int forced, int64_t* levels, int64_t* n_levels, adaspmv_iteration_report* reports,
+              int64_t max_reports) {
+    if (row0 < 0 || row0 + m.rows > m.cols) invalid("dist_bfs: the row block is outside the square matrix");
+    if (source < 0 || source >= m.cols) invalid("bfs: source out of range");
+    if (forced < -1 || forced > 7) invalid("bfs: forced kernel out of range");
+    const bool f64 = m.dtype == ADASPMV_F64;
+    switch (semiring) {
+        case ADASPMV_PLUS_TIMES:
+            f64 ? bfs_t<double, SR_PLUS_TIMES>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports, &d, row0)
+                : bfs_t<float, SR_PLUS_TIMES>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports, &d, row0);
+            break;
+        case ADASPMV_OR_AND:
+            f64 ? bfs_t<double, SR_OR_AND>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports, &d, row0)
+                : bfs_t<float, SR_OR_AND>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports, &d, row0);
+            break;
+        case ADASPMV_MIN_PLUS:
+            f64 ? bfs_t<double, SR_MIN_PLUS>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports, &d, row0)
+                : bfs_t<float, SR_MIN_PLUS>(ctx, m, source, b, forced, levels, n_levels, reports, max_reports, &d, row0);
             break;
         default: invalid("unknown semiring");
     }

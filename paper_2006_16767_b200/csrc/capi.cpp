@@ -23,6 +23,7 @@ struct adaspmv_vector : ada::Vector {};
 struct adaspmv_output : ada::Output {};
 struct adaspmv_bundle : ada::Bundle {};
 struct adaspmv_multi : ada::Multi {};
+struct adaspmv_dist : ada::Dist {};
 
 namespace {
 
@@ -1045,6 +1046,74 @@ int adaspmv_pagerank(adaspmv_ctx* ctx, const adaspmv_matrix* m, double damping, 
         need(m, "matrix");
         need(n_iters, "n_iters");
         ada::pagerank(*ctx, *m, damping, prune, max_iters, b, forced_kernel, rank, n_iters, reports,
+                      max_reports);
+    });
+}
+
+// ---- row-partitioned mode, one process per GPU (dist.cpp) ------------------
+int adaspmv_dist_unique_id(void* id128) {
+    return guarded([&] {
+        need(id128, "id");
+        ada::dist_unique_id(id128);
+    });
+}
+
+int adaspmv_dist_create_nccl(adaspmv_ctx* ctx, int rank, int world, const void* id128, adaspmv_dist** out) {
+    return guarded([&] {
+        bind(ctx);
+        need(id128, "id");
+        need(out, "out");
+        *out = static_cast<adaspmv_dist*>(ada::dist_create_nccl(*ctx, rank, world, id128));
+    });
+}
+
+int adaspmv_dist_create_host(adaspmv_ctx* ctx, int rank, int world, adaspmv_allgather_fn fn, void* user,
+                             adaspmv_dist** out) {
+    return guarded([&] {
+        bind(ctx);
+        need(out, "out");
+        *out = static_cast<adaspmv_dist*>(ada::dist_create_host(*ctx, rank, world, fn, user));
+    });
+}
+
+int adaspmv_dist_destroy(adaspmv_dist* d) {
+    if (!d) return ADASPMV_OK;
+    return guarded([&] {
+        bind(d->ctx);
+        delete static_cast<ada::Dist*>(d);
+    });
+}
+
+int adaspmv_dist_bcast_vector(adaspmv_dist* d, adaspmv_vector* x, int root) {
+    return guarded([&] {
+        need(d, "dist");
+        need(x, "vector");
+        bind(d->ctx);
+        if (x->ctx != d->ctx) ada::invalid("dist_bcast_vector: the vector belongs to another context");
+        ada::dist_bcast_vector(*d, *x, root);
+    });
+}
+
+int adaspmv_dist_allgather_output(adaspmv_dist* d, adaspmv_output* y, void* y_full_device, int64_t* total) {
+    return guarded([&] {
+        need(d, "dist");
+        need(y, "output");
+        need(y_full_device, "y_full");
+        bind(d->ctx);
+        const int64_t t = ada::dist_allgather_output(*d, *y, y_full_device);
+        if (total) *total = t;
+    });
+}
+
+int adaspmv_dist_bfs(adaspmv_dist* d, const adaspmv_matrix* block, int64_t row0, int64_t source, int semiring,
+                     const adaspmv_bundle* b, int forced_kernel, int64_t* levels, int64_t* n_levels,
+                     adaspmv_iteration_report* reports, int64_t max_reports) {
+    return guarded([&] {
+        need(d, "dist");
+        need(block, "matrix");
+        need(n_levels, "n_levels");
+        bind(d->ctx);
+        ada::bfs_dist(*d->ctx, *block, *d, row0, source, semiring, b, forced_kernel, levels, n_levels, reports,
                       max_reports);
     });
 }

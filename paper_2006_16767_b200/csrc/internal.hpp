@@ -277,6 +277,27 @@ struct Multi {
     std::vector<std::unique_ptr<MultiShard>> shards;
 };
 
+// The one-process-per-GPU row-partitioned mode's exchange (dist.cpp): NCCL
+// communicator, or the caller's host all-gather callback.
+struct Dist {
+    Context* ctx = nullptr;
+    int rank = 0, world = 1;
+    void* comm = nullptr;  // ncclComm_t
+    adaspmv_allgather_fn host_fn = nullptr;
+    void* host_user = nullptr;
+    std::vector<int64_t> counts;  // per-rank counts of the last allgatherv
+    DevBuf d_cnt;
+    std::vector<char> h_send, h_recv;
+    ~Dist();
+    void host_allgather(const void* send, size_t bytes, void* recv);
+    // every rank's `mine` (host; synchronises)
+    void allgather_count(int64_t mine, std::vector<int64_t>& all);
+    // concatenation in rank order of every rank's `count` elements of `elem`
+    // bytes into the device buffer `recv`; returns the total count
+    int64_t allgatherv(const void* send, int64_t count, size_t elem, void* recv);
+    void broadcast(void* buf, int64_t bytes, int root);
+};
+
 // One decision tree: flat node array.
 struct Tree {
     int target = 0;          // 0 pattern, 1 workload, 2 write-back
@@ -369,6 +390,17 @@ void run_kernel(Context& ctx, const Matrix& m, Vector& x, int kernel, const adas
 // binned K0/K2 (kernels_binned.cu)
 double matrix_gather_spread(Context& ctx, const Matrix& m);
 bool binned_preferred(const Matrix& m);
+// dist.cpp
+void dist_unique_id(void* out128);
+Dist* dist_create_nccl(Context& ctx, int rank, int world, const void* id128);
+Dist* dist_create_host(Context& ctx, int rank, int world, adaspmv_allgather_fn fn, void* user);
+void dist_bcast_vector(Dist& d, Vector& x, int root);
+int64_t dist_allgather_output(Dist& d, Output& y, void* y_full);
+// bfs.cu: BFS over a row block of a square matrix (rows row0 .. row0 +
+// m.rows - 1 of an m.cols x m.cols graph), frontiers exchanged through `d`
+void bfs_dist(Context& ctx, const Matrix& m, Dist& d, int64_t row0, int64_t source, int semiring, const Bundle* b,
+              int forced, int64_t* levels, int64_t* n_levels, adaspmv_iteration_report* reports,
+              int64_t max_reports);
 void output_ensure_dense(Context& ctx, Output& y);
 void output_ensure_sparse(Context& ctx, Output& y);
 int64_t output_nnz(Context& ctx, Output& y);

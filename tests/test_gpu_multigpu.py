@@ -1,6 +1,7 @@
-"""GPU: the row-partitioned mode's CUDA shard on one device (world size 1 over
-NCCL) -- the broadcast lands in device buffers handed to the library by
-pointer, y comes back as a torch view of the library's output."""
+"""GPU: paper_2006_16767_b200/multigpu.py on one device over the NCCL backend
+(world size 1): the library's NCCL transport (uid handed over by
+torch.distributed), x broadcast into the library's operand, per-rank
+selection, y all-gathered into a device tensor, and the library's dist BFS."""
 import os
 import socket
 
@@ -11,6 +12,7 @@ import torch.distributed as dist
 
 from paper_2006_16767_b200 import adaspmv as A
 from paper_2006_16767_b200 import multigpu as MG
+from paper_2006_16767_b200 import selector as S
 from paper_2006_16767_b200 import synth
 from tests.util import assert_dense_close, ref_and_bound
 
@@ -30,24 +32,25 @@ def pg():
     dist.destroy_process_group()
 
 
-def test_cuda_shard_multiply_and_bfs(pg, port):
+def test_row_block_matrix_nccl_world1(pg, port):
     rows, cols, ro, ci, vals = synth.random_csr(3000, 2500, 0.004, seed=3, dtype=np.float32)
+    bundle = A.SelectorBundle.load(S.DEFAULT_PATH)
+    rp = MG.RowBlockMatrix(rows, cols, ro, ci, vals, 0, bundle=bundle)
+    xd = np.random.default_rng(1).uniform(-1, 1, cols).astype(np.float32)
+    y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, xd)
+    xi, xv = synth.sparse_vector(cols, 40, seed=2, dtype=np.float32)
+    ys_ref, sbound = ref_and_bound(port, rows, ro, ci, vals, port.sparse_to_dense(cols, xi, xv))
     for kernel in (None, 1, 4, 7):
-        rp = MG.RowPartitioned.create(rows, cols, ro, ci, vals,
-                                      lambda r, c, a, b, v: MG.CudaShard(r, c, a, b, v, 0, kernel=kernel),
-                                      "cuda")
-        xd = np.random.default_rng(1).uniform(-1, 1, cols).astype(np.float32)
-        y = rp.multiply(x_dense=xd, gather=True).cpu().numpy()
-        y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, xd)
+        y = rp.multiply(x_dense=xd, gather=True, kernel=kernel).cpu().numpy()
         assert_dense_close(y, y_ref, bound, np.float32, f"dense kernel={kernel}")
-        xi, xv = synth.sparse_vector(cols, 40, seed=2, dtype=np.float32)
-        y = rp.multiply(x_sparse=(xi, xv)).cpu().numpy()
-        y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, port.sparse_to_dense(cols, xi, xv))
-        assert_dense_close(y, y_ref, bound, np.float32, f"sparse kernel={kernel}")
-    n, _, gro, gci, gv = synth.rmat(11, 8, seed=5)
-    g = MG.RowPartitioned.create(n, n, gro, gci, gv, lambda r, c, a, b, v: MG.CudaShard(r, c, a, b, v, 0, kernel=3),
-                                 "cuda")
-    levels, _ = g.bfs(0, A.OR_AND)
+        y = rp.multiply(x_sparse=(xi, xv), kernel=kernel).cpu().numpy()
+        assert_dense_close(y, ys_ref, sbound, np.float32, f"sparse kernel={kernel}")
+    rp.close()
+    n, _, gro, gci, _ = synth.rmat(11, 8, seed=5)
+    g = MG.RowBlockMatrix(n, n, gro, gci, None, 0, dtype=np.float32)
     co, ri, _ = port.csr_to_csc(n, n, gro, gci, np.ones(len(gci)))
-    exp, _ = port.bfs_queue(n, co, ri, 0)
-    assert np.array_equal(levels, exp)
+    exp, nl = port.bfs_queue(n, co, ri, 0)
+    for kernel in (-1, 3, 6):
+        levels, nl2, _ = g.bfs(0, A.OR_AND, kernel=kernel)
+        assert np.array_equal(levels, exp) and nl2 == nl, kernel
+    g.close()

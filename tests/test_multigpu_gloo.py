@@ -1,13 +1,24 @@
-"""CPU, world size 2 over gloo: the row-partitioned mode's partition and
-exchange logic (broadcast of dense / sparse x, all_gatherv of y blocks and of
-BFS frontiers).  The local compute is an oracle-backed stand-in for the CUDA
-shard (test infrastructure only); the GPU shard is covered by -m gpu tests."""
+"""CPU, world size 2 over gloo: the host side of the row-partitioned mode
+(paper_2006_16767_b200/multigpu.py, csrc/dist.cpp) without a GPU:
+
+* the nnz-balanced row cut (adaspmv_shard_rows, host C-ABI: the segment_of
+  search of partition.hpp:30-33 snapped to row starts) is the same on every
+  rank, covers every row once and is balanced;
+* `host_allgather`, the adaspmv_allgather_fn contract the library's host
+  transport calls (every rank's bytes in rank order), over the process group;
+* the exchange protocol of adaspmv_dist_bfs restated with the oracle as the
+  local compute (test infrastructure): every rank multiplies its row block
+  with the replicated frontier, keeps its newly reached rows, and the
+  frontier lists are all-gathered in rank order -- the levels equal a queue
+  BFS and the gathered frontier is sorted (SparseVector order,
+  sparse.hpp:113-130).  The CUDA path of the same protocol is
+  tests/test_gpu_dist.py."""
 import os
+import pickle
 import socket
 
 import numpy as np
 import pytest
-import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
@@ -22,68 +33,60 @@ def _free_port():
     return p
 
 
-class OracleShard:
-    def __init__(self, rows, cols, ro, ci, vals):
-        from oracle.oracle import Port
-        self.port = Port()
-        self.rows, self.cols, self.ro, self.ci, self.vals = rows, cols, ro, ci, vals
-        self.dtype = vals.dtype
-        self.co, self.ri, self.cv = self.port.csr_to_csc(rows, cols, ro, ci, vals)
-
-    def multiply(self, xi, xv, semiring=0):
-        xv = xv.cpu().numpy().astype(self.dtype)
-        if xi is None:
-            xd = xv
-        else:
-            xd = self.port.sparse_to_dense(self.cols, xi.cpu().numpy().astype(np.int64), xv)
-        if semiring == 2:  # min-plus on a pattern matrix: y_i = min_j (x_j + 1)
-            y = np.full(self.rows, np.inf)
-            for r in range(self.rows):
-                for k in range(self.ro[r], self.ro[r + 1]):
-                    c = self.ci[k]
-                    if np.isfinite(xd[c]) and (xi is None or c in set(xi.tolist())):
-                        y[r] = min(y[r], xd[c] + self.vals[k])
-            return torch.as_tensor(y.astype(self.dtype))
-        y = self.port.reference_multiply(self.rows, self.ro, self.ci, self.vals, xd)
-        return torch.as_tensor(y)
-
-
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2006_16767_b200 import multigpu as MG
         from oracle.oracle import Port
-        port_ = Port()
-        rows, cols, ro, ci, vals = synth.random_csr(300, 300, 0.03, seed=5, dtype=np.float64)
-        rp = MG.RowPartitioned.create(rows, cols, ro, ci, vals, OracleShard, "cpu")
-        # dense x from root 0, full y gathered
-        xd = np.random.default_rng(1).uniform(-1, 1, cols)
-        y = rp.multiply(x_dense=xd if rank == 0 else None, gather=True).numpy()
-        ref = port_.reference_multiply(rows, ro, ci, vals, xd)
-        ok_dense = np.allclose(y, ref, rtol=0, atol=1e-12)
-        # sparse x from root 1, local blocks only
-        xi, xv = synth.sparse_vector(cols, 20, seed=3)
-        yb = rp.multiply(x_sparse=(xi, xv) if rank == 1 else None, root=1).numpy()
-        r0, r1 = rp.row_range
-        ref2 = port_.reference_multiply(rows, ro, ci, vals, port_.sparse_to_dense(cols, xi, xv))[r0:r1]
-        ok_sparse = np.allclose(yb, ref2, rtol=0, atol=1e-12)
-        # BFS on a symmetric pattern graph vs a queue BFS
-        n, _, gro, gci, gv = synth.rmat(9, 8, seed=4)
-        g = MG.RowPartitioned.create(n, n, gro, gci, gv.astype(np.float64), OracleShard, "cpu")
-        levels, nl = g.bfs(0, semiring=1)
-        co, ri, _ = port_.csr_to_csc(n, n, gro, gci, np.ones(len(gci)))
-        exp, _ = port_.bfs_queue(n, co, ri, 0)
-        ok_bfs = np.array_equal(levels, exp)
-        balanced = abs(int(ro[rp.cuts[1]]) - int(ro[-1]) // 2) <= int(np.diff(ro).max())
-        q.put((rank, ok_dense, ok_sparse, ok_bfs, balanced))
+        from paper_2006_16767_b200 import multigpu as MG
+        P = Port()
+        # row cut
+        rows, cols, ro, ci, vals = synth.random_csr(500, 400, 0.02, seed=5, dtype=np.float64)
+        cuts = MG.shard_rows(ro, world)
+        all_cuts = MG.host_allgather(cuts.tobytes())
+        same = all(c == cuts.tobytes() for c in all_cuts)
+        covers = cuts[0] == 0 and cuts[-1] == rows and np.all(np.diff(cuts) >= 0)
+        share = np.diff(ro[cuts])
+        balanced = share.max() - share.min() <= 2 * int(np.diff(ro).max())
+        # the all-gather contract: rank order, byte-exact, equal sizes
+        got = MG.host_allgather(bytes([rank]) * 5)
+        contract = got == [bytes([r]) * 5 for r in range(world)]
+        # the dist BFS protocol with oracle blocks
+        n, _, gro, gci, _ = synth.rmat(9, 8, seed=4)
+        gc = MG.shard_rows(gro, world)
+        r0, r1 = int(gc[rank]), int(gc[rank + 1])
+        bro, bci, _ = MG.block(gro, gci, None, r0, r1)
+        bvals = np.ones(len(bci))
+        lv = np.full(r1 - r0, -1, np.int64)
+        src = 3
+        if r0 <= src < r1:
+            lv[src - r0] = 0
+        frontier = np.array([src], np.int64)
+        level, sorted_ok = 0, True
+        while len(frontier):
+            xd = np.zeros(n)
+            xd[frontier] = 1.0
+            y = P.reference_multiply(r1 - r0, bro, bci, bvals, xd)
+            new = np.nonzero((y != 0) & (lv < 0))[0]
+            level += 1
+            lv[new] = level
+            parts = MG.host_allgather(pickle.dumps(new + r0))
+            frontier = np.concatenate([pickle.loads(p) for p in parts]).astype(np.int64)
+            sorted_ok = sorted_ok and bool(np.all(np.diff(frontier) > 0))
+        full = np.concatenate([np.frombuffer(p, np.int64) for p in MG.host_allgather(lv.tobytes())])
+        co, ri, _ = P.csr_to_csc(n, n, gro, gci, np.ones(len(gci)))
+        exp, _ = P.bfs_queue(n, co, ri, src)
+        q.put((rank, bool(same), bool(covers), bool(balanced), bool(contract), bool(np.array_equal(full, exp)),
+               sorted_ok))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.timeout(300)
-def test_row_partitioned_gloo_world2():
+def test_row_partitioned_host_side_gloo_world2():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -93,8 +96,9 @@ def test_row_partitioned_gloo_world2():
     res = [q.get(timeout=240) for _ in procs]
     for p in procs:
         p.join(timeout=60)
-    for rank, a, b, c, d in res:
-        assert a, f"rank {rank}: dense multiply + all-gather mismatch"
-        assert b, f"rank {rank}: sparse broadcast block mismatch"
-        assert c, f"rank {rank}: BFS levels differ from queue BFS"
-        assert d, f"rank {rank}: row cut not nnz-balanced"
+    names = ("cuts identical on all ranks", "cuts cover the rows", "cut nnz-balanced", "all-gather contract",
+             "BFS levels == queue BFS", "gathered frontier sorted")
+    for r in res:
+        assert len(r) == 1 + len(names), r
+        for ok, what in zip(r[1:], names):
+            assert ok, f"rank {r[0]}: {what}"
