@@ -50,6 +50,23 @@ __device__ __forceinline__ double ld_stream(const double* p) {
     return r;
 }
 
+// four consecutive values (16-B aligned) in one or two 128-bit loads
+__device__ __forceinline__ void ld_stream4(const float* p, float (&a)[4]) {
+    const float4 v = ld_stream(reinterpret_cast<const float4*>(p));
+    a[0] = v.x;
+    a[1] = v.y;
+    a[2] = v.z;
+    a[3] = v.w;
+}
+__device__ __forceinline__ void ld_stream4(const double* p, double (&a)[4]) {
+    const double2 v0 = ld_stream(reinterpret_cast<const double2*>(p));
+    const double2 v1 = ld_stream(reinterpret_cast<const double2*>(p) + 1);
+    a[0] = v0.x;
+    a[1] = v0.y;
+    a[2] = v1.x;
+    a[3] = v1.y;
+}
+
 // KernelCounters (kernels.hpp:106-111) on the device, when the context asks
 // for them (adaspmv_ctx_set_counters): ctr[0] values_read = loads from the
 // matrix value array (kernels.hpp:108; every kernel loads a value exactly

@@ -136,8 +136,10 @@ constexpr int kRowTile = 256;
 
 // Row-bin layout of the binned K0/K2 execution (kernels_binned.cu): the CSC
 // order stably partitioned by bins of R rows; entry = (col & (2^cw-1)) <<
-// rbits | row - bin*R; chunk_off[b*nchunks + c] = first entry of bin b with
-// col >> cw == c ([nbins*nchunks] = nnz).  Tiles: CTA work units.
+// rbits | row - bin*R; each (bin, chunk = col >> cw) run padded to a multiple
+// of 128 entries (padding entry: row slot 2^rbits - 1, value 0) and stored
+// interleaved in 128-entry groups; chunk_off[b*nchunks + c] = first (padded)
+// entry of the run ([nbins*nchunks] = n_padded).  Tiles: CTA work units.
 struct BinLayout {
     bool built = false;
     int dtype = -1;
@@ -156,7 +158,7 @@ struct BinLayout {
     // heavy rows (degree > heavy_min) are left out of the bins (their entries
     // would serialise on one shared-memory slot) and run from the CSR as
     // segments of <= kHeavySeg entries: int64 (row, begin, end) triples
-    int64_t heavy_min = 0, nsegs = 0, n_light = 0;
+    int64_t heavy_min = 0, nsegs = 0, n_light = 0, n_padded = 0;
     DevBuf segs;
     DevBuf tiles, tile_bin, tile_multi;
 };

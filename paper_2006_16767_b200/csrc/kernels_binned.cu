@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <functional>
 #include <numeric>
 #include <vector>
@@ -101,17 +102,47 @@ __global__ void bin_expand_kernel(const int64_t* __restrict__ co, const int32_t*
     }
 }
 
+// Sorted position k (bins ascending, CSC order inside a bin) -> padded,
+// interleaved position: every (bin, chunk) run starts at a multiple of 128
+// entries (poff); inside a run, entry r of 128-group q lands at word
+// q*128 + (r % 32)*4 + r / 32 of that group, so lane l of a warp loads
+// entries {l, l+32, l+64, l+96} of the group as one 16-B word.
 template <class V>
-__global__ void bin_unpack_kernel(const PkVal<V>* __restrict__ pay, int64_t nnz,
-                                  uint32_t* __restrict__ pk, V* __restrict__ bv) {
-    const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+__global__ void bin_scatter_kernel(const PkVal<V>* __restrict__ pay, const uint32_t* __restrict__ keys,
+                                   int64_t nlight, int64_t nchunks, const int64_t* __restrict__ uoff,
+                                   const int64_t* __restrict__ poff, uint32_t* __restrict__ pk,
+                                   V* __restrict__ bv) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t k = i0; k < nnz; k += stride) {
-        const PkVal<V> p = pay[k];
-        pk[k] = p.pk;
-        bv[k] = p.val;
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nlight; k += stride) {
+        const int64_t b = keys[k];
+        const int64_t* u = uoff + b * nchunks;
+        int64_t lo = 0, hi = nchunks;  // chunk: largest c with u[c] <= k
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (u[mid] <= k) lo = mid;
+            else hi = mid;
+        }
+        const int64_t r = k - u[lo];
+        const int64_t dst = poff[b * nchunks + lo] + (r & ~int64_t(127)) + ((r & 31) << 2) + ((r >> 5) & 3);
+        const PkVal<V> v = pay[k];
+        pk[dst] = v.pk;
+        bv[dst] = v.val;
     }
 }
+
+template <class V>
+__global__ void bin_pad_fill_kernel(int64_t n, uint32_t pad, uint32_t* __restrict__ pk, V* __restrict__ bv) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n; k += stride) {
+        pk[k] = pad;
+        bv[k] = V(0);
+    }
+}
+
+struct PaddedCounts {
+    const unsigned long long* c;
+    __device__ int64_t operator()(int64_t i) const { return (static_cast<int64_t>(c[i]) + 127) & ~int64_t(127); }
+};
 
 struct U64Counts {
     const unsigned long long* c;
@@ -151,7 +182,7 @@ __global__ void gather_spread_kernel(const int64_t* __restrict__ ro, const int32
 // streamed through L2 and double the entries per x line (fewer L1
 // wavefronts per gather instruction).
 template <class V, int SR, bool MASKED, int CL = 1, int kBinUnroll = 8, bool NOALLOC = false,
-          int kBinThreads = 1024>
+          int kBinThreads = 1024, bool PIPE = false>
 __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
     int64_t tile0, const int64_t* __restrict__ bin_r0, int rbits, int cw, int64_t nchunks,
     const int64_t* __restrict__ tiles, const int32_t* __restrict__ tile_bin,
@@ -170,97 +201,123 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
     __syncthreads();
 
     const int64_t* __restrict__ co = chunk_off + bin * nchunks;
-    const uint32_t rmask = (1u << rbits) - 1u;
+    const uint32_t rmask = (1u << rbits) - 1u;  // row slot rmask marks a padding entry
+    unsigned n_used = 0;                        // entries consumed (KernelCounters)
     if (e0 < e1) {
-        // 32-bit entry offsets relative to the tile (a tile is < 2^32
-        // entries): the per-entry index, chunk and address arithmetic stays
-        // in 32-bit registers
-        const uint32_t n_e = static_cast<uint32_t>(e1 - e0);
-        if (!MASKED && threadIdx.x == 0) count_add(ctr, 0, n_e);  // every entry of the tile is consumed
-        const uint32_t* __restrict__ pkt = pk + e0;
-        const V* __restrict__ bvt = bv + e0;
-        // chunk of the thread's first entry: largest c with co[c] <= e (binary search)
-        const int64_t efirst = e0 + threadIdx.x;
-        int lo = 0, hi = static_cast<int>(nchunks);
+        // 128-entry groups: warp w takes groups g0 + w, g0 + w + NW, ...;
+        // lane l holds entries {l, l+32, l+64, l+96} of its group as one 16-B
+        // word, so warp instruction j of a group still gathers x for 32
+        // consecutive (column-sorted) entries.  Groups never straddle a chunk,
+        // so the chunk (high column bits) is walked once per group, warp-uniform.
+        constexpr int NW = kBinThreads / 32;
+        constexpr int GU = kBinUnroll / 4;  // groups per warp in flight
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int64_t g0 = e0 >> 7, g1 = e1 >> 7;
+        int lo = 0, hi = static_cast<int>(nchunks);  // chunk of the warp's first group
+        const int64_t efirst = (g0 + warp) << 7;
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
             if (__ldg(co + mid) <= efirst) lo = mid;
             else hi = mid;
         }
         int c = lo;
-        auto chunk_end = [&](int cc) -> uint32_t {  // end of chunk cc, tile-relative, clamped
-            const int64_t v = __ldg(co + cc + 1) - e0;
-            return v < static_cast<int64_t>(n_e) ? static_cast<uint32_t>(v) : n_e;
-        };
-        uint32_t nb = chunk_end(c);
-        uint32_t cbase = static_cast<uint32_t>(c) << cw;
-        constexpr uint32_t kStep = static_cast<uint32_t>(kBinThreads) * kBinUnroll;
-        auto load_batch = [&](uint32_t b, uint32_t* pp, V* aa) {
+        int64_t nb = __ldg(co + c + 1);
+        auto load_groups = [&](int64_t g, uint32_t (&p)[GU][4], V (&a)[GU][4], bool (&has)[GU]) {
 #pragma unroll
-            for (int j = 0; j < kBinUnroll; ++j) {
-                const uint32_t e = b + j * kBinThreads;
-                pp[j] = e < n_e ? static_cast<uint32_t>(ld_stream(reinterpret_cast<const int*>(pkt) + e)) : 0u;
-                // K2 loads a value only after its mask test (kernels.hpp:229-240)
-                if (S::kUsesValues && !MASKED) aa[j] = e < n_e ? ld_stream(bvt + e) : V(0);
-                else aa[j] = V(1);
+            for (int u = 0; u < GU; ++u) {
+                const int64_t gg = g + u * NW;
+                has[u] = gg < g1;
+                const int4 w = has[u] ? ld_stream(reinterpret_cast<const int4*>(pk + (gg << 7)) + lane)
+                                      : make_int4(static_cast<int>(rmask), static_cast<int>(rmask),
+                                                  static_cast<int>(rmask), static_cast<int>(rmask));
+                p[u][0] = static_cast<uint32_t>(w.x);
+                p[u][1] = static_cast<uint32_t>(w.y);
+                p[u][2] = static_cast<uint32_t>(w.z);
+                p[u][3] = static_cast<uint32_t>(w.w);
+                if (S::kUsesValues && !MASKED) {
+                    if (has[u]) ld_stream4(bv + (gg << 7) + 4 * lane, a[u]);
+                    else a[u][0] = a[u][1] = a[u][2] = a[u][3] = V(0);
+                } else {
+                    a[u][0] = a[u][1] = a[u][2] = a[u][3] = V(1);
+                }
             }
         };
-        for (uint32_t base = threadIdx.x; base < n_e; base += kStep) {
-            uint32_t p[kBinUnroll];
-            V a[kBinUnroll];
-            uint32_t col[kBinUnroll];
-            bool ok[kBinUnroll];
+        constexpr int64_t step = static_cast<int64_t>(NW) * GU;
+        uint32_t p[GU][4];
+        V a[GU][4];
+        bool has[GU];
+        if (PIPE) load_groups(g0 + warp, p, a, has);
+        for (int64_t g = g0 + warp; g < g1; g += step) {
+            if (!PIPE) load_groups(g, p, a, has);
+            uint32_t cb[GU];
 #pragma unroll
-            for (int j = 0; j < kBinUnroll; ++j) ok[j] = base + j * kBinThreads < n_e;
-            load_batch(base, p, a);
-#pragma unroll
-            for (int j = 0; j < kBinUnroll; ++j) {
-                const uint32_t e = base + j * kBinThreads;
-                if (ok[j] && e >= nb) {
+            for (int u = 0; u < GU; ++u) {
+                const int64_t e = (g + u * NW) << 7;
+                if (has[u] && e >= nb) {  // warp-uniform
                     do {
                         ++c;
-                        nb = chunk_end(c);
+                        nb = __ldg(co + c + 1);
                     } while (e >= nb);
-                    cbase = static_cast<uint32_t>(c) << cw;
                 }
-                col[j] = cbase + (p[j] >> rbits);
+                cb[u] = static_cast<uint32_t>(c) << cw;
             }
-            if (MASKED) {
+            bool ok[GU][4];
+            uint32_t col[GU][4];
 #pragma unroll
-                for (int j = 0; j < kBinUnroll; ++j)
-                    if (ok[j]) ok[j] = (__ldg(mask + (col[j] >> 5)) >> (col[j] & 31)) & 1u;
-                if (S::kUsesValues) {
+            for (int u = 0; u < GU; ++u)
 #pragma unroll
-                    for (int j = 0; j < kBinUnroll; ++j)
-                        if (ok[j]) a[j] = ld_stream(bvt + base + j * kBinThreads);
+                for (int j = 0; j < 4; ++j) {
+                    ok[u][j] = (p[u][j] & rmask) != rmask;
+                    col[u][j] = cb[u] + (p[u][j] >> rbits);
+                    if (MASKED && ok[u][j]) ok[u][j] = (__ldg(mask + (col[u][j] >> 5)) >> (col[u][j] & 31)) & 1u;
+                    n_used += ok[u][j];
                 }
-                if (ctr) {  // values_read: value loads (kernels.hpp:108)
-                    unsigned n = 0;
+            if (MASKED && S::kUsesValues) {  // K2 loads a value only after its mask test (kernels.hpp:229-240)
 #pragma unroll
-                    for (int j = 0; j < kBinUnroll; ++j) n += ok[j];
-                    count_add(ctr, 0, n);
-                }
+                for (int u = 0; u < GU; ++u)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (ok[u][j]) a[u][j] = __ldg(bv + ((g + u * NW) << 7) + 4 * lane + j);
             }
-            V xv[kBinUnroll];
+            V xv[GU][4];
 #pragma unroll
-            for (int j = 0; j < kBinUnroll; ++j)
-                xv[j] = ok[j] ? (NOALLOC ? ld_stream(x + col[j]) : __ldg(x + col[j])) : S::zero();
+            for (int u = 0; u < GU; ++u)
 #pragma unroll
-            for (int j = 0; j < kBinUnroll; ++j) {
-                if (!ok[j]) continue;
-                V* slot = ys + (p[j] & rmask);
-                if (SR == SR_PLUS_TIMES) {
-                    const V prod = a[j] * xv[j];
-                    // adding +-0 never changes a sum that starts at +0
-                    if (prod != V(0)) atomicAdd(slot, prod);
-                } else if (SR == SR_OR_AND) {
-                    if (xv[j] != V(0)) *reinterpret_cast<volatile V*>(slot) = V(1);
-                } else {
-                    const V v = a[j] + xv[j];
-                    if (v < *slot) AtomicCombine<SR_MIN_PLUS>::apply(slot, v);
+                for (int j = 0; j < 4; ++j)
+                    xv[u][j] = ok[u][j] ? (NOALLOC ? ld_stream(x + col[u][j]) : __ldg(x + col[u][j])) : S::zero();
+            uint32_t rw[GU][4];
+            V av[GU][4];
+#pragma unroll
+            for (int u = 0; u < GU; ++u)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    rw[u][j] = p[u][j] & rmask;
+                    av[u][j] = a[u][j];
                 }
-            }
+            // the next groups' entries stream in while this batch updates y
+            if (PIPE) load_groups(g + step, p, a, has);
+#pragma unroll
+            for (int u = 0; u < GU; ++u)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (!ok[u][j]) continue;
+                    V* slot = ys + rw[u][j];
+                    if (SR == SR_PLUS_TIMES) {
+                        const V prod = av[u][j] * xv[u][j];
+                        // adding +-0 never changes a sum that starts at +0
+                        if (prod != V(0)) atomicAdd(slot, prod);
+                    } else if (SR == SR_OR_AND) {
+                        if (xv[u][j] != V(0)) *reinterpret_cast<volatile V*>(slot) = V(1);
+                    } else {
+                        const V v = av[u][j] + xv[u][j];
+                        if (v < *slot) AtomicCombine<SR_MIN_PLUS>::apply(slot, v);
+                    }
+                }
         }
+    }
+    if (ctr) {  // values_read (kernels.hpp:108): entries consumed; under K2, value loads after the mask test
+        const unsigned n = warp_sum(n_used);
+        if ((threadIdx.x & 31) == 0) count_add(ctr, 0, n);
     }
     int lo = 0, hi = nr;
     const V* peer = nullptr;
@@ -506,15 +563,15 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
     plan_heavy(ctx, m, L);
     const int64_t nnz = m.nnz;
     const size_t z = static_cast<size_t>(std::max<int64_t>(nnz, 1));
-    L.pk.ensure(sizeof(uint32_t) * z);
-    L.bv.ensure(sizeof(V) * z);
     const int64_t nkeys = nbins * nchunks;
     L.chunk_off.ensure(sizeof(int64_t) * static_cast<size_t>(nkeys + 1));
-    DevBuf counts;
+    DevBuf counts, uoff;
     counts.ensure(sizeof(unsigned long long) * static_cast<size_t>(nkeys));
+    uoff.ensure(sizeof(int64_t) * static_cast<size_t>(nkeys + 1));
     ADA_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(unsigned long long) * static_cast<size_t>(nkeys), ctx.stream));
+    DevBuf k0, k1, p0, p1, cnt;
+    int which = 0;
     if (nnz > 0) {
-        DevBuf k0, k1, p0, p1, cnt;
         k0.ensure(sizeof(uint32_t) * z);
         k1.ensure(sizeof(uint32_t) * z);
         p0.ensure(sizeof(PkVal<V>) * z);
@@ -527,19 +584,40 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
                                              k0.as<uint32_t>(), p0.as<PkVal<V>>(),
                                              counts.as<unsigned long long>());
         ADA_LAUNCHED(ctx);
-        const int which = radix_sort_pairs<PkVal<V>>(ctx, k0.as<uint32_t>(), p0.as<PkVal<V>>(),
-                                                     k1.as<uint32_t>(), p1.as<PkVal<V>>(), nnz,
-                                                     bits_for(nbins + 1), cnt, ctx.scratch[5]);
-        const PkVal<V>* sorted = which ? p1.as<PkVal<V>>() : p0.as<PkVal<V>>();
-        const int64_t g = std::min<int64_t>((nnz + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 32);
-        bin_unpack_kernel<V><<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(sorted, nnz, L.pk.as<uint32_t>(),
-                                                                              L.bv.as<V>());
-        ADA_LAUNCHED(ctx);
-        ctx.sync();  // the sort buffers are released on return
+        which = radix_sort_pairs<PkVal<V>>(ctx, k0.as<uint32_t>(), p0.as<PkVal<V>>(), k1.as<uint32_t>(),
+                                           p1.as<PkVal<V>>(), nnz, bits_for(nbins + 1), cnt, ctx.scratch[5]);
     }
+    // unpadded run offsets (sorted positions) and padded ones (the layout)
+    int64_t* uo = uoff.as<int64_t>();
     int64_t* off = L.chunk_off.as<int64_t>();
-    scan3(ctx, nkeys, U64Counts{counts.as<unsigned long long>()}, WriteExclusive{off}, off + nkeys,
+    scan3(ctx, nkeys, U64Counts{counts.as<unsigned long long>()}, WriteExclusive{uo}, uo + nkeys, ctx.scratch[5]);
+    scan3(ctx, nkeys, PaddedCounts{counts.as<unsigned long long>()}, WriteExclusive{off}, off + nkeys,
           ctx.scratch[5]);
+    int64_t tot[2] = {0, 0};
+    ADA_CUDA(cudaMemcpyAsync(&tot[0], uo + nkeys, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
+    ADA_CUDA(cudaMemcpyAsync(&tot[1], off + nkeys, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    const int64_t nlight = tot[0], npad = tot[1];
+    L.n_light = nlight;
+    L.n_padded = npad;
+    // + 4 entries so an empty layout still has a valid allocation
+    L.pk.ensure(sizeof(uint32_t) * static_cast<size_t>(npad + 4));
+    L.bv.ensure(sizeof(V) * static_cast<size_t>(npad + 4));
+    if (npad > 0) {
+        const int64_t g = std::min<int64_t>((npad + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 32);
+        bin_pad_fill_kernel<V><<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(
+            npad, (1u << rbits) - 1u, L.pk.as<uint32_t>(), L.bv.as<V>());
+        ADA_LAUNCHED(ctx);
+    }
+    if (nlight > 0) {
+        const PkVal<V>* sorted = which ? p1.as<PkVal<V>>() : p0.as<PkVal<V>>();
+        const uint32_t* skeys = which ? k1.as<uint32_t>() : k0.as<uint32_t>();
+        const int64_t g = std::min<int64_t>((nlight + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 32);
+        bin_scatter_kernel<V><<<static_cast<unsigned>(g), 256, 0, ctx.stream>>>(
+            sorted, skeys, nlight, nchunks, uo, off, L.pk.as<uint32_t>(), L.bv.as<V>());
+        ADA_LAUNCHED(ctx);
+    }
+    ctx.sync();  // the sort buffers are released on return
     // per-bin entry counts on the host (tile planning)
     std::vector<int64_t> all(static_cast<size_t>(nkeys + 1));
     ADA_CUDA(cudaMemcpyAsync(all.data(), off, sizeof(int64_t) * all.size(), cudaMemcpyDeviceToHost, ctx.stream));
@@ -628,7 +706,9 @@ void plan_tiles(Context& ctx, const Matrix& m, BinLayout& L, int64_t cap_req, in
             const int64_t k = std::max<int64_t>((e - s + cl * cap - 1) / (cl * cap), 1);
             const int32_t mode = k > 1 ? 1 : (c0 > 0 ? 2 : 0);
             for (int64_t i = 0; i < k * cl; ++i)
-                ts.push_back(T{s + (e - s) * i / (k * cl), s + (e - s) * (i + 1) / (k * cl), static_cast<int32_t>(b), mode});
+                ts.push_back(T{s + (((e - s) * i / (k * cl)) & ~int64_t(127)),
+                                 i + 1 == k * cl ? e : s + (((e - s) * (i + 1) / (k * cl)) & ~int64_t(127)),
+                                 static_cast<int32_t>(b), mode});
             multi = multi || k > 1;
         }
         if (cl == 1) {
@@ -759,8 +839,20 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
             if (mask) launch(binned_row_kernel<V, SR, true, 2>, 2, t0, t1 - t0);
             else launch(binned_row_kernel<V, SR, false, 2>, 2, t0, t1 - t0);
         } else {
-            if (mask) launch(binned_row_kernel<V, SR, true, 1>, 1, t0, t1 - t0);
-            else launch(binned_row_kernel<V, SR, false, 1>, 1, t0, t1 - t0);
+            // fp32 K0: the next groups' entries stream in during the y updates
+            // (C2 x = 0.5: 145 vs 156 us); x gathers skip L1 allocation on
+            // matrices without hub columns (C2: 160 vs 162 us; R-MAT 22, whose
+            // hub columns reuse L1 lines: 564 vs 525 us, so skewed ones keep
+            // it); fp64 keeps the plain loop (the pipelined one spills at 64
+            // registers)
+            if (mask) {
+                launch(binned_row_kernel<V, SR, true, 1>, 1, t0, t1 - t0);
+            } else if constexpr (sizeof(V) == 4) {
+                if (m.feat[8] > 0.5) launch(binned_row_kernel<V, SR, false, 1, 8, false, 1024, true>, 1, t0, t1 - t0);
+                else launch(binned_row_kernel<V, SR, false, 1, 8, true, 1024, true>, 1, t0, t1 - t0);
+            } else {
+                launch(binned_row_kernel<V, SR, false, 1>, 1, t0, t1 - t0);
+            }
         }
     }
     if (L.nsegs > 0) {  // heavy rows, after the bins wrote their identity

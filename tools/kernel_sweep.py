@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--densities", default="1.0")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--layouts", default="0", help="row_layout values for K0/K2 (0 auto, 1 csr, 2 bins)")
+    ap.add_argument("--bin-rows", default="0", help="bin_rows overrides (rows per bin, 0 = auto)")
+    ap.add_argument("--tile-nnz", type=int, default=0, help="bin_tile_nnz override (0 = auto)")
     a = ap.parse_args()
     ctx = A.Context(0)
     ctx.set_timing(True)
@@ -54,9 +56,10 @@ def main():
             b_spmv = (rows + 1) * 8 + ro[-1] * (4 + V) + cols * V + rows * V
             yfirst = None
             for k in [int(s) for s in a.kernels.split(",")]:
-                for lanes, lay in [(int(s), int(l)) for s in a.lanes.split(",") for l in a.layouts.split(",")]:
+                for lanes, lay, br in [(int(s), int(l), int(b)) for s in a.lanes.split(",")
+                                       for l in a.layouts.split(",") for b in a.bin_rows.split(",")]:
                     x.prepare(k)
-                    cfg = A.KernelConfig(lanes_per_row=lanes, row_layout=lay)
+                    cfg = A.KernelConfig(lanes_per_row=lanes, row_layout=lay, bin_rows=br, bin_tile_nnz=a.tile_nnz)
                     A.run_kernel(m, k, x, cfg, out=out)
                     y = out.dense().values.astype(np.float64)
                     if yfirst is None:
@@ -70,7 +73,7 @@ def main():
                         A.run_kernel(m, k, x, cfg, out=out)
                         ts.append(out.elapsed())
                     t = float(np.median(ts))
-                    print(f"{name:7s} x={dens:<8g} k={k} lanes={lanes:2d} layout={lay} {t * 1e6:9.2f} us  "
+                    print(f"{name:7s} x={dens:<8g} k={k} lanes={lanes:2d} layout={lay} bin_rows={br} {t * 1e6:9.2f} us  "
                           f"maxdev={dev:.1e} "
                           f"B_spmv/t={b_spmv / t / 1e9:8.1f} GB/s ({100 * b_spmv / t / hbm:5.1f}% of HBM)",
                           flush=True)
