@@ -256,24 +256,175 @@ __global__ void __launch_bounds__(kNT) col_direct_emit_kernel(
     }
 }
 
+// ---------------------------------------------------------------------------
 // Segment sums of the row-sorted pair stream (reduce_sorted_pairs,
-// kernels.hpp:323-337): each head sums its run in order; flag = sum != zero.
-template <class V, int SR>
-__global__ void seg_reduce_kernel(int64_t n, const uint32_t* __restrict__ keys,
-                                  const V* __restrict__ vals, V* __restrict__ sums,
-                                  uint8_t* __restrict__ keep) {
-    using S = Semiring<SR, V>;
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t k = keys[i];
-    if (i > 0 && keys[i - 1] == k) {
-        keep[i] = 0;
-        return;
+// kernels.hpp:323-337) as a parallel segmented scan, so a hub row's long run
+// is summed by many threads instead of one: tiles of kSegTile pairs (kSegIPT
+// consecutive pairs per thread); pass 1 reduces each tile to (has a run head,
+// sum of its last run's part), pass 2 scans those across tiles (one CTA) into
+// each tile's carry-in, pass 3 rescans each tile with its carry-in and writes
+// the run's sum at the run's LAST pair (keep = sum != zero), where the
+// compaction picks it up in row order.  The combine order is a fixed tree:
+// deterministic run to run (not the reference's left-to-right order: fp sums
+// agree within the 8(c) tolerance).
+// ---------------------------------------------------------------------------
+constexpr int kSegNT = 256, kSegIPT = 8, kSegTile = kSegNT * kSegIPT;
+
+// Block-wide segmented scan of per-thread aggregates: returns the EXCLUSIVE
+// carry of thread t (the combined value of threads < t since the last head,
+// identity when none); *tile_inc gets the block's inclusive total.
+template <int NT, class V, class Add>
+__device__ __forceinline__ SegPair<V> block_seg_exclusive(SegPair<V> p, V ident, Add add, SegPair<V>* smem,
+                                                         SegPair<V>* tile_inc) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    SegPair<V> inc = warp_seg_inclusive(p, add);
+    if (lane == 31) smem[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        SegPair<V> w = lane < NW ? smem[lane] : SegPair<V>{0, ident};
+        SegPair<V> wi = warp_seg_inclusive(w, add);
+        if (lane < NW) smem[NW + 1 + lane] = wi;  // inclusive over warps
     }
-    V acc = vals[i];
-    for (int64_t j = i + 1; j < n && keys[j] == k; ++j) acc = S::add(acc, vals[j]);
-    sums[i] = acc;
-    keep[i] = acc != S::zero() ? 1 : 0;
+    __syncthreads();
+    // exclusive within the warp
+    SegPair<V> ex{0, ident};
+    {
+        const int f = __shfl_up_sync(kFull, inc.f, 1);
+        const V v = __shfl_up_sync(kFull, inc.v, 1);
+        if (lane > 0) ex = SegPair<V>{f, v};
+    }
+    if (warp > 0 && !ex.f) {  // nothing in this warp before me resets: add the earlier warps
+        const SegPair<V> pw = smem[NW + 1 + warp - 1];
+        ex.v = lane > 0 ? add(pw.v, ex.v) : pw.v;
+        ex.f = pw.f;
+    } else if (warp > 0 && lane == 0) {
+        ex = smem[NW + 1 + warp - 1];
+    }
+    *tile_inc = smem[NW + 1 + NW - 1];
+    __syncthreads();
+    return ex;
+}
+
+template <class V, int SR>
+struct SegAdd {
+    __device__ V operator()(V a, V b) const { return Semiring<SR, V>::add(a, b); }
+};
+
+// pass 1: per tile (any head in the tile, segmented total = its last run's part)
+template <class V, int SR>
+__global__ void __launch_bounds__(kSegNT) seg_tile_kernel(int64_t n, const uint32_t* __restrict__ keys,
+                                                          const V* __restrict__ vals,
+                                                          SegPair<V>* __restrict__ tiles) {
+    using S = Semiring<SR, V>;
+    __shared__ SegPair<V> sm[2 * (kSegNT / 32) + 2];
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kSegTile + threadIdx.x * kSegIPT;
+    SegPair<V> p{0, S::zero()};
+#pragma unroll
+    for (int q = 0; q < kSegIPT; ++q) {
+        const int64_t i = i0 + q;
+        if (i >= n) break;
+        const bool head = i == 0 || keys[i - 1] != keys[i];
+        if (head) p = SegPair<V>{1, vals[i]};
+        else p.v = S::add(p.v, vals[i]);
+    }
+    SegPair<V> tot;
+    block_seg_exclusive<kSegNT>(p, S::zero(), SegAdd<V, SR>{}, sm, &tot);
+    if (threadIdx.x == 0) tiles[blockIdx.x] = tot;
+}
+
+// pass 2 (one CTA of 1024): exclusive segmented scan over the tiles -> carry-in
+template <class V, int SR>
+__global__ void __launch_bounds__(1024) seg_carry_kernel(int64_t ntiles, SegPair<V>* __restrict__ tiles) {
+    using S = Semiring<SR, V>;
+    __shared__ SegPair<V> sm[2 * 32 + 2];
+    const int64_t per = (ntiles + 1023) / 1024;
+    const int64_t t0 = threadIdx.x * per, t1 = t0 + per < ntiles ? t0 + per : ntiles;
+    SegPair<V> p{0, S::zero()};
+    for (int64_t t = t0; t < t1; t += 8) {  // 8 independent loads in flight
+        SegPair<V> x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = t + u < t1 ? tiles[t + u] : SegPair<V>{0, S::zero()};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (x[u].f) p = x[u];
+            else p.v = S::add(p.v, x[u].v);
+        }
+    }
+    SegPair<V> tot;
+    SegPair<V> c = block_seg_exclusive<1024>(p, S::zero(), SegAdd<V, SR>{}, sm, &tot);
+    for (int64_t t = t0; t < t1; t += 8) {  // tiles[t] <- carry into tile t (its value before tile t)
+        SegPair<V> x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = t + u < t1 ? tiles[t + u] : SegPair<V>{0, S::zero()};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (t + u < t1) tiles[t + u] = c;
+            if (x[u].f) c = x[u];
+            else c.v = S::add(c.v, x[u].v);
+        }
+    }
+}
+
+// pass 3: rescan each tile from its carry-in; write each run's sum at its last pair
+template <class V, int SR>
+__global__ void __launch_bounds__(kSegNT) seg_final_kernel(int64_t n, const uint32_t* __restrict__ keys,
+                                                           const V* __restrict__ vals,
+                                                           const SegPair<V>* __restrict__ carry,
+                                                           V* __restrict__ sums, uint8_t* __restrict__ keep) {
+    using S = Semiring<SR, V>;
+    __shared__ SegPair<V> sm[2 * (kSegNT / 32) + 2];
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kSegTile + threadIdx.x * kSegIPT;
+    uint32_t k[kSegIPT + 1];
+    V v[kSegIPT];
+    bool hd[kSegIPT];
+    SegPair<V> p{0, S::zero()};
+#pragma unroll
+    for (int q = 0; q < kSegIPT; ++q) {
+        const int64_t i = i0 + q;
+        hd[q] = false;
+        v[q] = S::zero();
+        k[q] = 0;
+        if (i >= n) continue;
+        k[q] = keys[i];
+        v[q] = vals[i];
+        hd[q] = i == 0 || keys[i - 1] != k[q];
+        if (hd[q]) p = SegPair<V>{1, v[q]};
+        else p.v = S::add(p.v, v[q]);
+    }
+    k[kSegIPT] = i0 + kSegIPT < n ? keys[i0 + kSegIPT] : ~k[kSegIPT - 1];
+    SegPair<V> tot;
+    SegPair<V> ex = block_seg_exclusive<kSegNT>(p, S::zero(), SegAdd<V, SR>{}, sm, &tot);
+    const SegPair<V> cin = carry[blockIdx.x];
+    V acc = ex.f ? ex.v : (threadIdx.x > 0 ? S::add(cin.v, ex.v) : cin.v);
+#pragma unroll
+    for (int q = 0; q < kSegIPT; ++q) {
+        const int64_t i = i0 + q;
+        if (i >= n) break;
+        acc = hd[q] ? v[q] : S::add(acc, v[q]);
+        const bool last = i + 1 >= n || (q + 1 < kSegIPT ? k[q + 1] != k[q] : k[kSegIPT] != k[q]);
+        if (last) {
+            sums[i] = acc;
+            keep[i] = acc != S::zero() ? 1 : 0;
+        } else {
+            keep[i] = 0;
+        }
+    }
+}
+
+template <class V, int SR>
+void seg_reduce(Context& ctx, int64_t n, const uint32_t* keys, const V* vals, V* sums, uint8_t* keep,
+                DevBuf& tmp) {
+    if (n <= 0) return;
+    const int64_t ntiles = (n + kSegTile - 1) / kSegTile;
+    SegPair<V>* tiles = static_cast<SegPair<V>*>(tmp.ensure(sizeof(SegPair<V>) * static_cast<size_t>(ntiles)));
+    seg_tile_kernel<V, SR><<<static_cast<unsigned>(ntiles), kSegNT, 0, ctx.stream>>>(n, keys, vals, tiles);
+    ADA_LAUNCHED(ctx);
+    seg_carry_kernel<V, SR><<<1, 1024, 0, ctx.stream>>>(ntiles, tiles);
+    ADA_LAUNCHED(ctx);
+    seg_final_kernel<V, SR><<<static_cast<unsigned>(ntiles), kSegNT, 0, ctx.stream>>>(n, keys, vals, tiles, sums,
+                                                                                     keep);
+    ADA_LAUNCHED(ctx);
 }
 
 struct KeepIn {
@@ -382,18 +533,43 @@ __global__ void __launch_bounds__(kSmallNT) col_sort_small_kernel(
             __syncthreads();
         }
     }
-    // 3. reduce by key: heads sum their run in order
-    for (int i = threadIdx.x; i < n; i += kSmallNT) {
-        const uint32_t r = static_cast<uint32_t>(skey[i] >> 32);
-        int keep = 0;
-        if (i == 0 || static_cast<uint32_t>(skey[i - 1] >> 32) != r) {
-            V acc = sval[i];
-            for (int j = i + 1; j < n && static_cast<uint32_t>(skey[j] >> 32) == r; ++j)
-                acc = S::add(acc, sval[j]);
-            keep = acc != S::zero();
-            if (keep) sval[i] = acc;  // only heads are read back
+    // 3. reduce by key: segmented scan, kSmallPairs / kSmallNT consecutive
+    //    pairs per thread; a run's sum lands at its LAST pair
+    {
+        static_assert(kSmallPairs == kSmallNT * 4, "four pairs per thread");
+        __shared__ SegPair<V> ssm[2 * (kSmallNT / 32) + 2];
+        const int i0 = threadIdx.x * 4;
+        uint32_t kk[5];
+        V vv[4];
+        bool hd[4];
+        SegPair<V> p{0, S::zero()};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q;
+            kk[q] = 0;
+            vv[q] = S::zero();
+            hd[q] = false;
+            if (i >= n) continue;
+            kk[q] = static_cast<uint32_t>(skey[i] >> 32);
+            vv[q] = sval[i];
+            hd[q] = i == 0 || static_cast<uint32_t>(skey[i - 1] >> 32) != kk[q];
+            if (hd[q]) p = SegPair<V>{1, vv[q]};
+            else p.v = S::add(p.v, vv[q]);
         }
-        sflag[i] = keep;
+        kk[4] = i0 + 4 < n ? static_cast<uint32_t>(skey[i0 + 4] >> 32) : ~kk[3];
+        SegPair<V> tot;
+        const SegPair<V> ex = block_seg_exclusive<kSmallNT>(p, S::zero(), SegAdd<V, SR>{}, ssm, &tot);
+        V acc = ex.v;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q;
+            if (i >= n) break;
+            acc = hd[q] ? vv[q] : S::add(acc, vv[q]);
+            const bool last = i + 1 >= n || kk[q + 1] != kk[q];
+            const int keep = last && acc != S::zero();
+            if (keep) sval[i] = acc;  // only kept pairs are read back
+            sflag[i] = keep;
+        }
     }
     __syncthreads();
     // 4. compaction in row order
@@ -645,8 +821,7 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
     const V* sv = which ? v1 : v0;
     V* ssum = static_cast<V*>(sums.ensure(sizeof(V) * z));
     uint8_t* kp = static_cast<uint8_t*>(keep.ensure(z));
-    seg_reduce_kernel<V, SR><<<blocks_for(nnz_s, 256), 256, 0, ctx.stream>>>(nnz_s, sk, sv, ssum, kp);
-    ADA_LAUNCHED(ctx);
+    seg_reduce<V, SR>(ctx, nnz_s, sk, sv, ssum, kp, ctx.scratch[4]);
     scan3(ctx, nnz_s, KeepIn{kp}, KeepEpi<V>{sk, ssum, y_idx, y_val}, d_nnz, scan_tmp);
 }
 
@@ -675,8 +850,8 @@ int64_t sort_reduce_t(Context& ctx, int64_t n, const int32_t* d_rows, const void
     const V* sv = which ? pv1 : pv0;
     V* ssum = static_cast<V*>(sums.ensure(sizeof(V) * z));
     uint8_t* kp = static_cast<uint8_t*>(keep.ensure(z));
-    seg_reduce_kernel<V, SR_PLUS_TIMES><<<blocks_for(n, 256), 256, 0, ctx.stream>>>(n, sk, sv, ssum, kp);
-    ADA_LAUNCHED(ctx);
+    DevBuf seg_tmp;
+    seg_reduce<V, SR_PLUS_TIMES>(ctx, n, sk, sv, ssum, kp, seg_tmp);
     scan3(ctx, n, KeepIn{kp}, KeepEpi<V>{sk, ssum, out_idx, out_val}, ctx.dscal(1), scan_tmp);
     const int64_t r = ctx.fetch_scalar(ctx.dscal(1));
     return r;
