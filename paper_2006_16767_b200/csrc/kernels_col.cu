@@ -17,6 +17,7 @@
 // Inputs whose pair count fits one CTA (kSmallPairs) run emit + sort + reduce
 // + compaction in a single launch with no host synchronisation: the
 // latency-bound sparse end of the sweep.
+#include <type_traits>
 #include <algorithm>
 
 #include "device.cuh"
@@ -311,6 +312,44 @@ struct SegAdd {
     __device__ V operator()(V a, V b) const { return Semiring<SR, V>::add(a, b); }
 };
 
+// The kSegIPT consecutive pairs of one thread (+ the keys just before and
+// after): 16-B loads when the group is in range.
+template <class V>
+__device__ __forceinline__ void seg_load(int64_t n, int64_t i0, const uint32_t* __restrict__ keys,
+                                         const V* __restrict__ vals, V ident, uint32_t (&k)[kSegIPT + 2],
+                                         V (&v)[kSegIPT]) {
+    if (i0 + kSegIPT <= n) {
+        const uint4* kp = reinterpret_cast<const uint4*>(keys + i0);
+#pragma unroll
+        for (int q = 0; q < kSegIPT / 4; ++q) {
+            const uint4 w = kp[q];
+            k[1 + 4 * q] = w.x;
+            k[2 + 4 * q] = w.y;
+            k[3 + 4 * q] = w.z;
+            k[4 + 4 * q] = w.w;
+        }
+        constexpr int kVec = 16 / sizeof(V);
+        using VV = typename std::conditional<sizeof(V) == 4, float4, double2>::type;
+        const VV* vp = reinterpret_cast<const VV*>(vals + i0);
+#pragma unroll
+        for (int q = 0; q < kSegIPT / kVec; ++q) {
+            const VV w = vp[q];
+            const V* e = reinterpret_cast<const V*>(&w);
+#pragma unroll
+            for (int r = 0; r < kVec; ++r) v[q * kVec + r] = e[r];
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kSegIPT; ++q) {
+            const bool in = i0 + q < n;
+            k[1 + q] = in ? keys[i0 + q] : 0u;
+            v[q] = in ? vals[i0 + q] : ident;
+        }
+    }
+    k[0] = i0 > 0 && i0 <= n ? keys[i0 - 1] : ~k[1];
+    k[kSegIPT + 1] = i0 + kSegIPT < n ? keys[i0 + kSegIPT] : ~k[kSegIPT];
+}
+
 // pass 1: per tile (any head in the tile, segmented total = its last run's part)
 template <class V, int SR>
 __global__ void __launch_bounds__(kSegNT) seg_tile_kernel(int64_t n, const uint32_t* __restrict__ keys,
@@ -319,14 +358,15 @@ __global__ void __launch_bounds__(kSegNT) seg_tile_kernel(int64_t n, const uint3
     using S = Semiring<SR, V>;
     __shared__ SegPair<V> sm[2 * (kSegNT / 32) + 2];
     const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kSegTile + threadIdx.x * kSegIPT;
+    uint32_t k[kSegIPT + 2];
+    V v[kSegIPT];
+    seg_load(n, i0, keys, vals, S::zero(), k, v);
     SegPair<V> p{0, S::zero()};
 #pragma unroll
     for (int q = 0; q < kSegIPT; ++q) {
-        const int64_t i = i0 + q;
-        if (i >= n) break;
-        const bool head = i == 0 || keys[i - 1] != keys[i];
-        if (head) p = SegPair<V>{1, vals[i]};
-        else p.v = S::add(p.v, vals[i]);
+        if (i0 + q >= n) break;
+        if (k[q + 1] != k[q]) p = SegPair<V>{1, v[q]};  // head (k[0] of pair 0 differs when i0 == 0)
+        else p.v = S::add(p.v, v[q]);
     }
     SegPair<V> tot;
     block_seg_exclusive<kSegNT>(p, S::zero(), SegAdd<V, SR>{}, sm, &tot);
@@ -375,40 +415,39 @@ __global__ void __launch_bounds__(kSegNT) seg_final_kernel(int64_t n, const uint
     using S = Semiring<SR, V>;
     __shared__ SegPair<V> sm[2 * (kSegNT / 32) + 2];
     const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kSegTile + threadIdx.x * kSegIPT;
-    uint32_t k[kSegIPT + 1];
+    uint32_t k[kSegIPT + 2];
     V v[kSegIPT];
-    bool hd[kSegIPT];
+    seg_load(n, i0, keys, vals, S::zero(), k, v);
     SegPair<V> p{0, S::zero()};
 #pragma unroll
     for (int q = 0; q < kSegIPT; ++q) {
-        const int64_t i = i0 + q;
-        hd[q] = false;
-        v[q] = S::zero();
-        k[q] = 0;
-        if (i >= n) continue;
-        k[q] = keys[i];
-        v[q] = vals[i];
-        hd[q] = i == 0 || keys[i - 1] != k[q];
-        if (hd[q]) p = SegPair<V>{1, v[q]};
+        if (i0 + q >= n) break;
+        if (k[q + 1] != k[q]) p = SegPair<V>{1, v[q]};
         else p.v = S::add(p.v, v[q]);
     }
-    k[kSegIPT] = i0 + kSegIPT < n ? keys[i0 + kSegIPT] : ~k[kSegIPT - 1];
     SegPair<V> tot;
     SegPair<V> ex = block_seg_exclusive<kSegNT>(p, S::zero(), SegAdd<V, SR>{}, sm, &tot);
     const SegPair<V> cin = carry[blockIdx.x];
     V acc = ex.f ? ex.v : (threadIdx.x > 0 ? S::add(cin.v, ex.v) : cin.v);
+    uint8_t kp[kSegIPT];
 #pragma unroll
     for (int q = 0; q < kSegIPT; ++q) {
+        kp[q] = 0;
         const int64_t i = i0 + q;
-        if (i >= n) break;
-        acc = hd[q] ? v[q] : S::add(acc, v[q]);
-        const bool last = i + 1 >= n || (q + 1 < kSegIPT ? k[q + 1] != k[q] : k[kSegIPT] != k[q]);
-        if (last) {
+        if (i >= n) continue;
+        acc = k[q + 1] != k[q] ? v[q] : S::add(acc, v[q]);
+        if (i + 1 >= n || k[q + 2] != k[q + 1]) {  // the run's last pair
             sums[i] = acc;
-            keep[i] = acc != S::zero() ? 1 : 0;
-        } else {
-            keep[i] = 0;
+            kp[q] = acc != S::zero() ? 1 : 0;
         }
+    }
+    if (i0 + kSegIPT <= n) {
+        uint2 w;
+        w.x = kp[0] | (kp[1] << 8) | (kp[2] << 16) | (static_cast<uint32_t>(kp[3]) << 24);
+        w.y = kp[4] | (kp[5] << 8) | (kp[6] << 16) | (static_cast<uint32_t>(kp[7]) << 24);
+        *reinterpret_cast<uint2*>(keep + i0) = w;
+    } else {
+        for (int q = 0; q < kSegIPT && i0 + q < n; ++q) keep[i0 + q] = kp[q];
     }
 }
 
