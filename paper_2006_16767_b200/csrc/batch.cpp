@@ -66,7 +66,12 @@ void fetch_result(Context& c, const Matrix& m, Vector& v, Output& y, int kernel,
         // sparse costs 8 + V bytes per entry, dense V per row
         int64_t bound = -1;  // an upper bound of nnz_y
         if (kernel == 5 || kernel == 7) bound = output_nnz(c, y);
-        else if (kernel >= 4) bound = vector_nnz_s(c, v, m);
+        else if (kernel >= 4) {  // nnz_s bounds nnz_y; the degree profile's bound first (no device trip)
+            const int64_t ub = v.nnz >= 0 ? m.nnz_s_upper(v.nnz) : -1;
+            if (v.nnz_s >= 0 && v.nnz_s_matrix == m.id) bound = v.nnz_s;
+            else if (ub >= 0 && ub * (8 + vb) < m.rows * vb && ub <= r.capacity) bound = ub;
+            else bound = vector_nnz_s(c, v, m);
+        }
         else if (v.nnz_s >= 0 && v.nnz_s_matrix == m.id) bound = v.nnz_s;
         sparse = r.indices && bound >= 0 && bound * (8 + vb) < m.rows * vb && bound <= r.capacity;
         if (sparse && !(kernel == 5 || kernel == 7)) {

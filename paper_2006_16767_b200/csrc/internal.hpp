@@ -128,6 +128,7 @@ struct Context {
     int64_t fetch_scalar(const int64_t* d);
     // h_scalars[0..n) = d[0..n) (synchronises the stream)
     void fetch_scalars(const int64_t* d, int n);
+
 };
 
 // LB tiles of the row-major kernels: fixed kRowTile nonzeros per warp
@@ -184,6 +185,13 @@ struct Matrix {
     double feat[9] = {0};
     int64_t max_col_deg = 0;
     double avg_col = 0;
+    // column degrees, distinct values ascending with prefix counts / sums
+    // (host): sum of the k smallest / largest degrees bounds nnz_s of any
+    // operand with k distinct stored indices, so the selector can settle an
+    // nnz_s / m_sparsity split without the device reduction (selector.cpp)
+    std::vector<int64_t> cdeg, cdeg_cnt, cdeg_sum;  // cnt/sum: prefix over cdeg[< i]
+    int64_t nnz_s_lower(int64_t k) const;
+    int64_t nnz_s_upper(int64_t k) const;
     bool pattern = false;   // created without values (all 1.0)
     double gather_spread = 0;  // mean |col - row*n/m| over the nonzeros (columns)
     mutable std::unique_ptr<BinLayout> bins{new BinLayout()};

@@ -266,6 +266,30 @@ void compute_features(Context& ctx, Matrix& m) {
     f[7] = std::sqrt(var);
     // Gini: G = 2*sum_i i*d_(i) / (k*sum d) - (k+1)/k with d sorted ascending.
     // From the degree histogram c_v: positions C_<v + 1 .. C_<v + c_v carry v.
+    // column degree profile (selector bounds on nnz_s)
+    m.cdeg.clear();
+    m.cdeg_cnt.assign(1, 0);
+    m.cdeg_sum.assign(1, 0);
+    if (m.cols > 0) {
+        const int64_t nb = m.max_col_deg + 1;
+        DevBuf ch;
+        ch.ensure(sizeof(unsigned long long) * static_cast<size_t>(nb));
+        ADA_CUDA(cudaMemsetAsync(ch.p, 0, sizeof(unsigned long long) * static_cast<size_t>(nb), ctx.stream));
+        degree_hist_kernel<<<grid_for(ctx, m.cols, 256), 256, 0, ctx.stream>>>(
+            m.col_off.as<int64_t>(), m.cols, nb, ch.as<unsigned long long>());
+        ADA_LAUNCHED(ctx);
+        std::vector<unsigned long long> hc(static_cast<size_t>(nb));
+        ADA_CUDA(cudaMemcpyAsync(hc.data(), ch.p, sizeof(unsigned long long) * hc.size(), cudaMemcpyDeviceToHost,
+                                 ctx.stream));
+        ctx.sync();
+        for (int64_t d = 0; d < nb; ++d) {
+            const int64_t c = static_cast<int64_t>(hc[static_cast<size_t>(d)]);
+            if (!c) continue;
+            m.cdeg.push_back(d);
+            m.cdeg_cnt.push_back(m.cdeg_cnt.back() + c);
+            m.cdeg_sum.push_back(m.cdeg_sum.back() + c * d);
+        }
+    }
     const int64_t nbins = static_cast<int64_t>(mx) + 1;
     DevBuf hist;
     hist.ensure(sizeof(unsigned long long) * static_cast<size_t>(nbins));
@@ -429,6 +453,23 @@ Matrix* matrix_transpose(Context& ctx, const Matrix& src) {
         delete m;
         throw;
     }
+}
+
+// sum of the k smallest column degrees (k <= cols)
+int64_t Matrix::nnz_s_lower(int64_t k) const {
+    if (k <= 0 || cdeg.empty()) return 0;
+    // first distinct degree i with cdeg_cnt[i+1] >= k
+    const auto it = std::lower_bound(cdeg_cnt.begin() + 1, cdeg_cnt.end(), k);
+    if (it == cdeg_cnt.end()) return cdeg_sum.back();
+    const size_t i = static_cast<size_t>(it - cdeg_cnt.begin()) - 1;
+    return cdeg_sum[i] + (k - cdeg_cnt[i]) * cdeg[i];
+}
+// sum of the k largest column degrees
+int64_t Matrix::nnz_s_upper(int64_t k) const {
+    if (k <= 0 || cdeg.empty()) return 0;
+    const int64_t n = cdeg_cnt.back();
+    if (k >= n) return cdeg_sum.back();
+    return cdeg_sum.back() - nnz_s_lower(n - k);
 }
 
 }  // namespace ada

@@ -54,11 +54,35 @@ namespace {
 // Walks one tree (routing "value <= threshold -> left"),
 // pulling features lazily into `f` / `have`.
 int walk(Context& ctx, const Matrix& m, Vector& v, const Tree& t, double* f, uint32_t& have,
-         double* feature_s) {
+         uint32_t& consulted, double* feature_s) {
     int32_t i = 0;
     for (int guard = 0; guard < 1 << 20; ++guard) {
         const int32_t feat = t.feature[static_cast<size_t>(i)];
         if (feat < 0) return t.leaf[static_cast<size_t>(i)];
+        if (!(have & (1u << feat)) && (feat == 11 || feat == 12) && v.nnz >= 0 && v.n == m.cols &&
+            !(v.nnz_s >= 0 && v.nnz_s_matrix == m.id)) {
+            // nnz_s of k = nnz_x distinct columns lies between the sums of the
+            // k smallest and the k largest column degrees: when the whole
+            // interval is on one side of the split, route without the device
+            // reduction (the walk is the one the exact value would take)
+            double lo = static_cast<double>(m.nnz_s_lower(v.nnz));
+            double hi = static_cast<double>(m.nnz_s_upper(v.nnz));
+            if (feat == 12) {
+                const double nz = m.nnz > 0 ? static_cast<double>(m.nnz) : 1.0;
+                lo = m.nnz > 0 ? lo / nz : 0.0;
+                hi = m.nnz > 0 ? hi / nz : 0.0;
+            }
+            const double thr = t.threshold[static_cast<size_t>(i)];
+            if (hi <= thr || lo > thr) consulted |= 1u << feat;
+            if (hi <= thr) {
+                i = t.left[static_cast<size_t>(i)];
+                continue;
+            }
+            if (lo > thr) {
+                i = t.right[static_cast<size_t>(i)];
+                continue;
+            }
+        }
         if (!(have & (1u << feat))) {
             const auto t0 = std::chrono::steady_clock::now();
             features(ctx, m, v, 1u << feat, f);
@@ -81,25 +105,25 @@ int walk(Context& ctx, const Matrix& m, Vector& v, const Tree& t, double* f, uin
 int predict(Context& ctx, const Matrix& m, Vector& v, const Bundle& b, uint32_t* used, int* trees,
             double* feature_s) {
     double f[ADASPMV_NUM_FEATURES] = {0};
-    uint32_t have = 0;
+    uint32_t have = 0, consulted = 0;  // computed / routed on their bounds
     int nt = 0;
-    const int pattern = walk(ctx, m, v, b.trees[0], f, have, feature_s);
+    const int pattern = walk(ctx, m, v, b.trees[0], f, have, consulted, feature_s);
     ++nt;
-    const int lb = walk(ctx, m, v, b.trees[1], f, have, feature_s) == 1 ? 1 : 0;
+    const int lb = walk(ctx, m, v, b.trees[1], f, have, consulted, feature_s) == 1 ? 1 : 0;
     ++nt;
     int k;
     switch (pattern) {
         case 2: k = lb; break;      // SpMV
         case 1: k = 2 + lb; break;  // RowSpMSpV
         case 0: {
-            const int sort = walk(ctx, m, v, b.trees[2], f, have, feature_s) == 1 ? 1 : 0;
+            const int sort = walk(ctx, m, v, b.trees[2], f, have, consulted, feature_s) == 1 ? 1 : 0;
             ++nt;
             k = 4 + 2 * lb + sort;
             break;
         }
         default: throw Error(ADASPMV_ERR_FORMAT, "pattern tree produced an invalid class");
     }
-    if (used) *used = have;
+    if (used) *used = have | consulted;
     if (trees) *trees = nt;
     return k;
 }

@@ -352,6 +352,10 @@ void widen_indices(Context& ctx, int64_t n, const int32_t* in, int64_t* out) {
     ADA_LAUNCHED(ctx);
 }
 
+struct CountSum {
+    long long c, s;
+};
+
 // Selector features in ONE launch: every block reduces its share of
 // (count, sum) and adds it into two device accumulators; the last block to
 // finish (ticket) stores the totals into the context's mapped pinned scalars
@@ -365,11 +369,9 @@ __global__ void __launch_bounds__(256) reduce2_to_host_kernel(int64_t n, F f, un
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     long long c = 0, s = 0;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
-        const int64_t d = f(i);
-        if (d >= 0) {
-            ++c;
-            s += d;
-        }
+        const CountSum d = f(i);
+        c += d.c;
+        s += d.s;
     }
     c = warp_sum(c);
     s = warp_sum(s);
@@ -403,17 +405,50 @@ __global__ void __launch_bounds__(256) reduce2_to_host_kernel(int64_t n, F f, un
 struct SparseDeg {
     const int64_t* co;
     const int32_t* xi;
-    __device__ int64_t operator()(int64_t s) const {
+    __device__ CountSum operator()(int64_t s) const {
         const int32_t c = xi[s];
-        return co[c + 1] - co[c];
+        return CountSum{1, co[c + 1] - co[c]};
     }
 };
-// dense x: nonzeros count (-1 marks a zero)
+// dense x, four entries per item (16-B loads of x and of the offsets):
+// nonzeros count, weight = their column degrees
 template <class V>
-struct DenseDeg {
+struct DenseDeg4 {
     const V* x;
     const int64_t* co;
-    __device__ int64_t operator()(int64_t i) const { return x[i] != V(0) ? co[i + 1] - co[i] : -1; }
+    int64_t n;
+    __device__ CountSum operator()(int64_t g) const {
+        const int64_t i = g * 4;
+        CountSum r{0, 0};
+        if (i + 4 <= n) {
+            V v[4];
+            if constexpr (sizeof(V) == 4) {
+                const float4 w = *reinterpret_cast<const float4*>(x + i);
+                v[0] = w.x, v[1] = w.y, v[2] = w.z, v[3] = w.w;
+            } else {
+                const double2 a = *reinterpret_cast<const double2*>(x + i);
+                const double2 b = *reinterpret_cast<const double2*>(x + i + 2);
+                v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
+            }
+            const longlong2 o0 = *reinterpret_cast<const longlong2*>(co + i);
+            const longlong2 o1 = *reinterpret_cast<const longlong2*>(co + i + 2);
+            const int64_t o4 = co[i + 4];
+            const int64_t o[5] = {o0.x, o0.y, o1.x, o1.y, o4};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (v[q] != V(0)) {
+                    ++r.c;
+                    r.s += o[q + 1] - o[q];
+                }
+        } else {
+            for (int64_t j = i; j < n; ++j)
+                if (x[j] != V(0)) {
+                    ++r.c;
+                    r.s += co[j + 1] - co[j];
+                }
+        }
+        return r;
+    }
 };
 
 template <class F>
@@ -439,9 +474,9 @@ int64_t vector_nnz_s(Context& ctx, Vector& v, const Matrix& m) {
         }
     } else if (v.has_dense && v.dense_fill < 0 && v.n == m.cols) {  // user dense x: nnz_x and nnz_s in one pass
         if (v.dtype == ADASPMV_F64)
-            reduce2_to_host(ctx, v.n, DenseDeg<double>{v.dense.as<double>(), m.col_off.as<int64_t>()});
+            reduce2_to_host(ctx, (v.n + 3) / 4, DenseDeg4<double>{v.dense.as<double>(), m.col_off.as<int64_t>(), v.n});
         else
-            reduce2_to_host(ctx, v.n, DenseDeg<float>{v.dense.as<float>(), m.col_off.as<int64_t>()});
+            reduce2_to_host(ctx, (v.n + 3) / 4, DenseDeg4<float>{v.dense.as<float>(), m.col_off.as<int64_t>(), v.n});
         v.nnz = ctx.h_scalars[0];
         v.nnz_s = ctx.h_scalars[1];
     } else {

@@ -493,3 +493,66 @@ def test_kernel_counters(port, dt):
     out = A.run_kernel(m, 0, A.DenseVector(xd), out=A.MultiplyOutput(ctx))
     with pytest.raises(A.InvalidArgument):
         out.counters()
+
+
+def _random_tree(rng, depth, feats):
+    """A random full tree (SelectorBundle.from_trees dict) splitting on `feats`."""
+    feature, threshold, left, right, leaf = [], [], [], [], []
+
+    def node(d):
+        i = len(feature)
+        feature.append(-1), threshold.append(0.0), left.append(-1), right.append(-1), leaf.append(0)
+        if d == depth:
+            leaf[i] = int(rng.integers(0, 3))
+            return i
+        f = int(rng.choice(feats))
+        feature[i] = f
+        threshold[i] = float({11: rng.uniform(0, 4000), 12: rng.uniform(0, 0.4), 10: rng.uniform(0, 0.3),
+                              9: rng.uniform(0, 300), 2: rng.uniform(0, 40000), 5: rng.uniform(0, 30)}[f])
+        left[i] = node(d + 1)
+        right[i] = node(d + 1)
+        return i
+
+    node(0)
+    return {"feature": feature, "threshold": threshold, "left": left, "right": right, "leaf": leaf}
+
+
+@pytest.mark.gpu
+def test_selector_degree_bounds_route_like_exact_features(ctx):
+    """nnz_s / m_sparsity splits settled on the column-degree bounds (selector.cpp)
+    route exactly as the computed features would, and skip the device reduction
+    when the bound interval is on one side."""
+    rng = np.random.default_rng(5)
+    for mat_seed, (rows, cols, dens) in enumerate([(3000, 2000, 0.004), (500, 4000, 0.01)]):
+        r, c, ro, ci, vals = synth.random_csr(rows, cols, dens, seed=mat_seed + 40)
+        m = A.DualMatrix.from_csr(r, c, ro, ci, vals, ctx=ctx)
+        for t in range(25):
+            # the workload tree reads matrix features only (SPEC.md:227)
+            trees = [_random_tree(rng, 3, [9, 10, 11, 12]), _random_tree(rng, 2, [2, 5]),
+                     _random_tree(rng, 3, [9, 10, 11, 12])]
+            b = A.SelectorBundle.from_trees(trees)
+            for nx in (1, 3, 20, 200, cols // 2, cols):
+                xi = np.sort(rng.choice(cols, nx, replace=False))
+                xv = rng.uniform(-1, 1, nx)
+                fresh = A.DeviceVector(cols, np.float64, ctx)
+                fresh.set_sparse(xi, xv)
+                k_pruned, used_p, _ = A.predict_kernel(m, fresh, b)
+                exact = A.DeviceVector(cols, np.float64, ctx)
+                exact.set_sparse(xi, xv)
+                A.features(m, exact, (1 << 11) | (1 << 12))  # caches the exact nnz_s
+                k_exact, used_e, _ = A.predict_kernel(m, exact, b)
+                assert k_pruned.index() == k_exact.index(), (mat_seed, t, nx)
+                assert used_p == used_e
+    # a split far above any possible nnz_s is settled without a launch
+    r, c, ro, ci, vals = synth.random_csr(2000, 2000, 0.005, seed=3)
+    m = A.DualMatrix.from_csr(r, c, ro, ci, vals, ctx=ctx)
+    pat = {"feature": [12, -1, -1], "threshold": [0.5, 0, 0], "left": [1, -1, -1], "right": [2, -1, -1],
+           "leaf": [0, 0, 2]}
+    one = {"feature": [-1], "threshold": [0.0], "left": [-1], "right": [-1], "leaf": [0]}
+    b = A.SelectorBundle.from_trees([pat, one, one])
+    x = A.DeviceVector(c, np.float64, ctx)
+    x.set_sparse(np.array([4, 9]), np.array([1.0, 2.0]))
+    ctx.synchronize()
+    l0 = ctx.launches
+    k, used, _ = A.predict_kernel(m, x, b)
+    assert k.index() == 4 and used == 1 << 12 and ctx.launches == l0
