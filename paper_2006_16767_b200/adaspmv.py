@@ -31,6 +31,7 @@ absent, and CUDA errors surface as :class:`CudaError`.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import enum
 import os
 import re
@@ -1079,7 +1080,7 @@ class Dist:
         """-> (levels of this rank's rows or None, this rank's per-level reports)."""
         levels = np.empty(block.rows(), np.int64) if download_levels else None
         nl = C.c_int64()
-        reps = (_IterReport * max_reports)()
+        reps = _report_buffer(max_reports)
         _check(_lib.adaspmv_dist_bfs(self.h, block.h, int(row0), int(source), int(semiring),
                                      bundle.h if bundle else None, int(force_kernel), _ptr(levels),
                                      C.byref(nl), C.cast(reps, C.c_void_p), max_reports))
@@ -1179,7 +1180,7 @@ def bfs(m: DualMatrix, source: int = 0, semiring: int = OR_AND, bundle: Optional
     """Level-synchronous BFS -> (levels int64[n] or None, reports list)."""
     levels = np.empty(m.rows(), np.int64) if download_levels else None
     nl = C.c_int64()
-    reps = (_IterReport * max_reports)()
+    reps = _report_buffer(max_reports)
     _check(_lib.adaspmv_bfs(m.ctx.h, m.h, int(source), int(semiring), bundle.h if bundle else None,
                             int(force_kernel), _ptr(levels), C.byref(nl), C.cast(reps, C.c_void_p), max_reports))
     out = []
@@ -1189,6 +1190,19 @@ def bfs(m: DualMatrix, source: int = 0, semiring: int = OR_AND, bundle: Optional
                         feature_s=r.feature_s, predict_s=r.predict_s, convert_s=r.convert_s,
                         kernel_s=r.kernel_s))
     return levels, out
+
+
+_report_tls = threading.local()
+
+
+def _report_buffer(n: int):
+    """A per-thread reusable IterationReport array of >= n entries (a fresh
+    zeroed ctypes array of the default 4096 reports costs ~80 us per call)."""
+    buf = getattr(_report_tls, "buf", None)
+    if buf is None or len(buf) < n:
+        buf = (_IterReport * max(int(n), 1))()
+        _report_tls.buf = buf
+    return buf
 
 
 def _reports(reps, n, max_reports):
@@ -1207,7 +1221,7 @@ def pagerank_incremental(m: DualMatrix, damping: float = 0.85, prune: float = 1e
     """Incremental delta-propagation PageRank -> (rank float64[n] or None, reports)."""
     rank = np.empty(m.rows(), np.float64) if download_rank else None
     nit = C.c_int64()
-    reps = (_IterReport * max_reports)()
+    reps = _report_buffer(max_reports)
     _check(_lib.adaspmv_pagerank(m.ctx.h, m.h, float(damping), float(prune), int(max_iters),
                                  bundle.h if bundle else None, int(force_kernel), _ptr(rank), C.byref(nit),
                                  C.cast(reps, C.c_void_p), max_reports))

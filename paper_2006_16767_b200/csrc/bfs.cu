@@ -93,9 +93,19 @@ __global__ void fill_kernel(V* __restrict__ p, int64_t n, V v) {
     if (i < n) p[i] = v;
 }
 
-__global__ void init_block_levels_kernel(int32_t* lv, int64_t nr, int64_t src_local) {
+// levels of this block's rows (-1 = unvisited), and the first frontier
+// {source} with its value (no host copy, no synchronisation)
+template <class V>
+__global__ void init_block_levels_kernel(int32_t* lv, int64_t nr, int64_t src_local, int32_t* xi, V* xv,
+                                         int32_t source, V one, const int64_t* __restrict__ co,
+                                         volatile int64_t* host_nnz_s) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i < nr) lv[i] = i == src_local ? 0 : -1;
+    if (i == 0) {
+        xi[0] = source;
+        xv[0] = one;
+        *host_nnz_s = co[source + 1] - co[source];  // the first frontier's nnz_s (selector feature)
+    }
 }
 
 template <class V, int SR>
@@ -301,10 +311,6 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
     DevBuf lvb, gathered;
     int32_t* lv = static_cast<int32_t*>(lvb.ensure(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(nr, 1))));
     const int64_t src_local = source - row0;  // outside [0, nr): another rank's row
-    if (nr > 0) {
-        init_block_levels_kernel<<<static_cast<unsigned>((nr + 255) / 256), 256, 0, ctx.stream>>>(lv, nr, src_local);
-        ADA_LAUNCHED(ctx);
-    }
     Vector x;
     x.ctx = &ctx;
     x.n = n;
@@ -312,13 +318,16 @@ void bfs_t(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, int f
     {
         int32_t* xi = static_cast<int32_t*>(x.sp_idx.ensure(sizeof(int32_t) * static_cast<size_t>(n)));
         V* xv = static_cast<V*>(x.sp_val.ensure(sizeof(V) * static_cast<size_t>(n)));
-        const int32_t s32 = static_cast<int32_t>(source);
         const V one = SR == SR_MIN_PLUS ? V(0) : V(1);
-        ADA_CUDA(cudaMemcpyAsync(xi, &s32, sizeof(s32), cudaMemcpyHostToDevice, ctx.stream));
-        ADA_CUDA(cudaMemcpyAsync(xv, &one, sizeof(one), cudaMemcpyHostToDevice, ctx.stream));
+        init_block_levels_kernel<V><<<static_cast<unsigned>(std::max<int64_t>((nr + 255) / 256, 1)), 256, 0,
+                                      ctx.stream>>>(lv, nr, src_local, xi, xv, static_cast<int32_t>(source), one,
+                                                    m.col_off.as<int64_t>(), ctx.h_scalars_dev + kScanTotalSlot);
+        ADA_LAUNCHED(ctx);
+        ctx.sync();
         x.nnz = 1;
         x.has_sparse = true;
-        ctx.sync();
+        x.nnz_s = ctx.h_scalars[kScanTotalSlot];
+        x.nnz_s_matrix = m.id;
     }
     Output y;
     y.ctx = &ctx;
