@@ -71,7 +71,7 @@ struct DevTrees {
     const int32_t* right;
     const int32_t* leaf;
     const double* threshold;
-    int root[3];
+    int root[4];  // [3] = -1 without a workload_col tree (schema 1)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -116,7 +116,7 @@ __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees t
         f[11] = static_cast<double>(ns);
         f[12] = nnz > 0 ? static_cast<double>(ns) / static_cast<double>(nnz) : 0.0;
         const int pattern = tree_walk(trees, 0, f);
-        const int lb = tree_walk(trees, 1, f) == 1 ? 1 : 0;
+        const int lb = tree_walk(trees, pattern == 0 && trees.root[3] >= 0 ? 3 : 1, f) == 1 ? 1 : 0;
         if (pattern == 2) k = lb;
         else if (pattern == 1) k = 2 + lb;
         else k = 4 + 2 * lb + (tree_walk(trees, 2, f) == 1 ? 1 : 0);
@@ -416,7 +416,8 @@ namespace {
 void upload_trees(Context& ctx, const Bundle& b, BfsPlan& P) {
     std::vector<int32_t> feat, left, right, leaf;
     std::vector<double> thr;
-    for (int t = 0; t < 3; ++t) {
+    P.dt.root[3] = -1;
+    for (int t = 0; t < (b.has_col ? 4 : 3); ++t) {
         const Tree& tr = b.trees[t];
         const int32_t base = static_cast<int32_t>(feat.size());
         P.dt.root[t] = base;

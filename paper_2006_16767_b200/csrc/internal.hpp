@@ -326,7 +326,10 @@ struct Bundle {
     int schema_version = 1;
     std::string hardware_tag;
     std::string feature_order_hash;
-    Tree trees[3];
+    // [0] pattern, [1] workload, [2] write-back; schema 2 adds [3] the
+    // ColSpMSpV family's own workload tree (has_col)
+    Tree trees[4];
+    bool has_col = false;
 };
 
 // ---- entry points implemented in the .cu/.cpp files ------------------------

@@ -109,7 +109,9 @@ int predict(Context& ctx, const Matrix& m, Vector& v, const Bundle& b, uint32_t*
     int nt = 0;
     const int pattern = walk(ctx, m, v, b.trees[0], f, have, consulted, feature_s);
     ++nt;
-    const int lb = walk(ctx, m, v, b.trees[1], f, have, consulted, feature_s) == 1 ? 1 : 0;
+    // schema 2: the column family reads its own workload tree
+    const Tree& wt = pattern == 0 && b.has_col ? b.trees[3] : b.trees[1];
+    const int lb = walk(ctx, m, v, wt, f, have, consulted, feature_s) == 1 ? 1 : 0;
     ++nt;
     int k;
     switch (pattern) {
@@ -156,6 +158,7 @@ void validate_bundle(const Bundle& b) {
     check_tree(b.trees[0], 3);
     check_tree(b.trees[1], 2);
     check_tree(b.trees[2], 2);
+    if (b.has_col) check_tree(b.trees[3], 2);
 }
 
 // Text form of the SPEC.md:383 model file:
@@ -166,6 +169,9 @@ void validate_bundle(const Bundle& b) {
 //   <feature> <threshold> <left> <right> <leaf>      (N lines; leaf: feature -1)
 //   ... (three trees) ...
 //   end
+// Schema 2 (an extension, not in SPEC.md): a fourth tree `workload_col`, the
+// LB-vs-Direct decision of the ColSpMSpV family (the row patterns keep
+// `workload`); both workload trees may read every feature.
 Bundle* bundle_load(const std::string& path) {
     std::ifstream in(path);
     if (!in) throw Error(ADASPMV_ERR_FORMAT, "cannot open file: " + path);
@@ -173,21 +179,28 @@ Bundle* bundle_load(const std::string& path) {
     try {
         std::string tag;
         if (!(in >> tag >> b->schema_version) || tag != "adaspmv-bundle") bad("missing header");
-        if (b->schema_version != 1) bad("unsupported schema_version " + std::to_string(b->schema_version));
+        if (b->schema_version != 1 && b->schema_version != 2)
+            bad("unsupported schema_version " + std::to_string(b->schema_version));
+        const int ntrees = b->schema_version == 2 ? 4 : 3;
+        b->has_col = ntrees == 4;
         std::string key;
         if (!(in >> key >> b->hardware_tag) || key != "hardware_tag") bad("missing hardware_tag");
         if (!(in >> key >> b->feature_order_hash) || key != "feature_order_hash")
             bad("missing feature_order_hash");
         if (b->feature_order_hash != feature_order_hash()) bad("feature order hash mismatch");
-        bool seen[3] = {false, false, false};
-        for (int k = 0; k < 3; ++k) {
+        bool seen[4] = {false, false, false, false};
+        for (int k = 0; k < ntrees; ++k) {
             std::string tw, target, mw, nw;
             uint32_t mask = 0;
             long long n = 0;
             if (!(in >> tw >> target >> mw >> mask >> nw >> n) || tw != "tree" || mw != "mask" ||
                 nw != "nodes" || n <= 0 || n > (1 << 22))
                 bad("truncated or malformed tree header");
-            int idx = target == "pattern" ? 0 : target == "workload" ? 1 : target == "writeback" ? 2 : -1;
+            int idx = target == "pattern"                     ? 0
+                      : target == "workload"                  ? 1
+                      : target == "writeback"                 ? 2
+                      : target == "workload_col" && ntrees == 4 ? 3
+                                                              : -1;
             if (idx < 0 || seen[idx]) bad("unknown or repeated tree target '" + target + "'");
             seen[idx] = true;
             Tree& t = b->trees[idx];

@@ -43,12 +43,15 @@ def leaf(c: int) -> dict:
 
 
 def write_bundle(path, trees: dict, hardware_tag: str = "B200") -> None:
-    """trees: {"pattern": nodes, "workload": nodes, "writeback": nodes}."""
-    lines = ["adaspmv-bundle 1", f"hardware_tag {hardware_tag}", f"feature_order_hash {feature_order_hash()}"]
-    for t in TARGETS:
+    """trees: {"pattern": nodes, "workload": nodes, "writeback": nodes}; with a
+    "workload_col" tree the file is schema 2 (selector.cpp)."""
+    v2 = "workload_col" in trees
+    lines = [f"adaspmv-bundle {2 if v2 else 1}", f"hardware_tag {hardware_tag}",
+             f"feature_order_hash {feature_order_hash()}"]
+    for t in TARGETS + (("workload_col",) if v2 else ()):
         nd = trees[t]
         n = len(nd["feature"])
-        lines.append(f"tree {t} mask {MASKS[t]} nodes {n}")
+        lines.append(f"tree {t} mask {(MASKS_V2 if v2 else MASKS)[t]} nodes {n}")
         for i in range(n):
             lines.append(f"{int(nd['feature'][i])} {float(nd['threshold'][i]):.17g} {int(nd['left'][i])} "
                          f"{int(nd['right'][i])} {int(nd['leaf'][i])}")
@@ -61,7 +64,7 @@ def read_bundle(path) -> dict:
     assert toks[0] == "adaspmv-bundle"
     i = 6
     trees = {}
-    for _ in range(3):
+    for _ in range(4 if toks[1] == "2" else 3):
         _, target, _, mask, _, n = toks[i:i + 6]
         i += 6
         n = int(n)
@@ -79,14 +82,16 @@ def read_bundle(path) -> dict:
 
 
 def predict(trees: dict, f13) -> int:
-    """Host mirror of the cascade (SPEC.md:340-348) -> KernelId::index()."""
+    """Host mirror of the cascade (SPEC.md:340-348) -> KernelId::index().
+    Schema v2 (optional "workload_col" tree): the ColSpMSpV pattern reads its
+    own workload tree, the row patterns the "workload" one."""
     def walk(nd):
         i = 0
         while nd["feature"][i] >= 0:
             i = nd["left"][i] if f13[nd["feature"][i]] <= nd["threshold"][i] else nd["right"][i]
         return nd["leaf"][i]
     p = walk(trees["pattern"])
-    lb = walk(trees["workload"])
+    lb = walk(trees["workload_col"] if p == 0 and "workload_col" in trees else trees["workload"])
     if p == 2:
         return lb
     if p == 1:
@@ -222,6 +227,39 @@ def train_bundle(features, times, seed: int = 0, cost_sensitive: bool = True) ->
     for j, t in enumerate(TARGETS):
         trees[t], scores[t] = train_tree(F, lab[:, j], MASKS[t], seed=seed,
                                          cost=None if cst is None else cst[:, j])
+    return trees, scores
+
+
+# Schema v2: feature masks of the per-family workload trees (vector features
+# allowed: the column distribution depends on the frontier's degrees)
+MASKS_V2 = {"pattern": 0x1FFF, "workload": 0x1FFF, "workload_col": 0x1FFF, "writeback": MASKS["writeback"]}
+
+
+def train_bundle_v2(features, times, seed: int = 0) -> tuple[dict, dict]:
+    """Schema v2: pattern + write-back as train_bundle (cost-sensitive); the
+    workload decision split by pattern family, each tree trained on every
+    sample with its CONDITIONAL label (faster distribution within the family,
+    so a pattern mistake still gets a good distribution) and cost."""
+    F = np.asarray(features, np.float64)
+    t = np.asarray(times, np.float64)
+    lab = np.array([labels_from_times(x) for x in t])
+    cst = np.array([costs_from_times(x) for x in t])
+    trees, scores = {}, {}
+    trees["pattern"], scores["pattern"] = train_tree(F, lab[:, 0], MASKS_V2["pattern"], seed=seed, cost=cst[:, 0])
+    trees["writeback"], scores["writeback"] = train_tree(F, lab[:, 2], MASKS_V2["writeback"], seed=seed,
+                                                         cost=cst[:, 2])
+    # row family: direct vs LB of the better row pattern of the sample
+    rd = np.minimum(t[:, 0], t[:, 2])
+    rl = np.minimum(t[:, 1], t[:, 3])
+    y_row = (rl < rd).astype(int)
+    c_row = np.maximum(rd, rl) / np.minimum(rd, rl) - 1.0
+    trees["workload"], scores["workload"] = train_tree(F, y_row, MASKS_V2["workload"], seed=seed, cost=c_row)
+    cd = np.minimum(t[:, 4], t[:, 5])
+    cl = np.minimum(t[:, 6], t[:, 7])
+    y_col = (cl < cd).astype(int)
+    c_col = np.maximum(cd, cl) / np.minimum(cd, cl) - 1.0
+    trees["workload_col"], scores["workload_col"] = train_tree(F, y_col, MASKS_V2["workload_col"], seed=seed,
+                                                               cost=c_col)
     return trees, scores
 
 

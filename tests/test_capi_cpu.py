@@ -121,6 +121,20 @@ def test_bundle_files(tmp_path):
         A.SelectorBundle.load(p)
     with pytest.raises(A.InvalidArgument):
         A.SelectorBundle.from_trees([bad["pattern"], bad["workload"], bad["writeback"]])
+    # schema 2 (a workload tree for the ColSpMSpV family) round-trips and loads;
+    # the shipped v2 bundle too
+    v2 = dict(trees)
+    v2["workload_col"] = {"feature": [11, -1, -1], "threshold": [5000.0, 0, 0], "left": [1, -1, -1],
+                          "right": [2, -1, -1], "leaf": [-1, 0, 1]}
+    S.write_bundle(p, v2)
+    assert p.read_text().startswith("adaspmv-bundle 2") and S.read_bundle(p) == v2
+    A.SelectorBundle.load(p)
+    f = np.zeros(13)
+    f[12], f[11] = 0.01, 100.0  # Col; workload_col: nnz_s <= 5000 -> Direct; Sort
+    assert S.predict(v2, f) == 5
+    f[11] = 9000.0  # -> LB; write-back tree: nnz_s > 4096 -> Atomic
+    assert S.predict(v2, f) == 6
+    A.SelectorBundle.load(S.DEFAULT_PATH.parent / "b200_bundle_v2.txt")
 
 
 def test_no_gpu_fails_loudly():

@@ -556,3 +556,24 @@ def test_selector_degree_bounds_route_like_exact_features(ctx):
     l0 = ctx.launches
     k, used, _ = A.predict_kernel(m, x, b)
     assert k.index() == 4 and used == 1 << 12 and ctx.launches == l0
+
+
+@pytest.mark.gpu
+def test_selector_schema2_runtime_matches_host_mirror(ctx):
+    """The shipped schema-2 bundle: the runtime's cascade (selector.cpp) and the
+    host mirror (selector.predict) pick the same kernel on the same features."""
+    from paper_2006_16767_b200 import selector as S
+    path = S.DEFAULT_PATH.parent / "b200_bundle_v2.txt"
+    trees = S.read_bundle(path)
+    assert "workload_col" in trees
+    b = A.SelectorBundle.load(path)
+    rng = np.random.default_rng(3)
+    for seed, (rows, cols, dens) in enumerate([(4000, 4000, 0.002), (20000, 3000, 0.001), (3000, 30000, 0.002)]):
+        r, c, ro, ci, vals = synth.random_csr(rows, cols, dens, seed=seed + 60)
+        m = A.DualMatrix.from_csr(r, c, ro, ci, vals, ctx=ctx)
+        for nx in (1, 10, 100, 1000, cols // 3, cols):
+            xi = np.sort(rng.choice(cols, nx, replace=False))
+            x = A.SparseVector(cols, xi, rng.uniform(-1, 1, nx))
+            f = A.features(m, x)
+            k, _, _ = A.predict_kernel(m, x, b)
+            assert k.index() == S.predict(trees, f), (seed, nx)

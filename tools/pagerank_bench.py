@@ -47,11 +47,12 @@ def main():
         exp, it_exp = port.pagerank_incremental(n, ro, ci, a.damping, a.prune, a.max_iters)
         t_oracle = time.perf_counter() - t1
     bundle = A.SelectorBundle.load(S.DEFAULT_PATH)
+    bundle_v2 = A.SelectorBundle.load(S.DEFAULT_PATH.parent / "b200_bundle_v2.txt")
     res = {"scale": a.scale, "n": n, "nnz": int(ro[-1]), "damping": a.damping, "prune": a.prune,
            "dtype": a.dtype, "generate_s": round(gen, 1), "runs": {}}
     if exp is not None:
         res["oracle"] = {"iterations": it_exp, "seconds_1core": round(t_oracle, 3)}
-    modes = [("selector", bundle, -1), ("heuristic", None, -1)] + [(f"fixed_{k}", None, k) for k in range(8)]
+    modes = [("selector", bundle, -1), ("selector_v2", bundle_v2, -1), ("heuristic", None, -1)] + [(f"fixed_{k}", None, k) for k in range(8)]
     # f64: 1e-11 relative + 4 prune; f32: 2e-5 relative + the mass a pruning
     # decision that flips under fp32 rounding can move, prune / (1 - d) each
     rtol = 1e-11 if dt == np.float64 else 2e-5
@@ -94,7 +95,7 @@ def main():
     L = min(len(v["per_iter"]) for v in res["runs"].values())
     orc = sum(min(res["runs"][f"fixed_{k}"]["per_iter"][i]["kernel_ms"] for k in range(8)) for i in range(L))
     summ = {"best_fixed": best_fixed, "best_fixed_s": fixed[best_fixed]}
-    for pol in ("selector", "heuristic"):
+    for pol in ("selector", "selector_v2", "heuristic"):
         kp = sum(p["kernel_ms"] for p in res["runs"][pol]["per_iter"][:L])
         summ[f"{pol}_s"] = res["runs"][pol]["seconds"]
         summ[f"{pol}_kernel_regret"] = round(kp / max(orc, 1e-12), 3)
