@@ -495,7 +495,7 @@ def test_kernel_counters(port, dt):
         out.counters()
 
 
-def _random_tree(rng, depth, feats):
+def _random_tree(rng, depth, feats, nclasses=3):
     """A random full tree (SelectorBundle.from_trees dict) splitting on `feats`."""
     feature, threshold, left, right, leaf = [], [], [], [], []
 
@@ -503,7 +503,7 @@ def _random_tree(rng, depth, feats):
         i = len(feature)
         feature.append(-1), threshold.append(0.0), left.append(-1), right.append(-1), leaf.append(0)
         if d == depth:
-            leaf[i] = int(rng.integers(0, 3))
+            leaf[i] = int(rng.integers(0, nclasses))
             return i
         f = int(rng.choice(feats))
         feature[i] = f
@@ -528,8 +528,8 @@ def test_selector_degree_bounds_route_like_exact_features(ctx):
         m = A.DualMatrix.from_csr(r, c, ro, ci, vals, ctx=ctx)
         for t in range(25):
             # the workload tree reads matrix features only
-            trees = [_random_tree(rng, 3, [9, 10, 11, 12]), _random_tree(rng, 2, [2, 5]),
-                     _random_tree(rng, 3, [9, 10, 11, 12])]
+            trees = [_random_tree(rng, 3, [9, 10, 11, 12]), _random_tree(rng, 2, [2, 5], 2),
+                     _random_tree(rng, 3, [9, 10, 11, 12], 2)]
             b = A.SelectorBundle.from_trees(trees)
             for nx in (1, 3, 20, 200, cols // 2, cols):
                 xi = np.sort(rng.choice(cols, nx, replace=False))
