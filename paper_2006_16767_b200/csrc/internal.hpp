@@ -171,6 +171,11 @@ struct Matrix {
     uint64_t id = 0;
     DevBuf row_off, col_idx, vals;   // CSR
     DevBuf col_off, row_idx, cvals;  // CSC
+    // fp32 matrices: the CSC entries again as interleaved (row, value bits)
+    // 8-byte pairs, so the direct column kernel (K4) reads a support column's
+    // entries as one contiguous run (random columns: half the DRAM bursts of
+    // two separate arrays)
+    DevBuf cpairs;
     int64_t n_row_tiles = 0;
     // int64 [n_row_tiles+2]: [t] = first row of tile t's row window: the row
     // holding item t*kRowTile, or the first row starting there (so empty rows

@@ -46,7 +46,7 @@ template <class V, int G, int SR>
 __global__ void __launch_bounds__(kNT) col_direct_atomic_kernel(
     int64_t nnz_x, const int32_t* __restrict__ xi, const V* __restrict__ xv,
     const int64_t* __restrict__ co, const int32_t* __restrict__ ri, const V* __restrict__ cv,
-    V* __restrict__ y, unsigned long long* __restrict__ ctr) {
+    const uint2* __restrict__ cp, V* __restrict__ y, unsigned long long* __restrict__ ctr) {
     using S = Semiring<SR, V>;
     const int64_t gid = static_cast<int64_t>(blockIdx.x) * kNT + threadIdx.x;
     const int64_t s = gid / G;
@@ -63,8 +63,14 @@ __global__ void __launch_bounds__(kNT) col_direct_atomic_kernel(
         for (int j = 0; j < kU; ++j) {
             const int64_t k = k0 + j * G;
             if (k < e) {
-                r[j] = __ldg(ri + k);
-                a[j] = S::kUsesValues ? __ldg(cv + k) : V(1);
+                if (sizeof(V) == 4 && cp) {  // interleaved (row, value) pair: one 8-B load
+                    const uint2 pr = __ldg(cp + k);
+                    r[j] = static_cast<int>(pr.x);
+                    a[j] = S::kUsesValues ? static_cast<V>(__uint_as_float(pr.y)) : V(1);
+                } else {
+                    r[j] = __ldg(ri + k);
+                    a[j] = S::kUsesValues ? __ldg(cv + k) : V(1);
+                }
             } else {
                 r[j] = -1;
             }
@@ -653,7 +659,7 @@ void launch_direct_atomic(Context& ctx, const Matrix& m, Vector& x, int G, V* y)
     case GG:                                                                                 \
         col_direct_atomic_kernel<V, GG, SR><<<blocks, kNT, 0, ctx.stream>>>(                 \
             x.nnz, x.sp_idx.as<int32_t>(), x.sp_val.as<V>(), m.col_off.as<int64_t>(),        \
-            m.row_idx.as<int32_t>(), m.cvals.as<V>(), y, ctx.ctr);                           \
+            m.row_idx.as<int32_t>(), m.cvals.as<V>(), m.cpairs.as<uint2>(), y, ctx.ctr);     \
         break;
     switch (G) {
         ADA_G(1) ADA_G(2) ADA_G(4) ADA_G(8) ADA_G(16) ADA_G(32)

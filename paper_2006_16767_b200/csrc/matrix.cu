@@ -318,9 +318,26 @@ void compute_features(Context& ctx, Matrix& m) {
                             (k + 1.0) / k;
 }
 
+__global__ void csc_pairs_kernel(int64_t nnz, const int32_t* __restrict__ ri, const float* __restrict__ cv,
+                                 uint2* __restrict__ out) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz; k += stride)
+        out[k] = make_uint2(static_cast<uint32_t>(ri[k]), __float_as_uint(cv[k]));
+}
+
+// Matrix::cpairs of an fp32 matrix from its CSC
+void build_pairs(Context& ctx, Matrix& m) {
+    if (m.dtype != ADASPMV_F32 || m.nnz <= 0) return;
+    uint2* p = static_cast<uint2*>(m.cpairs.ensure(sizeof(uint2) * static_cast<size_t>(m.nnz)));
+    csc_pairs_kernel<<<grid_for(ctx, m.nnz, 256), 256, 0, ctx.stream>>>(m.nnz, m.row_idx.as<int32_t>(),
+                                                                       m.cvals.as<float>(), p);
+    ADA_LAUNCHED(ctx);
+}
+
 template <class V>
 void finish_matrix(Context& ctx, Matrix& m) {
     build_csc<V>(ctx, m);
+    build_pairs(ctx, m);
     build_tiles(ctx, m);
     compute_features(ctx, m);
     m.gather_spread = matrix_gather_spread(ctx, m);
@@ -444,6 +461,7 @@ Matrix* matrix_transpose(Context& ctx, const Matrix& src) {
         copy(m->col_off, src.row_off, sizeof(int64_t) * static_cast<size_t>(src.rows + 1));
         copy(m->row_idx, src.col_idx, sizeof(int32_t) * z);
         copy(m->cvals, src.vals, vb * z);
+        build_pairs(ctx, *m);
         build_tiles(ctx, *m);
         compute_features(ctx, *m);
         m->gather_spread = matrix_gather_spread(ctx, *m);
