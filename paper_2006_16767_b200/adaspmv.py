@@ -439,8 +439,8 @@ class Context:
         _check(_lib.adaspmv_ctx_set_counters(self.h, 1 if enable else 0))
 
     def set_bfs_loop(self, host_loop: bool = True):
-        """adaspmv_ctx_set_bfs_loop: True (default) = host-driven level loop,
-        False = device-resident (captured) BFS where it applies."""
+        """adaspmv_ctx_set_bfs_loop: True = host-driven level loop, False (the
+        context default) = the device-resident BFS graph where it applies."""
         _check(_lib.adaspmv_ctx_set_bfs_loop(self.h, int(bool(host_loop))))
 
     def set_timing(self, enable: bool = True):

@@ -18,13 +18,13 @@
 // three trees walked ON THE DEVICE over the same 13 features the host
 // selector reads (matrix features + nnz_x / x_sparsity / nnz_s / m_sparsity
 // from the frontier counters) -- is made by a one-warp kernel at the start
-// of the level.  Every kernel reads its sizes from device memory and exits
-// at once when its branch was not chosen, so a whole traversal is a fixed
-// launch sequence: it is captured once per (matrix, context, policy) into a
-// CUDA graph of kUnroll levels and replayed until the frontier is empty,
-// with ONE host synchronisation per replay (kUnroll levels) instead of one
-// per level.  Per-level reports (kernel, frontier size, effective nnz, device
-// time from %globaltimer) are logged on the device.
+// of the level.  The whole traversal is ONE CUDA graph built once per
+// (matrix, context, policy): a WHILE conditional node repeats a two-level
+// body; in each level the decision kernel sets IF(push) / IF(pull)
+// conditional handles so only the chosen branch's kernels run, every kernel
+// reading its sizes from device memory.  One graph launch and one host
+// synchronisation per traversal.  Per-level reports (kernel, frontier size,
+// effective nnz, device time from %globaltimer) are logged on the device.
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -32,12 +32,12 @@
 #include "device.cuh"
 #include "internal.hpp"
 #include "kernels.hpp"
+#include "prims.cuh"
 
 namespace ada {
 
 namespace {
 
-constexpr int kUnroll = 8;          // levels per graph replay (even: parity alternates)
 constexpr int kMaxLog = 1 << 16;    // per-level log capacity
 constexpr int kScanBlocks = 256;    // fixed grid of the eff-offset scan
 constexpr int kTile = 256;          // effective entries per push warp tile
@@ -54,9 +54,13 @@ struct alignas(8) BfsState {
     int kernel;                 // KernelId::index() selected for this level
     int done;
     int nlog;                   // levels logged
-    int pad;
+    int eff_ok;                 // the current frontier's eff offsets are valid (compaction / init wrote them)
+    long long tot;              // packed (count << kCntShift | nnz_s) of a pull level's compaction scan
+    int pending;                // a level ran since the last decision (its results not yet accounted)
+    int pad2;
 };
-static_assert(sizeof(BfsState) == 64, "BfsState is copied as 8 int64 words");
+static_assert(sizeof(BfsState) == 80, "BfsState is copied as 10 int64 words");
+constexpr int kCntShift = 36;  // pull compaction packing: nnz_s < 2^36, frontier < 2^27
 
 struct LogEntry {               // one row of adaspmv_iteration_report
     long long nnz_x, nnz_s;
@@ -91,11 +95,33 @@ __device__ int tree_walk(const DevTrees& t, int which, const double* f) {
 }
 
 // Start of a level: decide push / pull for the frontier of parity p.
+// The level's branch is selected by setting the graph's conditional
+// handles: IF(push) and IF(pull) bodies (only the chosen one runs), and the
+// WHILE handle that repeats the two-level body until the frontier is empty.
 __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees trees, int use_trees,
-                                  const double* mfeat, int64_t n, int64_t nnz, int vbytes) {
+                                  const double* mfeat, int64_t n, int64_t nnz, int vbytes, int64_t* eff,
+                                  cudaGraphConditionalHandle heff, cudaGraphConditionalHandle hpush,
+                                  cudaGraphConditionalHandle hpull, cudaGraphConditionalHandle hwhile) {
     if (threadIdx.x != 0) return;
+    cudaGraphSetConditional(heff, 0);
+    cudaGraphSetConditional(hpush, 0);
+    cudaGraphSetConditional(hpull, 0);
+    if (st->pending) {  // account for the level that produced this frontier
+        if (st->mode == kModePull) {  // its compaction scan's packed total; eff offsets written by the scan
+            const long long t = st->tot;
+            st->nf[p] = static_cast<unsigned long long>(t >> kCntShift);
+            st->ns[p] = static_cast<unsigned long long>(t & ((1ll << kCntShift) - 1));
+            eff[st->nf[p]] = static_cast<int64_t>(st->ns[p]);
+            st->eff_ok = 1;
+        } else {  // a push appended it (counters already set), unordered: offsets to be scanned
+            st->eff_ok = 0;
+        }
+        st->visited += static_cast<long long>(st->nf[p]);
+        st->pending = 0;
+    }
     if (st->done) {
         st->mode = kModeDone;
+        cudaGraphSetConditional(hwhile, 0);
         return;
     }
     const unsigned long long nf = st->nf[p], ns = st->ns[p];
@@ -103,6 +129,7 @@ __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees t
     if (nf == 0) {
         st->done = 1;
         st->mode = kModeDone;
+        cudaGraphSetConditional(hwhile, 0);
         if (st->nlog < kMaxLog) log[st->nlog].t0 = now;  // end stamp of the last level
         return;
     }
@@ -131,9 +158,13 @@ __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees t
     }
     st->kernel = k;
     st->mode = k >= 4 ? kModePush : kModePull;
+    cudaGraphSetConditional(k >= 4 ? hpush : hpull, 1);
+    if (k >= 4 && !st->eff_ok) cudaGraphSetConditional(heff, 1);
     st->level += 1;
     st->nf[p ^ 1] = 0;
     st->ns[p ^ 1] = 0;
+    st->tot = 0;
+    st->pending = 1;
     if (st->nlog < kMaxLog) {
         LogEntry& e = log[st->nlog];
         e.nnz_x = static_cast<long long>(nf);
@@ -143,11 +174,6 @@ __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees t
         e.t0 = now;
     }
     st->nlog += 1;
-}
-
-// End of a level: count the discovered vertices.
-__global__ void bfs_account_kernel(BfsState* st, int p) {
-    if (threadIdx.x == 0 && st->mode != kModeDone) st->visited += static_cast<long long>(st->nf[p ^ 1]);
 }
 
 // ---- eff offsets of the frontier (push only): fixed-grid reduce-then-scan
@@ -318,60 +344,61 @@ __global__ void __launch_bounds__(256) bfs_push_kernel(BfsState* st, int p, cons
     }
 }
 
-// Frontier bitmap of a pull level (n/8 bytes, L2-resident) from the frontier
-// list; cleared again by the same list after the pull, so it is all zero
-// between pull levels.
-__global__ void __launch_bounds__(256) bfs_fmask_kernel(const BfsState* st, int p, const int32_t* __restrict__ f,
-                                                        uint32_t* __restrict__ fm, int set) {
-    if (st->mode != kModePull) return;
-    const long long n = static_cast<long long>(st->nf[p]);
-    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += static_cast<long long>(gridDim.x) * 256) {
-        const int32_t c = f[i];
-        if (set) atomicOr(fm + (c >> 5), 1u << (c & 31));
-        else fm[c >> 5] = 0u;
-    }
-}
-
 // Output-masked pull with early exit (bfs.cu bfs_pull_kernel), G lanes per
-// row, grid-stride; frontier membership from the level's bitmap.
+// row, one group per row (full grid: the block scheduler balances rows that
+// run long); a row with a frontier neighbour (a column of the previous
+// level, read from the level array: no frontier bitmap to build and clear)
+// gets its level.
+// The next frontier is then compacted by a scan over the levels (no shared
+// append counter: the fat pull levels would serialise on it).
 template <int G>
-__global__ void __launch_bounds__(256) bfs_pull_dev_kernel(BfsState* st, int p, int64_t rows,
-                                                           const int64_t* __restrict__ ro,
-                                                           const int32_t* __restrict__ ci,
-                                                           const int64_t* __restrict__ co,
-                                                           const uint32_t* __restrict__ fm,
-                                                           int32_t* __restrict__ lv, int32_t* __restrict__ nf_out) {
-    if (st->mode != kModePull) return;
-    const int level = st->level;
-    const int q = p ^ 1;
+__global__ void __launch_bounds__(256) bfs_pull_mark_kernel(const BfsState* st, int64_t rows,
+                                                            const int64_t* __restrict__ ro,
+                                                            const int32_t* __restrict__ ci,
+                                                            int32_t* __restrict__ lv) {
+    const int level = st->level;  // frontier = the vertices of level - 1
     const int lane = threadIdx.x & 31;
     const int lg = threadIdx.x & (G - 1);
-    const long long stride = static_cast<long long>(gridDim.x) * (256 / G);
-    for (long long row0 = static_cast<long long>(blockIdx.x) * (256 / G); row0 < rows; row0 += stride) {
-        const long long row = row0 + (threadIdx.x / G);
-        const bool live = row < rows && lv[row] < 0;
-        bool hit = false;
-        if (live) {
-            const long long b = __ldg(ro + row), e = __ldg(ro + row + 1);
-            for (long long k0 = b + lg; k0 < e && !hit; k0 += G * 4) {
-                int c[4];
+    const long long row = (static_cast<long long>(blockIdx.x) * 256 + threadIdx.x) / G;
+    const bool live = row < rows && lv[row] < 0;
+    bool hit = false;
+    if (live) {
+        const long long b = __ldg(ro + row), e = __ldg(ro + row + 1);
+        for (long long k0 = b + lg; k0 < e && !hit; k0 += G * 4) {
+            int c[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) c[j] = k0 + j * G < e ? __ldg(ci + k0 + j * G) : -1;
+            for (int j = 0; j < 4; ++j) c[j] = k0 + j * G < e ? __ldg(ci + k0 + j * G) : -1;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) hit = hit || (c[j] >= 0 && ((__ldg(fm + (c[j] >> 5)) >> (c[j] & 31)) & 1u));
-            }
+            for (int j = 0; j < 4; ++j) hit = hit || (c[j] >= 0 && lv[c[j]] == level - 1);
         }
-        // OR over the row's G lanes; the group leader appends
-        const unsigned grp = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
-        const bool any = (__ballot_sync(kFull, hit) & grp) != 0u;
-        const bool claim = live && any && lg == 0;
-        if (claim) lv[row] = level;
-        append_claimed(claim, static_cast<int32_t>(row), co, st, q, nf_out, lane);
     }
+    const unsigned grp = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const bool any = (__ballot_sync(kFull, hit) & grp) != 0u;
+    if (live && any && lg == 0) lv[row] = level;
 }
 
+// compaction items: (row joined at this level) << kCntShift | its column degree
+struct LevelIn {
+    const int32_t* lv;
+    const int* level;
+    const int64_t* co;
+    __device__ int64_t operator()(int64_t r) const {
+        return lv[r] == *level ? (int64_t(1) << kCntShift) | (co[r + 1] - co[r]) : 0;
+    }
+};
+struct LevelEpi {  // the next frontier and its eff offsets (degree prefix)
+    int32_t* out;
+    int64_t* eff;
+    __device__ void operator()(int64_t r, int64_t p, int64_t v) const {
+        if (!v) return;
+        const int64_t slot = p >> kCntShift;
+        out[slot] = static_cast<int32_t>(r);
+        eff[slot] = p & ((int64_t(1) << kCntShift) - 1);
+    }
+};
+
 __global__ void bfs_init_kernel(BfsState* st, int32_t* lv, int64_t n, int64_t source, int32_t* f0,
-                                const int64_t* __restrict__ co) {
+                                const int64_t* __restrict__ co, int64_t* __restrict__ eff) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
         lv[i] = i == source ? 0 : -1;
@@ -386,6 +413,11 @@ __global__ void bfs_init_kernel(BfsState* st, int32_t* lv, int64_t n, int64_t so
         st->kernel = -1;
         st->done = 0;
         st->nlog = 0;
+        st->tot = 0;
+        st->pending = 0;
+        st->eff_ok = 1;
+        eff[0] = 0;
+        eff[1] = static_cast<int64_t>(st->ns[0]);
     }
 }
 
@@ -395,8 +427,9 @@ __global__ void bfs_init_kernel(BfsState* st, int32_t* lv, int64_t n, int64_t so
 struct BfsPlan {
     cudaStream_t stream = nullptr;
     uint64_t bundle_id = 0;  // 0 = heuristic
-    DevBuf state, log, f[2], eff, part, lv, fm, trees_i, trees_d, mfeat;
+    DevBuf state, log, f[2], eff, part, lv, trees_i, trees_d, mfeat;
     DevTrees dt{};
+    DevBuf scan_tmp;  // the pull compaction's tile sums (sized before capture)
     cudaGraphExec_t exec = nullptr;
     ~BfsPlan() {
         if (exec) cudaGraphExecDestroy(exec);
@@ -449,13 +482,47 @@ void upload_trees(Context& ctx, const Bundle& b, BfsPlan& P) {
 }
 
 template <int G>
-void launch_pull_g(cudaStream_t s, unsigned grid, BfsState* st, int p, const Matrix& m, const uint32_t* fm,
-                   int32_t* lv, int32_t* out) {
-    bfs_pull_dev_kernel<G><<<grid, 256, 0, s>>>(st, p, m.rows, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(),
-                                                m.col_off.as<int64_t>(), fm, lv, out);
+void launch_pull_mark(cudaStream_t s, unsigned grid, BfsState* st, const Matrix& m, int32_t* lv) {
+    bfs_pull_mark_kernel<G><<<grid, 256, 0, s>>>(st, m.rows, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), lv);
 }
 
-// Captures kUnroll levels (parity 0, 1, 0, ...) into a graph.
+// Appends IF(handle) to the graph being captured on `s`; its body is
+// captured from `body` on the side stream `s2` (the library's kernels take
+// the context's stream, so it is swapped for the duration).
+template <class F>
+void capture_if(Context& ctx, cudaStream_t s, cudaStream_t s2, cudaGraphConditionalHandle h, F body) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    ADA_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd));
+    cudaGraphNodeParams ip{};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = h;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t node;
+    ADA_CUDA(cudaGraphAddNode(&node, g, deps, nd, &ip));
+    ADA_CUDA(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t bg = ip.conditional.phGraph_out[0];
+    ADA_CUDA(cudaStreamBeginCaptureToGraph(s2, bg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    const cudaStream_t keep = ctx.stream;
+    ctx.stream = s2;
+    try {
+        body(s2);
+    } catch (...) {
+        ctx.stream = keep;
+        cudaStreamEndCapture(s2, &bg);
+        throw;
+    }
+    ctx.stream = keep;
+    ADA_CUDA(cudaStreamEndCapture(s2, &bg));
+}
+
+// The whole traversal as ONE graph: WHILE(frontier) { level p = 0; level
+// p = 1 }, a level being decide -> IF(push) {eff offsets, push} -> IF(pull)
+// {frontier bitmap, pull, compaction scan, bitmap clear} -> account.  Only
+// the chosen branch's kernels run; sizes live on the device.
 void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     const int64_t n = m.rows;
     P.stream = ctx.stream;
@@ -466,9 +533,7 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     P.eff.ensure(sizeof(int64_t) * static_cast<size_t>(n + 1));
     P.part.ensure(sizeof(long long) * kScanBlocks);
     P.lv.ensure(sizeof(int32_t) * static_cast<size_t>(n));
-    uint32_t* fm = static_cast<uint32_t*>(P.fm.ensure(sizeof(uint32_t) * static_cast<size_t>((n + 31) / 32)));
-    ADA_CUDA(cudaMemsetAsync(fm, 0, sizeof(uint32_t) * static_cast<size_t>((n + 31) / 32), ctx.stream));
-    const unsigned fm_grid = static_cast<unsigned>(ctx.sm_count) * 4;
+    P.scan_tmp.ensure(sizeof(int64_t) * static_cast<size_t>((n + kScanTile - 1) / kScanTile + 1));
     double* mf = static_cast<double*>(P.mfeat.ensure(sizeof(double) * 9));
     ADA_CUDA(cudaMemcpyAsync(mf, m.feat, sizeof(double) * 9, cudaMemcpyHostToDevice, ctx.stream));
     if (b) upload_trees(ctx, *b, P);
@@ -478,47 +543,70 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     int32_t* lv = P.lv.as<int32_t>();
     const int64_t* co = m.col_off.as<int64_t>();
     const unsigned push_grid = static_cast<unsigned>(ctx.sm_count) * 8;
-    // pull: G lanes per row (early exit: a row usually stops within its first
-    // entries)
     const int G = std::max(1, default_lanes_per_row(m.feat[5]) / 8);
-    // one group per row (a full grid, as the host loop's pull): the block
-    // scheduler balances rows that run long (no frontier neighbour, no early
-    // exit) -- a capped grid-stride grid measured 6-7x slower on C3's pull levels
     const unsigned pull_grid = static_cast<unsigned>(std::max<int64_t>((n * G + 255) / 256, 1));
     cudaGraph_t graph = nullptr;
-    ADA_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
+    ADA_CUDA(cudaGraphCreate(&graph, 0));
+    cudaStream_t s2 = nullptr;
+    ADA_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    struct Cleanup {
+        cudaGraph_t* g;
+        cudaStream_t s;
+        ~Cleanup() {
+            if (*g) cudaGraphDestroy(*g);
+            cudaStreamDestroy(s);
+        }
+    } cleanup{&graph, s2};
+    cudaGraphConditionalHandle hw, heff[2], hpush[2], hpull[2];
+    ADA_CUDA(cudaGraphConditionalHandleCreate(&hw, graph, 1, cudaGraphCondAssignDefault));
+    for (int q = 0; q < 2; ++q) {
+        ADA_CUDA(cudaGraphConditionalHandleCreate(&heff[q], graph, 0, cudaGraphCondAssignDefault));
+        ADA_CUDA(cudaGraphConditionalHandleCreate(&hpush[q], graph, 0, cudaGraphCondAssignDefault));
+        ADA_CUDA(cudaGraphConditionalHandleCreate(&hpull[q], graph, 0, cudaGraphCondAssignDefault));
+    }
+    cudaGraphNodeParams wp{};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = hw;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    ADA_CUDA(cudaGraphAddNode(&wnode, graph, nullptr, 0, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    cudaStream_t s = ctx.stream;
+    ADA_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     try {
-        for (int L = 0; L < kUnroll; ++L) {
-            const int p = L & 1;
-            bfs_decide_kernel<<<1, 32, 0, ctx.stream>>>(st, lg, p, P.dt, b ? 1 : 0, mf, n, m.nnz, m.vbytes());
-            bfs_eff_partial_kernel<<<kScanBlocks, 256, 0, ctx.stream>>>(st, p, P.f[p].as<int32_t>(), co,
-                                                                        P.part.as<long long>());
-            bfs_eff_top_kernel<<<1, kScanBlocks, 0, ctx.stream>>>(st, P.part.as<long long>());
-            bfs_eff_write_kernel<<<kScanBlocks, 256, 0, ctx.stream>>>(st, p, P.f[p].as<int32_t>(), co,
-                                                                      P.part.as<long long>(), P.eff.as<int64_t>());
-            bfs_push_kernel<<<push_grid, 256, 0, ctx.stream>>>(st, p, P.f[p].as<int32_t>(), P.eff.as<int64_t>(), co,
-                                                               m.row_idx.as<int32_t>(), lv, P.f[p ^ 1].as<int32_t>());
-            int32_t* out = P.f[p ^ 1].as<int32_t>();
-            bfs_fmask_kernel<<<fm_grid, 256, 0, ctx.stream>>>(st, p, P.f[p].as<int32_t>(), fm, 1);
-            switch (G) {
-                case 1: launch_pull_g<1>(ctx.stream, pull_grid, st, p, m, fm, lv, out); break;
-                case 2: launch_pull_g<2>(ctx.stream, pull_grid, st, p, m, fm, lv, out); break;
-                case 4: launch_pull_g<4>(ctx.stream, pull_grid, st, p, m, fm, lv, out); break;
-                default: launch_pull_g<8>(ctx.stream, pull_grid, st, p, m, fm, lv, out); break;
-            }
-            bfs_fmask_kernel<<<fm_grid, 256, 0, ctx.stream>>>(st, p, P.f[p].as<int32_t>(), fm, 0);
-            bfs_account_kernel<<<1, 32, 0, ctx.stream>>>(st, p);
+        for (int p = 0; p < 2; ++p) {
+            bfs_decide_kernel<<<1, 32, 0, s>>>(st, lg, p, P.dt, b ? 1 : 0, mf, n, m.nnz, m.vbytes(),
+                                               P.eff.as<int64_t>(), heff[p], hpush[p], hpull[p], hw);
+            capture_if(ctx, s, s2, heff[p], [&](cudaStream_t cs) {  // a push after a push: scan the offsets
+                bfs_eff_partial_kernel<<<kScanBlocks, 256, 0, cs>>>(st, p, P.f[p].as<int32_t>(), co,
+                                                                    P.part.as<long long>());
+                bfs_eff_top_kernel<<<1, kScanBlocks, 0, cs>>>(st, P.part.as<long long>());
+                bfs_eff_write_kernel<<<kScanBlocks, 256, 0, cs>>>(st, p, P.f[p].as<int32_t>(), co,
+                                                                  P.part.as<long long>(), P.eff.as<int64_t>());
+            });
+            capture_if(ctx, s, s2, hpush[p], [&](cudaStream_t cs) {
+                bfs_push_kernel<<<push_grid, 256, 0, cs>>>(st, p, P.f[p].as<int32_t>(), P.eff.as<int64_t>(), co,
+                                                           m.row_idx.as<int32_t>(), lv, P.f[p ^ 1].as<int32_t>());
+            });
+            capture_if(ctx, s, s2, hpull[p], [&](cudaStream_t cs) {
+                switch (G) {
+                    case 1: launch_pull_mark<1>(cs, pull_grid, st, m, lv); break;
+                    case 2: launch_pull_mark<2>(cs, pull_grid, st, m, lv); break;
+                    case 4: launch_pull_mark<4>(cs, pull_grid, st, m, lv); break;
+                    default: launch_pull_mark<8>(cs, pull_grid, st, m, lv); break;
+                }
+                scan3(ctx, n, LevelIn{lv, &st->level, co}, LevelEpi{P.f[p ^ 1].as<int32_t>(), P.eff.as<int64_t>()},
+                      reinterpret_cast<int64_t*>(&st->tot), P.scan_tmp);
+            });
         }
         ADA_CUDA(cudaGetLastError());
     } catch (...) {
-        cudaStreamEndCapture(ctx.stream, &graph);
-        if (graph) cudaGraphDestroy(graph);
+        cudaStreamEndCapture(s, &body);
         throw;
     }
-    ADA_CUDA(cudaStreamEndCapture(ctx.stream, &graph));
-    const cudaError_t e = cudaGraphInstantiate(&P.exec, graph, 0);
-    cudaGraphDestroy(graph);
-    ADA_CUDA(e);
+    ADA_CUDA(cudaStreamEndCapture(s, &body));
+    ADA_CUDA(cudaGraphInstantiate(&P.exec, graph, 0));
 }
 
 }  // namespace
@@ -537,22 +625,17 @@ void bfs_graph(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, i
     BfsState* st = P.state.as<BfsState>();
     const unsigned ig = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 16));
     bfs_init_kernel<<<ig, 256, 0, ctx.stream>>>(st, P.lv.as<int32_t>(), n, source, P.f[0].as<int32_t>(),
-                                                m.col_off.as<int64_t>());
+                                                m.col_off.as<int64_t>(), P.eff.as<int64_t>());
     ADA_LAUNCHED(ctx);
-    // replay kUnroll levels at a time; one synchronisation per replay reads
-    // the done flag (copied into the mapped host scalars by the last kernel)
-    int64_t replays = 0;
-    for (;;) {
-        ADA_CUDA(cudaGraphLaunch(P.exec, ctx.stream));
-        ctx.launches += kUnroll * 9;
-        ++replays;
-        copy_scalars_kernel_launch(ctx, reinterpret_cast<const int64_t*>(st), ctx.h_scalars_dev,
-                                   static_cast<int>(sizeof(BfsState) / sizeof(int64_t)));
-        ctx.sync();
-        const BfsState* hs = reinterpret_cast<const BfsState*>(ctx.h_scalars);
-        if (hs->done) break;
-        if (replays > (n / kUnroll) + 2) throw Error(ADASPMV_ERR_INTERNAL, "bfs: level loop did not terminate");
-    }
+    // the whole traversal: one graph launch, one synchronisation (the state
+    // comes back through the mapped host scalars)
+    ADA_CUDA(cudaGraphLaunch(P.exec, ctx.stream));
+    ++ctx.launches;
+    copy_scalars_kernel_launch(ctx, reinterpret_cast<const int64_t*>(st), ctx.h_scalars_dev,
+                               static_cast<int>(sizeof(BfsState) / sizeof(int64_t)));
+    ctx.sync();
+    if (!reinterpret_cast<const BfsState*>(ctx.h_scalars)->done)
+        throw Error(ADASPMV_ERR_INTERNAL, "bfs: device level loop ended without an empty frontier");
     const BfsState* hs = reinterpret_cast<const BfsState*>(ctx.h_scalars);
     const int nlog = hs->nlog;
     *n_levels = nlog;

@@ -100,7 +100,7 @@ struct Context {
     int64_t launches = 0;
     bool timing = false;  // bracket every run with CUDA events (adaspmv_output_elapsed)
     bool counters = false;  // KernelCounters per run (adaspmv_ctx_set_counters)
-    bool bfs_host_loop = true;  // adaspmv_ctx_set_bfs_loop: host-driven BFS level loop (default) or the captured one
+    bool bfs_host_loop = false;  // adaspmv_ctx_set_bfs_loop: host-driven BFS level loop, or the device graph (default)
     unsigned long long* ctr = nullptr;  // the running output's device counters (kernels' last argument)
     // general scratch (reused by every call; calls on a context are serialised)
     // [0..3] sort write-back keys/values (double buffered), [4] vector scans,
