@@ -29,15 +29,17 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
+// Items of a tile are read STRIPED (item base + j*kScanThreads + t to thread
+// t, j < kScanItems), so each warp load covers 32 consecutive items.
 template <class In>
 __global__ void __launch_bounds__(kScanThreads) scan_tile_sums_kernel(int64_t n, In in,
                                                                        int64_t* tile_sums) {
     __shared__ int64_t sm[kScanThreads / 32 + 1];
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x;
     int64_t s = 0;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j)
-        if (base + j < n) s += in(base + j);
+        if (base + j * kScanThreads < n) s += in(base + j * kScanThreads);
     int64_t total;
     (void)block_exclusive_sum<kScanThreads>(s, sm, &total);
     if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
@@ -52,24 +54,41 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(int64_t n, In 
                                                                   const int64_t* tile_offsets,
                                                                   int64_t* d_total,
                                                                   int single) {
-    __shared__ int64_t sm[kScanThreads / 32 + 1];
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
-    int64_t v[kScanItems];
-    int64_t s = 0;
+    // striped items: row j of the tile = items [j*256, (j+1)*256), warp w
+    // holds its 32-item slice; prefixes: warp scan within the slice, then
+    // the slices' totals in (row, warp) order
+    constexpr int NW = kScanThreads / 32;
+    __shared__ int64_t wt[kScanItems * NW];
+    __shared__ int64_t woff[kScanItems * NW + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x;
+    int64_t v[kScanItems], inc[kScanItems];
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        v[j] = base + j < n ? in(base + j) : 0;
-        s += v[j];
+        const int64_t i = base + j * kScanThreads;
+        v[j] = i < n ? in(i) : 0;
+        inc[j] = warp_inclusive_sum(v[j]);
+        if (lane == 31) wt[j * NW + warp] = inc[j];
     }
-    int64_t total;
-    int64_t p = block_exclusive_sum<kScanThreads>(s, sm, &total);
-    if (!single) p += tile_offsets[blockIdx.x];
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the kScanItems * NW slice totals (64 <= 2 per lane)
+        static_assert(kScanItems * NW == 64, "two slice totals per lane");
+        const int64_t a = wt[2 * lane], b = wt[2 * lane + 1];
+        const int64_t pair = a + b;
+        const int64_t pinc = warp_inclusive_sum(pair);
+        const int64_t pex = pinc - pair;
+        woff[2 * lane] = pex;
+        woff[2 * lane + 1] = pex + a;
+        if (lane == 31) woff[kScanItems * NW] = pinc;
+    }
+    __syncthreads();
+    const int64_t off = single ? 0 : tile_offsets[blockIdx.x];
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        if (base + j < n) epi(base + j, p, v[j]);
-        p += v[j];
+        const int64_t i = base + j * kScanThreads;
+        if (i < n) epi(i, off + woff[j * NW + warp] + inc[j] - v[j], v[j]);
     }
-    if (single && threadIdx.x == 0 && d_total) *d_total = total;
+    if (single && threadIdx.x == 0 && d_total) *d_total = woff[kScanItems * NW];
 }
 
 __global__ void scan_zero_kernel(int64_t* p);
