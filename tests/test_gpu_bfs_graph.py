@@ -4,7 +4,7 @@ for every semiring on pattern matrices and OR_AND on valued ones, under the
 built-in policy and the trained selector (whose trees are walked on the
 device: its per-level choices must equal the host selector's on the same
 frontiers), on graphs deeper than one graph replay (kUnroll = 8 levels),
-disconnected graphs and isolated sources."""
+disconnected graphs, isolated sources and a 3001-level path."""
 import numpy as np
 import pytest
 
@@ -56,9 +56,10 @@ def test_device_loop_levels(ctx, port, name, n, ro, ci, sr):
     m = A.DualMatrix.from_csr(n, n, ro, ci, None, dtype=np.float32, ctx=ctx)
     co, ri, _ = port.csr_to_csc(n, n, ro, ci, np.ones(len(ci)))
     bundle = A.SelectorBundle.load(S.DEFAULT_PATH)
+    bundle_v2 = A.SelectorBundle.load(S.DEFAULT_PATH.parent / "b200_bundle_v2.txt")  # schema 2 on the device
     for src in sorted({0, n - 1, 3 % n}):
         exp, nl = port.bfs_queue(n, co, ri, src)
-        for kw in (dict(), dict(bundle=bundle)):
+        for kw in (dict(), dict(bundle=bundle), dict(bundle=bundle_v2)):
             ctx.set_bfs_loop(False)
             lv, reps = A.bfs(m, src, sr, **kw)
             assert np.array_equal(lv, exp), (name, src, kw.keys())
@@ -88,3 +89,15 @@ def test_device_loop_valued_or_and_and_levels_download_optional(ctx, port):
     # valued matrix under plus-times: values decide y_i != 0, so the host loop runs
     lv, reps = A.bfs(m, 0, A.PLUS_TIMES)
     assert all(r["exec_mode"] != A.EXEC_FUSED_PUSH_LB or r["kernel"] >= 4 for r in reps)
+
+
+def test_device_loop_deep_path(ctx, port):
+    """3001 levels: the graph's WHILE node runs 1501 two-level bodies."""
+    n = 3001
+    ro, ci = _sym(n, [(i, i + 1) for i in range(n - 1)])
+    m = A.DualMatrix.from_csr(n, n, ro, ci, None, dtype=np.float32, ctx=ctx)
+    ctx.set_bfs_loop(False)
+    lv, reps = A.bfs(m, 0, A.OR_AND)
+    assert np.array_equal(lv, np.arange(n)) and len(reps) == n
+    lv, reps = A.bfs(m, n // 2, A.MIN_PLUS)
+    assert np.array_equal(lv, np.abs(np.arange(n) - n // 2)) and len(reps) == n // 2 + 1
