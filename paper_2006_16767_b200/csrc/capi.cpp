@@ -1,7 +1,6 @@
 // capi.cpp -- the extern "C" boundary (include/adaspmv_cuda.h).  Every entry
 // point catches exceptions and returns an adaspmv_status; the message of the
 // last failure is kept per thread (adaspmv_last_error).
-#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -30,7 +30,6 @@
 
 #include <algorithm>
 #include <array>
-#include <cstdlib>
 #include <functional>
 #include <numeric>
 #include <vector>
