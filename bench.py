@@ -597,6 +597,15 @@ def run_ours_multi(args, rank, world):
             "clocks": clk.summary(),
             "setup_s": {"generate": round(gen_s, 1)},
         }
+    if "C5" in args.configs.split(","):
+        del m
+        torch.cuda.empty_cache()
+        try:
+            c5 = ours_c5(local, rank, world, bundle, peaks()[0], ctx, stream, dist=dist)
+        except Exception as e:  # never lose the headline line to the largest config
+            c5 = {"error": f"{type(e).__name__}: {e}"}
+        if rank == 0:
+            line["configs"] = {"C5": c5}
     dist.destroy_process_group()
     return line
 
@@ -835,6 +844,159 @@ def ours_c4(local, bundle, hbm, flush, cpu, reps=3):
     torch.cuda.empty_cache()
     if cpu:
         res["cpu_reference"] = cpu_c4(c4h, pts)
+    return res
+
+
+C5_SCALE = int(os.environ.get("ADASPMV_BENCH_C5_SCALE", "26"))  # override only for dry runs
+C5_DENS = (0.00001, 0.001, 0.1, 1.0)
+
+
+def ours_c5(local, rank, world, bundle, hbm, ctx, stream, dist=None, reps=3):
+    """C5 (configs[4]): R-MAT scale 26 (device generator, ~2.1 G stored
+    entries) cut into `world` nnz-balanced row blocks (adaspmv_shard_rows,
+    partition.hpp:30-33), one per rank.  Per x density: x drawn on rank 0 and
+    broadcast over NCCL (N > 1), each rank's selector + multiply on its block;
+    time = broadcast (events) + multiply (library events), max over ranks.
+    BFS from vertex 0 (OR_AND): N = 1 the device-graph BFS, N > 1 the
+    row-partitioned BFS with the frontier all-gathered every level
+    (adaspmv_dist_bfs); wall time max over ranks.  No CPU reference at this
+    size (the reference BFS on 2.1 G edges takes minutes)."""
+    import torch
+
+    from paper_2006_16767_b200 import adaspmv as A
+    from paper_2006_16767_b200 import synth_device as SD
+    dev = torch.device("cuda", local)
+    t0 = time.time()
+    n, ro, ci = SD.rmat_device(C5_SCALE)
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+    nnz_all = int(ro[-1].item())
+    ro_h = ro.cpu().numpy()
+    cuts = A.shard_rows(ro_h, world)
+    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    b0, b1 = int(ro_h[r0]), int(ro_h[r1])
+    bro = (ro[r0:r1 + 1] - b0).contiguous()
+    bci = ci[b0:b1].clone() if world > 1 else ci
+    ro = ci = None
+    torch.cuda.empty_cache()
+    t0 = time.time()
+    m = A.DualMatrix.from_device(r1 - r0, n, b1 - b0, bro.data_ptr(), bci.data_ptr(), None, np.float32, ctx)
+    ctx.synchronize()
+    build_s = time.time() - t0
+    del bro, bci
+    torch.cuda.empty_cache()
+    deg_h = np.diff(ro_h[r0:r1 + 1])
+    x = A.DeviceVector(n, np.float32, ctx)
+    out = A.MultiplyOutput(ctx)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(26)
+    pts = []
+    ctx.set_timing(True)
+    for d in C5_DENS:
+        # x: rank 0 draws the support and values, the others receive them
+        nx = torch.zeros(1, dtype=torch.int64, device=dev)
+        if rank == 0:
+            if d >= 1.0:
+                idx = torch.arange(n, dtype=torch.int32, device=dev)
+            else:
+                idx = torch.nonzero(torch.rand(n, generator=gen, device=dev) < d).flatten().to(torch.int32)
+            val = torch.rand(idx.numel(), generator=gen, device=dev, dtype=torch.float32) + 0.5
+            nx[0] = idx.numel()
+        if dist is not None:
+            dist.broadcast(nx, 0)
+        k_x = int(nx.item())
+        if rank != 0:
+            idx = torch.empty(k_x, dtype=torch.int32, device=dev)
+            val = torch.empty(k_x, dtype=torch.float32, device=dev)
+
+        def exchange():
+            if dist is not None:
+                dist.broadcast(idx, 0)
+                dist.broadcast(val, 0)
+
+        exchange()
+        torch.cuda.synchronize()
+        x.set_sparse_device(k_x, idx.data_ptr(), val.data_ptr())
+        nnz_s_local = A.effective_nnz(m, x)
+        k = A.predict_kernel(m, x, bundle)[0].index()
+        x.prepare(k)
+        A.run_kernel(m, k, x, out=out)  # lazy layouts before timing
+        ts = []
+        for _ in range(reps):
+            torch.cuda._sleep(GATE_CYCLES)
+            ev[0].record(stream)
+            exchange()
+            ev[1].record(stream)
+            x.set_sparse_device(k_x, idx.data_ptr(), val.data_ptr())
+            x.prepare(k)
+            torch.cuda._sleep(GATE_CYCLES)
+            A.run_kernel(m, k, x, out=out)
+            ts.append(out.elapsed() + ev[0].elapsed_time(ev[1]) * 1e-3)
+        t = statistics.median(ts)
+        tt = torch.tensor([t, float(nnz_s_local)], dtype=torch.float64, device=dev)
+        if dist is not None:
+            tmax = tt.clone()
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+            t, nnz_s = float(tmax[0].item()), int(tt[1].item())
+        else:
+            nnz_s = nnz_s_local
+        b_alg, _ = alg_bytes(n, n, nnz_all, k_x, nnz_s, 0)
+        pts.append({"x_sparsity": d, "nnz_x": k_x, "nnz_s": nnz_s, "selected_rank0": A_name(k),
+                    "ms": round(t * 1e3, 4), "gflops": round(2 * nnz_s / t / 1e9, 2),
+                    "alg_GBps": round(b_alg / t / 1e9, 1),
+                    "roofline_frac_aggregate": round(b_alg / t / 1e9 / (hbm * world), 4)})
+    ctx.set_timing(False)
+    # BFS from vertex 0
+    walls = []
+    if dist is None:
+        lv, _ = A.bfs(m, 0, A.OR_AND)
+        for _ in range(reps):
+            ctx.synchronize()
+            t1 = time.perf_counter()
+            A.bfs(m, 0, A.OR_AND, download_levels=False)
+            walls.append(time.perf_counter() - t1)
+        levels = lv
+    else:
+        from paper_2006_16767_b200.multigpu import make_dist
+        D = make_dist(ctx)
+        try:
+            levels, _ = D.bfs(m, r0, 0, A.OR_AND)
+            for _ in range(reps):
+                dist.barrier()
+                torch.cuda.synchronize()
+                t1 = time.perf_counter()
+                D.bfs(m, r0, 0, A.OR_AND, download_levels=False)
+                torch.cuda.synchronize()
+                walls.append(time.perf_counter() - t1)
+        finally:
+            D.close()
+    reached = levels >= 0
+    loc = torch.tensor([float(reached.sum()), float(deg_h[reached].sum()), float(levels.max() + 1),
+                        statistics.median(walls)], dtype=torch.float64, device=dev)
+    if dist is not None:
+        tot = loc.clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        mx = loc.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        reached_n, edges, nlev, wall = int(tot[0].item()), int(tot[1].item()), int(mx[2].item()), float(mx[3].item())
+    else:
+        reached_n, edges, nlev, wall = int(loc[0].item()), int(loc[1].item()), int(loc[2].item()), float(loc[3].item())
+    flops = sum(2 * p_["nnz_s"] for p_ in pts)
+    res = {"workload": f"C5 R-MAT scale {C5_SCALE} (device generator), {nnz_all:,} stored entries, "
+                       f"{world} nnz-balanced row block(s), fp32 pattern values",
+           "n": n, "nnz": nnz_all, "n_gpus": world, "shard_rows": [int(c) for c in cuts],
+           "timing": "per point: x broadcast (events, N > 1) + multiply (library events), GPU gated, median of "
+                     f"{reps}, max over ranks; BFS wall time, max over ranks",
+           "points": pts, "value": round(flops / sum(p_["ms"] * 1e-3 for p_ in pts) / 1e9, 3), "unit": "GFLOP/s",
+           "bfs": {"ms": round(wall * 1e3, 4), "gteps": round(edges / wall / 1e9, 2), "levels": nlev,
+                   "reached": reached_n, "edges_traversed": edges,
+                   "mode": "device-graph BFS" if dist is None else "row-partitioned BFS, frontier all-gathered"},
+           "setup_s": {"generate": round(gen_s, 2), "build": round(build_s, 2)},
+           "cpu_reference": None}
+    del m, x, out
+    torch.cuda.empty_cache()
     return res
 
 
@@ -1080,6 +1242,15 @@ def run_ours(args, rank, world):
             cfgs["C3"] = ours_c3(local, bundle, hbm_peak, cpu)
         if "C4" in want:
             cfgs["C4"] = ours_c4(local, bundle, hbm_peak, flush, cpu)
+        if "C5" in want:
+            try:
+                c5ctx = A.Context(local)
+                c5stream = torch.cuda.ExternalStream(c5ctx.stream, device=torch.device("cuda", local))
+                with torch.cuda.stream(c5stream):
+                    cfgs["C5"] = ours_c5(local, 0, 1, bundle, hbm_peak, c5ctx, c5stream)
+                del c5ctx
+            except Exception as e:  # never lose the headline line to the largest config
+                cfgs["C5"] = {"error": f"{type(e).__name__}: {e}"}
         line["configs"] = cfgs
     return line
 
@@ -1114,13 +1285,13 @@ def main():
     ap.add_argument("--bundle", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lanes", type=int, default=3, help="streams of the e2e batch pipeline")
-    ap.add_argument("--configs", default="C1,C3,C4",
-                    help="other single-GPU configurations carried in the line ('' = none); N = 1 only")
+    ap.add_argument("--configs", default="C1,C3,C4,C5",
+                    help="other configurations carried in the line ('' = none); N > 1 runs carry C5 only")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
-    if world > 1:
-        args.configs = ""
+    if world > 1:  # the partitioned runs carry configs[4] (C5) only
+        args.configs = "C5" if "C5" in args.configs.split(",") else ""
     if args.impl == "reference":
         line = run_reference(args, rank, world)
     else:
