@@ -428,7 +428,10 @@ def run_ours_multi(args, rank, world):
     if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
         os.environ["NCCL_DEBUG"] = "WARN"
     if backend == "nccl":
-        dist.init_process_group("nccl", device_id=dev)
+        # a collective that never completes (a rank failing alone) aborts
+        # after 10 minutes instead of holding the job forever
+        import datetime
+        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(minutes=10))
     else:
         dist.init_process_group(backend)
     stream = torch.cuda.Stream(device=dev)
