@@ -156,11 +156,13 @@ struct BinLayout {
     int64_t tile_cap = -1, tile_cap_req = -1, ntiles = 0, panel_chunks = -1;
     std::vector<int64_t> panel_tile0;  // first tile of each column panel, [npanels] = ntiles
     bool multi = false;       // some bin is split into several tiles
-    // heavy rows (degree > heavy_min) are left out of the bins (their entries
-    // would serialise on one shared-memory slot) and run from the CSR as
-    // segments of <= kHeavySeg entries: int64 (row, begin, end) triples
-    int64_t heavy_min = 0, nsegs = 0, n_light = 0, n_padded = 0;
-    DevBuf segs;
+    // heavy rows (degree > heavy_min) leave the light bins (contiguous row
+    // ranges, bins [0, nlight)) for heavy bins of up to rh rows each (bins
+    // [nlight, nbins)): hrows = the heavy rows ascending (int32), hbits = their
+    // bitmap (the light bins' write-back skips them)
+    int64_t heavy_min = 0, nheavy = 0, nlight = 0, n_binned = 0, n_padded = 0;
+    int rh = 1;
+    DevBuf hrows, hbits;
     DevBuf tiles, tile_bin, tile_multi;
 };
 

@@ -52,16 +52,28 @@ struct PkVal {
     V val;
 };
 
+// Rows of the bins: light bins are contiguous row ranges [r0[b], r0[b+1]);
+// heavy bins (b >= nlight) hold up to rh heavy rows each, listed in hrows
+// (ascending), slot s of heavy bin h = row hrows[h*rh + s].  hbits marks the
+// heavy rows (they lie inside light bins' ranges but are written by their
+// heavy bin).
+struct BinRows {
+    const int64_t* r0;
+    int64_t nlight;
+    const int32_t* hrows;
+    int64_t nheavy;
+    int rh;
+    const uint32_t* hbits;
+};
+
 // One warp per column of the CSC: key = bin of the row, payload = packed
-// entry; counts per (bin, chunk) for the chunk offsets.
-// Entries of heavy rows (degree > heavy_min) get the sentinel key nbins and
-// are not counted: they sort behind every bin and are never streamed.
+// entry; counts per (bin, chunk) for the chunk offsets.  A heavy row
+// (hpos[row] >= 0) goes to heavy bin nlight + hpos / rh, slot hpos % rh.
 template <class V>
 __global__ void bin_expand_kernel(const int64_t* __restrict__ co, const int32_t* __restrict__ ri,
                                   const V* __restrict__ cv, int64_t cols, const int64_t* __restrict__ r0s,
-                                  int rbits, int cw, int64_t nchunks, const int64_t* __restrict__ ro,
-                                  int64_t heavy_min, int64_t nbins, uint32_t* __restrict__ keys,
-                                  PkVal<V>* __restrict__ pay,
+                                  int rbits, int cw, int64_t nchunks, const int32_t* __restrict__ hpos, int rh,
+                                  int64_t nlight, uint32_t* __restrict__ keys, PkVal<V>* __restrict__ pay,
                                   unsigned long long* __restrict__ counts) {
     const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -74,22 +86,25 @@ __global__ void bin_expand_kernel(const int64_t* __restrict__ co, const int32_t*
         int run = 0;
         for (int64_t k = b + lane; k < e; k += 32) {
             const int64_t row = ri[k];
-            if (heavy_min > 0 && __ldg(ro + row + 1) - __ldg(ro + row) > heavy_min) {
-                keys[k] = static_cast<uint32_t>(nbins);
-                pay[k] = PkVal<V>{0u, V(0)};
-                continue;
+            const int32_t hp = hpos ? __ldg(hpos + row) : -1;
+            int64_t bin;
+            uint32_t rl;
+            if (hp >= 0) {
+                bin = nlight + hp / rh;
+                rl = static_cast<uint32_t>(hp % rh);
+            } else {
+                int64_t lo = 0, hi = nlight;  // bin: largest b with r0s[b] <= row
+                while (hi - lo > 1) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (__ldg(r0s + mid) <= row) lo = mid;
+                    else hi = mid;
+                }
+                bin = lo;
+                rl = static_cast<uint32_t>(row - __ldg(r0s + bin));
             }
-            int64_t lo = 0, hi = nbins;  // bin: largest b with r0s[b] <= row
-            while (hi - lo > 1) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (__ldg(r0s + mid) <= row) lo = mid;
-                else hi = mid;
-            }
-            const int64_t bin = lo;
             keys[k] = static_cast<uint32_t>(bin);
-            const uint32_t rl = static_cast<uint32_t>(row - __ldg(r0s + bin));
             pay[k] = PkVal<V>{((static_cast<uint32_t>(j) & cmask) << rbits) | rl, cv[k]};
-            // rows ascend within the column: count runs of equal bins per lane
+            // runs of equal bins per lane (rows ascend within the column)
             if (bin != prev_bin) {
                 if (run) atomicAdd(counts + prev_bin * nchunks + chunk, static_cast<unsigned long long>(run));
                 prev_bin = bin;
@@ -183,7 +198,7 @@ __global__ void gather_spread_kernel(const int64_t* __restrict__ ro, const int32
 template <class V, int SR, bool MASKED, int CL = 1, int kBinUnroll = 8, bool NOALLOC = false,
           int kBinThreads = 1024, bool PIPE = false>
 __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
-    int64_t tile0, const int64_t* __restrict__ bin_r0, int rbits, int cw, int64_t nchunks,
+    int64_t tile0, BinRows br, int rbits, int cw, int64_t nchunks,
     const int64_t* __restrict__ tiles, const int32_t* __restrict__ tile_bin,
     const int32_t* __restrict__ tile_multi, const int64_t* __restrict__ chunk_off,
     const uint32_t* __restrict__ pk, const V* __restrict__ bv, const V* __restrict__ x,
@@ -194,8 +209,17 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
     const int64_t t = tile0 + blockIdx.x;
     const int64_t bin = tile_bin[t];
     const int64_t e0 = tiles[2 * t], e1 = tiles[2 * t + 1];
-    const int64_t r0 = bin_r0[bin];
-    const int nr = static_cast<int>(bin_r0[bin + 1] - r0);
+    int64_t r0 = 0;
+    int nr;
+    const int32_t* __restrict__ rmap = nullptr;  // heavy bin: slot -> row
+    if (bin < br.nlight) {
+        r0 = br.r0[bin];
+        nr = static_cast<int>(br.r0[bin + 1] - r0);
+    } else {
+        const int64_t hb = (bin - br.nlight) * br.rh;
+        nr = static_cast<int>(min(static_cast<int64_t>(br.rh), br.nheavy - hb));
+        rmap = br.hrows + hb;
+    }
     for (int i = threadIdx.x; i < nr; i += kBinThreads) ys[i] = S::zero();
     __syncthreads();
 
@@ -333,24 +357,28 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
         __syncthreads();
     }
     const int mode = tile_multi[t];
-    if (mode == 0) {  // the tile owns its bin's rows: plain coalesced stores
-        for (int i = lo + static_cast<int>(threadIdx.x); i < hi; i += kBinThreads)
-            y[r0 + i] = CL == 2 ? S::add(ys[i], peer[i]) : ys[i];
-    } else if (mode == 2) {  // owns the rows in a later column panel: y += segment
-        for (int i = lo + static_cast<int>(threadIdx.x); i < hi; i += kBinThreads) {
-            const V v = CL == 2 ? S::add(ys[i], peer[i]) : ys[i];
-            if (v != S::zero()) y[r0 + i] = S::add(y[r0 + i], v);
+    for (int i = lo + static_cast<int>(threadIdx.x); i < hi; i += kBinThreads) {
+        const V v = CL == 2 ? S::add(ys[i], peer[i]) : ys[i];
+        int64_t row;
+        if (rmap) {
+            row = rmap[i];
+        } else {
+            row = r0 + i;
+            // a heavy row inside this range is written by its heavy bin
+            if (br.hbits && ((br.hbits[row >> 5] >> (row & 31)) & 1u)) continue;
         }
-    } else {               // partial segment: combine into the identity-filled y
-        for (int i = lo + static_cast<int>(threadIdx.x); i < hi; i += kBinThreads) {
-            const V v = CL == 2 ? S::add(ys[i], peer[i]) : ys[i];
-            if (v != S::zero()) AtomicCombine<SR>::apply(y + r0 + i, v);
+        if (mode == 0) {  // the tile owns its bin's rows: plain stores
+            y[row] = v;
+        } else if (mode == 2) {  // owns the rows in a later column panel: y += segment
+            if (v != S::zero()) y[row] = S::add(y[row], v);
+        } else if (v != S::zero()) {  // partial segment: combine into the identity-filled y
+            AtomicCombine<SR>::apply(y + row, v);
         }
     }
     if constexpr (CL == 2) cooperative_groups::this_cluster().sync();  // peer reads done before exit
 }
 
-constexpr int64_t kHeavySeg = 8192;  // entries per heavy-row segment (one CTA)
+constexpr int64_t kHeavySeg = 8192;  // heavy-row threshold scale (rows of degree > kHeavySeg / 2)
 
 __global__ void heavy_rows_kernel(const int64_t* __restrict__ ro, int64_t rows, int64_t heavy_min,
                                   int64_t* __restrict__ list, unsigned long long* __restrict__ count) {
@@ -366,45 +394,20 @@ __global__ void heavy_rows_kernel(const int64_t* __restrict__ ro, int64_t rows, 
     }
 }
 
-// One CTA per heavy-row segment: strided (coalesced) pass over its CSR
-// entries, CTA reduction, one atomic combine into y[row] (which the binned
-// kernel left at the identity).
-template <class V, int SR, bool MASKED>
-__global__ void __launch_bounds__(256) heavy_seg_kernel(const int64_t* __restrict__ segs,
-                                                        const int32_t* __restrict__ ci,
-                                                        const V* __restrict__ vals,
-                                                        const V* __restrict__ x,
-                                                        const uint32_t* __restrict__ mask,
-                                                        V* __restrict__ y,
-                                                        unsigned long long* __restrict__ ctr) {
-    using S = Semiring<SR, V>;
-    __shared__ V red[8];
-    unsigned cnt = 0;
-    const int64_t row = segs[3 * blockIdx.x], b = segs[3 * blockIdx.x + 1], e = segs[3 * blockIdx.x + 2];
-    V acc = S::zero();
-    for (int64_t k = b + threadIdx.x; k < e; k += 256) {
-        const int c = __ldg(ci + k);
-        if (MASKED && !((__ldg(mask + (c >> 5)) >> (c & 31)) & 1u)) continue;
-        acc = S::fma(S::kUsesValues ? __ldg(vals + k) : V(1), __ldg(x + c), acc);
-        ++cnt;
-    }
-    count_add(ctr, 0, cnt);
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) acc = S::add(acc, __shfl_xor_sync(kFull, acc, d));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        V t = red[0];
-#pragma unroll
-        for (int w = 1; w < 8; ++w) t = S::add(t, red[w]);
-        if (t != S::zero()) AtomicCombine<SR>::apply(y + row, t);
+__global__ void heavy_pos_kernel(const int32_t* __restrict__ hrows, int64_t nh, int32_t* __restrict__ hpos,
+                                 uint32_t* __restrict__ hbits) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < nh) {
+        const int32_t r = hrows[i];
+        hpos[r] = static_cast<int32_t>(i);
+        atomicOr(hbits + (r >> 5), 1u << (r & 31));
     }
 }
 
-// Heavy rows of the matrix as (row, begin, end) segments of <= kHeavySeg
-// entries, sorted by row (device list; the count crosses to the host once).
-void plan_heavy(Context& ctx, const Matrix& m, BinLayout& L) {
-    L.nsegs = 0;
+// Heavy rows (degree > heavy_min), ascending, and their position map (for the
+// expansion) and bitmap (for the light bins' write-back).
+void plan_heavy(Context& ctx, const Matrix& m, BinLayout& L, DevBuf& hpos) {
+    L.nheavy = 0;
     if (L.heavy_min <= 0 || m.rows == 0) return;
     DevBuf list, cnt;
     unsigned long long* dcount = static_cast<unsigned long long*>(cnt.ensure(sizeof(unsigned long long)));
@@ -422,21 +425,22 @@ void plan_heavy(Context& ctx, const Matrix& m, BinLayout& L) {
     std::vector<int64_t> h(3 * static_cast<size_t>(n));
     ADA_CUDA(cudaMemcpyAsync(h.data(), list.p, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
-    std::vector<std::array<int64_t, 3>> rs(static_cast<size_t>(n));
-    for (size_t i = 0; i < rs.size(); ++i) rs[i] = {h[3 * i], h[3 * i + 1], h[3 * i + 2]};
-    std::sort(rs.begin(), rs.end());
-    std::vector<int64_t> segs;
-    for (const auto& r : rs)
-        for (int64_t b = r[1]; b < r[2]; b += kHeavySeg) {
-            segs.push_back(r[0]);
-            segs.push_back(b);
-            segs.push_back(std::min(b + kHeavySeg, r[2]));
-        }
-    L.nsegs = static_cast<int64_t>(segs.size() / 3);
-    L.segs.ensure(sizeof(int64_t) * segs.size());
-    ADA_CUDA(cudaMemcpyAsync(L.segs.p, segs.data(), sizeof(int64_t) * segs.size(), cudaMemcpyHostToDevice,
+    std::vector<int32_t> rows(static_cast<size_t>(n));
+    for (size_t i = 0; i < rows.size(); ++i) rows[i] = static_cast<int32_t>(h[3 * i]);
+    std::sort(rows.begin(), rows.end());
+    L.nheavy = static_cast<int64_t>(n);
+    L.hrows.ensure(sizeof(int32_t) * rows.size());
+    ADA_CUDA(cudaMemcpyAsync(L.hrows.p, rows.data(), sizeof(int32_t) * rows.size(), cudaMemcpyHostToDevice,
                              ctx.stream));
-    ctx.sync();
+    int32_t* hp = static_cast<int32_t*>(hpos.ensure(sizeof(int32_t) * static_cast<size_t>(m.rows)));
+    ADA_CUDA(cudaMemsetAsync(hp, 0xff, sizeof(int32_t) * static_cast<size_t>(m.rows), ctx.stream));
+    const size_t nw = static_cast<size_t>((m.rows + 31) / 32);
+    uint32_t* hb = static_cast<uint32_t*>(L.hbits.ensure(sizeof(uint32_t) * nw));
+    ADA_CUDA(cudaMemsetAsync(hb, 0, sizeof(uint32_t) * nw, ctx.stream));
+    heavy_pos_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx.stream>>>(L.hrows.as<int32_t>(),
+                                                                                     L.nheavy, hp, hb);
+    ADA_LAUNCHED(ctx);
+    ctx.sync();  // host rows go out of scope
 }
 
 struct LightDegIn {
@@ -513,19 +517,21 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
     nbins = std::max<int64_t>(nbins, 1);
     // heavy rows: a row whose entries would put several lanes of one warp
     // instruction on the same shared-memory slot (degree well above the
-    // column-sorted window a warp covers) runs from the CSR instead
+    // column-sorted window a warp covers) leaves the light bins for the heavy
+    // bins (heavy rows only: their column-sorted window is narrow enough
+    // that a row rarely recurs in it)
     const int64_t per_bin = m.nnz / nbins + 1;
     L.heavy_min = m.feat[3] > static_cast<double>(kHeavySeg / 2)
                       ? std::max<int64_t>(kHeavySeg / 2, per_bin / 512) : 0;
     // Skewed (power-law) matrices: hub rows meet hub columns, so in the low
     // columns of a bin the same rows recur inside one warp's 32-entry window
     // and serialise on their shared-memory slots even at modest degree.
-    // The CSR-segment path does not profit from zeros in x as the bins do,
-    // so the cut trades dense-x against half-dense-x time.  Measured on B200
-    // (K0, x density 0.3 / 0.6 / 1.0; cut 4096 / 2048 / 1024 / 512):
-    //   R-MAT 22  501 550 654 / 486 509 566 / 486 507 566 / 509 521 548 us
-    //   R-MAT 20  105 157 269 / 142 159 183 / 116 126 143 / 116 126 144 us
-    if (m.feat[8] > 0.5 && m.feat[3] > 1024.0) L.heavy_min = 1024;
+    // With the heavy rows in heavy bins (not CSR segments) a low cut pays;
+    // K0 on B200, x = 100 %, cut 128 / 256 / 512 / 1024 / 2048:
+    //   R-MAT 22  409 / 402 / 413 / 509 / 519 us
+    //   R-MAT 26  8.31 / 8.61 / 8.63 / 9.14 / 9.74 ms   (spmv_lb 0.65 / 11.4 ms)
+    if (m.feat[8] > 0.5 && m.feat[3] > 256.0) L.heavy_min = 256;
+    if (L.cluster == 2) L.heavy_min = 0;  // cluster pairs: light bins only
     std::vector<int64_t> cuts;
     if (L.force_rows > 0 || L.cluster == 2 || m.nnz == 0) {  // equal-height bins
         const int64_t R0 = std::max<int64_t>((m.rows + nbins - 1) / nbins, 1);
@@ -557,9 +563,13 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
     L.R = R;
     L.rbits = rbits;
     L.cw = cw;
-    L.nbins = nbins;
     L.nchunks = nchunks;
-    plan_heavy(ctx, m, L);
+    DevBuf hpos;
+    plan_heavy(ctx, m, L, hpos);
+    L.nlight = nbins;
+    L.rh = static_cast<int>(R);
+    if (L.nheavy > 0) nbins += (L.nheavy + R - 1) / R;  // heavy bins after the light ones
+    L.nbins = nbins;
     const int64_t nnz = m.nnz;
     const size_t z = static_cast<size_t>(std::max<int64_t>(nnz, 1));
     const int64_t nkeys = nbins * nchunks;
@@ -579,7 +589,7 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
         bin_expand_kernel<V><<<static_cast<unsigned>(std::max<int64_t>((warps * 32 + 255) / 256, 1)), 256, 0,
                                ctx.stream>>>(m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(),
                                              m.cvals.as<V>(), m.cols, L.bin_r0.as<int64_t>(), rbits, cw, nchunks,
-                                             m.row_off.as<int64_t>(), L.nsegs ? L.heavy_min : 0, nbins,
+                                             L.nheavy ? hpos.as<int32_t>() : nullptr, L.rh, L.nlight,
                                              k0.as<uint32_t>(), p0.as<PkVal<V>>(),
                                              counts.as<unsigned long long>());
         ADA_LAUNCHED(ctx);
@@ -597,7 +607,7 @@ void build_layout(Context& ctx, const Matrix& m, BinLayout& L) {
     ADA_CUDA(cudaMemcpyAsync(&tot[1], off + nkeys, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
     const int64_t nlight = tot[0], npad = tot[1];
-    L.n_light = nlight;
+    L.n_binned = nlight;
     L.n_padded = npad;
     // + 4 entries so an empty layout still has a valid allocation
     L.pk.ensure(sizeof(uint32_t) * static_cast<size_t>(npad + 4));
@@ -824,7 +834,9 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
         at[0].val.clusterDim.z = 1;
         lc.attrs = at;
         lc.numAttrs = 1;
-        ADA_CUDA(cudaLaunchKernelEx(&lc, kern, t0, static_cast<const int64_t*>(L.bin_r0.as<int64_t>()), L.rbits,
+        const BinRows br{L.bin_r0.as<int64_t>(), L.nlight, L.hrows.as<int32_t>(), L.nheavy, L.rh,
+                         L.nheavy ? L.hbits.as<uint32_t>() : nullptr};
+        ADA_CUDA(cudaLaunchKernelEx(&lc, kern, t0, br, L.rbits,
                                     L.cw, L.nchunks, L.tiles.as<int64_t>(),
                                     L.tile_bin.as<int32_t>(), L.tile_multi.as<int32_t>(),
                                     L.chunk_off.as<int64_t>(), L.pk.as<uint32_t>(), L.bv.as<V>(), x, mask, y,
@@ -853,12 +865,6 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
                 launch(binned_row_kernel<V, SR, false, 1>, 1, t0, t1 - t0);
             }
         }
-    }
-    if (L.nsegs > 0) {  // heavy rows, after the bins wrote their identity
-        auto hk = mask ? heavy_seg_kernel<V, SR, true> : heavy_seg_kernel<V, SR, false>;
-        hk<<<static_cast<unsigned>(L.nsegs), 256, 0, ctx.stream>>>(L.segs.as<int64_t>(), m.col_idx.as<int32_t>(),
-                                                                  m.vals.as<V>(), x, mask, y, ctx.ctr);
-        ADA_LAUNCHED(ctx);
     }
 }
 
