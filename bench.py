@@ -199,6 +199,19 @@ def ref_c2_step(M, ops, best, repeats=3):
     return [ref_time(M, k, op, repeats) for op, k in zip(ops, best)]
 
 
+_V2 = {}
+
+
+def _v2_bundle():
+    """The optional schema-2 selector bundle (None when absent), loaded once."""
+    if "b" not in _V2:
+        from paper_2006_16767_b200 import adaspmv as A
+        from paper_2006_16767_b200 import selector as S
+        p = S.DEFAULT_PATH.parent / "b200_bundle_v2.txt"
+        _V2["b"] = A.SelectorBundle.load(p) if p.exists() else None
+    return _V2["b"]
+
+
 def _cpu_meta(ref, threads, sample):
     from oracle.oracle import host_cpu_model
     return {"cores": threads, "kind": "reference", "sample": sample, "cpu": host_cpu_model(),
@@ -715,6 +728,7 @@ def ours_c1(local, bundle, hbm, flush, cpu):
             x.set_sparse(xi, xv)
         nnz_s = int(co[xi].sum())
         k_sel = A.predict_kernel(m, x, bundle)[0].index()
+        k_v2 = A.predict_kernel(m, x, _v2_bundle())[0].index() if _v2_bundle() else None
         c = A.KernelConfig()._c()
         ts = []
         for k in range(8):
@@ -733,7 +747,8 @@ def ours_c1(local, bundle, hbm, flush, cpu):
             "t_best_us": round(min(ts) * 1e6, 2), "regret": round(t_sel / min(ts), 3),
             "gflops_sel": round(2 * nnz_s / t_sel / 1e9, 2), "alg_bytes": int(b_alg),
             "roofline_frac": round(b_alg / t_sel / 1e9 / hbm, 4),
-            "t_kernels_us": [round(t * 1e6, 2) for t in ts]})
+            "t_kernels_us": [round(t * 1e6, 2) for t in ts],
+            "schema2": None if k_v2 is None else {"selected": A_name(k_v2), "regret": round(ts[k_v2] / min(ts), 3)}})
     res["value"] = round(flops / tot / 1e9, 3)
     res["unit"] = "GFLOP/s"
     if cpu:
@@ -828,6 +843,7 @@ def ours_c4(local, bundle, hbm, flush, cpu, reps=3):
             if k == 5:
                 nnz_y = out.nnz()
         k_sel = A.predict_kernel(m, x, bundle)[0].index()
+        k_v2 = A.predict_kernel(m, x, _v2_bundle())[0].index() if _v2_bundle() else None
         t_sel = ts[k_sel]
         b_alg, _ = alg_bytes(mr, nc, nnz, len(xi), nnz_s, nnz_y)
         flops += 2 * nnz_s
@@ -838,7 +854,8 @@ def ours_c4(local, bundle, hbm, flush, cpu, reps=3):
             "t_best_us": round(min(ts) * 1e6, 2), "regret": round(t_sel / min(ts), 3),
             "gflops_sel": round(2 * nnz_s / t_sel / 1e9, 2), "alg_bytes": int(b_alg),
             "roofline_frac": round(b_alg / t_sel / 1e9 / hbm, 4),
-            "t_kernels_us": [round(t * 1e6, 2) for t in ts]})
+            "t_kernels_us": [round(t * 1e6, 2) for t in ts],
+            "schema2": None if k_v2 is None else {"selected": A_name(k_v2), "regret": round(ts[k_v2] / min(ts), 3)}})
     res["value"] = round(flops / tot / 1e9, 3)
     res["unit"] = "GFLOP/s"
     res["setup_s"] = {"generate": round(gen_s, 2)}
@@ -923,31 +940,44 @@ def ours_c5(local, rank, world, bundle, hbm, ctx, stream, dist=None, reps=3):
         x.set_sparse_device(k_x, idx.data_ptr(), val.data_ptr())
         nnz_s_local = A.effective_nnz(m, x)
         k = A.predict_kernel(m, x, bundle)[0].index()
-        x.prepare(k)
-        A.run_kernel(m, k, x, out=out)  # lazy layouts before timing
-        ts = []
-        for _ in range(reps):
-            torch.cuda._sleep(GATE_CYCLES)
-            ev[0].record(stream)
-            exchange()
-            ev[1].record(stream)
-            x.set_sparse_device(k_x, idx.data_ptr(), val.data_ptr())
-            x.prepare(k)
-            torch.cuda._sleep(GATE_CYCLES)
-            A.run_kernel(m, k, x, out=out)
-            ts.append(out.elapsed() + ev[0].elapsed_time(ev[1]) * 1e-3)
-        t = statistics.median(ts)
-        tt = torch.tensor([t, float(nnz_s_local)], dtype=torch.float64, device=dev)
+        k2 = A.predict_kernel(m, x, _v2_bundle())[0].index() if _v2_bundle() else None
+
+        def time_kernel(kk):
+            x.prepare(kk)
+            A.run_kernel(m, kk, x, out=out)  # lazy layouts before timing
+            ts = []
+            for _ in range(reps):
+                torch.cuda._sleep(GATE_CYCLES)
+                ev[0].record(stream)
+                exchange()
+                ev[1].record(stream)
+                x.set_sparse_device(k_x, idx.data_ptr(), val.data_ptr())
+                x.prepare(kk)
+                torch.cuda._sleep(GATE_CYCLES)
+                A.run_kernel(m, kk, x, out=out)
+                ts.append(out.elapsed() + ev[0].elapsed_time(ev[1]) * 1e-3)
+            t_ = statistics.median(ts)
+            if dist is not None:
+                tm = torch.tensor([t_], dtype=torch.float64, device=dev)
+                dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+                t_ = float(tm.item())
+            return t_
+
+        t = time_kernel(k)
+        # the schema-2 choice is timed when it differs on ANY rank (every rank
+        # must take part in the same broadcasts / reductions)
+        need2 = torch.tensor([0.0 if k2 in (None, k) else 1.0], dtype=torch.float64, device=dev)
         if dist is not None:
-            tmax = tt.clone()
-            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+            dist.all_reduce(need2, op=dist.ReduceOp.MAX)
+        t2 = time_kernel(k if k2 is None else k2) if need2.item() > 0 else t
+        tt = torch.tensor([float(nnz_s_local)], dtype=torch.float64, device=dev)
+        if dist is not None:
             dist.all_reduce(tt, op=dist.ReduceOp.SUM)
-            t, nnz_s = float(tmax[0].item()), int(tt[1].item())
-        else:
-            nnz_s = nnz_s_local
+        nnz_s = int(tt[0].item())
         b_alg, _ = alg_bytes(n, n, nnz_all, k_x, nnz_s, 0)
         pts.append({"x_sparsity": d, "nnz_x": k_x, "nnz_s": nnz_s, "selected_rank0": A_name(k),
                     "ms": round(t * 1e3, 4), "gflops": round(2 * nnz_s / t / 1e9, 2),
+                    "schema2": None if k2 is None else {"selected_rank0": A_name(k2), "ms": round(t2 * 1e3, 4)},
                     "alg_GBps": round(b_alg / t / 1e9, 1),
                     "roofline_frac_aggregate": round(b_alg / t / 1e9 / (hbm * world), 4)})
     ctx.set_timing(False)
@@ -1069,6 +1099,13 @@ def run_ours(args, rank, world):
     for dv in dvs:
         k, _, _ = A.predict_kernel(m, dv, bundle)
         chosen.append(k.index())
+    # the schema-2 bundle's choices on the same operands (reported beside the
+    # default SPEC cascade, from the same all-kernel timings)
+    v2_path = S.DEFAULT_PATH.parent / "b200_bundle_v2.txt"
+    chosen_v2 = []
+    if v2_path.exists():
+        b2 = A.SelectorBundle.load(v2_path)
+        chosen_v2 = [A.predict_kernel(m, dv, b2)[0].index() for dv in dvs]
     for i, dv in enumerate(dvs):  # operand conversions happen once, untimed
         dv.prepare(chosen[i])
     l0 = ctx.launches
@@ -1223,6 +1260,14 @@ def run_ours(args, rank, world):
                      "step_share": round(per_point[top] / sum(per_point), 4),
                      "dominant_point": SPARSITIES[dom]},
         "selector_regret": round(regret_total, 4),
+        "selector_schema2": ({"bundle": v2_path.name, "selected": [A_name(k) for k in chosen_v2],
+                              "regret_per_point": [round(kernel_t[i][k] / min(kernel_t[i]), 3)
+                                                   for i, k in enumerate(chosen_v2)],
+                              "regret": round(sum(kernel_t[i][k] for i, k in enumerate(chosen_v2))
+                                              / sum(min(r) for r in kernel_t), 4),
+                              "note": "the optional schema-2 bundle (workload tree per pattern family) on the same "
+                                      "operands and kernel timings; the line's value uses the default SPEC cascade"}
+                             if chosen_v2 else None),
         "overhead": overhead,
         "gpu_launches": int(launches),
         "points": points,
