@@ -18,9 +18,14 @@
 // Layout (Matrix::BinLayout, built once on the device from the CSC): the CSC
 // order (columns ascending, rows ascending within a column: csr_to_csc,
 // sparse.hpp:157-178) stably partitioned by bin.  Entry word =
-// (col & (2^cw - 1)) << rbits | (row - bin_row0); columns are split in chunks
-// of 2^cw (cw = 32 - rbits) whose offsets per bin are stored, so an entry is
-// 4 B of index + V of value -- the same bytes per nonzero as the CSR.
+// (col & (2^cw - 1)) << rbits | slot; columns are split in chunks of 2^cw
+// (cw = 32 - rbits) whose offsets per bin are stored, so an entry is 4 B of
+// index + V of value -- the same bytes per nonzero as the CSR.  Every
+// (bin, chunk) run is padded to 128-entry groups stored interleaved (lane l
+// loads entries {l, l+32, l+64, l+96} of a group with one 16-B load).
+// Light bins are contiguous row ranges (slot = row - bin_row0); rows of high
+// degree (power-law hubs) go to heavy bins holding only heavy rows (slot ->
+// row through a map), where a row rarely recurs inside a warp's window.
 //
 // Summation order inside a row is not the reference's (shared-memory atomics
 // in column order), so results match within the floating-point tolerance of

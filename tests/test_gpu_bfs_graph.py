@@ -3,7 +3,7 @@ against the queue BFS and the host-driven loop (adaspmv_ctx_set_bfs_loop),
 for every semiring on pattern matrices and OR_AND on valued ones, under the
 built-in policy and the trained selector (whose trees are walked on the
 device: its per-level choices must equal the host selector's on the same
-frontiers), on graphs deeper than one graph replay (kUnroll = 8 levels),
+frontiers), on graphs of many WHILE iterations (two levels per iteration),
 disconnected graphs, isolated sources and a 3001-level path."""
 import numpy as np
 import pytest
@@ -27,7 +27,7 @@ def _sym(n, edges):
 
 def _graphs():
     out = []
-    # path of 40 vertices: 40 levels = 5 graph replays
+    # path of 40 vertices: 40 levels = 20 iterations of the graph's WHILE body
     out.append(("path40", 40, *_sym(40, [(i, i + 1) for i in range(39)])))
     # two components + an isolated vertex
     out.append(("disconnected", 12, *_sym(12, [(0, 1), (1, 2), (2, 0), (4, 5), (5, 6)])))

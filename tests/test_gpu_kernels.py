@@ -438,10 +438,11 @@ def test_atomic_output_reuse(ctx, port, dt):
 
 
 @pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
-def test_binned_skewed_rows_cut_to_csr_segments(ctx, port, dt):
-    """A power-law matrix (Gini > 0.5, rows above the 1024 cut): its heavy
-    rows run as CSR segments after the bins (kernels_binned.cu) -- every
-    density, K0 and K2, against the oracle; OR_AND bit-equal to the CSR run."""
+def test_binned_skewed_rows_in_heavy_bins(ctx, port, dt):
+    """A power-law matrix (Gini > 0.5, rows above the 256 cut): its heavy rows
+    leave the light bins for the heavy bins (kernels_binned.cu: slot -> row
+    map, the light bins skip them at write-back) -- every density, K0 and K2,
+    against the oracle; OR_AND and MIN_PLUS bit-equal to the CSR run."""
     rows, cols, ro, ci, vals = synth.rmat(15, 32, seed=5, values="uniform")
     vals = np.asarray(vals, dt)
     assert np.diff(ro).max() > 1024
@@ -458,6 +459,9 @@ def test_binned_skewed_rows_cut_to_csr_segments(ctx, port, dt):
             b = A.run_kernel(m, k, xs, A.KernelConfig(semiring=A.OR_AND, row_layout=2))
             c = A.run_kernel(m, k, xs, A.KernelConfig(semiring=A.OR_AND, row_layout=1))
             assert b.dense().values.tobytes() == c.dense().values.tobytes(), (k, nx)
+            b = A.run_kernel(m, k, xs, A.KernelConfig(semiring=A.MIN_PLUS, row_layout=2))
+            c = A.run_kernel(m, k, xs, A.KernelConfig(semiring=A.MIN_PLUS, row_layout=1))
+            assert b.dense().values.tobytes() == c.dense().values.tobytes(), ("min_plus", k, nx)
 
 
 @pytest.mark.parametrize("dt", DTYPES, ids=["f64", "f32"])
