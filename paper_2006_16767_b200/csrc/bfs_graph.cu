@@ -26,6 +26,7 @@
 // synchronisation per traversal.  Per-level reports (kernel, frontier size,
 // effective nnz, device time from %globaltimer) are logged on the device.
 #include <algorithm>
+#include <functional>
 #include <cstring>
 #include <vector>
 
@@ -43,6 +44,9 @@ constexpr int kScanBlocks = 256;    // fixed grid of the eff-offset scan
 constexpr int kTile = 256;          // effective entries per push warp tile
 constexpr int kWin = 128;           // support positions staged per warp tile
 enum { kModeDone = 0, kModePush = 1, kModePull = 2 };
+// bodies of a level's SWITCH node (any other value: no body runs)
+enum { kBranchEffPush = 0, kBranchPush = 1, kBranchPull = 2, kBranchPushSmall = 3, kBranchNone = 4 };
+constexpr unsigned long long kSmallPush = 4096;  // effective entries of a frontier pushed without offsets
 
 // Device-side loop state (one per plan).
 struct alignas(8) BfsState {
@@ -100,12 +104,9 @@ __device__ int tree_walk(const DevTrees& t, int which, const double* f) {
 // WHILE handle that repeats the two-level body until the frontier is empty.
 __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees trees, int use_trees,
                                   const double* mfeat, int64_t n, int64_t nnz, int vbytes, int64_t* eff,
-                                  cudaGraphConditionalHandle heff, cudaGraphConditionalHandle hpush,
-                                  cudaGraphConditionalHandle hpull, cudaGraphConditionalHandle hwhile) {
+                                  cudaGraphConditionalHandle hbranch, cudaGraphConditionalHandle hwhile) {
     if (threadIdx.x != 0) return;
-    cudaGraphSetConditional(heff, 0);
-    cudaGraphSetConditional(hpush, 0);
-    cudaGraphSetConditional(hpull, 0);
+    cudaGraphSetConditional(hbranch, kBranchNone);
     if (st->pending) {  // account for the level that produced this frontier
         if (st->mode == kModePull) {  // its compaction scan's packed total; eff offsets written by the scan
             const long long t = st->tot;
@@ -158,8 +159,10 @@ __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees t
     }
     st->kernel = k;
     st->mode = k >= 4 ? kModePush : kModePull;
-    cudaGraphSetConditional(k >= 4 ? hpush : hpull, 1);
-    if (k >= 4 && !st->eff_ok) cudaGraphSetConditional(heff, 1);
+    cudaGraphSetConditional(hbranch, k < 4        ? kBranchPull
+                                     : st->eff_ok ? kBranchPush
+                                     : ns <= kSmallPush ? kBranchPushSmall
+                                                        : kBranchEffPush);
     st->level += 1;
     st->nf[p ^ 1] = 0;
     st->ns[p ^ 1] = 0;
@@ -397,6 +400,28 @@ struct LevelEpi {  // the next frontier and its eff offsets (degree prefix)
     }
 };
 
+// Push of a small frontier (<= kSmallPush effective entries) that a push
+// appended (no eff offsets): one block per frontier vertex, its column walked
+// by the block's warps -- one launch instead of the offset scan + LB push.
+__global__ void __launch_bounds__(256) bfs_push_small_kernel(BfsState* st, int p, const int32_t* __restrict__ f,
+                                                             const int64_t* __restrict__ co,
+                                                             const int32_t* __restrict__ ri,
+                                                             int32_t* __restrict__ lv, int32_t* __restrict__ nf_out) {
+    const long long nx = static_cast<long long>(st->nf[p]);
+    const int level = st->level;
+    const int lane = threadIdx.x & 31;
+    for (long long s = blockIdx.x; s < nx; s += gridDim.x) {
+        const int32_t v = f[s];
+        const long long b = __ldg(co + v), e = __ldg(co + v + 1);
+        for (long long k0 = b + (threadIdx.x & ~31); k0 < e; k0 += 256) {  // warp-uniform trip count
+            const long long k = k0 + lane;
+            const int32_t r = k < e ? __ldg(ri + k) : 0;
+            const bool claim = k < e && lv[r] < 0 && atomicCAS(lv + r, -1, level) == -1;
+            append_claimed(claim, r, co, st, p ^ 1, nf_out, lane);
+        }
+    }
+}
+
 __global__ void bfs_init_kernel(BfsState* st, int32_t* lv, int64_t n, int64_t source, int32_t* f0,
                                 const int64_t* __restrict__ co, int64_t* __restrict__ eff) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -486,11 +511,13 @@ void launch_pull_mark(cudaStream_t s, unsigned grid, BfsState* st, const Matrix&
     bfs_pull_mark_kernel<G><<<grid, 256, 0, s>>>(st, m.rows, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), lv);
 }
 
-// Appends IF(handle) to the graph being captured on `s`; its body is
-// captured from `body` on the side stream `s2` (the library's kernels take
-// the context's stream, so it is swapped for the duration).
+// Appends SWITCH(handle) with one body per element of `bodies` to the graph
+// being captured on `s`; body i is captured from bodies[i] on the side stream
+// `s2` (the library's kernels take the context's stream, so it is swapped for
+// the duration).
 template <class F>
-void capture_if(Context& ctx, cudaStream_t s, cudaStream_t s2, cudaGraphConditionalHandle h, F body) {
+void capture_switch(Context& ctx, cudaStream_t s, cudaStream_t s2, cudaGraphConditionalHandle h,
+                    const std::vector<F>& bodies) {
     cudaStreamCaptureStatus cs;
     cudaGraph_t g = nullptr;
     const cudaGraphNode_t* deps = nullptr;
@@ -499,24 +526,26 @@ void capture_if(Context& ctx, cudaStream_t s, cudaStream_t s2, cudaGraphConditio
     cudaGraphNodeParams ip{};
     ip.type = cudaGraphNodeTypeConditional;
     ip.conditional.handle = h;
-    ip.conditional.type = cudaGraphCondTypeIf;
-    ip.conditional.size = 1;
+    ip.conditional.type = cudaGraphCondTypeSwitch;
+    ip.conditional.size = static_cast<unsigned>(bodies.size());
     cudaGraphNode_t node;
     ADA_CUDA(cudaGraphAddNode(&node, g, deps, nd, &ip));
     ADA_CUDA(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
-    cudaGraph_t bg = ip.conditional.phGraph_out[0];
-    ADA_CUDA(cudaStreamBeginCaptureToGraph(s2, bg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     const cudaStream_t keep = ctx.stream;
-    ctx.stream = s2;
-    try {
-        body(s2);
-    } catch (...) {
+    for (size_t i = 0; i < bodies.size(); ++i) {
+        cudaGraph_t bg = ip.conditional.phGraph_out[i];
+        ADA_CUDA(cudaStreamBeginCaptureToGraph(s2, bg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        ctx.stream = s2;
+        try {
+            bodies[i](s2);
+        } catch (...) {
+            ctx.stream = keep;
+            cudaStreamEndCapture(s2, &bg);
+            throw;
+        }
         ctx.stream = keep;
-        cudaStreamEndCapture(s2, &bg);
-        throw;
+        ADA_CUDA(cudaStreamEndCapture(s2, &bg));
     }
-    ctx.stream = keep;
-    ADA_CUDA(cudaStreamEndCapture(s2, &bg));
 }
 
 // The whole traversal as ONE graph: WHILE(frontier) { level p = 0; level
@@ -534,6 +563,7 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     P.part.ensure(sizeof(long long) * kScanBlocks);
     P.lv.ensure(sizeof(int32_t) * static_cast<size_t>(n));
     P.scan_tmp.ensure(sizeof(int64_t) * static_cast<size_t>((n + kScanTile - 1) / kScanTile + 1));
+
     double* mf = static_cast<double*>(P.mfeat.ensure(sizeof(double) * 9));
     ADA_CUDA(cudaMemcpyAsync(mf, m.feat, sizeof(double) * 9, cudaMemcpyHostToDevice, ctx.stream));
     if (b) upload_trees(ctx, *b, P);
@@ -557,13 +587,10 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
             cudaStreamDestroy(s);
         }
     } cleanup{&graph, s2};
-    cudaGraphConditionalHandle hw, heff[2], hpush[2], hpull[2];
+    cudaGraphConditionalHandle hw, hbranch[2];
     ADA_CUDA(cudaGraphConditionalHandleCreate(&hw, graph, 1, cudaGraphCondAssignDefault));
-    for (int q = 0; q < 2; ++q) {
-        ADA_CUDA(cudaGraphConditionalHandleCreate(&heff[q], graph, 0, cudaGraphCondAssignDefault));
-        ADA_CUDA(cudaGraphConditionalHandleCreate(&hpush[q], graph, 0, cudaGraphCondAssignDefault));
-        ADA_CUDA(cudaGraphConditionalHandleCreate(&hpull[q], graph, 0, cudaGraphCondAssignDefault));
-    }
+    for (int q = 0; q < 2; ++q)
+        ADA_CUDA(cudaGraphConditionalHandleCreate(&hbranch[q], graph, kBranchNone, cudaGraphCondAssignDefault));
     cudaGraphNodeParams wp{};
     wp.type = cudaGraphNodeTypeConditional;
     wp.conditional.handle = hw;
@@ -577,19 +604,19 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     try {
         for (int p = 0; p < 2; ++p) {
             bfs_decide_kernel<<<1, 32, 0, s>>>(st, lg, p, P.dt, b ? 1 : 0, mf, n, m.nnz, m.vbytes(),
-                                               P.eff.as<int64_t>(), heff[p], hpush[p], hpull[p], hw);
-            capture_if(ctx, s, s2, heff[p], [&](cudaStream_t cs) {  // a push after a push: scan the offsets
+                                               P.eff.as<int64_t>(), hbranch[p], hw);
+            auto eff_scan = [&, p](cudaStream_t cs) {  // offsets of a frontier a push appended
                 bfs_eff_partial_kernel<<<kScanBlocks, 256, 0, cs>>>(st, p, P.f[p].as<int32_t>(), co,
                                                                     P.part.as<long long>());
                 bfs_eff_top_kernel<<<1, kScanBlocks, 0, cs>>>(st, P.part.as<long long>());
                 bfs_eff_write_kernel<<<kScanBlocks, 256, 0, cs>>>(st, p, P.f[p].as<int32_t>(), co,
                                                                   P.part.as<long long>(), P.eff.as<int64_t>());
-            });
-            capture_if(ctx, s, s2, hpush[p], [&](cudaStream_t cs) {
+            };
+            auto push = [&, p](cudaStream_t cs) {
                 bfs_push_kernel<<<push_grid, 256, 0, cs>>>(st, p, P.f[p].as<int32_t>(), P.eff.as<int64_t>(), co,
                                                            m.row_idx.as<int32_t>(), lv, P.f[p ^ 1].as<int32_t>());
-            });
-            capture_if(ctx, s, s2, hpull[p], [&](cudaStream_t cs) {
+            };
+            auto pull = [&, p](cudaStream_t cs) {
                 switch (G) {
                     case 1: launch_pull_mark<1>(cs, pull_grid, st, m, lv); break;
                     case 2: launch_pull_mark<2>(cs, pull_grid, st, m, lv); break;
@@ -598,7 +625,19 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
                 }
                 scan3(ctx, n, LevelIn{lv, &st->level, co}, LevelEpi{P.f[p ^ 1].as<int32_t>(), P.eff.as<int64_t>()},
                       reinterpret_cast<int64_t*>(&st->tot), P.scan_tmp);
-            });
+            };
+            std::vector<std::function<void(cudaStream_t)>> bodies(4);
+            bodies[kBranchEffPush] = [&](cudaStream_t cs) {
+                eff_scan(cs);
+                push(cs);
+            };
+            bodies[kBranchPush] = push;
+            bodies[kBranchPull] = pull;
+            bodies[kBranchPushSmall] = [&, p](cudaStream_t cs) {
+                bfs_push_small_kernel<<<static_cast<unsigned>(ctx.sm_count) * 2, 256, 0, cs>>>(
+                    st, p, P.f[p].as<int32_t>(), co, m.row_idx.as<int32_t>(), lv, P.f[p ^ 1].as<int32_t>());
+            };
+            capture_switch(ctx, s, s2, hbranch[p], bodies);
         }
         ADA_CUDA(cudaGetLastError());
     } catch (...) {
