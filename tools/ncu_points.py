@@ -35,8 +35,8 @@ def main():
         m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
     else:
         from paper_2006_16767_b200 import synth_device as SD
-        if a.input == "rmat22":
-            n, ro, ci = SD.rmat_device(22)
+        if a.input in ("rmat22", "rmat26"):
+            n, ro, ci = SD.rmat_device(26 if a.input == "rmat26" else 22)
             rows = cols = n
             vals = torch.rand(ci.numel(), device="cuda", dtype=torch.float32) + 0.5
         elif a.input == "c4":
