@@ -45,7 +45,9 @@ constexpr int kTile = 256;          // effective entries per push warp tile
 constexpr int kWin = 128;           // support positions staged per warp tile
 enum { kModeDone = 0, kModePush = 1, kModePull = 2 };
 // bodies of a level's SWITCH node (any other value: no body runs)
-enum { kBranchEffPush = 0, kBranchPush = 1, kBranchPull = 2, kBranchPushSmall = 3, kBranchNone = 4 };
+enum { kBranchEffPush = 0, kBranchPush = 1, kBranchPull = 2, kBranchPushSmall = 3, kBranchCompactPush = 4,
+       kBranchNone = 5 };
+constexpr int kSpread = 256;  // a pull level's (count, degree) counters, spread against contention
 constexpr unsigned long long kSmallPush = 4096;  // effective entries of a frontier pushed without offsets
 
 // Device-side loop state (one per plan).
@@ -61,7 +63,7 @@ struct alignas(8) BfsState {
     int eff_ok;                 // the current frontier's eff offsets are valid (compaction / init wrote them)
     long long tot;              // packed (count << kCntShift | nnz_s) of a pull level's compaction scan
     int pending;                // a level ran since the last decision (its results not yet accounted)
-    int pad2;
+    int list_ok;                // the current frontier exists as a list (a pull only marks levels)
 };
 static_assert(sizeof(BfsState) == 80, "BfsState is copied as 10 int64 words");
 constexpr int kCntShift = 36;  // pull compaction packing: nnz_s < 2^36, frontier < 2^27
@@ -103,18 +105,32 @@ __device__ int tree_walk(const DevTrees& t, int which, const double* f) {
 // handles: IF(push) and IF(pull) bodies (only the chosen one runs), and the
 // WHILE handle that repeats the two-level body until the frontier is empty.
 __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees trees, int use_trees,
-                                  const double* mfeat, int64_t n, int64_t nnz, int vbytes, int64_t* eff,
-                                  cudaGraphConditionalHandle hbranch, cudaGraphConditionalHandle hwhile) {
+                                  const double* mfeat, int64_t n, int64_t nnz, int vbytes,
+                                  unsigned long long* pcnt, cudaGraphConditionalHandle hbranch,
+                                  cudaGraphConditionalHandle hwhile) {
+    // a pull level left its frontier as marks + spread (count, degree) counters:
+    // the warp sums and clears them
+    unsigned long long pc = 0, pd = 0;
+    const bool pulled = st->pending && st->mode == kModePull;
+    if (pulled) {
+        for (int i = threadIdx.x; i < kSpread; i += 32) {
+            pc += pcnt[2 * i];
+            pd += pcnt[2 * i + 1];
+            pcnt[2 * i] = pcnt[2 * i + 1] = 0;
+        }
+        pc = warp_sum(pc);
+        pd = warp_sum(pd);
+    }
     if (threadIdx.x != 0) return;
     cudaGraphSetConditional(hbranch, kBranchNone);
     if (st->pending) {  // account for the level that produced this frontier
-        if (st->mode == kModePull) {  // its compaction scan's packed total; eff offsets written by the scan
-            const long long t = st->tot;
-            st->nf[p] = static_cast<unsigned long long>(t >> kCntShift);
-            st->ns[p] = static_cast<unsigned long long>(t & ((1ll << kCntShift) - 1));
-            eff[st->nf[p]] = static_cast<int64_t>(st->ns[p]);
-            st->eff_ok = 1;
+        if (pulled) {
+            st->nf[p] = pc;
+            st->ns[p] = pd;
+            st->list_ok = 0;
+            st->eff_ok = 0;
         } else {  // a push appended it (counters already set), unordered: offsets to be scanned
+            st->list_ok = 1;
             st->eff_ok = 0;
         }
         st->visited += static_cast<long long>(st->nf[p]);
@@ -159,8 +175,9 @@ __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees t
     }
     st->kernel = k;
     st->mode = k >= 4 ? kModePush : kModePull;
-    cudaGraphSetConditional(hbranch, k < 4        ? kBranchPull
-                                     : st->eff_ok ? kBranchPush
+    cudaGraphSetConditional(hbranch, k < 4              ? kBranchPull
+                                     : !st->list_ok     ? kBranchCompactPush
+                                     : st->eff_ok       ? kBranchPush
                                      : ns <= kSmallPush ? kBranchPushSmall
                                                         : kBranchEffPush);
     st->level += 1;
@@ -358,7 +375,9 @@ template <int G>
 __global__ void __launch_bounds__(256) bfs_pull_mark_kernel(const BfsState* st, int64_t rows,
                                                             const int64_t* __restrict__ ro,
                                                             const int32_t* __restrict__ ci,
-                                                            int32_t* __restrict__ lv) {
+                                                            const int64_t* __restrict__ co,
+                                                            int32_t* __restrict__ lv,
+                                                            unsigned long long* __restrict__ pcnt) {
     const int level = st->level;  // frontier = the vertices of level - 1
     const int lane = threadIdx.x & 31;
     const int lg = threadIdx.x & (G - 1);
@@ -377,16 +396,28 @@ __global__ void __launch_bounds__(256) bfs_pull_mark_kernel(const BfsState* st, 
     }
     const unsigned grp = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
     const bool any = (__ballot_sync(kFull, hit) & grp) != 0u;
-    if (live && any && lg == 0) lv[row] = level;
+    const bool join = live && any && lg == 0;
+    if (join) lv[row] = level;
+    // the level's size and effective nnz, one spread counter update per warp
+    const unsigned long long c = __popc(__ballot_sync(kFull, join));
+    if (c) {
+        const unsigned long long d = warp_sum(join ? static_cast<unsigned long long>(__ldg(co + row + 1) - __ldg(co + row)) : 0ull);
+        if (lane == 0) {
+            const int slot = static_cast<int>((blockIdx.x * 8u + (threadIdx.x >> 5)) % kSpread);
+            atomicAdd(pcnt + 2 * slot, c);
+            atomicAdd(pcnt + 2 * slot + 1, d);
+        }
+    }
 }
 
 // compaction items: (row joined at this level) << kCntShift | its column degree
-struct LevelIn {
+struct LevelIn {  // rows of level *level + off
     const int32_t* lv;
     const int* level;
+    int off;
     const int64_t* co;
     __device__ int64_t operator()(int64_t r) const {
-        return lv[r] == *level ? (int64_t(1) << kCntShift) | (co[r + 1] - co[r]) : 0;
+        return lv[r] == *level + off ? (int64_t(1) << kCntShift) | (co[r + 1] - co[r]) : 0;
     }
 };
 struct LevelEpi {  // the next frontier and its eff offsets (degree prefix)
@@ -422,6 +453,12 @@ __global__ void __launch_bounds__(256) bfs_push_small_kernel(BfsState* st, int p
     }
 }
 
+// eff[nnz_x] = nnz_s after a compaction (the scan's epilogue writes the
+// offsets of the entries only)
+__global__ void bfs_eff_tail_kernel(const BfsState* st, int p, int64_t* __restrict__ eff) {
+    if (threadIdx.x == 0) eff[st->nf[p]] = static_cast<int64_t>(st->ns[p]);
+}
+
 __global__ void bfs_init_kernel(BfsState* st, int32_t* lv, int64_t n, int64_t source, int32_t* f0,
                                 const int64_t* __restrict__ co, int64_t* __restrict__ eff) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -441,6 +478,7 @@ __global__ void bfs_init_kernel(BfsState* st, int32_t* lv, int64_t n, int64_t so
         st->tot = 0;
         st->pending = 0;
         st->eff_ok = 1;
+        st->list_ok = 1;
         eff[0] = 0;
         eff[1] = static_cast<int64_t>(st->ns[0]);
     }
@@ -454,7 +492,8 @@ struct BfsPlan {
     uint64_t bundle_id = 0;  // 0 = heuristic
     DevBuf state, log, f[2], eff, part, lv, trees_i, trees_d, mfeat;
     DevTrees dt{};
-    DevBuf scan_tmp;  // the pull compaction's tile sums (sized before capture)
+    DevBuf scan_tmp;  // the compaction's tile sums (sized before capture)
+    DevBuf pcnt;      // a pull level's spread (count, degree) counters
     cudaGraphExec_t exec = nullptr;
     ~BfsPlan() {
         if (exec) cudaGraphExecDestroy(exec);
@@ -507,8 +546,10 @@ void upload_trees(Context& ctx, const Bundle& b, BfsPlan& P) {
 }
 
 template <int G>
-void launch_pull_mark(cudaStream_t s, unsigned grid, BfsState* st, const Matrix& m, int32_t* lv) {
-    bfs_pull_mark_kernel<G><<<grid, 256, 0, s>>>(st, m.rows, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(), lv);
+void launch_pull_mark(cudaStream_t s, unsigned grid, BfsState* st, const Matrix& m, int32_t* lv,
+                      unsigned long long* pcnt) {
+    bfs_pull_mark_kernel<G><<<grid, 256, 0, s>>>(st, m.rows, m.row_off.as<int64_t>(), m.col_idx.as<int32_t>(),
+                                                 m.col_off.as<int64_t>(), lv, pcnt);
 }
 
 // Appends SWITCH(handle) with one body per element of `bodies` to the graph
@@ -563,6 +604,8 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     P.part.ensure(sizeof(long long) * kScanBlocks);
     P.lv.ensure(sizeof(int32_t) * static_cast<size_t>(n));
     P.scan_tmp.ensure(sizeof(int64_t) * static_cast<size_t>((n + kScanTile - 1) / kScanTile + 1));
+    P.pcnt.ensure(sizeof(unsigned long long) * 2 * kSpread);
+    ADA_CUDA(cudaMemsetAsync(P.pcnt.p, 0, sizeof(unsigned long long) * 2 * kSpread, ctx.stream));
 
     double* mf = static_cast<double*>(P.mfeat.ensure(sizeof(double) * 9));
     ADA_CUDA(cudaMemcpyAsync(mf, m.feat, sizeof(double) * 9, cudaMemcpyHostToDevice, ctx.stream));
@@ -604,7 +647,7 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     try {
         for (int p = 0; p < 2; ++p) {
             bfs_decide_kernel<<<1, 32, 0, s>>>(st, lg, p, P.dt, b ? 1 : 0, mf, n, m.nnz, m.vbytes(),
-                                               P.eff.as<int64_t>(), hbranch[p], hw);
+                                               P.pcnt.as<unsigned long long>(), hbranch[p], hw);
             auto eff_scan = [&, p](cudaStream_t cs) {  // offsets of a frontier a push appended
                 bfs_eff_partial_kernel<<<kScanBlocks, 256, 0, cs>>>(st, p, P.f[p].as<int32_t>(), co,
                                                                     P.part.as<long long>());
@@ -616,17 +659,26 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
                 bfs_push_kernel<<<push_grid, 256, 0, cs>>>(st, p, P.f[p].as<int32_t>(), P.eff.as<int64_t>(), co,
                                                            m.row_idx.as<int32_t>(), lv, P.f[p ^ 1].as<int32_t>());
             };
-            auto pull = [&, p](cudaStream_t cs) {
+            auto pull = [&, p](cudaStream_t cs) {  // marks only; the list is compacted if a push needs it
+                unsigned long long* pc = P.pcnt.as<unsigned long long>();
                 switch (G) {
-                    case 1: launch_pull_mark<1>(cs, pull_grid, st, m, lv); break;
-                    case 2: launch_pull_mark<2>(cs, pull_grid, st, m, lv); break;
-                    case 4: launch_pull_mark<4>(cs, pull_grid, st, m, lv); break;
-                    default: launch_pull_mark<8>(cs, pull_grid, st, m, lv); break;
+                    case 1: launch_pull_mark<1>(cs, pull_grid, st, m, lv, pc); break;
+                    case 2: launch_pull_mark<2>(cs, pull_grid, st, m, lv, pc); break;
+                    case 4: launch_pull_mark<4>(cs, pull_grid, st, m, lv, pc); break;
+                    default: launch_pull_mark<8>(cs, pull_grid, st, m, lv, pc); break;
                 }
-                scan3(ctx, n, LevelIn{lv, &st->level, co}, LevelEpi{P.f[p ^ 1].as<int32_t>(), P.eff.as<int64_t>()},
-                      reinterpret_cast<int64_t*>(&st->tot), P.scan_tmp);
             };
-            std::vector<std::function<void(cudaStream_t)>> bodies(4);
+            auto compact = [&, p](cudaStream_t) {  // the frontier (rows of level - 1) as a list + eff
+                scan3(ctx, n, LevelIn{lv, &st->level, -1, co},
+                      LevelEpi{P.f[p].as<int32_t>(), P.eff.as<int64_t>()}, reinterpret_cast<int64_t*>(&st->tot),
+                      P.scan_tmp);
+                bfs_eff_tail_kernel<<<1, 32, 0, ctx.stream>>>(st, p, P.eff.as<int64_t>());
+            };
+            std::vector<std::function<void(cudaStream_t)>> bodies(5);
+            bodies[kBranchCompactPush] = [&](cudaStream_t cs) {
+                compact(cs);
+                push(cs);
+            };
             bodies[kBranchEffPush] = [&](cudaStream_t cs) {
                 eff_scan(cs);
                 push(cs);
