@@ -16,6 +16,8 @@ from paper_2006_16767_b200 import synth_device as SD  # noqa: E402
 
 
 def main():
+    import os
+    panels = [int(v) for v in os.environ.get("PANELS_KIB", "0").split(",")]
     for scale in [int(a) for a in sys.argv[1:]] or [22]:
         ctx = A.Context(0)
         n, ro, ci = SD.rmat_device(scale)
@@ -34,21 +36,23 @@ def main():
             xd = (torch.rand(n, generator=g, device="cuda") < d).float() * (torch.rand(n, generator=g, device="cuda") + 0.5)
             x = A.DeviceVector(n, np.float32, ctx)
             x.set_dense_device(xd.data_ptr())
-            ys, ts = [], []
-            for k in (0, 1):
+            ys, ts, names = [], [], []
+            for k, pk in [(0, pk) for pk in panels] + [(1, 0)]:
+                cfg = A.KernelConfig(bin_panel_kib=pk)
                 x.prepare(k)
-                A.run_kernel(m, k, x, out=out)
+                A.run_kernel(m, k, x, cfg, out=out)
                 t = []
                 for _ in range(5):
                     with torch.cuda.stream(stream):
                         torch.cuda._sleep(400_000)
-                    A.run_kernel(m, k, x, out=out)
+                    A.run_kernel(m, k, x, cfg, out=out)
                     t.append(out.elapsed())
                 ts.append(statistics.median(t))
+                names.append(f"K{k}" + (f"/panel {pk} KiB" if pk else ""))
                 ys.append(out.dense().values.astype(np.float64))
-            dev = float(np.max(np.abs(ys[0] - ys[1]) / (np.abs(ys[1]) + 1e-3)))
-            print(f"rmat{scale} x={d}: K0 {ts[0] * 1e6:9.1f} us  K1 {ts[1] * 1e6:9.1f} us  max rel dev {dev:.1e}",
-                  flush=True)
+            dev = max(float(np.max(np.abs(y - ys[-1]) / (np.abs(ys[-1]) + 1e-3))) for y in ys)
+            print(f"rmat{scale} x={d}: " + "  ".join(f"{nm} {t * 1e6:9.1f} us" for nm, t in zip(names, ts))
+                  + f"  max rel dev {dev:.1e}", flush=True)
         del m, out, x, ctx
         torch.cuda.empty_cache()
 
