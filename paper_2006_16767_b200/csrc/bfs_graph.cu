@@ -6,27 +6,47 @@
 // boolean semiring, or a pattern matrix under plus-times / min-plus, where
 // y_i != identity iff row i has a frontier neighbour) every level is one of
 //
-//   push  (column choices K4-K7): K6's load-balanced tiles over the
-//         frontier's effective entries (eff offsets = scan of the frontier's
-//         column degrees); each unvisited row is claimed once (atomicCAS on
-//         its level) and appended to the next frontier (warp-aggregated);
+//   push  (column choices K4-K7): each unvisited row reached from the
+//         frontier is claimed once (atomicCAS on its level) and appended to
+//         the next frontier list (one counter update per warp and batch);
 //   pull  (row choices K0-K3): the output-masked row pull (K2/K3 with the
 //         visited rows skipped); a frontier neighbour is a column whose level
-//         is the previous level, and a row stops at its first one;
+//         is the previous level, and a row stops at its first one.  A pull
+//         only marks levels and counts the new frontier (size, effective
+//         nnz) in spread counters: no list is built.
 //
 // and the choice -- the built-in bytes model, or the trained selector's
-// three trees walked ON THE DEVICE over the same 13 features the host
-// selector reads (matrix features + nnz_x / x_sparsity / nnz_s / m_sparsity
-// from the frontier counters) -- is made by a one-warp kernel at the start
-// of the level.  The whole traversal is ONE CUDA graph built once per
-// (matrix, context, policy): a WHILE conditional node repeats a two-level
-// body; in each level the decision kernel sets IF(push) / IF(pull)
-// conditional handles so only the chosen branch's kernels run, every kernel
-// reading its sizes from device memory.  One graph launch and one host
-// synchronisation per traversal.  Per-level reports (kernel, frontier size,
-// effective nnz, device time from %globaltimer) are logged on the device.
+// trees walked ON THE DEVICE over the same 13 features the host selector
+// reads (matrix features + nnz_x / x_sparsity / nnz_s / m_sparsity from the
+// frontier counters; the splits on matrix features folded on the host, so
+// the walk is a few shared-memory nodes) -- is made by a one-warp kernel at
+// the start of the level.  The whole traversal is ONE CUDA graph built once
+// per (matrix, context, policy): a WHILE conditional node repeats a
+// two-level body; in each level the decision kernel sets a SWITCH handle so
+// only the chosen branch runs, every kernel reading its sizes from device
+// memory:
+//
+//   Push      the source's push over K6's load-balanced tiles (eff offsets
+//             written by the init kernel);
+//   Pull      the masked pull, 4 rows per thread;
+//   MarkPush  a push from the previous (pull) level's marks, one pass over
+//             the level array; vertices of high degree become chunk tasks
+//             for a second, grid-wide kernel;
+//   ListPush  the same over the list a push appended;
+//   Tail      small frontiers pushed level after level by one block, with
+//             the per-level decision made in the kernel (one node for the
+//             whole tail of the traversal).
+//
+// Kernel nodes inside conditional bodies cost ~5 us each and a
+// WHILE/SWITCH level ~6 us on B200 (tools/microbench/graph_cond_mb.cu), so
+// every branch is at most two kernels and none needs a scan.  One graph
+// launch and one host synchronisation per traversal.  Per-level reports
+// (kernel, frontier size, effective nnz, device time from %globaltimer) are
+// logged on the device.
 #include <algorithm>
 #include <functional>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -40,15 +60,14 @@ namespace ada {
 namespace {
 
 constexpr int kMaxLog = 1 << 16;    // per-level log capacity
-constexpr int kScanBlocks = 256;    // fixed grid of the eff-offset scan
 constexpr int kTile = 256;          // effective entries per push warp tile
 constexpr int kWin = 128;           // support positions staged per warp tile
 enum { kModeDone = 0, kModePush = 1, kModePull = 2 };
 // bodies of a level's SWITCH node (any other value: no body runs)
-enum { kBranchEffPush = 0, kBranchPush = 1, kBranchPull = 2, kBranchPushSmall = 3, kBranchCompactPush = 4,
-       kBranchNone = 5 };
+enum { kBranchPush = 0, kBranchPull = 1, kBranchTail = 2, kBranchMarkPush = 3, kBranchListPush = 4, kBranchNone = 5 };
 constexpr int kSpread = 256;  // a pull level's (count, degree) counters, spread against contention
-constexpr unsigned long long kSmallPush = 4096;  // effective entries of a frontier pushed without offsets
+constexpr unsigned long long kTailMax = 4096;    // frontier size the one-block tail loop takes
+constexpr unsigned long long kTailEdges = 8192;  // and its effective entries
 
 // Device-side loop state (one per plan).
 struct alignas(8) BfsState {
@@ -60,18 +79,19 @@ struct alignas(8) BfsState {
     int kernel;                 // KernelId::index() selected for this level
     int done;
     int nlog;                   // levels logged
-    int eff_ok;                 // the current frontier's eff offsets are valid (compaction / init wrote them)
-    long long tot;              // packed (count << kCntShift | nnz_s) of a pull level's compaction scan
+    int eff_ok;                 // the current frontier's eff offsets are valid (init wrote them)
     int pending;                // a level ran since the last decision (its results not yet accounted)
     int list_ok;                // the current frontier exists as a list (a pull only marks levels)
 };
-static_assert(sizeof(BfsState) == 80, "BfsState is copied as 10 int64 words");
-constexpr int kCntShift = 36;  // pull compaction packing: nnz_s < 2^36, frontier < 2^27
+static_assert(sizeof(BfsState) % 8 == 0, "BfsState is copied as int64 words");
 
 struct LogEntry {               // one row of adaspmv_iteration_report
     long long nnz_x, nnz_s;
     int kernel, exec_mode;
     unsigned long long t0;      // %globaltimer at the level's decision (ns)
+#ifdef ADA_BFS_TRACE
+    unsigned long long tk0, tk1;  // first block start / last block end of the level's kernels
+#endif
 };
 
 // Flattened decision trees for the device walk.
@@ -82,7 +102,21 @@ struct DevTrees {
     const int32_t* leaf;
     const double* threshold;
     int root[4];  // [3] = -1 without a workload_col tree (schema 1)
+    // The same trees specialised to the matrix: every split on a matrix
+    // feature (0-8, fixed for the traversal) folded on the host, leaving only
+    // splits on the frontier features 9-12 -- a few nodes, staged in shared
+    // memory by the deciding kernel (a walk through global memory is a chain
+    // of dependent loads per node, ~10 us per decision).  nsmall = 0: use
+    // the full trees.
+    const struct SmallNode* small;
+    int nsmall;
+    int sroot[4];
 };
+struct SmallNode {
+    double thr;
+    int16_t feat, left, right, leaf;
+};
+constexpr int kSmallNodes = 256;
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -90,7 +124,32 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-__device__ int tree_walk(const DevTrees& t, int which, const double* f) {
+// Diagnostic build (-DADA_BFS_TRACE): the level's kernels record their
+// first-block start / last-block end in its log entry.
+#ifdef ADA_BFS_TRACE
+__device__ LogEntry* g_bfs_log;
+#define BFS_TRACE_BEGIN(st) \
+    if (threadIdx.x == 0 && (st)->nlog > 0) atomicMin(&g_bfs_log[(st)->nlog - 1].tk0, globaltimer())
+#define BFS_TRACE_END(st)                                                                          \
+    do {                                                                                           \
+        __syncthreads();                                                                           \
+        if (threadIdx.x == 0 && (st)->nlog > 0) atomicMax(&g_bfs_log[(st)->nlog - 1].tk1, globaltimer()); \
+    } while (0)
+#else
+#define BFS_TRACE_BEGIN(st)
+#define BFS_TRACE_END(st)
+#endif
+
+__device__ int tree_walk(const DevTrees& t, const SmallNode* sn, int which, const double* f) {
+    if (sn) {
+        int i = t.sroot[which];
+        for (int guard = 0; guard < kSmallNodes; ++guard) {
+            const SmallNode& nd = sn[i];
+            if (nd.feat < 0) return nd.leaf;
+            i = f[nd.feat] <= nd.thr ? nd.left : nd.right;  // <= goes left
+        }
+        return 0;
+    }
     int i = t.root[which];
     for (int guard = 0; guard < 4096; ++guard) {
         const int32_t feat = t.feature[i];
@@ -100,14 +159,51 @@ __device__ int tree_walk(const DevTrees& t, int which, const double* f) {
     return 0;
 }
 
+// Stages the specialised trees in shared memory (all threads of the calling
+// group take part; returns nullptr when they are not available).
+__device__ __forceinline__ const SmallNode* stage_trees(const DevTrees& t, int use_trees, SmallNode* buf, int tid,
+                                                        int nthreads) {
+    if (!use_trees || t.nsmall <= 0) return nullptr;
+    for (int i = tid; i < t.nsmall; i += nthreads) buf[i] = t.small[i];
+    return buf;
+}
+
+// The kernel for a frontier of nf vertices / ns effective entries: the
+// trained selector's trees (SPEC.md:226 feature order, as selector.cpp reads
+// them) or the built-in bytes model (bfs.cu heuristic_kernel).  `visited`
+// counts the frontier.
+__device__ int bfs_choose(const DevTrees& trees, const SmallNode* sn, int use_trees, const double* mfeat, int64_t n,
+                          int64_t nnz, int vbytes, long long visited, unsigned long long nf, unsigned long long ns) {
+    if (use_trees) {
+        double f[ADASPMV_NUM_FEATURES];
+        for (int i = 0; i < 9; ++i) f[i] = sn ? 0.0 : mfeat[i];  // folded into the specialised trees
+        f[9] = static_cast<double>(nf);
+        f[10] = n > 0 ? static_cast<double>(nf) / static_cast<double>(n) : 0.0;
+        f[11] = static_cast<double>(ns);
+        f[12] = nnz > 0 ? static_cast<double>(ns) / static_cast<double>(nnz) : 0.0;
+        const int pattern = tree_walk(trees, sn, 0, f);
+        const int lb = tree_walk(trees, sn, pattern == 0 && trees.root[3] >= 0 ? 3 : 1, f) == 1 ? 1 : 0;
+        if (pattern == 2) return lb;
+        if (pattern == 1) return 2 + lb;
+        return 4 + 2 * lb + (tree_walk(trees, sn, 2, f) == 1 ? 1 : 0);
+    }
+    // SURVEY.md 8(d) push / masked-pull bytes
+    const double unvisited = n > 0 ? 1.0 - static_cast<double>(visited) / static_cast<double>(n) : 0.0;
+    const double push = static_cast<double>(nf) * 20.0 + static_cast<double>(ns) * (4.0 + vbytes) +
+                        (ns <= 4096 ? 0.0 : static_cast<double>(n) * vbytes);
+    const double pull = static_cast<double>(n + 1) * 8.0 + static_cast<double>(nnz) * 4.0 * unvisited +
+                        static_cast<double>(n) / 8.0 + static_cast<double>(n) * vbytes * unvisited;
+    return push <= pull ? (ns <= 4096 ? 7 : 6) : 2;
+}
+
 // Start of a level: decide push / pull for the frontier of parity p.
 // The level's branch is selected by setting the graph's conditional
 // handles: IF(push) and IF(pull) bodies (only the chosen one runs), and the
 // WHILE handle that repeats the two-level body until the frontier is empty.
 __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees trees, int use_trees,
                                   const double* mfeat, int64_t n, int64_t nnz, int vbytes,
-                                  unsigned long long* pcnt, cudaGraphConditionalHandle hbranch,
-                                  cudaGraphConditionalHandle hwhile) {
+                                  unsigned long long* pcnt, unsigned long long* bigc,
+                                  cudaGraphConditionalHandle hbranch, cudaGraphConditionalHandle hwhile) {
     // a pull level left its frontier as marks + spread (count, degree) counters:
     // the warp sums and clears them
     unsigned long long pc = 0, pd = 0;
@@ -121,8 +217,12 @@ __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees t
         pc = warp_sum(pc);
         pd = warp_sum(pd);
     }
+    __shared__ SmallNode s_tree[kSmallNodes];
+    const SmallNode* sn = stage_trees(trees, use_trees, s_tree, threadIdx.x, 32);
+    __syncwarp();
     if (threadIdx.x != 0) return;
     cudaGraphSetConditional(hbranch, kBranchNone);
+    *bigc = 0;  // the scan push's big-vertex tasks of this level
     if (st->pending) {  // account for the level that produced this frontier
         if (pulled) {
             st->nf[p] = pc;
@@ -150,40 +250,17 @@ __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees t
         if (st->nlog < kMaxLog) log[st->nlog].t0 = now;  // end stamp of the last level
         return;
     }
-    int k;
-    if (use_trees) {
-        // the 13 features in frozen order, as selector.cpp reads them
-        double f[ADASPMV_NUM_FEATURES];
-        for (int i = 0; i < 9; ++i) f[i] = mfeat[i];
-        f[9] = static_cast<double>(nf);
-        f[10] = n > 0 ? static_cast<double>(nf) / static_cast<double>(n) : 0.0;
-        f[11] = static_cast<double>(ns);
-        f[12] = nnz > 0 ? static_cast<double>(ns) / static_cast<double>(nnz) : 0.0;
-        const int pattern = tree_walk(trees, 0, f);
-        const int lb = tree_walk(trees, pattern == 0 && trees.root[3] >= 0 ? 3 : 1, f) == 1 ? 1 : 0;
-        if (pattern == 2) k = lb;
-        else if (pattern == 1) k = 2 + lb;
-        else k = 4 + 2 * lb + (tree_walk(trees, 2, f) == 1 ? 1 : 0);
-    } else {
-        // bfs.cu heuristic_kernel: SURVEY.md 8(d) push / masked-pull bytes
-        const double unvisited = n > 0 ? 1.0 - static_cast<double>(st->visited) / static_cast<double>(n) : 0.0;
-        const double push = static_cast<double>(nf) * 20.0 + static_cast<double>(ns) * (4.0 + vbytes) +
-                            (ns <= 4096 ? 0.0 : static_cast<double>(n) * vbytes);
-        const double pull = static_cast<double>(n + 1) * 8.0 + static_cast<double>(nnz) * 4.0 * unvisited +
-                            static_cast<double>(n) / 8.0 + static_cast<double>(n) * vbytes * unvisited;
-        k = push <= pull ? (ns <= 4096 ? 7 : 6) : 2;
-    }
+    const int k = bfs_choose(trees, sn, use_trees, mfeat, n, nnz, vbytes, st->visited, nf, ns);
     st->kernel = k;
     st->mode = k >= 4 ? kModePush : kModePull;
-    cudaGraphSetConditional(hbranch, k < 4              ? kBranchPull
-                                     : !st->list_ok     ? kBranchCompactPush
-                                     : st->eff_ok       ? kBranchPush
-                                     : ns <= kSmallPush ? kBranchPushSmall
-                                                        : kBranchEffPush);
+    cudaGraphSetConditional(hbranch, k < 4                                ? kBranchPull
+                                     : !st->list_ok                       ? kBranchMarkPush
+                                     : st->eff_ok                         ? kBranchPush
+                                     : ns <= kTailEdges && nf <= kTailMax ? kBranchTail
+                                                                          : kBranchListPush);
     st->level += 1;
     st->nf[p ^ 1] = 0;
     st->ns[p ^ 1] = 0;
-    st->tot = 0;
     st->pending = 1;
     if (st->nlog < kMaxLog) {
         LogEntry& e = log[st->nlog];
@@ -192,67 +269,12 @@ __global__ void bfs_decide_kernel(BfsState* st, LogEntry* log, int p, DevTrees t
         e.kernel = k;
         e.exec_mode = k >= 4 ? ADASPMV_EXEC_FUSED_PUSH_LB : ADASPMV_EXEC_MASKED_PULL;
         e.t0 = now;
+#ifdef ADA_BFS_TRACE
+        e.tk0 = ~0ull;
+        e.tk1 = 0;
+#endif
     }
     st->nlog += 1;
-}
-
-// ---- eff offsets of the frontier (push only): fixed-grid reduce-then-scan
-__global__ void __launch_bounds__(256) bfs_eff_partial_kernel(const BfsState* st, int p, const int32_t* __restrict__ f,
-                                                              const int64_t* __restrict__ co,
-                                                              long long* __restrict__ part) {
-    if (st->mode != kModePush) return;
-    const long long n = static_cast<long long>(st->nf[p]);
-    const long long chunk = (n + gridDim.x - 1) / gridDim.x;
-    const long long b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
-    long long s = 0;
-    for (long long i = b0 + threadIdx.x; i < b1; i += 256) {
-        const int32_t c = f[i];
-        s += co[c + 1] - co[c];
-    }
-    __shared__ long long red[8];
-    s = warp_sum(s);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        long long t = 0;
-        for (int w = 0; w < 8; ++w) t += red[w];
-        part[blockIdx.x] = t;
-    }
-}
-
-__global__ void __launch_bounds__(kScanBlocks) bfs_eff_top_kernel(const BfsState* st, long long* __restrict__ part) {
-    if (st->mode != kModePush) return;
-    __shared__ long long sm[kScanBlocks / 32 + 1];
-    const long long v = part[threadIdx.x];
-    long long tot;
-    const long long ex = block_exclusive_sum<kScanBlocks>(v, sm, &tot);
-    part[threadIdx.x] = ex;
-}
-
-__global__ void __launch_bounds__(256) bfs_eff_write_kernel(const BfsState* st, int p, const int32_t* __restrict__ f,
-                                                            const int64_t* __restrict__ co,
-                                                            const long long* __restrict__ part,
-                                                            int64_t* __restrict__ eff) {
-    if (st->mode != kModePush) return;
-    const long long n = static_cast<long long>(st->nf[p]);
-    const long long chunk = (n + gridDim.x - 1) / gridDim.x;
-    const long long b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
-    if (b0 >= b1) return;  // block-uniform
-    __shared__ long long sm[256 / 32 + 1];
-    long long run = part[blockIdx.x];
-    for (long long i0 = b0; i0 < b1; i0 += 256) {
-        const long long i = i0 + threadIdx.x;
-        long long d = 0;
-        if (i < b1) {
-            const int32_t c = f[i];
-            d = co[c + 1] - co[c];
-        }
-        long long tot;
-        const long long ex = block_exclusive_sum<256>(d, sm, &tot);
-        if (i < b1) eff[i] = run + ex;
-        run += tot;
-    }
-    if (b1 == n && threadIdx.x == 0) eff[n] = run;
 }
 
 // largest s in [lo, hi) with eff[s] <= pos (warp-cooperative; eff[lo] <= pos)
@@ -270,23 +292,6 @@ __device__ __forceinline__ long long warp_seg(const int64_t* __restrict__ eff, l
     return lo + (31 - __clz(b));
 }
 
-// Appends `row` (when `claim`) to the next frontier: one counter update per
-// warp instruction, slots by rank among the claiming lanes.
-__device__ __forceinline__ void append_claimed(bool claim, int32_t row, const int64_t* __restrict__ co,
-                                               BfsState* st, int q, int32_t* __restrict__ nf_out, int lane) {
-    const unsigned ballot = __ballot_sync(kFull, claim);
-    if (ballot == 0u) return;
-    const long long deg = warp_sum(claim ? static_cast<long long>(__ldg(co + row + 1) - __ldg(co + row)) : 0ll);
-    const int leader = __ffs(ballot) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) {
-        base = atomicAdd(&st->nf[q], static_cast<unsigned long long>(__popc(ballot)));
-        atomicAdd(&st->ns[q], static_cast<unsigned long long>(deg));
-    }
-    base = __shfl_sync(kFull, base, leader);
-    if (claim) nf_out[base + __popc(ballot & lanemask_lt())] = row;
-}
-
 // Push over K6's load-balanced tiles (kernels_col.cu col_lb_kernel MODE 2),
 // grid-stride over the tiles of the frontier's effective entries.
 __global__ void __launch_bounds__(256) bfs_push_kernel(BfsState* st, int p, const int32_t* __restrict__ f,
@@ -294,6 +299,7 @@ __global__ void __launch_bounds__(256) bfs_push_kernel(BfsState* st, int p, cons
                                                        const int64_t* __restrict__ co,
                                                        const int32_t* __restrict__ ri, int32_t* __restrict__ lv,
                                                        int32_t* __restrict__ nf_out) {
+    BFS_TRACE_BEGIN(st);
     if (st->mode != kModePush) return;
     constexpr int kW = 8, kJ = kTile / 32;
     __shared__ long long s_base[kW][kWin];
@@ -356,21 +362,49 @@ __global__ void __launch_bounds__(256) bfs_push_kernel(BfsState* st, int p, cons
         int r[kJ];
 #pragma unroll
         for (int j = 0; j < kJ; ++j) r[j] = kidx[j] >= 0 ? ld_stream(ri + kidx[j]) : 0;
+        // claims of the whole tile, appended with one counter update per warp
+        // and tile (per instruction, the fat levels serialise on the counters)
+        unsigned bal[kJ];
+        long long deg = 0;
+        int cnt = 0;
+        // all the tile's level reads, then all its claims, in flight together
+        int lr[kJ];
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) lr[j] = kidx[j] >= 0 ? lv[r[j]] : 0;
+        bool claim[kJ];
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) claim[j] = lr[j] < 0 && atomicCAS(lv + r[j], -1, level) == -1;
 #pragma unroll
         for (int j = 0; j < kJ; ++j) {
-            const bool claim = kidx[j] >= 0 && lv[r[j]] < 0 && atomicCAS(lv + r[j], -1, level) == -1;
-            append_claimed(claim, r[j], co, st, q, nf_out, lane);
+            bal[j] = __ballot_sync(kFull, claim[j]);
+            cnt += __popc(bal[j]);
+            if (claim[j]) deg += __ldg(co + r[j] + 1) - __ldg(co + r[j]);
+        }
+        if (cnt == 0) continue;  // warp-uniform
+        deg = warp_sum(deg);
+        unsigned long long base = 0;
+        if (lane == 0) {
+            base = atomicAdd(&st->nf[q], static_cast<unsigned long long>(cnt));
+            atomicAdd(&st->ns[q], static_cast<unsigned long long>(deg));
+        }
+        base = __shfl_sync(kFull, base, 0);
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+            if ((bal[j] >> lane) & 1u) nf_out[base + __popc(bal[j] & lanemask_lt())] = r[j];
+            base += __popc(bal[j]);
         }
     }
+    BFS_TRACE_END(st);
 }
 
 // Output-masked pull with early exit (bfs.cu bfs_pull_kernel), G lanes per
-// row, one group per row (full grid: the block scheduler balances rows that
-// run long); a row with a frontier neighbour (a column of the previous
-// level, read from the level array: no frontier bitmap to build and clear)
-// gets its level.
-// The next frontier is then compacted by a scan over the levels (no shared
-// append counter: the fat pull levels would serialise on it).
+// row; a row with a frontier neighbour (a column of the previous level, read
+// from the level array: no frontier bitmap to build and clear) gets its
+// level.  A resident grid strides over 256-thread row windows: a full grid
+// (one block per window, 16 K blocks on C3) pays ~10 us of block launches
+// per level on B200 (tools/microbench/graph_cond_mb.cu), and the fine
+// interleave of windows keeps rows that run long spread over the SMs.
+// A push after a pull reads the marks (MarkPush): no list is compacted.
 template <int G>
 __global__ void __launch_bounds__(256) bfs_pull_mark_kernel(const BfsState* st, int64_t rows,
                                                             const int64_t* __restrict__ ro,
@@ -381,27 +415,40 @@ __global__ void __launch_bounds__(256) bfs_pull_mark_kernel(const BfsState* st, 
     const int level = st->level;  // frontier = the vertices of level - 1
     const int lane = threadIdx.x & 31;
     const int lg = threadIdx.x & (G - 1);
-    const long long row = (static_cast<long long>(blockIdx.x) * 256 + threadIdx.x) / G;
-    const bool live = row < rows && lv[row] < 0;
-    bool hit = false;
-    if (live) {
-        const long long b = __ldg(ro + row), e = __ldg(ro + row + 1);
-        for (long long k0 = b + lg; k0 < e && !hit; k0 += G * 4) {
-            int c[4];
+    const unsigned grp = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    unsigned long long c = 0, d = 0;  // this lane's joins and their column degrees (lane 0 sums the warp)
+    const long long total = rows * G;
+    for (long long base = static_cast<long long>(blockIdx.x) * 256; base < total;
+         base += static_cast<long long>(gridDim.x) * 256) {  // block-uniform trip count
+        const long long row = (base + threadIdx.x) / G;
+        const bool live = row < rows && lv[row] < 0;
+        bool hit = false;
+        if (live) {
+            const long long b = __ldg(ro + row), e = __ldg(ro + row + 1);
+            for (long long k0 = b + lg; k0 < e && !hit; k0 += G * 4) {
+                // 4 neighbours' levels in flight at once (a short-circuit
+                // chain would serialise the 4 dependent loads)
+                int cc[4], lc[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) c[j] = k0 + j * G < e ? __ldg(ci + k0 + j * G) : -1;
+                for (int j = 0; j < 4; ++j) cc[j] = k0 + j * G < e ? __ldg(ci + k0 + j * G) : -1;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) hit = hit || (c[j] >= 0 && lv[c[j]] == level - 1);
+                for (int j = 0; j < 4; ++j) lc[j] = cc[j] >= 0 ? lv[cc[j]] : -2;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) hit |= lc[j] == level - 1;
+            }
+        }
+        const bool any = (__ballot_sync(kFull, hit) & grp) != 0u;
+        const bool join = live && any && lg == 0;
+        if (join) {
+            lv[row] = level;
+            c += 1;
+            d += static_cast<unsigned long long>(__ldg(co + row + 1) - __ldg(co + row));
         }
     }
-    const unsigned grp = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
-    const bool any = (__ballot_sync(kFull, hit) & grp) != 0u;
-    const bool join = live && any && lg == 0;
-    if (join) lv[row] = level;
     // the level's size and effective nnz, one spread counter update per warp
-    const unsigned long long c = __popc(__ballot_sync(kFull, join));
+    c = warp_sum(c);
     if (c) {
-        const unsigned long long d = warp_sum(join ? static_cast<unsigned long long>(__ldg(co + row + 1) - __ldg(co + row)) : 0ull);
+        d = warp_sum(d);
         if (lane == 0) {
             const int slot = static_cast<int>((blockIdx.x * 8u + (threadIdx.x >> 5)) % kSpread);
             atomicAdd(pcnt + 2 * slot, c);
@@ -410,53 +457,412 @@ __global__ void __launch_bounds__(256) bfs_pull_mark_kernel(const BfsState* st, 
     }
 }
 
-// compaction items: (row joined at this level) << kCntShift | its column degree
-struct LevelIn {  // rows of level *level + off
-    const int32_t* lv;
-    const int* level;
-    int off;
-    const int64_t* co;
-    __device__ int64_t operator()(int64_t r) const {
-        return lv[r] == *level + off ? (int64_t(1) << kCntShift) | (co[r + 1] - co[r]) : 0;
-    }
-};
-struct LevelEpi {  // the next frontier and its eff offsets (degree prefix)
-    int32_t* out;
-    int64_t* eff;
-    __device__ void operator()(int64_t r, int64_t p, int64_t v) const {
-        if (!v) return;
-        const int64_t slot = p >> kCntShift;
-        out[slot] = static_cast<int32_t>(r);
-        eff[slot] = p & ((int64_t(1) << kCntShift) - 1);
-    }
-};
+// The pull with one lane per row, 4 rows per thread (consecutive: one 16-B
+// level load) and their first kProbe neighbours' levels in flight together:
+// a thread holding one row waits ~4 dependent round trips (level, offsets,
+// neighbour, its level) per row, and with ~14 rows per thread per level on
+// C3 those chains, not bandwidth, set the level's time.  Rows not settled
+// by the probe continue 4 neighbours at a time.
+constexpr int kProbe = 2;
 
-// Push of a small frontier (<= kSmallPush effective entries) that a push
-// appended (no eff offsets): one block per frontier vertex, its column walked
-// by the block's warps -- one launch instead of the offset scan + LB push.
-__global__ void __launch_bounds__(256) bfs_push_small_kernel(BfsState* st, int p, const int32_t* __restrict__ f,
+__global__ void __launch_bounds__(256) bfs_pull_mark4_kernel(const BfsState* st, int64_t rows,
+                                                             const int64_t* __restrict__ ro,
+                                                             const int32_t* __restrict__ ci,
                                                              const int64_t* __restrict__ co,
-                                                             const int32_t* __restrict__ ri,
-                                                             int32_t* __restrict__ lv, int32_t* __restrict__ nf_out) {
-    const long long nx = static_cast<long long>(st->nf[p]);
+                                                             int32_t* __restrict__ lv,
+                                                             unsigned long long* __restrict__ pcnt) {
+    BFS_TRACE_BEGIN(st);
     const int level = st->level;
     const int lane = threadIdx.x & 31;
-    for (long long s = blockIdx.x; s < nx; s += gridDim.x) {
-        const int32_t v = f[s];
-        const long long b = __ldg(co + v), e = __ldg(co + v + 1);
-        for (long long k0 = b + (threadIdx.x & ~31); k0 < e; k0 += 256) {  // warp-uniform trip count
-            const long long k = k0 + lane;
-            const int32_t r = k < e ? __ldg(ri + k) : 0;
-            const bool claim = k < e && lv[r] < 0 && atomicCAS(lv + r, -1, level) == -1;
-            append_claimed(claim, r, co, st, p ^ 1, nf_out, lane);
+    unsigned long long c = 0, d = 0;
+    for (long long base = static_cast<long long>(blockIdx.x) * 1024; base < rows;
+         base += static_cast<long long>(gridDim.x) * 1024) {
+        const long long r0 = base + threadIdx.x * 4;
+        if (r0 >= rows) continue;
+        int l4[4];
+        if (r0 + 3 < rows) {
+            const int4 t = *reinterpret_cast<const int4*>(lv + r0);
+            l4[0] = t.x;
+            l4[1] = t.y;
+            l4[2] = t.z;
+            l4[3] = t.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) l4[j] = r0 + j < rows ? lv[r0 + j] : 0;
         }
+        bool live[4];
+        bool any_live = false;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            live[j] = l4[j] < 0;
+            any_live |= live[j];
+        }
+        if (!any_live) continue;
+        long long off[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) off[j] = r0 + j <= rows ? __ldg(ro + r0 + j) : 0;
+        int cc[4][kProbe];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int t = 0; t < kProbe; ++t)
+                cc[j][t] = live[j] && off[j] + t < off[j + 1] ? __ldg(ci + off[j] + t) : -1;
+        int lc[4][kProbe];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int t = 0; t < kProbe; ++t) lc[j][t] = cc[j][t] >= 0 ? lv[cc[j][t]] : -2;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (!live[j]) continue;
+            bool hit = false;
+#pragma unroll
+            for (int t = 0; t < kProbe; ++t) hit |= lc[j][t] == level - 1;
+            const long long e = off[j + 1];
+            for (long long k0 = off[j] + kProbe; k0 < e && !hit; k0 += 4) {
+                int c4[4], l4n[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) c4[u] = k0 + u < e ? __ldg(ci + k0 + u) : -1;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) l4n[u] = c4[u] >= 0 ? lv[c4[u]] : -2;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) hit |= l4n[u] == level - 1;
+            }
+            if (hit) {
+                lv[r0 + j] = level;
+                c += 1;
+                d += static_cast<unsigned long long>(__ldg(co + r0 + j + 1) - __ldg(co + r0 + j));
+            }
+        }
+    }
+    c = warp_sum(c);
+    if (c) {
+        d = warp_sum(d);
+        if (lane == 0) {
+            const int slot = static_cast<int>((blockIdx.x * 8u + (threadIdx.x >> 5)) % kSpread);
+            atomicAdd(pcnt + 2 * slot, c);
+            atomicAdd(pcnt + 2 * slot + 1, d);
+        }
+    }
+    BFS_TRACE_END(st);
+}
+
+// Push without offsets: the frontier is read either from the previous
+// level's marks (a pull left no list: every vertex with lv == level - 1) or
+// from the list a push appended, in one pass -- no compaction or offset scan
+// (3-5 kernel nodes per level through the graph machinery).  A resident grid
+// strides over 256-vertex windows; each warp flattens the effective entries
+// of its 32 vertices (degree prefix in registers, the owning lane found by a
+// 5-step shuffle search) and moves them 4 per lane at a time with all loads,
+// level reads and claims in flight together.  Vertices of degree >
+// kBigDeg become (vertex, chunk) tasks of kBigChunk entries, appended with
+// ONE 64-bit atomic (count << 40 | tasks) so the list's task starts ascend,
+// and bfs_big_push_kernel spreads them over the whole grid.
+constexpr int kBigDeg = 256;
+constexpr int kBigChunk = 2048;
+constexpr int kBigShift = 40;
+
+__device__ __forceinline__ void claim_and_append(const int32_t (&r)[4], int32_t* __restrict__ lv, int level,
+                                                 const int64_t* __restrict__ co, BfsState* st, int q,
+                                                 int32_t* __restrict__ nf_out, int lane) {
+    int lr[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) lr[j] = r[j] >= 0 ? lv[r[j]] : 0;
+    bool claim[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) claim[j] = lr[j] < 0 && atomicCAS(lv + r[j], -1, level) == -1;
+    unsigned bal[4];
+    int cnt = 0;
+    long long deg = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        bal[j] = __ballot_sync(kFull, claim[j]);
+        cnt += __popc(bal[j]);
+        if (claim[j]) deg += __ldg(co + r[j] + 1) - __ldg(co + r[j]);
+    }
+    if (cnt == 0) return;  // warp-uniform
+    deg = warp_sum(deg);
+    unsigned long long base = 0;
+    if (lane == 0) {
+        base = atomicAdd(&st->nf[q], static_cast<unsigned long long>(cnt));
+        atomicAdd(&st->ns[q], static_cast<unsigned long long>(deg));
+    }
+    base = __shfl_sync(kFull, base, 0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (claim[j]) nf_out[base + __popc(bal[j] & lanemask_lt())] = r[j];
+        base += __popc(bal[j]);
     }
 }
 
-// eff[nnz_x] = nnz_s after a compaction (the scan's epilogue writes the
-// offsets of the entries only)
-__global__ void bfs_eff_tail_kernel(const BfsState* st, int p, int64_t* __restrict__ eff) {
-    if (threadIdx.x == 0) eff[st->nf[p]] = static_cast<int64_t>(st->ns[p]);
+// One warp pushes the frontier vertices its lanes hold (v < 0: none).
+__device__ __forceinline__ void push_members(int32_t v, int level, int q, const int64_t* __restrict__ co,
+                                             const int32_t* __restrict__ ri, int32_t* __restrict__ lv, BfsState* st,
+                                             int32_t* __restrict__ nf_out, unsigned long long* __restrict__ bigc,
+                                             uint2* __restrict__ bigl, int lane) {
+    long long b = 0, deg = 0;
+    if (v >= 0) {
+        b = __ldg(co + v);
+        deg = __ldg(co + v + 1) - b;
+    }
+    if (deg > kBigDeg) {
+        const unsigned long long nch = static_cast<unsigned long long>((deg + kBigChunk - 1) / kBigChunk);
+        const unsigned long long old = atomicAdd(bigc, (1ull << kBigShift) + nch);
+        bigl[old >> kBigShift] =
+            make_uint2(static_cast<unsigned>(v), static_cast<unsigned>(old & ((1ull << kBigShift) - 1)));
+        deg = 0;
+    }
+    const long long incl = warp_inclusive_sum(deg);
+    const long long wtot = __shfl_sync(kFull, incl, 31);
+    const long long excl = incl - deg;
+    for (long long e0 = 0; e0 < wtot; e0 += 128) {  // warp-uniform trip count
+        int32_t r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const long long e = e0 + j * 32 + lane;
+            int lo = 0;  // largest lane whose exclusive prefix <= e (every lane shuffles)
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int cand = lo + step;
+                const long long ev = __shfl_sync(kFull, excl, cand & 31);
+                if (cand < 32 && ev <= e) lo = cand;
+            }
+            const long long ob = __shfl_sync(kFull, b, lo), oe = __shfl_sync(kFull, excl, lo);
+            r[j] = e < wtot ? __ldg(ri + ob + (e - oe)) : -1;
+        }
+        claim_and_append(r, lv, level, co, st, q, nf_out, lane);
+    }
+}
+
+// Warp-granular grid stride.  List mode: 32 list entries per warp window.
+// Mark mode: 128 vertices per warp window (one 16-B level load per lane),
+// the members gathered through shared memory and pushed 32 at a time -- a
+// frontier of a few % of the vertices costs ~4 dependent round trips per
+// 128 vertices, not per 32.
+template <bool kList>
+__global__ void __launch_bounds__(256) bfs_scan_push_kernel(BfsState* st, int p, const int32_t* __restrict__ fl,
+                                                            int64_t n, const int64_t* __restrict__ co,
+                                                            const int32_t* __restrict__ ri, int32_t* __restrict__ lv,
+                                                            int32_t* __restrict__ nf_out,
+                                                            unsigned long long* __restrict__ bigc,
+                                                            uint2* __restrict__ bigl) {
+    __shared__ int32_t s_mem[8][128];
+    BFS_TRACE_BEGIN(st);
+    const int level = st->level;
+    const int q = p ^ 1;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const long long gw = static_cast<long long>(blockIdx.x) * 8 + wib;
+    const long long nw = static_cast<long long>(gridDim.x) * 8;
+    if (kList) {
+        const long long cnt = static_cast<long long>(st->nf[p]);
+        for (long long w = gw; w * 32 < cnt; w += nw) {
+            const long long i = w * 32 + lane;
+            push_members(i < cnt ? fl[i] : -1, level, q, co, ri, lv, st, nf_out, bigc, bigl, lane);
+        }
+    } else {
+        for (long long w = gw; w * 128 < n; w += nw) {
+            const long long v0 = w * 128 + lane * 4;
+            int l4[4];
+            if (v0 + 3 < n) {
+                const int4 t = *reinterpret_cast<const int4*>(lv + v0);
+                l4[0] = t.x;
+                l4[1] = t.y;
+                l4[2] = t.z;
+                l4[3] = t.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) l4[j] = v0 + j < n ? lv[v0 + j] : 0;
+            }
+            int mine = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mine += l4[j] == level - 1;
+            const int incl = warp_inclusive_sum(mine);
+            const int tot = __shfl_sync(kFull, incl, 31);
+            if (tot == 0) continue;  // warp-uniform
+            int o = incl - mine;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (l4[j] == level - 1) s_mem[wib][o++] = static_cast<int32_t>(v0 + j);
+            __syncwarp();
+            for (int k = 0; k < tot; k += 32)
+                push_members(k + lane < tot ? s_mem[wib][k + lane] : -1, level, q, co, ri, lv, st, nf_out, bigc, bigl,
+                             lane);
+            __syncwarp();
+        }
+    }
+    BFS_TRACE_END(st);
+}
+
+// The big vertices' chunks: task t -> (vertex, chunk) by a search over the
+// ascending task starts; 256 threads x 8 entries per task.
+__global__ void __launch_bounds__(256) bfs_big_push_kernel(BfsState* st, int p, const int64_t* __restrict__ co,
+                                                           const int32_t* __restrict__ ri, int32_t* __restrict__ lv,
+                                                           int32_t* __restrict__ nf_out,
+                                                           const unsigned long long* __restrict__ bigc,
+                                                           const uint2* __restrict__ bigl) {
+    BFS_TRACE_BEGIN(st);
+    const unsigned long long c = *bigc;
+    const long long nb = static_cast<long long>(c >> kBigShift);
+    const long long ntask = static_cast<long long>(c & ((1ull << kBigShift) - 1));
+    if (ntask == 0) return;
+    const int level = st->level;
+    const int lane = threadIdx.x & 31;
+    for (long long t = blockIdx.x; t < ntask; t += gridDim.x) {
+        long long lo = 0, hi = nb;  // largest entry with start <= t
+        while (hi - lo > 1) {
+            const long long mid = (lo + hi) >> 1;
+            if (static_cast<long long>(bigl[mid].y) <= t) lo = mid;
+            else hi = mid;
+        }
+        const uint2 ent = bigl[lo];
+        const long long b = __ldg(co + ent.x), e = __ldg(co + ent.x + 1);
+        const long long c0 = b + (t - static_cast<long long>(ent.y)) * kBigChunk;
+        const long long c1 = min(e, c0 + kBigChunk);
+        for (long long k0 = c0 + (threadIdx.x & ~31) * 4; k0 < c1; k0 += 256 * 4) {  // warp-uniform
+            int32_t r[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const long long k = k0 + j * 32 + lane;
+                r[j] = k < c1 ? __ldg(ri + k) : -1;
+            }
+            claim_and_append(r, lv, level, co, st, p ^ 1, nf_out, lane);
+        }
+    }
+    BFS_TRACE_END(st);
+}
+
+// The tail of a traversal: a small frontier (<= kTailMax vertices, <=
+// kTailEdges effective entries) that a push appended is pushed by ONE block,
+// and so are the following levels while the decision for them is again a
+// small push -- one kernel node for the whole tail instead of a decision, a
+// SWITCH and a push per level (~11 us each through the graph machinery:
+// tools/microbench/graph_cond_mb.cu).  Each continued level is decided and
+// logged exactly as bfs_decide_kernel would (same bfs_choose, same
+// accounting); on exit the last frontier is left, pending, at parity p ^ 1
+// for the graph's next decision.
+__global__ void __launch_bounds__(1024) bfs_tail_kernel(BfsState* st, LogEntry* log, int p, int32_t* __restrict__ f0,
+                                                        int32_t* __restrict__ f1, const int64_t* __restrict__ co,
+                                                        const int32_t* __restrict__ ri, int32_t* __restrict__ lv,
+                                                        DevTrees trees, int use_trees, const double* mfeat, int64_t n,
+                                                        int64_t nnz, int vbytes) {
+    __shared__ unsigned long long s_nf, s_ns;
+    __shared__ int s_go;
+    __shared__ int s_eff[kTailMax + 1];  // the frontier's degree prefix
+    __shared__ int32_t s_v[kTailMax];    // and its vertices
+    __shared__ int s_scan[1024 / 32 + 1];
+    __shared__ SmallNode s_tree[kSmallNodes];
+    const SmallNode* sn = stage_trees(trees, use_trees, s_tree, threadIdx.x, 1024);  // the loop syncs first
+    const int lane = threadIdx.x & 31;
+    int cp = p;  // parity of the frontier being pushed
+    for (;;) {
+        const int32_t* fin = cp ? f1 : f0;
+        int32_t* fout = cp ? f0 : f1;
+        const int nx = static_cast<int>(st->nf[cp]);
+        const int level = st->level;
+        // the frontier's effective entries flattened over the block (<= 4 per
+        // thread): every edge's loads are independent, not a per-vertex walk
+        int d[kTailMax / 1024], loc = 0;
+#pragma unroll
+        for (int j = 0; j < kTailMax / 1024; ++j) {
+            const int i = threadIdx.x * (kTailMax / 1024) + j;
+            d[j] = 0;
+            if (i < nx) {
+                const int32_t v = fin[i];
+                s_v[i] = v;
+                d[j] = static_cast<int>(__ldg(co + v + 1) - __ldg(co + v));
+            }
+            loc += d[j];
+        }
+        int tot;
+        int ex = block_exclusive_sum<1024>(loc, s_scan, &tot);
+#pragma unroll
+        for (int j = 0; j < kTailMax / 1024; ++j) {
+            const int i = threadIdx.x * (kTailMax / 1024) + j;
+            if (i < nx) s_eff[i] = ex;
+            ex += d[j];
+        }
+        if (threadIdx.x == 0) s_nf = s_ns = 0;
+        __syncthreads();
+        constexpr int kE = kTailEdges / 1024;
+        int32_t r[kE];
+#pragma unroll
+        for (int j = 0; j < kE; ++j) {
+            const int e = threadIdx.x + j * 1024;
+            r[j] = -1;
+            if (e < tot) {
+                int lo = 0, hi = nx;  // largest i with s_eff[i] <= e
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_eff[mid] <= e) lo = mid;
+                    else hi = mid;
+                }
+                r[j] = __ldg(ri + __ldg(co + s_v[lo]) + (e - s_eff[lo]));
+            }
+        }
+        int lr[kE];
+#pragma unroll
+        for (int j = 0; j < kE; ++j) lr[j] = r[j] >= 0 ? lv[r[j]] : 0;
+        bool claim[kE];
+#pragma unroll
+        for (int j = 0; j < kE; ++j) claim[j] = lr[j] < 0 && atomicCAS(lv + r[j], -1, level) == -1;
+#pragma unroll
+        for (int j = 0; j < kE; ++j) {
+            const unsigned bal = __ballot_sync(kFull, claim[j]);
+            if (bal == 0u) continue;
+            const unsigned long long dg =
+                warp_sum(claim[j] ? static_cast<unsigned long long>(__ldg(co + r[j] + 1) - __ldg(co + r[j])) : 0ull);
+            unsigned long long base = 0;
+            if (lane == 0) {
+                base = atomicAdd(&s_nf, static_cast<unsigned long long>(__popc(bal)));
+                atomicAdd(&s_ns, dg);
+            }
+            base = __shfl_sync(kFull, base, 0);
+            if (claim[j]) fout[base + __popc(bal & lanemask_lt())] = r[j];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned long long nf = s_nf, ns = s_ns;
+            st->nf[cp ^ 1] = nf;
+            st->ns[cp ^ 1] = ns;
+            int go = 0;
+            if (nf > 0 && nf <= kTailMax && ns <= kTailEdges) {
+                const long long visited = st->visited + static_cast<long long>(nf);
+                const int k = bfs_choose(trees, sn, use_trees, mfeat, n, nnz, vbytes, visited, nf, ns);
+                if (k >= 4) {  // the next level is a small push again: account and continue
+                    go = 1;
+                    st->visited = visited;
+                    st->level = level + 1;
+                    st->kernel = k;
+                    st->nf[cp] = 0;
+                    st->ns[cp] = 0;
+                    if (st->nlog < kMaxLog) {
+                        LogEntry& le = log[st->nlog];
+                        le.nnz_x = static_cast<long long>(nf);
+                        le.nnz_s = static_cast<long long>(ns);
+                        le.kernel = k;
+                        le.exec_mode = ADASPMV_EXEC_FUSED_PUSH_LB;
+                        le.t0 = globaltimer();
+                    }
+                    st->nlog += 1;
+                }
+            }
+            s_go = go;
+        }
+        __syncthreads();
+        if (!s_go) break;
+        cp ^= 1;
+    }
+    // the last frontier sits at parity cp ^ 1; the next decision reads p ^ 1
+    if (cp != p) {
+        const long long nx = static_cast<long long>(st->nf[p]);
+        int32_t* dst = p ? f0 : f1;
+        const int32_t* src = p ? f1 : f0;
+        for (long long i = threadIdx.x; i < nx; i += 1024) dst[i] = src[i];
+        if (threadIdx.x == 0) {
+            st->nf[p ^ 1] = st->nf[p];
+            st->ns[p ^ 1] = st->ns[p];
+        }
+    }
 }
 
 __global__ void bfs_init_kernel(BfsState* st, int32_t* lv, int64_t n, int64_t source, int32_t* f0,
@@ -475,8 +881,7 @@ __global__ void bfs_init_kernel(BfsState* st, int32_t* lv, int64_t n, int64_t so
         st->kernel = -1;
         st->done = 0;
         st->nlog = 0;
-        st->tot = 0;
-        st->pending = 0;
+            st->pending = 0;
         st->eff_ok = 1;
         st->list_ok = 1;
         eff[0] = 0;
@@ -490,10 +895,10 @@ __global__ void bfs_init_kernel(BfsState* st, int32_t* lv, int64_t n, int64_t so
 struct BfsPlan {
     cudaStream_t stream = nullptr;
     uint64_t bundle_id = 0;  // 0 = heuristic
-    DevBuf state, log, f[2], eff, part, lv, trees_i, trees_d, mfeat;
+    DevBuf state, log, f[2], eff, lv, trees_i, trees_d, trees_small, mfeat;
     DevTrees dt{};
-    DevBuf scan_tmp;  // the compaction's tile sums (sized before capture)
     DevBuf pcnt;      // a pull level's spread (count, degree) counters
+    DevBuf bigc, bigl;  // the scan push's big-vertex tasks (counter, list)
     cudaGraphExec_t exec = nullptr;
     ~BfsPlan() {
         if (exec) cudaGraphExecDestroy(exec);
@@ -510,7 +915,7 @@ bool bfs_graph_applicable(const Matrix& m, int semiring, int forced) {
 
 namespace {
 
-void upload_trees(Context& ctx, const Bundle& b, BfsPlan& P) {
+void upload_trees(Context& ctx, const Bundle& b, const double* m_feat, BfsPlan& P) {
     std::vector<int32_t> feat, left, right, leaf;
     std::vector<double> thr;
     P.dt.root[3] = -1;
@@ -542,6 +947,46 @@ void upload_trees(Context& ctx, const Bundle& b, BfsPlan& P) {
     P.dt.right = di + 2 * nn;
     P.dt.leaf = di + 3 * nn;
     P.dt.threshold = dd;
+    // specialised copy: fold the splits on matrix features (the comparison
+    // the device walk would make, on the same doubles)
+    std::vector<SmallNode> sm;
+    bool fits = true;
+    std::function<int(const Tree&, int)> add = [&](const Tree& tr, int i) -> int {
+        while (tr.feature[static_cast<size_t>(i)] >= 0 && tr.feature[static_cast<size_t>(i)] < 9) {
+            const size_t u = static_cast<size_t>(i);
+            i = m_feat[tr.feature[u]] <= tr.threshold[u] ? tr.left[u] : tr.right[u];
+        }
+        const size_t u = static_cast<size_t>(i);
+        const int me = static_cast<int>(sm.size());
+        if (me >= kSmallNodes) {
+            fits = false;
+            return 0;
+        }
+        sm.push_back(SmallNode{0.0, -1, 0, 0, 0});
+        if (tr.feature[u] < 0) {
+            sm[static_cast<size_t>(me)].leaf = static_cast<int16_t>(tr.leaf[u]);
+            return me;
+        }
+        const int l = add(tr, tr.left[u]);
+        const int r = add(tr, tr.right[u]);
+        if (!fits) return 0;
+        SmallNode& nd = sm[static_cast<size_t>(me)];
+        nd.thr = tr.threshold[u];
+        nd.feat = static_cast<int16_t>(tr.feature[u]);
+        nd.left = static_cast<int16_t>(l);
+        nd.right = static_cast<int16_t>(r);
+        return me;
+    };
+    P.dt.sroot[3] = -1;
+    for (int t = 0; t < (b.has_col ? 4 : 3) && fits; ++t) P.dt.sroot[t] = add(b.trees[t], 0);
+    P.dt.nsmall = 0;
+    P.dt.small = nullptr;
+    if (fits && !sm.empty()) {
+        SmallNode* ds = static_cast<SmallNode*>(P.trees_small.ensure(sizeof(SmallNode) * sm.size()));
+        ADA_CUDA(cudaMemcpyAsync(ds, sm.data(), sizeof(SmallNode) * sm.size(), cudaMemcpyHostToDevice, ctx.stream));
+        P.dt.small = ds;
+        P.dt.nsmall = static_cast<int>(sm.size());
+    }
     ctx.sync();  // host vectors go out of scope
 }
 
@@ -590,9 +1035,8 @@ void capture_switch(Context& ctx, cudaStream_t s, cudaStream_t s2, cudaGraphCond
 }
 
 // The whole traversal as ONE graph: WHILE(frontier) { level p = 0; level
-// p = 1 }, a level being decide -> IF(push) {eff offsets, push} -> IF(pull)
-// {frontier bitmap, pull, compaction scan, bitmap clear} -> account.  Only
-// the chosen branch's kernels run; sizes live on the device.
+// p = 1 }, a level being decide -> SWITCH(branch).  Only the chosen
+// branch's kernels run; sizes live on the device.
 void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     const int64_t n = m.rows;
     P.stream = ctx.stream;
@@ -601,15 +1045,21 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     P.log.ensure(sizeof(LogEntry) * kMaxLog);
     for (auto& f : P.f) f.ensure(sizeof(int32_t) * static_cast<size_t>(n));
     P.eff.ensure(sizeof(int64_t) * static_cast<size_t>(n + 1));
-    P.part.ensure(sizeof(long long) * kScanBlocks);
     P.lv.ensure(sizeof(int32_t) * static_cast<size_t>(n));
-    P.scan_tmp.ensure(sizeof(int64_t) * static_cast<size_t>((n + kScanTile - 1) / kScanTile + 1));
     P.pcnt.ensure(sizeof(unsigned long long) * 2 * kSpread);
+    P.bigc.ensure(sizeof(unsigned long long));
+    P.bigl.ensure(sizeof(uint2) * static_cast<size_t>(std::min<int64_t>(n, m.nnz / (kBigDeg + 1) + 1)));
     ADA_CUDA(cudaMemsetAsync(P.pcnt.p, 0, sizeof(unsigned long long) * 2 * kSpread, ctx.stream));
 
     double* mf = static_cast<double*>(P.mfeat.ensure(sizeof(double) * 9));
     ADA_CUDA(cudaMemcpyAsync(mf, m.feat, sizeof(double) * 9, cudaMemcpyHostToDevice, ctx.stream));
-    if (b) upload_trees(ctx, *b, P);
+    if (b) upload_trees(ctx, *b, m.feat, P);
+#ifdef ADA_BFS_TRACE
+    {
+        LogEntry* lp = P.log.as<LogEntry>();
+        ADA_CUDA(cudaMemcpyToSymbolAsync(g_bfs_log, &lp, sizeof(lp), 0, cudaMemcpyHostToDevice, ctx.stream));
+    }
+#endif
     ctx.sync();
     BfsState* st = P.state.as<BfsState>();
     LogEntry* lg = P.log.as<LogEntry>();
@@ -617,7 +1067,20 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     const int64_t* co = m.col_off.as<int64_t>();
     const unsigned push_grid = static_cast<unsigned>(ctx.sm_count) * 8;
     const int G = std::max(1, default_lanes_per_row(m.feat[5]) / 8);
-    const unsigned pull_grid = static_cast<unsigned>(std::max<int64_t>((n * G + 255) / 256, 1));
+    // grid-stride kernels: exactly the resident blocks (a second wave of a
+    // grid-stride grid would start late and finish its full share late)
+    auto resident = [&](const void* fn) {
+        int nb = 0;
+        ADA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 256, 0));
+        return static_cast<unsigned>(std::max(1, nb) * ctx.sm_count);
+    };
+    const unsigned pull4_grid = std::min<unsigned>(
+        resident(reinterpret_cast<const void*>(&bfs_pull_mark4_kernel)),
+        static_cast<unsigned>(std::max<int64_t>((n + 1023) / 1024, 1)));
+    const unsigned scan_grid = resident(reinterpret_cast<const void*>(&bfs_scan_push_kernel<false>));
+    const unsigned big_grid = resident(reinterpret_cast<const void*>(&bfs_big_push_kernel));
+    const unsigned pull_grid = static_cast<unsigned>(
+        std::max<int64_t>(std::min<int64_t>((n * G + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 8), 1));
     cudaGraph_t graph = nullptr;
     ADA_CUDA(cudaGraphCreate(&graph, 0));
     cudaStream_t s2 = nullptr;
@@ -647,47 +1110,48 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     try {
         for (int p = 0; p < 2; ++p) {
             bfs_decide_kernel<<<1, 32, 0, s>>>(st, lg, p, P.dt, b ? 1 : 0, mf, n, m.nnz, m.vbytes(),
-                                               P.pcnt.as<unsigned long long>(), hbranch[p], hw);
-            auto eff_scan = [&, p](cudaStream_t cs) {  // offsets of a frontier a push appended
-                bfs_eff_partial_kernel<<<kScanBlocks, 256, 0, cs>>>(st, p, P.f[p].as<int32_t>(), co,
-                                                                    P.part.as<long long>());
-                bfs_eff_top_kernel<<<1, kScanBlocks, 0, cs>>>(st, P.part.as<long long>());
-                bfs_eff_write_kernel<<<kScanBlocks, 256, 0, cs>>>(st, p, P.f[p].as<int32_t>(), co,
-                                                                  P.part.as<long long>(), P.eff.as<int64_t>());
-            };
+                                               P.pcnt.as<unsigned long long>(), P.bigc.as<unsigned long long>(),
+                                               hbranch[p], hw);
             auto push = [&, p](cudaStream_t cs) {
                 bfs_push_kernel<<<push_grid, 256, 0, cs>>>(st, p, P.f[p].as<int32_t>(), P.eff.as<int64_t>(), co,
                                                            m.row_idx.as<int32_t>(), lv, P.f[p ^ 1].as<int32_t>());
             };
-            auto pull = [&, p](cudaStream_t cs) {  // marks only; the list is compacted if a push needs it
+            auto pull = [&, p](cudaStream_t cs) {  // marks only: a push after it reads the marks
                 unsigned long long* pc = P.pcnt.as<unsigned long long>();
                 switch (G) {
-                    case 1: launch_pull_mark<1>(cs, pull_grid, st, m, lv, pc); break;
+                    case 1:
+                        bfs_pull_mark4_kernel<<<pull4_grid, 256, 0, cs>>>(st, m.rows, m.row_off.as<int64_t>(),
+                                                                          m.col_idx.as<int32_t>(),
+                                                                          m.col_off.as<int64_t>(), lv, pc);
+                        break;
                     case 2: launch_pull_mark<2>(cs, pull_grid, st, m, lv, pc); break;
                     case 4: launch_pull_mark<4>(cs, pull_grid, st, m, lv, pc); break;
                     default: launch_pull_mark<8>(cs, pull_grid, st, m, lv, pc); break;
                 }
             };
-            auto compact = [&, p](cudaStream_t) {  // the frontier (rows of level - 1) as a list + eff
-                scan3(ctx, n, LevelIn{lv, &st->level, -1, co},
-                      LevelEpi{P.f[p].as<int32_t>(), P.eff.as<int64_t>()}, reinterpret_cast<int64_t*>(&st->tot),
-                      P.scan_tmp);
-                bfs_eff_tail_kernel<<<1, 32, 0, ctx.stream>>>(st, p, P.eff.as<int64_t>());
+            auto scan_push = [&, p](cudaStream_t cs, bool list) {  // one pass + the big vertices' tasks
+                unsigned long long* bc = P.bigc.as<unsigned long long>();
+                uint2* bl = P.bigl.as<uint2>();
+                if (list)
+                    bfs_scan_push_kernel<true><<<scan_grid, 256, 0, cs>>>(st, p, P.f[p].as<int32_t>(), n, co,
+                                                                          m.row_idx.as<int32_t>(), lv,
+                                                                          P.f[p ^ 1].as<int32_t>(), bc, bl);
+                else
+                    bfs_scan_push_kernel<false><<<scan_grid, 256, 0, cs>>>(st, p, nullptr, n, co,
+                                                                           m.row_idx.as<int32_t>(), lv,
+                                                                           P.f[p ^ 1].as<int32_t>(), bc, bl);
+                bfs_big_push_kernel<<<big_grid, 256, 0, cs>>>(st, p, co, m.row_idx.as<int32_t>(), lv,
+                                                               P.f[p ^ 1].as<int32_t>(), bc, bl);
             };
             std::vector<std::function<void(cudaStream_t)>> bodies(5);
-            bodies[kBranchCompactPush] = [&](cudaStream_t cs) {
-                compact(cs);
-                push(cs);
-            };
-            bodies[kBranchEffPush] = [&](cudaStream_t cs) {
-                eff_scan(cs);
-                push(cs);
-            };
             bodies[kBranchPush] = push;
             bodies[kBranchPull] = pull;
-            bodies[kBranchPushSmall] = [&, p](cudaStream_t cs) {
-                bfs_push_small_kernel<<<static_cast<unsigned>(ctx.sm_count) * 2, 256, 0, cs>>>(
-                    st, p, P.f[p].as<int32_t>(), co, m.row_idx.as<int32_t>(), lv, P.f[p ^ 1].as<int32_t>());
+            bodies[kBranchMarkPush] = [&](cudaStream_t cs) { scan_push(cs, false); };
+            bodies[kBranchListPush] = [&](cudaStream_t cs) { scan_push(cs, true); };
+            bodies[kBranchTail] = [&, p](cudaStream_t cs) {
+                bfs_tail_kernel<<<1, 1024, 0, cs>>>(st, lg, p, P.f[0].as<int32_t>(), P.f[1].as<int32_t>(), co,
+                                                    m.row_idx.as<int32_t>(), lv, P.dt, b ? 1 : 0, mf, n, m.nnz,
+                                                    m.vbytes());
             };
             capture_switch(ctx, s, s2, hbranch[p], bodies);
         }
@@ -746,6 +1210,12 @@ void bfs_graph(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, i
             r.convert_s = 0;  // no format conversion: the frontier is produced in the form the level reads
             const unsigned long long t1 = h[static_cast<size_t>(i + 1)].t0, t0 = h[static_cast<size_t>(i)].t0;
             r.kernel_s = t1 > t0 ? static_cast<double>(t1 - t0) * 1e-9 : 0.0;
+#ifdef ADA_BFS_TRACE
+            const LogEntry& le = h[static_cast<size_t>(i)];
+            std::fprintf(stderr, "bfs trace level %d: kernels %.1f us (start +%.1f us after the decision)\n", i,
+                         le.tk1 > le.tk0 ? (le.tk1 - le.tk0) * 1e-3 : 0.0,
+                         le.tk0 != ~0ull && le.tk0 > t0 ? (le.tk0 - t0) * 1e-3 : 0.0);
+#endif
         }
     }
     if (!levels) return;
