@@ -122,7 +122,26 @@ struct AtomicCombine;
 
 template <>
 struct AtomicCombine<SR_PLUS_TIMES> {
-    __device__ static void apply(float* p, float v) { atomicAdd(p, v); }
+    // The hardware float reduction (REDG.E.ADD.F32.FTZ) flushes subnormal
+    // operands and results to zero; the reference's float sums keep them.
+    // An addend below 2^-100 takes an IEEE compare-and-swap add instead
+    // (FADD keeps subnormals), so a row whose terms are all tiny is summed
+    // exactly like the reference; for a larger addend the flush of a
+    // subnormal operand or result is <= 2^-126 absolute, far inside the fp32
+    // tolerance of a row bound >= 2^-100.
+    __device__ static void apply(float* p, float v) {
+        if (fabsf(v) >= 0x1p-100f) {
+            atomicAdd(p, v);
+            return;
+        }
+        if (v == 0.f) return;  // adding +-0 never changes a sum that starts at +0
+        unsigned* a = reinterpret_cast<unsigned*>(p);
+        unsigned old = *reinterpret_cast<volatile unsigned*>(a), assumed;
+        do {
+            assumed = old;
+            old = atomicCAS(a, assumed, __float_as_uint(__uint_as_float(assumed) + v));
+        } while (old != assumed);
+    }
     __device__ static void apply(double* p, double v) { atomicAdd(p, v); }
 };
 template <>

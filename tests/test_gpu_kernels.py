@@ -581,3 +581,32 @@ def test_selector_schema2_runtime_matches_host_mirror(ctx):
             f = A.features(m, x)
             k, _, _ = A.predict_kernel(m, x, b)
             assert k.index() == S.predict(trees, f), (seed, nx)
+
+
+@pytest.mark.parametrize("nx_frac", [1.0, 0.3])
+def test_subnormal_products_fp32(ctx, port, nx_frac):
+    # the hardware float reduction (REDG.E.ADD.F32.FTZ)
+    # flushes subnormals; the reference's float sums keep them.  Entries and x
+    # of ~1e-20 give products of ~1e-40 (subnormal in fp32): every kernel must
+    # sum them like the reference.  Tolerance: the fp32 rtol of the row bound
+    # plus the absolute rounding of subnormal arithmetic (half an ulp of
+    # 2^-149 per product and per add).
+    rows, cols, ro, ci, vals = synth.random_csr(3000, 2500, 0.004, seed=11, dtype=np.float32)
+    rng = np.random.default_rng(5)
+    vals = (rng.uniform(1.0, 2.0, len(vals)) * 1e-20).astype(np.float32)
+    m = A.DualMatrix.from_csr(rows, cols, ro, ci, vals, ctx=ctx)
+    nx = max(1, int(cols * nx_frac))
+    xi = np.sort(rng.choice(cols, nx, replace=False)).astype(np.int64)
+    xv = (rng.uniform(1.0, 2.0, nx) * 1e-20).astype(np.float32)
+    xd = port.sparse_to_dense(cols, xi, xv)
+    y_ref, bound = ref_and_bound(port, rows, ro, ci, np.asarray(vals, np.float64),
+                                 np.asarray(xd, np.float32).astype(np.float64))
+    assert 0 < np.max(np.abs(y_ref)) < 1.17e-38  # the row sums themselves are subnormal
+    deg = np.diff(ro)
+    allowed = 1e-5 * bound + (2 * deg + 1) * 2.0 ** -149
+    for k in range(8):
+        x = A.SparseVector(cols, xi, xv) if k >= 4 else A.DenseVector(np.asarray(xd, np.float32))
+        y = np.asarray(A.run_kernel(m, k, x).dense().values, np.float64)
+        bad = np.abs(y - y_ref) > allowed
+        assert not bad.any(), (f"k={k}: {int(bad.sum())} rows flushed/off, e.g. row {int(np.argmax(bad))} "
+                               f"y={y[np.argmax(bad)]!r} ref={y_ref[np.argmax(bad)]!r}")
