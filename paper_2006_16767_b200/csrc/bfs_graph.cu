@@ -406,20 +406,17 @@ __global__ void __launch_bounds__(256) bfs_push_kernel(BfsState* st, int p, cons
 // interleave of windows keeps rows that run long spread over the SMs.
 // A push after a pull reads the marks (MarkPush): no list is compacted.
 template <int G>
-__global__ void __launch_bounds__(256) bfs_pull_mark_kernel(const BfsState* st, int64_t rows,
-                                                            const int64_t* __restrict__ ro,
-                                                            const int32_t* __restrict__ ci,
-                                                            const int64_t* __restrict__ co,
-                                                            int32_t* __restrict__ lv,
-                                                            unsigned long long* __restrict__ pcnt) {
-    const int level = st->level;  // frontier = the vertices of level - 1
+__device__ __forceinline__ void pull_body(long long bid, long long nblk, int level, int64_t rows,
+                                          const int64_t* __restrict__ ro, const int32_t* __restrict__ ci,
+                                          const int64_t* __restrict__ co, int32_t* __restrict__ lv,
+                                          unsigned long long* __restrict__ pcnt) {
+    // level: of the rows this step discovers (frontier = the vertices of level - 1)
     const int lane = threadIdx.x & 31;
     const int lg = threadIdx.x & (G - 1);
     const unsigned grp = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
     unsigned long long c = 0, d = 0;  // this lane's joins and their column degrees (lane 0 sums the warp)
     const long long total = rows * G;
-    for (long long base = static_cast<long long>(blockIdx.x) * 256; base < total;
-         base += static_cast<long long>(gridDim.x) * 256) {  // block-uniform trip count
+    for (long long base = bid * 256; base < total; base += nblk * 256) {  // block-uniform trip count
         const long long row = (base + threadIdx.x) / G;
         const bool live = row < rows && lv[row] < 0;
         bool hit = false;
@@ -450,11 +447,21 @@ __global__ void __launch_bounds__(256) bfs_pull_mark_kernel(const BfsState* st, 
     if (c) {
         d = warp_sum(d);
         if (lane == 0) {
-            const int slot = static_cast<int>((blockIdx.x * 8u + (threadIdx.x >> 5)) % kSpread);
+            const int slot = static_cast<int>((bid * 8 + (threadIdx.x >> 5)) % kSpread);
             atomicAdd(pcnt + 2 * slot, c);
             atomicAdd(pcnt + 2 * slot + 1, d);
         }
     }
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) bfs_pull_mark_kernel(const BfsState* st, int64_t rows,
+                                                            const int64_t* __restrict__ ro,
+                                                            const int32_t* __restrict__ ci,
+                                                            const int64_t* __restrict__ co,
+                                                            int32_t* __restrict__ lv,
+                                                            unsigned long long* __restrict__ pcnt) {
+    pull_body<G>(blockIdx.x, gridDim.x, st->level, rows, ro, ci, co, lv, pcnt);
 }
 
 // The pull with one lane per row, 4 rows per thread (consecutive: one 16-B
@@ -465,19 +472,14 @@ __global__ void __launch_bounds__(256) bfs_pull_mark_kernel(const BfsState* st, 
 // by the probe continue 4 neighbours at a time.
 constexpr int kProbe = 2;
 
-__global__ void __launch_bounds__(256) bfs_pull_mark4_kernel(const BfsState* st, int64_t rows,
-                                                             const int64_t* __restrict__ ro,
-                                                             const int32_t* __restrict__ ci,
-                                                             const int64_t* __restrict__ co,
-                                                             int32_t* __restrict__ lv,
-                                                             unsigned long long* __restrict__ pcnt) {
-    BFS_TRACE_BEGIN(st);
-    const int level = st->level;
+__device__ __forceinline__ void pull4_body(long long bid, long long nblk, int level, int64_t rows,
+                                           const int64_t* __restrict__ ro, const int32_t* __restrict__ ci,
+                                           const int64_t* __restrict__ co, int32_t* __restrict__ lv,
+                                           unsigned long long* __restrict__ pcnt) {
     const int lane = threadIdx.x & 31;
     unsigned long long c = 0, d = 0;
-    for (long long base = static_cast<long long>(blockIdx.x) * 1024; base < rows;
-         base += static_cast<long long>(gridDim.x) * 1024) {
-        const long long r0 = base + threadIdx.x * 4;
+    for (long long w = bid; w * 1024 < rows; w += nblk) {
+        const long long r0 = w * 1024 + threadIdx.x * 4;
         if (r0 >= rows) continue;
         int l4[4];
         if (r0 + 3 < rows) {
@@ -539,11 +541,21 @@ __global__ void __launch_bounds__(256) bfs_pull_mark4_kernel(const BfsState* st,
     if (c) {
         d = warp_sum(d);
         if (lane == 0) {
-            const int slot = static_cast<int>((blockIdx.x * 8u + (threadIdx.x >> 5)) % kSpread);
+            const int slot = static_cast<int>((bid * 8 + (threadIdx.x >> 5)) % kSpread);
             atomicAdd(pcnt + 2 * slot, c);
             atomicAdd(pcnt + 2 * slot + 1, d);
         }
     }
+}
+
+__global__ void __launch_bounds__(256) bfs_pull_mark4_kernel(const BfsState* st, int64_t rows,
+                                                             const int64_t* __restrict__ ro,
+                                                             const int32_t* __restrict__ ci,
+                                                             const int64_t* __restrict__ co,
+                                                             int32_t* __restrict__ lv,
+                                                             unsigned long long* __restrict__ pcnt) {
+    BFS_TRACE_BEGIN(st);
+    pull4_body(blockIdx.x, gridDim.x, st->level, rows, ro, ci, co, lv, pcnt);
     BFS_TRACE_END(st);
 }
 
@@ -563,8 +575,8 @@ constexpr int kBigChunk = 2048;
 constexpr int kBigShift = 40;
 
 __device__ __forceinline__ void claim_and_append(const int32_t (&r)[4], int32_t* __restrict__ lv, int level,
-                                                 const int64_t* __restrict__ co, BfsState* st, int q,
-                                                 int32_t* __restrict__ nf_out, int lane) {
+                                                 const int64_t* __restrict__ co, unsigned long long* out_nf,
+                                                 unsigned long long* out_ns, int32_t* __restrict__ nf_out, int lane) {
     int lr[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) lr[j] = r[j] >= 0 ? lv[r[j]] : 0;
@@ -584,8 +596,8 @@ __device__ __forceinline__ void claim_and_append(const int32_t (&r)[4], int32_t*
     deg = warp_sum(deg);
     unsigned long long base = 0;
     if (lane == 0) {
-        base = atomicAdd(&st->nf[q], static_cast<unsigned long long>(cnt));
-        atomicAdd(&st->ns[q], static_cast<unsigned long long>(deg));
+        base = atomicAdd(out_nf, static_cast<unsigned long long>(cnt));
+        atomicAdd(out_ns, static_cast<unsigned long long>(deg));
     }
     base = __shfl_sync(kFull, base, 0);
 #pragma unroll
@@ -596,8 +608,9 @@ __device__ __forceinline__ void claim_and_append(const int32_t (&r)[4], int32_t*
 }
 
 // One warp pushes the frontier vertices its lanes hold (v < 0: none).
-__device__ __forceinline__ void push_members(int32_t v, int level, int q, const int64_t* __restrict__ co,
-                                             const int32_t* __restrict__ ri, int32_t* __restrict__ lv, BfsState* st,
+__device__ __forceinline__ void push_members(int32_t v, int level, const int64_t* __restrict__ co,
+                                             const int32_t* __restrict__ ri, int32_t* __restrict__ lv,
+                                             unsigned long long* out_nf, unsigned long long* out_ns,
                                              int32_t* __restrict__ nf_out, unsigned long long* __restrict__ bigc,
                                              uint2* __restrict__ bigl, int lane) {
     long long b = 0, deg = 0;
@@ -630,7 +643,7 @@ __device__ __forceinline__ void push_members(int32_t v, int level, int q, const 
             const long long ob = __shfl_sync(kFull, b, lo), oe = __shfl_sync(kFull, excl, lo);
             r[j] = e < wtot ? __ldg(ri + ob + (e - oe)) : -1;
         }
-        claim_and_append(r, lv, level, co, st, q, nf_out, lane);
+        claim_and_append(r, lv, level, co, out_nf, out_ns, nf_out, lane);
     }
 }
 
@@ -640,24 +653,20 @@ __device__ __forceinline__ void push_members(int32_t v, int level, int q, const 
 // frontier of a few % of the vertices costs ~4 dependent round trips per
 // 128 vertices, not per 32.
 template <bool kList>
-__global__ void __launch_bounds__(256) bfs_scan_push_kernel(BfsState* st, int p, const int32_t* __restrict__ fl,
-                                                            int64_t n, const int64_t* __restrict__ co,
-                                                            const int32_t* __restrict__ ri, int32_t* __restrict__ lv,
-                                                            int32_t* __restrict__ nf_out,
-                                                            unsigned long long* __restrict__ bigc,
-                                                            uint2* __restrict__ bigl) {
-    __shared__ int32_t s_mem[8][128];
-    BFS_TRACE_BEGIN(st);
-    const int level = st->level;
-    const int q = p ^ 1;
+__device__ __forceinline__ void scan_push_body(long long bid, long long nblk, int level, const int32_t* __restrict__ fl,
+                                               long long cnt, int64_t n, const int64_t* __restrict__ co,
+                                               const int32_t* __restrict__ ri, int32_t* __restrict__ lv,
+                                               unsigned long long* out_nf, unsigned long long* out_ns,
+                                               int32_t* __restrict__ nf_out, unsigned long long* __restrict__ bigc,
+                                               uint2* __restrict__ bigl, int32_t (*s_mem)[128]) {
+    // level: of the vertices this step discovers; cnt: list length (list mode)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const long long gw = static_cast<long long>(blockIdx.x) * 8 + wib;
-    const long long nw = static_cast<long long>(gridDim.x) * 8;
+    const long long gw = bid * 8 + wib;
+    const long long nw = nblk * 8;
     if (kList) {
-        const long long cnt = static_cast<long long>(st->nf[p]);
         for (long long w = gw; w * 32 < cnt; w += nw) {
             const long long i = w * 32 + lane;
-            push_members(i < cnt ? fl[i] : -1, level, q, co, ri, lv, st, nf_out, bigc, bigl, lane);
+            push_members(i < cnt ? fl[i] : -1, level, co, ri, lv, out_nf, out_ns, nf_out, bigc, bigl, lane);
         }
     } else {
         for (long long w = gw; w * 128 < n; w += nw) {
@@ -685,29 +694,39 @@ __global__ void __launch_bounds__(256) bfs_scan_push_kernel(BfsState* st, int p,
                 if (l4[j] == level - 1) s_mem[wib][o++] = static_cast<int32_t>(v0 + j);
             __syncwarp();
             for (int k = 0; k < tot; k += 32)
-                push_members(k + lane < tot ? s_mem[wib][k + lane] : -1, level, q, co, ri, lv, st, nf_out, bigc, bigl,
-                             lane);
+                push_members(k + lane < tot ? s_mem[wib][k + lane] : -1, level, co, ri, lv, out_nf, out_ns, nf_out,
+                             bigc, bigl, lane);
             __syncwarp();
         }
     }
+}
+
+template <bool kList>
+__global__ void __launch_bounds__(256) bfs_scan_push_kernel(BfsState* st, int p, const int32_t* __restrict__ fl,
+                                                            int64_t n, const int64_t* __restrict__ co,
+                                                            const int32_t* __restrict__ ri, int32_t* __restrict__ lv,
+                                                            int32_t* __restrict__ nf_out,
+                                                            unsigned long long* __restrict__ bigc,
+                                                            uint2* __restrict__ bigl) {
+    __shared__ int32_t s_mem[8][128];
+    BFS_TRACE_BEGIN(st);
+    const int q = p ^ 1;
+    scan_push_body<kList>(blockIdx.x, gridDim.x, st->level, fl, kList ? static_cast<long long>(st->nf[p]) : 0, n, co,
+                          ri, lv, &st->nf[q], &st->ns[q], nf_out, bigc, bigl, s_mem);
     BFS_TRACE_END(st);
 }
 
 // The big vertices' chunks: task t -> (vertex, chunk) by a search over the
 // ascending task starts; 256 threads x 8 entries per task.
-__global__ void __launch_bounds__(256) bfs_big_push_kernel(BfsState* st, int p, const int64_t* __restrict__ co,
-                                                           const int32_t* __restrict__ ri, int32_t* __restrict__ lv,
-                                                           int32_t* __restrict__ nf_out,
-                                                           const unsigned long long* __restrict__ bigc,
-                                                           const uint2* __restrict__ bigl) {
-    BFS_TRACE_BEGIN(st);
-    const unsigned long long c = *bigc;
+__device__ __forceinline__ void big_push_body(long long bid, long long nblk, int level,
+                                              const int64_t* __restrict__ co, const int32_t* __restrict__ ri,
+                                              int32_t* __restrict__ lv, unsigned long long* out_nf,
+                                              unsigned long long* out_ns, int32_t* __restrict__ nf_out,
+                                              unsigned long long c, const uint2* __restrict__ bigl) {
     const long long nb = static_cast<long long>(c >> kBigShift);
     const long long ntask = static_cast<long long>(c & ((1ull << kBigShift) - 1));
-    if (ntask == 0) return;
-    const int level = st->level;
     const int lane = threadIdx.x & 31;
-    for (long long t = blockIdx.x; t < ntask; t += gridDim.x) {
+    for (long long t = bid; t < ntask; t += nblk) {
         long long lo = 0, hi = nb;  // largest entry with start <= t
         while (hi - lo > 1) {
             const long long mid = (lo + hi) >> 1;
@@ -725,9 +744,21 @@ __global__ void __launch_bounds__(256) bfs_big_push_kernel(BfsState* st, int p, 
                 const long long k = k0 + j * 32 + lane;
                 r[j] = k < c1 ? __ldg(ri + k) : -1;
             }
-            claim_and_append(r, lv, level, co, st, p ^ 1, nf_out, lane);
+            claim_and_append(r, lv, level, co, out_nf, out_ns, nf_out, lane);
         }
     }
+}
+
+__global__ void __launch_bounds__(256) bfs_big_push_kernel(BfsState* st, int p, const int64_t* __restrict__ co,
+                                                           const int32_t* __restrict__ ri, int32_t* __restrict__ lv,
+                                                           int32_t* __restrict__ nf_out,
+                                                           const unsigned long long* __restrict__ bigc,
+                                                           const uint2* __restrict__ bigl) {
+    const unsigned long long c = *bigc;
+    if ((c & ((1ull << kBigShift) - 1)) == 0) return;
+    BFS_TRACE_BEGIN(st);
+    const int q = p ^ 1;
+    big_push_body(blockIdx.x, gridDim.x, st->level, co, ri, lv, &st->nf[q], &st->ns[q], nf_out, c, bigl);
     BFS_TRACE_END(st);
 }
 
@@ -889,6 +920,207 @@ __global__ void bfs_init_kernel(BfsState* st, int32_t* lv, int64_t n, int64_t so
     }
 }
 
+// ---------------------------------------------------------------------------
+// The whole traversal as ONE cooperative persistent kernel (the default when
+// the device supports cooperative launch): the level bodies above run
+// grid-strided over exactly the co-resident blocks, separated by grid
+// barriers -- one per pull level, one or two per push level -- instead of
+// the graph's per-level decision node, SWITCH and kernel nodes (~15 us per
+// level through the graph machinery).  Every block makes the same decision
+// from the same counters (no broadcast needed); block 0 alone logs and keeps
+// the bookkeeping.  Per-level counters rotate over 3 slots: slot (L+1) % 3
+// is written by step L, read by every block after the barrier that ends it,
+// and block 0 zeroes slot (L+2) % 3 during step L (its last readers passed
+// the barrier ending step L-1, its next writers start after the one ending
+// step L).
+struct PSlot {
+    unsigned long long nf, ns, bigc, pulled;
+    unsigned long long pc[2 * kSpread];
+};
+
+struct PArgs {
+    BfsState* st;
+    LogEntry* log;
+    int32_t* lv;
+    const int64_t* ro;
+    const int32_t* ci;
+    const int64_t* co;
+    const int32_t* ri;
+    int32_t* f[2];
+    PSlot* slots;
+    unsigned* bar;  // [0] root arrivals, [1] generation, then the group counters
+    uint2* bigl;
+    DevTrees trees;
+    int use_trees;
+    const double* mfeat;
+    int64_t n, nnz;
+    int vbytes;
+};
+
+// Visibility: every block reads what the others wrote in earlier steps
+// (levels, lists, counters, tasks) with plain loads.  The barrier's
+// gpu-scope fences after the generation flips (release by the last
+// arrival, acquire by each waiter, then bar.sync) order those writes before
+// the loads and drop the SM's stale L1 lines, as grid.sync() does.
+// Grid barrier over co-resident blocks (cooperative launch), two-level:
+// a block arrives on one of kBarGroups group counters (own 128-B lines) and
+// the last arrival of a group on the root; the last root arrival resets and
+// bumps the generation the others wait on.  One flat counter serialises all
+// ~740 same-address atomics (~10 us per barrier on B200, measured).
+constexpr int kBarGroups = 32;
+constexpr int kBarStride = 32;  // unsigned words per counter (128 B)
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblk) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        const unsigned ng = nblk < kBarGroups ? nblk : kBarGroups;
+        const unsigned grp = blockIdx.x % ng;
+        const unsigned gsize = nblk / ng + (grp < nblk % ng ? 1u : 0u);
+        unsigned* gc = bar + kBarStride * (1 + grp);
+        __threadfence();
+        bool last = false;
+        if (atomicAdd(gc, 1u) == gsize - 1) {
+            atomicExch(gc, 0u);
+            last = atomicAdd(bar, 1u) == ng - 1;
+        }
+        if (last) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) bfs_persist_kernel(PArgs a) {
+    __shared__ int32_t s_mem[8][128];
+    __shared__ SmallNode s_tree[kSmallNodes];
+    __shared__ unsigned long long s_red[2][8];
+    __shared__ int s_k;
+    const SmallNode* sn = stage_trees(a.trees, a.use_trees, s_tree, threadIdx.x, 256);
+    const long long bid = blockIdx.x, nblk = gridDim.x;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    long long visited = 0;
+    int nlog = 0;
+    bool list = true;  // the frontier exists as a list (a pull leaves marks)
+    for (int L = 0;; ++L) {
+        PSlot* cur = a.slots + L % 3;
+        PSlot* nxt = a.slots + (L + 1) % 3;
+        // the frontier F_L: a push's counters, or the pull's spread counters
+        unsigned long long nf, ns;
+        if (__ldcg(&cur->pulled)) {
+            unsigned long long c = 0, d = 0;
+            for (int i = threadIdx.x; i < kSpread; i += 256) {
+                c += __ldcg(cur->pc + 2 * i);
+                d += __ldcg(cur->pc + 2 * i + 1);
+            }
+            c = warp_sum(c);
+            d = warp_sum(d);
+            if (lane == 0) {
+                s_red[0][wib] = c;
+                s_red[1][wib] = d;
+            }
+            __syncthreads();
+            nf = ns = 0;
+            for (int w = 0; w < 8; ++w) {
+                nf += s_red[0][w];
+                ns += s_red[1][w];
+            }
+            __syncthreads();
+        } else {
+            nf = __ldcg(&cur->nf);
+            ns = __ldcg(&cur->ns);
+        }
+        const unsigned long long now = globaltimer();
+        if (nf == 0) {  // every block leaves here, on the same step
+            if (bid == 0 && threadIdx.x == 0) {
+                if (nlog < kMaxLog) a.log[nlog].t0 = now;  // end stamp of the last level
+                a.st->nlog = nlog;
+                a.st->visited = visited;
+                a.st->level = L;
+                a.st->done = 1;
+                a.st->mode = kModeDone;
+            }
+            return;
+        }
+        visited += static_cast<long long>(nf);
+        if (threadIdx.x == 0)
+            s_k = bfs_choose(a.trees, sn, a.use_trees, a.mfeat, a.n, a.nnz, a.vbytes, visited, nf, ns);
+        __syncthreads();
+        const int k = s_k;
+        if (bid == 0) {
+            if (threadIdx.x == 0 && nlog < kMaxLog) {
+                LogEntry& e = a.log[nlog];
+                e.nnz_x = static_cast<long long>(nf);
+                e.nnz_s = static_cast<long long>(ns);
+                e.kernel = k;
+                e.exec_mode = k >= 4 ? ADASPMV_EXEC_FUSED_PUSH_LB : ADASPMV_EXEC_MASKED_PULL;
+                e.t0 = now;
+            }
+            PSlot* z = a.slots + (L + 2) % 3;
+            for (int i = threadIdx.x; i < 2 * kSpread; i += 256) z->pc[i] = 0;
+            if (threadIdx.x == 0) z->nf = z->ns = z->bigc = z->pulled = 0;
+        }
+        ++nlog;
+        const int level = L + 1;  // of the vertices this step discovers
+        if (k < 4) {
+            if (G == 1) pull4_body(bid, nblk, level, a.n, a.ro, a.ci, a.co, a.lv, nxt->pc);
+            else pull_body<G>(bid, nblk, level, a.n, a.ro, a.ci, a.co, a.lv, nxt->pc);
+            if (bid == 0 && threadIdx.x == 0) nxt->pulled = 1;
+            list = false;
+#ifdef ADA_BFS_TRACE
+            __syncthreads();
+            if (bid == 0 && threadIdx.x == 0 && nlog - 1 < kMaxLog) a.log[nlog - 1].tk0 = globaltimer();
+#endif
+            grid_barrier(a.bar, static_cast<unsigned>(nblk));
+#ifdef ADA_BFS_TRACE
+            if (bid == 0 && threadIdx.x == 0 && nlog - 1 < kMaxLog) a.log[nlog - 1].tk1 = globaltimer();
+#endif
+        } else {
+            int32_t* fin = a.f[L & 1];
+            int32_t* fout = a.f[(L + 1) & 1];
+            if (list)
+                scan_push_body<true>(bid, nblk, level, fin, static_cast<long long>(nf), a.n, a.co, a.ri, a.lv,
+                                     &nxt->nf, &nxt->ns, fout, &nxt->bigc, a.bigl, s_mem);
+            else
+                scan_push_body<false>(bid, nblk, level, nullptr, 0, a.n, a.co, a.ri, a.lv, &nxt->nf, &nxt->ns, fout,
+                                      &nxt->bigc, a.bigl, s_mem);
+            list = true;
+#ifdef ADA_BFS_TRACE
+            __syncthreads();
+            if (bid == 0 && threadIdx.x == 0 && nlog - 1 < kMaxLog) a.log[nlog - 1].tk0 = globaltimer();
+#endif
+            grid_barrier(a.bar, static_cast<unsigned>(nblk));
+#ifdef ADA_BFS_TRACE
+            if (bid == 0 && threadIdx.x == 0 && nlog - 1 < kMaxLog) a.log[nlog - 1].tk1 = globaltimer();
+#endif
+            const unsigned long long c = *reinterpret_cast<volatile unsigned long long*>(&nxt->bigc);
+            if (c & ((1ull << kBigShift) - 1)) {
+                big_push_body(bid, nblk, level, a.co, a.ri, a.lv, &nxt->nf, &nxt->ns, fout, c, a.bigl);
+                grid_barrier(a.bar, static_cast<unsigned>(nblk));
+            }
+        }
+    }
+}
+
+__global__ void bfs_persist_init_kernel(PSlot* slots, unsigned* bar, const int64_t* __restrict__ co, int64_t source) {
+    for (int s = 0; s < 3; ++s) {
+        for (int i = threadIdx.x; i < 2 * kSpread; i += blockDim.x) slots[s].pc[i] = 0;
+        if (threadIdx.x == 0) slots[s].nf = slots[s].ns = slots[s].bigc = slots[s].pulled = 0;
+    }
+    for (int i = threadIdx.x; i < kBarStride * (1 + kBarGroups); i += blockDim.x) bar[i] = 0;
+    if (threadIdx.x == 0) {
+        slots[0].nf = 1;
+        slots[0].ns = static_cast<unsigned long long>(co[source + 1] - co[source]);
+    }
+}
+
 }  // namespace
 
 // One captured traversal plan: buffers, flattened trees and the graph.
@@ -899,6 +1131,9 @@ struct BfsPlan {
     DevTrees dt{};
     DevBuf pcnt;      // a pull level's spread (count, degree) counters
     DevBuf bigc, bigl;  // the scan push's big-vertex tasks (counter, list)
+    DevBuf slots, bar;  // the persistent kernel's rotating counters and grid barrier
+    int persist_G = 0;  // > 0: one cooperative persistent kernel (pull lanes G) instead of the graph
+    unsigned persist_grid = 0;
     cudaGraphExec_t exec = nullptr;
     ~BfsPlan() {
         if (exec) cudaGraphExecDestroy(exec);
@@ -1061,6 +1296,25 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     }
 #endif
     ctx.sync();
+    {  // the persistent kernel when the device can co-schedule it (ADASPMV_BFS_PERSIST=0: the graph)
+        const char* env = std::getenv("ADASPMV_BFS_PERSIST");
+        int coop = 0;
+        ADA_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx.device));
+        const int G = std::max(1, default_lanes_per_row(m.feat[5]) / 8);
+        const void* fn = G == 1   ? reinterpret_cast<const void*>(&bfs_persist_kernel<1>)
+                         : G == 2 ? reinterpret_cast<const void*>(&bfs_persist_kernel<2>)
+                         : G == 4 ? reinterpret_cast<const void*>(&bfs_persist_kernel<4>)
+                                  : reinterpret_cast<const void*>(&bfs_persist_kernel<8>);
+        int nb = 0;
+        ADA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 256, 0));
+        if (coop && nb > 0 && !(env && std::atoi(env) == 0)) {
+            P.persist_G = G == 1 || G == 2 || G == 4 ? G : 8;
+            P.persist_grid = static_cast<unsigned>(nb * ctx.sm_count);
+            P.slots.ensure(sizeof(PSlot) * 3);
+            P.bar.ensure(sizeof(unsigned) * kBarStride * (1 + kBarGroups));
+            return;
+        }
+    }
     BfsState* st = P.state.as<BfsState>();
     LogEntry* lg = P.log.as<LogEntry>();
     int32_t* lv = P.lv.as<int32_t>();
@@ -1182,10 +1436,43 @@ void bfs_graph(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, i
     bfs_init_kernel<<<ig, 256, 0, ctx.stream>>>(st, P.lv.as<int32_t>(), n, source, P.f[0].as<int32_t>(),
                                                 m.col_off.as<int64_t>(), P.eff.as<int64_t>());
     ADA_LAUNCHED(ctx);
-    // the whole traversal: one graph launch, one synchronisation (the state
-    // comes back through the mapped host scalars)
-    ADA_CUDA(cudaGraphLaunch(P.exec, ctx.stream));
-    ++ctx.launches;
+    // the whole traversal: one persistent kernel (or one graph launch), one
+    // synchronisation (the state comes back through the mapped host scalars)
+    if (P.persist_G > 0) {
+        PSlot* slots = P.slots.as<PSlot>();
+        unsigned* bar = P.bar.as<unsigned>();
+        bfs_persist_init_kernel<<<1, 256, 0, ctx.stream>>>(slots, bar, m.col_off.as<int64_t>(), source);
+        ADA_LAUNCHED(ctx);
+        PArgs a{};
+        a.st = st;
+        a.log = P.log.as<LogEntry>();
+        a.lv = P.lv.as<int32_t>();
+        a.ro = m.row_off.as<int64_t>();
+        a.ci = m.col_idx.as<int32_t>();
+        a.co = m.col_off.as<int64_t>();
+        a.ri = m.row_idx.as<int32_t>();
+        a.f[0] = P.f[0].as<int32_t>();
+        a.f[1] = P.f[1].as<int32_t>();
+        a.slots = slots;
+        a.bar = bar;
+        a.bigl = P.bigl.as<uint2>();
+        a.trees = P.dt;
+        a.use_trees = b ? 1 : 0;
+        a.mfeat = P.mfeat.as<double>();
+        a.n = n;
+        a.nnz = m.nnz;
+        a.vbytes = m.vbytes();
+        void* args[] = {&a};
+        const void* fn = P.persist_G == 1   ? reinterpret_cast<const void*>(&bfs_persist_kernel<1>)
+                         : P.persist_G == 2 ? reinterpret_cast<const void*>(&bfs_persist_kernel<2>)
+                         : P.persist_G == 4 ? reinterpret_cast<const void*>(&bfs_persist_kernel<4>)
+                                            : reinterpret_cast<const void*>(&bfs_persist_kernel<8>);
+        ADA_CUDA(cudaLaunchCooperativeKernel(fn, dim3(P.persist_grid), dim3(256), args, 0, ctx.stream));
+        ++ctx.launches;
+    } else {
+        ADA_CUDA(cudaGraphLaunch(P.exec, ctx.stream));
+        ++ctx.launches;
+    }
     copy_scalars_kernel_launch(ctx, reinterpret_cast<const int64_t*>(st), ctx.h_scalars_dev,
                                static_cast<int>(sizeof(BfsState) / sizeof(int64_t)));
     ctx.sync();
@@ -1212,9 +1499,13 @@ void bfs_graph(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, i
             r.kernel_s = t1 > t0 ? static_cast<double>(t1 - t0) * 1e-9 : 0.0;
 #ifdef ADA_BFS_TRACE
             const LogEntry& le = h[static_cast<size_t>(i)];
-            std::fprintf(stderr, "bfs trace level %d: kernels %.1f us (start +%.1f us after the decision)\n", i,
-                         le.tk1 > le.tk0 ? (le.tk1 - le.tk0) * 1e-3 : 0.0,
-                         le.tk0 != ~0ull && le.tk0 > t0 ? (le.tk0 - t0) * 1e-3 : 0.0);
+            if (P.persist_G > 0)
+                std::fprintf(stderr, "bfs trace level %d: block 0 body %.1f us, first barrier %.1f us\n", i,
+                             (le.tk0 - t0) * 1e-3, (le.tk1 - le.tk0) * 1e-3);
+            else
+                std::fprintf(stderr, "bfs trace level %d: kernels %.1f us (start +%.1f us after the decision)\n", i,
+                             le.tk1 > le.tk0 ? (le.tk1 - le.tk0) * 1e-3 : 0.0,
+                             le.tk0 != ~0ull && le.tk0 > t0 ? (le.tk0 - t0) * 1e-3 : 0.0);
 #endif
         }
     }

@@ -4,7 +4,9 @@ for every semiring on pattern matrices and OR_AND on valued ones, under the
 built-in policy and the trained selector (whose trees are walked on the
 device: its per-level choices must equal the host selector's on the same
 frontiers), on graphs of many WHILE iterations (two levels per iteration),
-disconnected graphs, isolated sources and a 3001-level path."""
+disconnected graphs, isolated sources and a 3001-level path -- in both
+device forms: the cooperative persistent kernel (default) and the CUDA
+graph (ADASPMV_BFS_PERSIST=0)."""
 import numpy as np
 import pytest
 
@@ -44,15 +46,32 @@ def _graphs():
     ro2 = np.zeros(3001, np.int64)
     np.add.at(ro2, rr + 1, 1)
     out.append(("random3000", 3000, np.cumsum(ro2), cc.astype(np.int64)))
+    # ~120 neighbours per vertex: the pull runs 4 lanes per row (G = 4)
+    rows, cols, ro, ci, _ = synth.random_csr(2000, 2000, 0.03, seed=6)
+    a = np.zeros((2000, 2000), bool)
+    a[np.repeat(np.arange(2000), np.diff(ro)), ci] = True
+    a = a | a.T
+    np.fill_diagonal(a, False)
+    rr, cc = np.nonzero(a)
+    ro3 = np.zeros(2001, np.int64)
+    np.add.at(ro3, rr + 1, 1)
+    out.append(("dense2000", 2000, np.cumsum(ro3), cc.astype(np.int64)))
     return out
 
 
 GRAPHS = _graphs()
 
 
+@pytest.fixture(params=["persistent", "graph"])
+def device_form(request, monkeypatch):
+    # read when a matrix's traversal plan is built (first BFS on it)
+    monkeypatch.setenv("ADASPMV_BFS_PERSIST", "1" if request.param == "persistent" else "0")
+    return request.param
+
+
 @pytest.mark.parametrize("name,n,ro,ci", GRAPHS, ids=[g[0] for g in GRAPHS])
 @pytest.mark.parametrize("sr", [A.OR_AND, A.MIN_PLUS, A.PLUS_TIMES], ids=["or_and", "min_plus", "plus_times"])
-def test_device_loop_levels(ctx, port, name, n, ro, ci, sr):
+def test_device_loop_levels(ctx, port, device_form, name, n, ro, ci, sr):
     m = A.DualMatrix.from_csr(n, n, ro, ci, None, dtype=np.float32, ctx=ctx)
     co, ri, _ = port.csr_to_csc(n, n, ro, ci, np.ones(len(ci)))
     bundle = A.SelectorBundle.load(S.DEFAULT_PATH)
@@ -91,7 +110,7 @@ def test_device_loop_valued_or_and_and_levels_download_optional(ctx, port):
     assert all(r["exec_mode"] != A.EXEC_FUSED_PUSH_LB or r["kernel"] >= 4 for r in reps)
 
 
-def test_device_loop_deep_path(ctx, port):
+def test_device_loop_deep_path(ctx, port, device_form):
     """3001 levels: the graph's WHILE node runs 1501 two-level bodies."""
     n = 3001
     ro, ci = _sym(n, [(i, i + 1) for i in range(n - 1)])
