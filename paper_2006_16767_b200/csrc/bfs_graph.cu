@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(256) bfs_pull_mark4_kernel(const BfsState* st,
 // ONE 64-bit atomic (count << 40 | tasks) so the list's task starts ascend,
 // and bfs_big_push_kernel spreads them over the whole grid.
 constexpr int kBigDeg = 256;
-constexpr int kBigChunk = 2048;
+constexpr int kBigChunk = 1024;
 constexpr int kBigShift = 40;
 
 __device__ __forceinline__ void claim_and_append(const int32_t (&r)[4], int32_t* __restrict__ lv, int level,
@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(256) bfs_scan_push_kernel(BfsState* st, int p,
 }
 
 // The big vertices' chunks: task t -> (vertex, chunk) by a search over the
-// ascending task starts; 256 threads x 8 entries per task.
+// ascending task starts; 256 threads x 4 entries per task.
 __device__ __forceinline__ void big_push_body(long long bid, long long nblk, int level,
                                               const int64_t* __restrict__ co, const int32_t* __restrict__ ri,
                                               int32_t* __restrict__ lv, unsigned long long* out_nf,
