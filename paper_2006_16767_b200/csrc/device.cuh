@@ -120,6 +120,16 @@ struct Semiring<SR_OR_AND, V> {
 template <int SR>
 struct AtomicCombine;
 
+// IEEE (subnormal-keeping) float add by compare-and-swap.
+__device__ __forceinline__ void atomic_add_f32_exact(float* p, float v) {
+    unsigned* a = reinterpret_cast<unsigned*>(p);
+    unsigned old = 0u, assumed;  // first guess +0: the first CAS returns the current value
+    do {
+        assumed = old;
+        old = atomicCAS(a, assumed, __float_as_uint(__uint_as_float(assumed) + v));
+    } while (old != assumed);
+}
+
 template <>
 struct AtomicCombine<SR_PLUS_TIMES> {
     // The hardware float reduction (REDG.E.ADD.F32.FTZ) flushes subnormal
@@ -130,20 +140,16 @@ struct AtomicCombine<SR_PLUS_TIMES> {
     // subnormal operand or result is <= 2^-126 absolute, far inside the fp32
     // tolerance of a row bound >= 2^-100.
     __device__ static void apply(float* p, float v) {
-        if (fabsf(v) >= 0x1p-100f) {
-            atomicAdd(p, v);
-            return;
-        }
-        if (v == 0.f) return;  // adding +-0 never changes a sum that starts at +0
-        unsigned* a = reinterpret_cast<unsigned*>(p);
-        unsigned old = *reinterpret_cast<volatile unsigned*>(a), assumed;
-        do {
-            assumed = old;
-            old = atomicCAS(a, assumed, __float_as_uint(__uint_as_float(assumed) + v));
-        } while (old != assumed);
+        const bool tiny = fabsf(v) < 0x1p-100f;  // NaN: not tiny
+        if (!tiny) atomicAdd(p, v);               // predicated RED, no branch
+        else if (v != 0.f) atomic_add_f32_exact(p, v);  // adding +-0 never changes a sum that starts at +0
     }
     __device__ static void apply(double* p, double v) { atomicAdd(p, v); }
+    // the addend is known to be outside the subnormal range
+    __device__ static void apply_fast(float* p, float v) { atomicAdd(p, v); }
+    __device__ static void apply_fast(double* p, double v) { atomicAdd(p, v); }
 };
+
 template <>
 struct AtomicCombine<SR_OR_AND> {
     __device__ static void apply(float* p, float v) {
@@ -152,6 +158,8 @@ struct AtomicCombine<SR_OR_AND> {
     __device__ static void apply(double* p, double v) {
         if (v != 0.0) *reinterpret_cast<volatile double*>(p) = 1.0;
     }
+    template <class V>
+    __device__ static void apply_fast(V* p, V v) { apply(p, v); }
 };
 template <>
 struct AtomicCombine<SR_MIN_PLUS> {
@@ -166,7 +174,37 @@ struct AtomicCombine<SR_MIN_PLUS> {
         if (iv >= 0) atomicMin(reinterpret_cast<long long*>(p), iv);
         else atomicMax(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(iv));
     }
+    template <class V>
+    __device__ static void apply_fast(V* p, V v) { apply(p, v); }
 };
+
+// A batch of N write-backs y[r[j]] (+)= v[j] (ok[j]).  `safe`: the caller
+// knows no addend can be below 2^-100 in magnitude (|x| * min|a| >= 2^-100,
+// decided once per support column or warp tile, ahead of the products), so
+// the hardware reductions issue exactly as plain atomicAdd; otherwise each
+// addend is checked and the subnormal-range ones take the IEEE CAS add.  A
+// per-entry branch on the product's magnitude in the common path would stall
+// every write-back on its product (C4 K6: +15-20 %, measured).
+template <int SR, class V, int N>
+__device__ __forceinline__ void combine_batch(V* y, const int (&r)[N], const V (&v)[N], const bool (&ok)[N],
+                                              bool safe) {
+    if (SR != SR_PLUS_TIMES || sizeof(V) != 4 || safe) {
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+            if (ok[j]) AtomicCombine<SR>::apply_fast(y + r[j], v[j]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+            if (ok[j]) AtomicCombine<SR>::apply(y + r[j], v[j]);
+    }
+}
+
+// the per-column / per-tile test behind `safe` (fp32 plus-times only)
+template <int SR, class V>
+__device__ __forceinline__ bool addends_normal(V x, float amin) {
+    if constexpr (SR != SR_PLUS_TIMES || sizeof(V) != 4) return true;
+    else return fabsf(static_cast<float>(x)) * amin >= 0x1p-100f;  // NaN: not safe
+}
 
 // ---- warp / block scans ---------------------------------------------------------
 template <class T>

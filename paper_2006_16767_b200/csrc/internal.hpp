@@ -200,6 +200,7 @@ struct Matrix {
     int64_t nnz_s_lower(int64_t k) const;
     int64_t nnz_s_upper(int64_t k) const;
     bool pattern = false;   // created without values (all 1.0)
+    float amin = 1.0f;      // fp32: smallest nonzero |a| (the atomic write-backs' subnormal-range check)
     double gather_spread = 0;  // mean |col - row*n/m| over the nonzeros (columns)
     mutable std::unique_ptr<BinLayout> bins{new BinLayout()};
     // column-normalised pattern copy for PageRank (pagerank.cu), built once

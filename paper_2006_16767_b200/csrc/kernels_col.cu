@@ -46,7 +46,7 @@ template <class V, int G, int SR>
 __global__ void __launch_bounds__(kNT) col_direct_atomic_kernel(
     int64_t nnz_x, const int32_t* __restrict__ xi, const V* __restrict__ xv,
     const int64_t* __restrict__ co, const int32_t* __restrict__ ri, const V* __restrict__ cv,
-    const uint2* __restrict__ cp, V* __restrict__ y, unsigned long long* __restrict__ ctr) {
+    const uint2* __restrict__ cp, V* __restrict__ y, unsigned long long* __restrict__ ctr, float amin) {
     using S = Semiring<SR, V>;
     const int64_t gid = static_cast<int64_t>(blockIdx.x) * kNT + threadIdx.x;
     const int64_t s = gid / G;
@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kNT) col_direct_atomic_kernel(
     if (s >= nnz_x) return;  // no cross-lane communication below
     const int32_t col = __ldg(xi + s);
     const V xval = __ldg(xv + s);
+    const bool safe = addends_normal<SR>(xval, amin);  // once per column (device.cuh combine_batch)
     const int64_t b = __ldg(co + col), e = __ldg(co + col + 1);
     if (ctr && lg == 0) count_add(ctr, 0, static_cast<unsigned long long>(e - b));  // the column's entries
     for (int64_t k0 = b + lg; k0 < e; k0 += G * kU) {
@@ -75,9 +76,14 @@ __global__ void __launch_bounds__(kNT) col_direct_atomic_kernel(
                 r[j] = -1;
             }
         }
+        V pv[kU];
+        bool ok[kU];
 #pragma unroll
-        for (int j = 0; j < kU; ++j)
-            if (r[j] >= 0) AtomicCombine<SR>::apply(y + r[j], S::mul(a[j], xval));
+        for (int j = 0; j < kU; ++j) {
+            ok[j] = r[j] >= 0;
+            pv[j] = S::mul(a[j], xval);
+        }
+        combine_batch<SR>(y, r, pv, ok, safe);
     }
 }
 
@@ -123,7 +129,7 @@ __global__ void __launch_bounds__(kNT) col_lb_kernel(
     const int32_t* __restrict__ ri, const V* __restrict__ cv, V* __restrict__ y,
     uint32_t* __restrict__ keys, V* __restrict__ pvals, unsigned long long* __restrict__ ctr,
     int32_t* __restrict__ lv = nullptr, int32_t level = 0, unsigned long long* __restrict__ bfs_cnt = nullptr,
-    V bfs_value = V(1)) {
+    V bfs_value = V(1), float amin = 3.0e38f) {
     using S = Semiring<SR, V>;
     constexpr bool EMIT = MODE == 1;
     constexpr int kW = kNT / 32;
@@ -224,16 +230,24 @@ __global__ void __launch_bounds__(kNT) col_lb_kernel(
         }
         return;
     }
+    if (EMIT) {
 #pragma unroll
-    for (int j = 0; j < kJ; ++j) {
-        if (kidx[j] < 0) continue;
-        const V prod = S::mul(a[j], xval[j]);
-        if (EMIT) {
+        for (int j = 0; j < kJ; ++j) {
+            if (kidx[j] < 0) continue;
             keys[tb + 32 * j + lane] = static_cast<uint32_t>(r[j]);
-            pvals[tb + 32 * j + lane] = prod;
-        } else {
-            AtomicCombine<SR>::apply(y + r[j], prod);
+            pvals[tb + 32 * j + lane] = S::mul(a[j], xval[j]);
         }
+    } else {
+        V pv[kJ];
+        bool ok[kJ];
+        bool normal = true;  // the tile's x values rule out subnormal-range products (device.cuh)
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+            ok[j] = kidx[j] >= 0;
+            pv[j] = S::mul(a[j], xval[j]);
+            normal = normal && (!ok[j] || addends_normal<SR>(xval[j], amin));
+        }
+        combine_batch<SR>(y, r, pv, ok, __all_sync(kFull, normal));
     }
 }
 
@@ -659,7 +673,7 @@ void launch_direct_atomic(Context& ctx, const Matrix& m, Vector& x, int G, V* y)
     case GG:                                                                                 \
         col_direct_atomic_kernel<V, GG, SR><<<blocks, kNT, 0, ctx.stream>>>(                 \
             x.nnz, x.sp_idx.as<int32_t>(), x.sp_val.as<V>(), m.col_off.as<int64_t>(),        \
-            m.row_idx.as<int32_t>(), m.cvals.as<V>(), m.cpairs.as<uint2>(), y, ctx.ctr);     \
+            m.row_idx.as<int32_t>(), m.cvals.as<V>(), m.cpairs.as<uint2>(), y, ctx.ctr, m.amin); \
         break;
     switch (G) {
         ADA_G(1) ADA_G(2) ADA_G(4) ADA_G(8) ADA_G(16) ADA_G(32)
@@ -813,7 +827,7 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
         col_lb_kernel<V, SR, 0><<<static_cast<unsigned>((tiles + 7) / 8), kNT, 0, ctx.stream>>>(
             x.nnz, nnz_s, tiles, x.eff.as<int64_t>(), x.sp_idx.as<int32_t>(), x.sp_val.as<V>(),
             m.col_off.as<int64_t>(), m.row_idx.as<int32_t>(), m.cvals.as<V>(), y_dense, nullptr,
-            nullptr, ctx.ctr);
+            nullptr, ctx.ctr, nullptr, 0, nullptr, V(1), m.amin);
         ADA_LAUNCHED(ctx);
         return;
     }

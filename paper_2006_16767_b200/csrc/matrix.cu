@@ -325,13 +325,37 @@ __global__ void csc_pairs_kernel(int64_t nnz, const int32_t* __restrict__ ri, co
         out[k] = make_uint2(static_cast<uint32_t>(ri[k]), __float_as_uint(cv[k]));
 }
 
-// Matrix::cpairs of an fp32 matrix from its CSC
+// smallest nonzero |v| as float bits (positive floats order like their bits)
+__global__ void min_abs_nonzero_kernel(int64_t n, const float* __restrict__ v, unsigned* __restrict__ out) {
+    unsigned best = 0x7f800000u;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n; k += stride) {
+        const unsigned b = __float_as_uint(fabsf(v[k]));
+        if (b != 0u && b < best) best = b;
+    }
+    best = __reduce_min_sync(0xffffffffu, best);
+    if ((threadIdx.x & 31) == 0) atomicMin(out, best);
+}
+
+// Matrix::cpairs of an fp32 matrix from its CSC, and Matrix::amin
 void build_pairs(Context& ctx, Matrix& m) {
     if (m.dtype != ADASPMV_F32 || m.nnz <= 0) return;
     uint2* p = static_cast<uint2*>(m.cpairs.ensure(sizeof(uint2) * static_cast<size_t>(m.nnz)));
     csc_pairs_kernel<<<grid_for(ctx, m.nnz, 256), 256, 0, ctx.stream>>>(m.nnz, m.row_idx.as<int32_t>(),
                                                                        m.cvals.as<float>(), p);
     ADA_LAUNCHED(ctx);
+    DevBuf mb;
+    unsigned* d = static_cast<unsigned*>(mb.ensure(sizeof(unsigned)));
+    const unsigned inf = 0x7f800000u;
+    ADA_CUDA(cudaMemcpyAsync(d, &inf, sizeof(unsigned), cudaMemcpyHostToDevice, ctx.stream));
+    min_abs_nonzero_kernel<<<grid_for(ctx, m.nnz, 256), 256, 0, ctx.stream>>>(m.nnz, m.cvals.as<float>(), d);
+    ADA_LAUNCHED(ctx);
+    unsigned h = inf;
+    ADA_CUDA(cudaMemcpyAsync(&h, d, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    float a;
+    std::memcpy(&a, &h, sizeof(a));
+    m.amin = h >= inf ? 3.0e38f : a;  // no nonzero value: nothing to check
 }
 
 template <class V>
