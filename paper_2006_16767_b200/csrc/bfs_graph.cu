@@ -955,6 +955,8 @@ struct PArgs {
     const double* mfeat;
     int64_t n, nnz;
     int vbytes;
+    int64_t source;
+    int64_t* host_state;  // mapped host copy of the final BfsState (Context::h_scalars)
 };
 
 // Visibility: every block reads what the others wrote in earlier steps
@@ -1009,6 +1011,22 @@ __global__ void __launch_bounds__(256) bfs_persist_kernel(PArgs a) {
     long long visited = 0;
     int nlog = 0;
     bool list = true;  // the frontier exists as a list (a pull leaves marks)
+    // prologue (no separate init launches): levels, the first frontier, the
+    // counter slots; the barrier's own words return to 0 after every barrier
+    for (long long i = bid * 256 + threadIdx.x; i < a.n; i += nblk * 256) a.lv[i] = i == a.source ? 0 : -1;
+    if (bid == 0) {
+        for (int s3 = 0; s3 < 3; ++s3) {
+            for (int i = threadIdx.x; i < 2 * kSpread; i += 256) a.slots[s3].pc[i] = 0;
+            if (threadIdx.x == 0) a.slots[s3].nf = a.slots[s3].ns = a.slots[s3].bigc = a.slots[s3].pulled = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            a.f[0][0] = static_cast<int32_t>(a.source);
+            a.slots[0].nf = 1;
+            a.slots[0].ns = static_cast<unsigned long long>(a.co[a.source + 1] - a.co[a.source]);
+        }
+    }
+    grid_barrier(a.bar, static_cast<unsigned>(nblk));
     for (int L = 0;; ++L) {
         PSlot* cur = a.slots + L % 3;
         PSlot* nxt = a.slots + (L + 1) % 3;
@@ -1041,11 +1059,18 @@ __global__ void __launch_bounds__(256) bfs_persist_kernel(PArgs a) {
         if (nf == 0) {  // every block leaves here, on the same step
             if (bid == 0 && threadIdx.x == 0) {
                 if (nlog < kMaxLog) a.log[nlog].t0 = now;  // end stamp of the last level
-                a.st->nlog = nlog;
-                a.st->visited = visited;
-                a.st->level = L;
-                a.st->done = 1;
-                a.st->mode = kModeDone;
+                BfsState fin{};
+                fin.nlog = nlog;
+                fin.visited = visited;
+                fin.level = L;
+                fin.done = 1;
+                fin.mode = kModeDone;
+                *a.st = fin;
+                // straight into the mapped host scalars: no copy launch after the traversal
+                const int64_t* w = reinterpret_cast<const int64_t*>(&fin);
+                volatile int64_t* h = a.host_state;
+                for (size_t i = 0; i < sizeof(BfsState) / sizeof(int64_t); ++i) h[i] = w[i];
+                __threadfence_system();
             }
             return;
         }
@@ -1106,18 +1131,6 @@ __global__ void __launch_bounds__(256) bfs_persist_kernel(PArgs a) {
                 grid_barrier(a.bar, static_cast<unsigned>(nblk));
             }
         }
-    }
-}
-
-__global__ void bfs_persist_init_kernel(PSlot* slots, unsigned* bar, const int64_t* __restrict__ co, int64_t source) {
-    for (int s = 0; s < 3; ++s) {
-        for (int i = threadIdx.x; i < 2 * kSpread; i += blockDim.x) slots[s].pc[i] = 0;
-        if (threadIdx.x == 0) slots[s].nf = slots[s].ns = slots[s].bigc = slots[s].pulled = 0;
-    }
-    for (int i = threadIdx.x; i < kBarStride * (1 + kBarGroups); i += blockDim.x) bar[i] = 0;
-    if (threadIdx.x == 0) {
-        slots[0].nf = 1;
-        slots[0].ns = static_cast<unsigned long long>(co[source + 1] - co[source]);
     }
 }
 
@@ -1312,6 +1325,8 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
             P.persist_grid = static_cast<unsigned>(nb * ctx.sm_count);
             P.slots.ensure(sizeof(PSlot) * 3);
             P.bar.ensure(sizeof(unsigned) * kBarStride * (1 + kBarGroups));
+            ADA_CUDA(cudaMemsetAsync(P.bar.p, 0, sizeof(unsigned) * kBarStride * (1 + kBarGroups), ctx.stream));
+            ctx.sync();
             return;
         }
     }
@@ -1432,17 +1447,12 @@ void bfs_graph(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, i
     }
     BfsPlan& P = *plan;
     BfsState* st = P.state.as<BfsState>();
-    const unsigned ig = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 16));
-    bfs_init_kernel<<<ig, 256, 0, ctx.stream>>>(st, P.lv.as<int32_t>(), n, source, P.f[0].as<int32_t>(),
-                                                m.col_off.as<int64_t>(), P.eff.as<int64_t>());
-    ADA_LAUNCHED(ctx);
-    // the whole traversal: one persistent kernel (or one graph launch), one
-    // synchronisation (the state comes back through the mapped host scalars)
+    // the whole traversal: one persistent kernel (or init + one graph launch
+    // + a copy), one synchronisation (the state comes back through the
+    // mapped host scalars)
     if (P.persist_G > 0) {
         PSlot* slots = P.slots.as<PSlot>();
         unsigned* bar = P.bar.as<unsigned>();
-        bfs_persist_init_kernel<<<1, 256, 0, ctx.stream>>>(slots, bar, m.col_off.as<int64_t>(), source);
-        ADA_LAUNCHED(ctx);
         PArgs a{};
         a.st = st;
         a.log = P.log.as<LogEntry>();
@@ -1462,19 +1472,27 @@ void bfs_graph(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, i
         a.n = n;
         a.nnz = m.nnz;
         a.vbytes = m.vbytes();
+        a.source = source;
+        a.host_state = ctx.h_scalars_dev;
         void* args[] = {&a};
         const void* fn = P.persist_G == 1   ? reinterpret_cast<const void*>(&bfs_persist_kernel<1>)
                          : P.persist_G == 2 ? reinterpret_cast<const void*>(&bfs_persist_kernel<2>)
                          : P.persist_G == 4 ? reinterpret_cast<const void*>(&bfs_persist_kernel<4>)
                                             : reinterpret_cast<const void*>(&bfs_persist_kernel<8>);
+        reinterpret_cast<BfsState*>(ctx.h_scalars)->done = 0;
         ADA_CUDA(cudaLaunchCooperativeKernel(fn, dim3(P.persist_grid), dim3(256), args, 0, ctx.stream));
         ++ctx.launches;
     } else {
+        const unsigned ig =
+            static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 16));
+        bfs_init_kernel<<<ig, 256, 0, ctx.stream>>>(st, P.lv.as<int32_t>(), n, source, P.f[0].as<int32_t>(),
+                                                    m.col_off.as<int64_t>(), P.eff.as<int64_t>());
+        ADA_LAUNCHED(ctx);
         ADA_CUDA(cudaGraphLaunch(P.exec, ctx.stream));
         ++ctx.launches;
+        copy_scalars_kernel_launch(ctx, reinterpret_cast<const int64_t*>(st), ctx.h_scalars_dev,
+                                   static_cast<int>(sizeof(BfsState) / sizeof(int64_t)));
     }
-    copy_scalars_kernel_launch(ctx, reinterpret_cast<const int64_t*>(st), ctx.h_scalars_dev,
-                               static_cast<int>(sizeof(BfsState) / sizeof(int64_t)));
     ctx.sync();
     if (!reinterpret_cast<const BfsState*>(ctx.h_scalars)->done)
         throw Error(ADASPMV_ERR_INTERNAL, "bfs: device level loop ended without an empty frontier");
