@@ -1145,11 +1145,17 @@ struct BfsPlan {
     DevBuf pcnt;      // a pull level's spread (count, degree) counters
     DevBuf bigc, bigl;  // the scan push's big-vertex tasks (counter, list)
     DevBuf slots, bar;  // the persistent kernel's rotating counters and grid barrier
+    // the per-level log in mapped pinned host memory: the reports are read
+    // after the traversal's one synchronisation, no copy (the diagnostic
+    // trace build keeps it on the device: it updates entries atomically)
+    LogEntry* hlog = nullptr;
+    LogEntry* dlog = nullptr;
     int persist_G = 0;  // > 0: one cooperative persistent kernel (pull lanes G) instead of the graph
     unsigned persist_grid = 0;
     cudaGraphExec_t exec = nullptr;
     ~BfsPlan() {
         if (exec) cudaGraphExecDestroy(exec);
+        if (hlog) cudaFreeHost(hlog);
     }
 };
 
@@ -1290,7 +1296,12 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     P.stream = ctx.stream;
     P.bundle_id = b ? b->id : 0;
     P.state.ensure(sizeof(BfsState));
-    P.log.ensure(sizeof(LogEntry) * kMaxLog);
+#ifdef ADA_BFS_TRACE
+    P.dlog = static_cast<LogEntry*>(P.log.ensure(sizeof(LogEntry) * kMaxLog));
+#else
+    ADA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&P.hlog), sizeof(LogEntry) * kMaxLog, cudaHostAllocMapped));
+    ADA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&P.dlog), P.hlog, 0));
+#endif
     for (auto& f : P.f) f.ensure(sizeof(int32_t) * static_cast<size_t>(n));
     P.eff.ensure(sizeof(int64_t) * static_cast<size_t>(n + 1));
     P.lv.ensure(sizeof(int32_t) * static_cast<size_t>(n));
@@ -1304,7 +1315,7 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     if (b) upload_trees(ctx, *b, m.feat, P);
 #ifdef ADA_BFS_TRACE
     {
-        LogEntry* lp = P.log.as<LogEntry>();
+        LogEntry* lp = P.dlog;
         ADA_CUDA(cudaMemcpyToSymbolAsync(g_bfs_log, &lp, sizeof(lp), 0, cudaMemcpyHostToDevice, ctx.stream));
     }
 #endif
@@ -1331,7 +1342,7 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
         }
     }
     BfsState* st = P.state.as<BfsState>();
-    LogEntry* lg = P.log.as<LogEntry>();
+    LogEntry* lg = P.dlog;
     int32_t* lv = P.lv.as<int32_t>();
     const int64_t* co = m.col_off.as<int64_t>();
     const unsigned push_grid = static_cast<unsigned>(ctx.sm_count) * 8;
@@ -1455,7 +1466,7 @@ void bfs_graph(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, i
         unsigned* bar = P.bar.as<unsigned>();
         PArgs a{};
         a.st = st;
-        a.log = P.log.as<LogEntry>();
+        a.log = P.dlog;
         a.lv = P.lv.as<int32_t>();
         a.ro = m.row_off.as<int64_t>();
         a.ci = m.col_idx.as<int32_t>();
@@ -1502,8 +1513,13 @@ void bfs_graph(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, i
     if (reports && max_reports > 0) {
         const int nr = static_cast<int>(std::min<int64_t>(std::min<int64_t>(nlog, max_reports), kMaxLog - 1));
         std::vector<LogEntry> h(static_cast<size_t>(nr + 1));
-        ADA_CUDA(cudaMemcpyAsync(h.data(), P.log.p, sizeof(LogEntry) * h.size(), cudaMemcpyDeviceToHost, ctx.stream));
-        ctx.sync();
+        if (P.hlog) {
+            std::memcpy(h.data(), P.hlog, sizeof(LogEntry) * h.size());
+        } else {
+            ADA_CUDA(cudaMemcpyAsync(h.data(), P.dlog, sizeof(LogEntry) * h.size(), cudaMemcpyDeviceToHost,
+                                     ctx.stream));
+            ctx.sync();
+        }
         for (int i = 0; i < nr; ++i) {
             adaspmv_iteration_report& r = reports[i];
             r.iteration = i;
