@@ -124,12 +124,14 @@ int adaspmv_ctx_set_timing(adaspmv_ctx* ctx, int enable);
 /* BFS level loop of adaspmv_bfs: 1 = the host-driven loop (one
  * synchronisation per level); 0 (default) = device-resident where it applies
  * (membership-only levels -- OR_AND, or a pattern matrix -- under the
- * built-in policy or a selector bundle): the whole traversal is one CUDA
- * graph whose WHILE / IF conditional nodes run only the chosen branch of each
- * level, the level decisions, frontier updates and the selector's tree walk
- * on the device, one host synchronisation per traversal (C3 R-MAT 22:
- * 0.39-0.43 ms vs 0.52 ms for the host loop).  Forced kernels and values-
- * dependent semirings on weighted matrices always use the host loop. */
+ * built-in policy or a selector bundle): the whole traversal is one
+ * cooperative persistent kernel (grid barriers between levels; the level
+ * decisions, frontier updates and the selector's tree walk on the device;
+ * one launch and one host synchronisation per traversal -- C3 R-MAT 22:
+ * 0.19 ms vs 0.52 ms for the host loop), or, with ADASPMV_BFS_PERSIST=0 in
+ * the environment, one CUDA graph whose WHILE / SWITCH conditional nodes run
+ * only the chosen branch of each level.  Forced kernels and values-dependent
+ * semirings on weighted matrices always use the host loop. */
 int adaspmv_ctx_set_bfs_loop(adaspmv_ctx* ctx, int host_loop);
 const char* adaspmv_version(void);
 
