@@ -877,7 +877,7 @@ def ours_c5(local, rank, world, bundle, hbm, ctx, stream, dist=None, reps=3):
     partition.hpp:30-33), one per rank.  Per x density: x drawn on rank 0 and
     broadcast over NCCL (N > 1), each rank's selector + multiply on its block;
     time = broadcast (events) + multiply (library events), max over ranks.
-    BFS from vertex 0 (OR_AND): N = 1 the device-graph BFS, N > 1 the
+    BFS from vertex 0 (OR_AND): N = 1 the device-resident (persistent-kernel) BFS, N > 1 the
     row-partitioned BFS with the frontier all-gathered every level
     (adaspmv_dist_bfs); wall time max over ranks.  No CPU reference at this
     size (the reference BFS on 2.1 G edges takes minutes)."""
@@ -1025,7 +1025,7 @@ def ours_c5(local, rank, world, bundle, hbm, ctx, stream, dist=None, reps=3):
            "points": pts, "value": round(flops / sum(p_["ms"] * 1e-3 for p_ in pts) / 1e9, 3), "unit": "GFLOP/s",
            "bfs": {"ms": round(wall * 1e3, 4), "gteps": round(edges / wall / 1e9, 2), "levels": nlev,
                    "reached": reached_n, "edges_traversed": edges,
-                   "mode": "device-graph BFS" if dist is None else "row-partitioned BFS, frontier all-gathered"},
+                   "mode": "device-resident BFS (one persistent kernel)" if dist is None else "row-partitioned BFS, frontier all-gathered"},
            "setup_s": {"generate": round(gen_s, 2), "build": round(build_s, 2)},
            "cpu_reference": None}
     del m, x, out
