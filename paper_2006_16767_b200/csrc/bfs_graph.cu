@@ -1291,6 +1291,8 @@ void capture_switch(Context& ctx, cudaStream_t s, cudaStream_t s2, cudaGraphCond
 // The whole traversal as ONE graph: WHILE(frontier) { level p = 0; level
 // p = 1 }, a level being decide -> SWITCH(branch).  Only the chosen
 // branch's kernels run; sizes live on the device.
+void build_graph(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P);
+
 void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
     const int64_t n = m.rows;
     P.stream = ctx.stream;
@@ -1334,6 +1336,7 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
         if (coop && nb > 0 && !(env && std::atoi(env) == 0)) {
             P.persist_G = G == 1 || G == 2 || G == 4 ? G : 8;
             P.persist_grid = static_cast<unsigned>(nb * ctx.sm_count);
+            if (env && std::atoi(env) == 2) P.persist_grid *= 4;  // test hook: a grid that cannot be co-scheduled
             P.slots.ensure(sizeof(PSlot) * 3);
             P.bar.ensure(sizeof(unsigned) * kBarStride * (1 + kBarGroups));
             ADA_CUDA(cudaMemsetAsync(P.bar.p, 0, sizeof(unsigned) * kBarStride * (1 + kBarGroups), ctx.stream));
@@ -1341,6 +1344,13 @@ void build_plan(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
             return;
         }
     }
+    build_graph(ctx, m, b, P);
+}
+
+// The CUDA-graph form of the traversal (see the header).
+void build_graph(Context& ctx, const Matrix& m, const Bundle* b, BfsPlan& P) {
+    const int64_t n = m.rows;
+    double* mf = P.mfeat.as<double>();
     BfsState* st = P.state.as<BfsState>();
     LogEntry* lg = P.dlog;
     int32_t* lv = P.lv.as<int32_t>();
@@ -1491,9 +1501,19 @@ void bfs_graph(Context& ctx, const Matrix& m, int64_t source, const Bundle* b, i
                          : P.persist_G == 4 ? reinterpret_cast<const void*>(&bfs_persist_kernel<4>)
                                             : reinterpret_cast<const void*>(&bfs_persist_kernel<8>);
         reinterpret_cast<BfsState*>(ctx.h_scalars)->done = 0;
-        ADA_CUDA(cudaLaunchCooperativeKernel(fn, dim3(P.persist_grid), dim3(256), args, 0, ctx.stream));
-        ++ctx.launches;
-    } else {
+        const cudaError_t le = cudaLaunchCooperativeKernel(fn, dim3(P.persist_grid), dim3(256), args, 0, ctx.stream);
+        if (le == cudaErrorCooperativeLaunchTooLarge || le == cudaErrorNotSupported) {
+            // the grid cannot be co-scheduled here (e.g. SMs held by MPS
+            // clients): this plan falls back to the graph form for good
+            (void)cudaGetLastError();
+            P.persist_G = 0;
+            build_graph(ctx, m, b, P);
+        } else {
+            ADA_CUDA(le);
+            ++ctx.launches;
+        }
+    }
+    if (P.persist_G == 0) {
         const unsigned ig =
             static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx.sm_count) * 16));
         bfs_init_kernel<<<ig, 256, 0, ctx.stream>>>(st, P.lv.as<int32_t>(), n, source, P.f[0].as<int32_t>(),

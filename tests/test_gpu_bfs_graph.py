@@ -120,3 +120,17 @@ def test_device_loop_deep_path(ctx, port, device_form):
     assert np.array_equal(lv, np.arange(n)) and len(reps) == n
     lv, reps = A.bfs(m, n // 2, A.MIN_PLUS)
     assert np.array_equal(lv, np.abs(np.arange(n) - n // 2)) and len(reps) == n // 2 + 1
+
+
+def test_persistent_launch_fallback(ctx, port, monkeypatch):
+    # a grid the device cannot co-schedule (test hook ADASPMV_BFS_PERSIST=2):
+    # the plan falls back to the graph form and the traversal is still exact
+    monkeypatch.setenv("ADASPMV_BFS_PERSIST", "2")
+    n, _, ro, ci, _ = synth.rmat(12, 8, seed=9)
+    m = A.DualMatrix.from_csr(n, n, ro, ci, None, dtype=np.float32, ctx=ctx)
+    co, ri, _ = port.csr_to_csc(n, n, ro, ci, np.ones(len(ci)))
+    ctx.set_bfs_loop(False)
+    for _ in range(2):  # the second call runs the fallen-back plan directly
+        lv, reps = A.bfs(m, 0, A.OR_AND)
+        exp, nl = port.bfs_queue(n, co, ri, 0)
+        assert np.array_equal(lv, exp) and len(reps) == nl
