@@ -166,6 +166,18 @@ struct BinLayout {
     DevBuf tiles, tile_bin, tile_multi;
 };
 
+// Heavy-column segment table of the row-segmented column write-back
+// (kernels_colseg.cu): columns with >= lmin entries, and for each of them the
+// absolute CSC position where each R-row segment starts.
+struct ColSegs {
+    bool built = false;
+    int64_t R = 0, nseg = 0, nheavy = 0, lmin = 0, heavy_nnz = 0;  // heavy_nnz: entries in heavy columns
+    DevBuf hid;    // int32 [cols]: heavy id, or -1
+    DevBuf hcols;  // int32 [nheavy]: heavy id -> column
+    DevBuf cnt;    // build scratch
+    DevBuf tab;    // int64 [(nseg + 1) * nheavy]: tab[b * nheavy + h]
+};
+
 struct Matrix {
     Context* ctx = nullptr;
     int64_t rows = 0, cols = 0, nnz = 0;
@@ -203,6 +215,7 @@ struct Matrix {
     float amin = 1.0f;      // fp32: smallest nonzero |a| (the atomic write-backs' subnormal-range check)
     double gather_spread = 0;  // mean |col - row*n/m| over the nonzeros (columns)
     mutable std::unique_ptr<BinLayout> bins{new BinLayout()};
+    mutable std::unique_ptr<ColSegs> csegs{new ColSegs()};  // row-segmented K6 (built on first use)
     // column-normalised pattern copy for PageRank (pagerank.cu), built once
     mutable std::unique_ptr<Matrix> colnorm;
     // captured device-resident BFS loop (bfs_graph.cu), built on first use

@@ -45,6 +45,12 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
 
 // K4-K7 (kernels_col.cu).  Atomic -> dense y (y_dense); sort -> sparse y
 // (y_idx, y_val, *d_nnz on device).  x is the sparse operand.
+// row-segmented atomic column write-back (kernels_colseg.cu), used by K4/K6
+// when ADASPMV_COLSEG=1 (colseg_mode() == 1; 0 or unset: off)
+int colseg_mode();
+template <class V, int SR>
+bool run_col_segmented(Context& ctx, const Matrix& m, Vector& x, V* y);
+
 template <class V, int SR>
 void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort, bool private_acc,
                    int lanes, V* y_dense, int32_t* y_idx, V* y_val, int64_t* d_nnz,

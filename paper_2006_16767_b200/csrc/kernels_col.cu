@@ -812,6 +812,12 @@ void run_col_major(Context& ctx, const Matrix& m, Vector& x, bool lb, bool sort,
     const int G = lanes > 0 ? lanes : default_lanes_per_row(m.avg_col);
     *h_nnz = -1;
     if (!sort) {
+        // row-segmented write-back (kernels_colseg.cu: every row stored once,
+        // no identity fill), opt-in with ADASPMV_COLSEG=1 -- measured at par
+        // with the L2-atomic path on C4 and slower on C2, so not the default
+        if (x.nnz > 0 && m.nnz > 0 && !private_acc && colseg_mode() == 1 &&
+            run_col_segmented<V, SR>(ctx, m, x, y_dense))
+            return;
         // atomic write-back into a dense y initialised to the identity
         fill_value<V, SR>(ctx, y_dense, m.rows);
         if (x.nnz == 0 || m.nnz == 0) return;
