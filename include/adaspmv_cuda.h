@@ -425,6 +425,13 @@ int adaspmv_dist_destroy(adaspmv_dist* d);
 int adaspmv_dist_bcast_vector(adaspmv_dist* d, adaspmv_vector* x, int root);
 /* Every rank's dense y block, in rank order, into y_full (device, sum of the
  * blocks' rows values); *total gets that sum. */
+/* A full-y buffer of `bytes` bytes on this rank's device, IPC-shared with
+ * every rank (collective).  adaspmv_dist_allgather_output into it writes each
+ * rank's block straight into every rank's buffer with peer stores over
+ * NVLink / NVSwitch (csrc/peer.cu) instead of NCCL broadcasts.  Freed with
+ * the dist.  Replaces: the y all-gather after a row-partitioned multiply
+ * (partition.hpp:30-56 row blocks). */
+int adaspmv_dist_alloc_peer_output(adaspmv_dist* d, int64_t bytes, void** y_full_device);
 int adaspmv_dist_allgather_output(adaspmv_dist* d, adaspmv_output* y, void* y_full_device, int64_t* total);
 /* BFS (as adaspmv_bfs) over the square matrix whose rows row0 .. row0 +
  * rows(block) - 1 this rank holds; every level each rank multiplies its block

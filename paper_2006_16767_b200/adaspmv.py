@@ -204,6 +204,7 @@ def load(path: Optional[os.PathLike] = None):
         "adaspmv_dist_destroy": [vp],
         "adaspmv_dist_bcast_vector": [vp, vp, C.c_int],
         "adaspmv_dist_allgather_output": [vp, vp, vp, P(i64)],
+        "adaspmv_dist_alloc_peer_output": [vp, i64, P(vp)],
         "adaspmv_dist_bfs": [vp, vp, i64, i64, C.c_int, vp, C.c_int, vp, P(i64), vp, i64],
     }
     for name, args in sigs.items():
@@ -1067,6 +1068,13 @@ class Dist:
     def bcast_vector(self, x: "DeviceVector", root: int = 0):
         _check(_lib.adaspmv_dist_bcast_vector(self.h, x.h, int(root)))
         return x
+
+    def alloc_peer_output(self, nbytes: int) -> int:
+        """Collective: a full-y device buffer shared with every rank (CUDA
+        IPC); allgather_output into it uses peer stores over NVLink."""
+        p = C.c_void_p()
+        _check(_lib.adaspmv_dist_alloc_peer_output(self.h, int(nbytes), C.byref(p)))
+        return int(p.value)
 
     def allgather_output(self, y: "MultiplyOutput", y_full_ptr: int) -> int:
         """Every rank's dense y block into the device buffer at y_full_ptr."""

@@ -1094,6 +1094,15 @@ int adaspmv_dist_bcast_vector(adaspmv_dist* d, adaspmv_vector* x, int root) {
     });
 }
 
+int adaspmv_dist_alloc_peer_output(adaspmv_dist* d, int64_t bytes, void** y_full_device) {
+    return guarded([&] {
+        need(d, "dist");
+        need(y_full_device, "y_full_device");
+        bind(d->ctx);
+        *y_full_device = ada::dist_alloc_peer_output(*d, bytes);
+    });
+}
+
 int adaspmv_dist_allgather_output(adaspmv_dist* d, adaspmv_output* y, void* y_full_device, int64_t* total) {
     return guarded([&] {
         need(d, "dist");

@@ -131,6 +131,7 @@ Dist* dist_create_host(Context& ctx, int rank, int world, adaspmv_allgather_fn f
 }
 
 Dist::~Dist() {
+    dist_release_peers(*this);
     if (comm) {
         const NcclApi& a = nccl();
         if (a.ok) a.CommDestroy(static_cast<ncclComm_t>(comm));
@@ -140,6 +141,21 @@ Dist::~Dist() {
 void Dist::host_allgather(const void* send, size_t bytes, void* recv) {
     if (host_fn(host_user, send, static_cast<int64_t>(bytes), recv) != 0)
         throw Error(ADASPMV_ERR_INTERNAL, "dist: the all-gather callback failed");
+}
+
+void Dist::allgather_bytes(const void* send, size_t bytes, void* recv) {
+    if (!comm) {
+        host_allgather(send, bytes, recv);
+        return;
+    }
+    const NcclApi& a = nccl();
+    Context& c = *ctx;
+    char* d = static_cast<char*>(d_bytes.ensure(bytes * static_cast<size_t>(world + 1)));
+    ADA_CUDA(cudaMemcpyAsync(d + bytes * world, send, bytes, cudaMemcpyHostToDevice, c.stream));
+    nccl_check(a.AllGather(d + bytes * world, d, bytes, ncclUint8, static_cast<ncclComm_t>(comm), c.stream),
+               "ncclAllGather");
+    ADA_CUDA(cudaMemcpyAsync(recv, d, bytes * world, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
 }
 
 void Dist::allgather_count(int64_t mine, std::vector<int64_t>& all) {
@@ -159,6 +175,7 @@ void Dist::allgather_count(int64_t mine, std::vector<int64_t>& all) {
 }
 
 int64_t Dist::allgatherv(const void* send, int64_t count, size_t elem, void* recv) {
+    if (peer_buf && recv == peer_buf) return dist_peer_allgatherv(*this, send, count, elem);  // NVLink puts (peer.cu)
     allgather_count(count, counts);
     int64_t total = 0, maxc = 0;
     for (int64_t v : counts) {

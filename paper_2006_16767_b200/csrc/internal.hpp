@@ -319,8 +319,18 @@ struct Dist {
     std::vector<int64_t> counts;  // per-rank counts of the last allgatherv
     DevBuf d_cnt;
     std::vector<char> h_send, h_recv;
+    DevBuf d_bytes;
+    // peer transport of the y all-gather (peer.cu): this rank's full-y buffer
+    // (cudaMalloc, IPC-exported) and every rank's, mapped here
+    void* peer_buf = nullptr;
+    int64_t peer_bytes = 0;
+    std::vector<void*> peer_ptrs;
+    std::vector<char> peer_opened;  // 1: opened from another process's IPC handle
+    DevBuf d_peers;                 // device copy of peer_ptrs
     ~Dist();
     void host_allgather(const void* send, size_t bytes, void* recv);
+    // every rank's `bytes` host bytes, in rank order (synchronises)
+    void allgather_bytes(const void* send, size_t bytes, void* recv);
     // every rank's `mine` (host; synchronises)
     void allgather_count(int64_t mine, std::vector<int64_t>& all);
     // concatenation in rank order of every rank's `count` elements of `elem`
@@ -328,6 +338,11 @@ struct Dist {
     int64_t allgatherv(const void* send, int64_t count, size_t elem, void* recv);
     void broadcast(void* buf, int64_t bytes, int root);
 };
+
+// peer.cu: the y all-gather as direct peer stores (CUDA IPC over NVLink)
+void* dist_alloc_peer_output(Dist& d, int64_t bytes);  // collective
+void dist_release_peers(Dist& d);
+int64_t dist_peer_allgatherv(Dist& d, const void* send, int64_t count, size_t elem);
 
 // One decision tree: flat node array.
 struct Tree {

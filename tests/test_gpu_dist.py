@@ -13,6 +13,7 @@
 * world 2 as two processes over gloo (paper_2006_16767_b200/multigpu.py,
   the structure bench.py runs at N > 1 with NCCL), both on cuda:0.
 """
+import ctypes as C
 import os
 import socket
 import threading
@@ -27,6 +28,11 @@ from paper_2006_16767_b200 import synth
 from tests.util import assert_dense_close, ref_and_bound
 
 pytestmark = pytest.mark.gpu
+
+
+def _cuda_driver():
+    """libcuda (the rank threads' current context is the device's primary one)."""
+    return C.CDLL("libcuda.so.1")
 
 
 class ThreadAllgather:
@@ -130,6 +136,44 @@ def test_dist_spmv_bcast_allgather(port, world):
 
 
 @pytest.mark.parametrize("world", [2, 3])
+def test_dist_peer_allgather(port, world):
+    """The y all-gather as peer stores (csrc/peer.cu) into the library's
+    IPC-shared full-y buffer: every rank's K0 block lands in every rank's
+    buffer, repeated (entry/exit barriers) and with fp32 blocks of odd length
+    (the byte tail of the 16-B put)."""
+    for dt in (np.float64, np.float32):
+        rows, cols, ro, ci, vals = synth.random_csr(3001, 1500, 0.01, seed=world, dtype=dt)
+        cuts = np.linspace(0, rows, world + 1).astype(np.int64)
+        xd = np.random.default_rng(1).uniform(-1, 1, cols).astype(dt)
+        y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, xd)
+
+        def rank_fn(r, ctx, d):
+            r0, r1 = int(cuts[r]), int(cuts[r + 1])
+            bro, bci, bv = _block(ro, ci, vals, r0, r1)
+            m = A.DualMatrix.from_csr(r1 - r0, cols, bro, bci, bv, ctx=ctx)
+            x = A.DeviceVector(cols, dt, ctx)
+            out = A.MultiplyOutput(ctx)
+            ptr = d.alloc_peer_output(rows * np.dtype(dt).itemsize)
+            full = []
+            for it in range(3):
+                x.set_dense(xd * (it + 1))
+                A.run_kernel(m, 0, x, out=out)
+                assert d.allgather_output(out, ptr) == rows
+                ctx.synchronize()
+                h = np.empty(rows, dt)
+                assert _cuda_driver().cuMemcpyDtoH_v2(C.c_void_p(h.ctypes.data), C.c_uint64(ptr),
+                                                      C.c_size_t(h.nbytes)) == 0
+                full.append(h)
+            return full
+
+        res = run_ranks(world, rank_fn)
+        for r in range(world):
+            for it in range(3):
+                assert_dense_close(res[r][it], y_ref * (it + 1), bound * (it + 1), dt,
+                                   f"peer all-gather rank {r} iter {it} {np.dtype(dt).name}")
+
+
+@pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("sr", [A.OR_AND, A.MIN_PLUS, A.PLUS_TIMES])
 def test_dist_bfs_levels(port, world, sr):
     bundle = A.SelectorBundle.load(S.DEFAULT_PATH)
@@ -211,7 +255,16 @@ def _proc(rank, world, port_no, q):
         ok_y = bool(np.all(np.abs(y - y_ref) <= 1e-12 * bound + 1e-300))
         yb = h.multiply(x_dense=np.ones(cols), gather=False, kernel=1).cpu().numpy()
         ok_block = yb.shape[0] == h.r1 - h.r0
-        q.put((rank, ok_bfs, ok_y, ok_block))
+        # the peer transport across processes: IPC handles opened on the same device
+        ptr = h.dist.alloc_peer_output(rows * 8)
+        h.multiply(x_sparse=(xi, xv), root=1, gather=False, kernel=6)
+        ok_peer = h.dist.allgather_output(h.out, ptr) == rows
+        h.ctx.synchronize()
+        yp = np.empty(rows, np.float64)
+        ok_peer = ok_peer and _cuda_driver().cuMemcpyDtoH_v2(C.c_void_p(yp.ctypes.data), C.c_uint64(ptr),
+                                                             C.c_size_t(yp.nbytes)) == 0
+        ok_peer = ok_peer and bool(np.all(np.abs(yp - y_ref) <= 1e-12 * bound + 1e-300))
+        q.put((rank, ok_bfs, ok_y, ok_block, ok_peer))
         g.close()
         h.close()
     except Exception as e:  # noqa: BLE001
@@ -235,5 +288,5 @@ def test_dist_two_processes_gloo_host_transport():
     for p in ps:
         p.join(timeout=60)
     for g in got:
-        assert len(g) == 4, g
+        assert len(g) == 5, g
         assert all(g[1:]), g
