@@ -432,6 +432,14 @@ int adaspmv_dist_bcast_vector(adaspmv_dist* d, adaspmv_vector* x, int root);
  * the dist.  Replaces: the y all-gather after a row-partitioned multiply
  * (partition.hpp:30-56 row blocks). */
 int adaspmv_dist_alloc_peer_output(adaspmv_dist* d, int64_t bytes, void** y_full_device);
+/* Kernel `kernel_index` on this rank's row block AND the y all-gather in one
+ * call: the row-bin K0/K2 store epilogue writes every row into every rank's
+ * peer output as it finishes it (the transfer overlaps the multiply bin by
+ * bin); other kernels are followed by the put kernel.  y also receives the
+ * local block.  *fused (optional) = 1 when the epilogue did it.  Collective. */
+int adaspmv_dist_run_allgather(adaspmv_dist* d, const adaspmv_matrix* block, adaspmv_vector* x, int kernel_index,
+                               const adaspmv_config* cfg, adaspmv_output* y, void* y_full_device, int64_t* total,
+                               int* fused);
 int adaspmv_dist_allgather_output(adaspmv_dist* d, adaspmv_output* y, void* y_full_device, int64_t* total);
 /* BFS (as adaspmv_bfs) over the square matrix whose rows row0 .. row0 +
  * rows(block) - 1 this rank holds; every level each rank multiplies its block

@@ -205,6 +205,7 @@ def load(path: Optional[os.PathLike] = None):
         "adaspmv_dist_bcast_vector": [vp, vp, C.c_int],
         "adaspmv_dist_allgather_output": [vp, vp, vp, P(i64)],
         "adaspmv_dist_alloc_peer_output": [vp, i64, P(vp)],
+        "adaspmv_dist_run_allgather": [vp, vp, vp, C.c_int, vp, vp, vp, P(i64), P(C.c_int)],
         "adaspmv_dist_bfs": [vp, vp, i64, i64, C.c_int, vp, C.c_int, vp, P(i64), vp, i64],
     }
     for name, args in sigs.items():
@@ -1075,6 +1076,18 @@ class Dist:
         p = C.c_void_p()
         _check(_lib.adaspmv_dist_alloc_peer_output(self.h, int(nbytes), C.byref(p)))
         return int(p.value)
+
+    def run_allgather(self, block: DualMatrix, kid: int, x: "DeviceVector", y_full_ptr: int,
+                      cfg: Optional[KernelConfig] = None, out: Optional["MultiplyOutput"] = None):
+        """Collective: kernel `kid` on this rank's block with the y all-gather
+        into the peer output fused into its store epilogue (row-bin K0/K2) or
+        following it.  Returns (total rows, fused)."""
+        out = out or MultiplyOutput(self.ctx)
+        c = (cfg or KernelConfig())._c()
+        tot, fused = C.c_int64(), C.c_int()
+        _check(_lib.adaspmv_dist_run_allgather(self.h, block.h, x.h, int(kid), C.byref(c), out.h,
+                                               C.c_void_p(y_full_ptr), C.byref(tot), C.byref(fused)))
+        return tot.value, bool(fused.value)
 
     def allgather_output(self, y: "MultiplyOutput", y_full_ptr: int) -> int:
         """Every rank's dense y block into the device buffer at y_full_ptr."""

@@ -1103,6 +1103,23 @@ int adaspmv_dist_alloc_peer_output(adaspmv_dist* d, int64_t bytes, void** y_full
     });
 }
 
+int adaspmv_dist_run_allgather(adaspmv_dist* d, const adaspmv_matrix* block, adaspmv_vector* x, int kernel_index,
+                               const adaspmv_config* cfg, adaspmv_output* y, void* y_full_device, int64_t* total,
+                               int* fused) {
+    return guarded([&] {
+        need(d, "dist");
+        need(block, "matrix");
+        need(x, "vector");
+        need(y, "output");
+        need(y_full_device, "y_full");
+        bind(d->ctx);
+        adaspmv_config c{};
+        if (cfg) c = *cfg;
+        const int64_t t = ada::dist_run_allgather(*d, *block, *x, kernel_index, c, *y, y_full_device, fused);
+        if (total) *total = t;
+    });
+}
+
 int adaspmv_dist_allgather_output(adaspmv_dist* d, adaspmv_output* y, void* y_full_device, int64_t* total) {
     return guarded([&] {
         need(d, "dist");

@@ -102,6 +102,13 @@ struct Context {
     bool counters = false;  // KernelCounters per run (adaspmv_ctx_set_counters)
     bool bfs_host_loop = false;  // adaspmv_ctx_set_bfs_loop: host-driven BFS level loop, or the device graph (default)
     unsigned long long* ctr = nullptr;  // the running output's device counters (kernels' last argument)
+    // fused distributed y all-gather (peer.cu dist_run_allgather): while set,
+    // a kernel whose store epilogue supports it also writes each row to every
+    // rank's full y (peer_dst[world], at row peer_row0 + row) and sets peer_fused
+    char* const* peer_dst = nullptr;
+    int peer_world = 0;
+    int64_t peer_row0 = 0;
+    bool peer_fused = false;
     // general scratch (reused by every call; calls on a context are serialised)
     // [0..3] sort write-back keys/values (double buffered), [4] vector scans,
     // [5] matrix build scans, [6..9] radix counts / scan / segment sums / flags
@@ -343,6 +350,11 @@ struct Dist {
 void* dist_alloc_peer_output(Dist& d, int64_t bytes);  // collective
 void dist_release_peers(Dist& d);
 int64_t dist_peer_allgatherv(Dist& d, const void* send, int64_t count, size_t elem);
+// kernel `k` on this rank's row block, its y rows stored into every rank's
+// full y (the peer output) by the kernel's own epilogue where it can (the
+// row-bin K0/K2), else by the put kernel; *fused reports which
+int64_t dist_run_allgather(Dist& d, const Matrix& m, Vector& x, int k, const adaspmv_config& cfg, Output& y,
+                           void* y_full, int* fused);
 
 // One decision tree: flat node array.
 struct Tree {

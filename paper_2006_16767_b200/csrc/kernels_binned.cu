@@ -39,6 +39,8 @@
 #include <numeric>
 #include <vector>
 
+#include <type_traits>
+
 #include "device.cuh"
 #include "internal.hpp"
 #include "kernels.hpp"
@@ -201,13 +203,14 @@ __global__ void gather_spread_kernel(const int64_t* __restrict__ ro, const int32
 // streamed through L2 and double the entries per x line (fewer L1
 // wavefronts per gather instruction).
 template <class V, int SR, bool MASKED, int CL = 1, int kBinUnroll = 8, bool NOALLOC = false,
-          int kBinThreads = 1024, bool PIPE = false>
+          int kBinThreads = 1024, bool PIPE = false, bool FUSE = false>
 __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
     int64_t tile0, BinRows br, int rbits, int cw, int64_t nchunks,
     const int64_t* __restrict__ tiles, const int32_t* __restrict__ tile_bin,
     const int32_t* __restrict__ tile_multi, const int64_t* __restrict__ chunk_off,
     const uint32_t* __restrict__ pk, const V* __restrict__ bv, const V* __restrict__ x,
-    const uint32_t* __restrict__ mask, V* __restrict__ y, unsigned long long* __restrict__ ctr) {
+    const uint32_t* __restrict__ mask, V* __restrict__ y, unsigned long long* __restrict__ ctr,
+    char* const* __restrict__ peers, int npeers, int64_t peer_row0) {
     using S = Semiring<SR, V>;
     extern __shared__ __align__(16) unsigned char bin_smem[];
     V* ys = reinterpret_cast<V*>(bin_smem);
@@ -374,6 +377,10 @@ __global__ void __launch_bounds__(kBinThreads, 1) binned_row_kernel(
         }
         if (mode == 0) {  // the tile owns its bin's rows: plain stores
             y[row] = v;
+            // fused y all-gather (peer.cu): the same row into every rank's
+            // full y over NVLink, at this rank's block offset
+            if constexpr (FUSE)
+                for (int p = 0; p < npeers; ++p) reinterpret_cast<V*>(peers[p])[peer_row0 + row] = v;
         } else if (mode == 2) {  // owns the rows in a later column panel: y += segment
             if (v != S::zero()) y[row] = S::add(y[row], v);
         } else if (v != S::zero()) {  // partial segment: combine into the identity-filled y
@@ -823,6 +830,12 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
     lk.unlock();
     if (m.rows == 0) return;
     if (L.multi) fill_value<V, SR>(ctx, y, m.rows);
+    // the distributed y all-gather rides on the store epilogue when every
+    // tile owns its rows (plain stores, one pass over the panels)
+    const bool fuse = ctx.peer_dst && !L.multi && L.panel_tile0.size() == 2 && L.cluster == 1;
+    char* const* peers = fuse ? ctx.peer_dst : nullptr;
+    const int npeers = fuse ? ctx.peer_world : 0;
+    if (fuse) ctx.peer_fused = true;
     const size_t smem = sizeof(V) * static_cast<size_t>(L.R);
     const int nt = 1024;
     auto launch = [&](auto kern, int cl, int64_t t0, int64_t nt_) {
@@ -845,7 +858,7 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
                                     L.cw, L.nchunks, L.tiles.as<int64_t>(),
                                     L.tile_bin.as<int32_t>(), L.tile_multi.as<int32_t>(),
                                     L.chunk_off.as<int64_t>(), L.pk.as<uint32_t>(), L.bv.as<V>(), x, mask, y,
-                                    ctx.ctr));
+                                    ctx.ctr, peers, npeers, ctx.peer_row0));
         ADA_LAUNCHED(ctx);
     };
     for (size_t p = 0; p + 1 < L.panel_tile0.size(); ++p) {  // panels in column order, same stream
@@ -861,14 +874,24 @@ void run_row_binned(Context& ctx, const Matrix& m, const V* x, const uint32_t* m
             // hub columns reuse L1 lines: 564 vs 525 us, so skewed ones keep
             // it); fp64 keeps the plain loop (the pipelined one spills at 64
             // registers)
-            if (mask) {
-                launch(binned_row_kernel<V, SR, true, 1>, 1, t0, t1 - t0);
-            } else if constexpr (sizeof(V) == 4) {
-                if (m.feat[8] > 0.5) launch(binned_row_kernel<V, SR, false, 1, 8, false, 1024, true>, 1, t0, t1 - t0);
-                else launch(binned_row_kernel<V, SR, false, 1, 8, true, 1024, true>, 1, t0, t1 - t0);
+#define ADA_BIN_LAUNCH(F)                                                                                     \
+    if (mask) {                                                                                               \
+        launch(binned_row_kernel<V, SR, true, 1, 8, false, 1024, false, F>, 1, t0, t1 - t0);                  \
+    } else if constexpr (sizeof(V) == 4) {                                                                    \
+        if (m.feat[8] > 0.5)                                                                                  \
+            launch(binned_row_kernel<V, SR, false, 1, 8, false, 1024, true, F>, 1, t0, t1 - t0);              \
+        else                                                                                                  \
+            launch(binned_row_kernel<V, SR, false, 1, 8, true, 1024, true, F>, 1, t0, t1 - t0);               \
+    } else {                                                                                                  \
+        launch(binned_row_kernel<V, SR, false, 1, 8, false, 1024, false, F>, 1, t0, t1 - t0);                 \
+    }
+            // F: the fused all-gather epilogue (only when requested)
+            if (fuse) {
+                ADA_BIN_LAUNCH(true)
             } else {
-                launch(binned_row_kernel<V, SR, false, 1>, 1, t0, t1 - t0);
+                ADA_BIN_LAUNCH(false)
             }
+#undef ADA_BIN_LAUNCH
         }
     }
 }

@@ -116,4 +116,47 @@ int64_t dist_peer_allgatherv(Dist& d, const void* send, int64_t count, size_t el
     return total;
 }
 
+int64_t dist_run_allgather(Dist& d, const Matrix& m, Vector& x, int k, const adaspmv_config& cfg, Output& y,
+                           void* y_full, int* fused) {
+    if (!d.peer_buf || y_full != d.peer_buf) invalid("dist: y_full must be the peer output (adaspmv_dist_alloc_peer_output)");
+    Context& c = *d.ctx;
+    c.sync();  // this rank's earlier work on its full y is done ...
+    d.allgather_count(m.rows, d.counts);  // ... everywhere (entry barrier), and the block offsets
+    int64_t total = 0, off = 0;
+    for (int g = 0; g < d.world; ++g) {
+        if (g < d.rank) off += d.counts[static_cast<size_t>(g)];
+        total += d.counts[static_cast<size_t>(g)];
+    }
+    const size_t elem = static_cast<size_t>(m.vbytes());
+    if (static_cast<int64_t>(total * elem) > d.peer_bytes) invalid("dist: the peer output is too small");
+    c.peer_dst = d.d_peers.as<char*>();
+    c.peer_world = d.world;
+    c.peer_row0 = off;
+    c.peer_fused = false;
+    try {
+        run_kernel(c, m, x, k, cfg, y);
+    } catch (...) {
+        c.peer_dst = nullptr;
+        c.peer_world = 0;
+        throw;
+    }
+    const bool f = c.peer_fused;
+    c.peer_dst = nullptr;
+    c.peer_world = 0;
+    c.peer_fused = false;
+    if (!f && m.rows > 0) {  // the put kernel after the multiply
+        output_ensure_dense(c, y);
+        const int64_t bytes = m.rows * static_cast<int64_t>(elem);
+        const int64_t blocks = std::min<int64_t>((bytes / 16 + 255) / 256 + 1, static_cast<int64_t>(c.sm_count) * 8);
+        peer_put_kernel<<<static_cast<unsigned>(blocks), 256, 0, c.stream>>>(
+            static_cast<const char*>(y.dense.p), bytes, d.d_peers.as<char*>(), d.world, off * static_cast<int64_t>(elem));
+        ADA_LAUNCHED(c);
+    }
+    if (fused) *fused = f ? 1 : 0;
+    c.sync();
+    std::vector<int64_t> done;
+    d.allgather_count(0, done);  // exit barrier: every rank's stores are complete
+    return total;
+}
+
 }  // namespace ada

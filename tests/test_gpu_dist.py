@@ -174,6 +174,67 @@ def test_dist_peer_allgather(port, world):
 
 
 @pytest.mark.parametrize("world", [2, 3])
+def test_dist_fused_allgather_epilogue(port, world):
+    """adaspmv_dist_run_allgather: the row-bin K0/K2 store epilogue writes each
+    row into every rank's full y (fused = True); K1 (CSR) and K6 (column) are
+    followed by the put kernel (fused = False).  Every rank's buffer must hold
+    the whole y, three rounds in a row, under all three semirings for K0."""
+    dt = np.float32
+    rows, cols, ro, ci, vals = synth.random_csr(6007, 4000, 0.004, seed=world + 10, dtype=dt)
+    cuts = np.linspace(0, rows, world + 1).astype(np.int64)
+    xd = np.random.default_rng(2).uniform(-1, 1, cols).astype(dt)
+    y_ref, bound = ref_and_bound(port, rows, ro, ci, vals, xd)
+    xi = np.nonzero(xd)[0].astype(np.int64)
+
+    def rank_fn(r, ctx, d):
+        r0, r1 = int(cuts[r]), int(cuts[r + 1])
+        bro, bci, bv = _block(ro, ci, vals, r0, r1)
+        m = A.DualMatrix.from_csr(r1 - r0, cols, bro, bci, bv, ctx=ctx)
+        x = A.DeviceVector(cols, dt, ctx)
+        ptr = d.alloc_peer_output(rows * 4)
+        got = []
+        for it, (k, cfg) in enumerate(((0, A.KernelConfig(row_layout=2)), (2, A.KernelConfig(row_layout=2)),
+                                       (1, None), (6, None), (0, A.KernelConfig(row_layout=2)))):
+            if k == 6:
+                x.set_sparse(xi, xd[xi])
+            else:
+                x.set_dense(xd)
+            x.prepare(k)
+            try:
+                tot, fused = d.run_allgather(m, k, x, ptr, cfg)
+            except Exception as e:
+                raise AssertionError(f"rank {r} iteration {it} K{k}: {e}") from e
+            assert tot == rows
+            h = np.empty(rows, dt)
+            assert _cuda_driver().cuMemcpyDtoH_v2(C.c_void_p(h.ctypes.data), C.c_uint64(ptr),
+                                                  C.c_size_t(h.nbytes)) == 0
+            got.append((k, fused, h))
+        # semirings through the fused epilogue (OR_AND / MIN_PLUS exact)
+        for sr in (A.OR_AND, A.MIN_PLUS):
+            xs = np.where(xd > 0, xd, np.inf).astype(dt) if sr == A.MIN_PLUS else xd
+            x.set_dense(xs)
+            x.prepare(0)
+            tot, fused = d.run_allgather(m, 0, x, ptr, A.KernelConfig(row_layout=2, semiring=sr))
+            h = np.empty(rows, dt)
+            assert _cuda_driver().cuMemcpyDtoH_v2(C.c_void_p(h.ctypes.data), C.c_uint64(ptr),
+                                                  C.c_size_t(h.nbytes)) == 0
+            got.append((("sr", sr), fused, h, xs))
+        return got
+
+    res = run_ranks(world, rank_fn)
+    for r in range(world):
+        for item in res[r]:
+            k, fused, h = item[:3]
+            if isinstance(k, tuple):
+                sr, xs = k[1], item[3]
+                ref = port.semiring_multiply(rows, ro, ci, vals, xs, sr)
+                assert fused and h.tobytes() == ref.tobytes(), (r, sr)
+            else:
+                assert fused == (k in (0, 2)), (r, k, fused)
+                assert_dense_close(h, y_ref, bound, dt, f"world {world} rank {r} K{k} fused={fused}")
+
+
+@pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("sr", [A.OR_AND, A.MIN_PLUS, A.PLUS_TIMES])
 def test_dist_bfs_levels(port, world, sr):
     bundle = A.SelectorBundle.load(S.DEFAULT_PATH)
