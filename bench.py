@@ -88,7 +88,7 @@ class ClockSampler:
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device=0, period_ms=50):
+    def __init__(self, device=0, period_ms=10):
         self.device = device
         self.period_ms = period_ms
         self.rows = []
@@ -96,6 +96,7 @@ class ClockSampler:
         self._t = None
         self._first = threading.Event()
         self._on = False
+        self._grab = False  # a window shorter than one period: keep the next sample
 
     def _run(self):
         # one long-lived `nvidia-smi -lms` reader: a sample every period_ms
@@ -105,32 +106,61 @@ class ClockSampler:
             if not line:
                 continue
             self._first.set()
-            if self._on:
+            if self._on or (self._grab and not self.rows):
                 self.rows.append([s.strip() for s in line.split(",")])
 
+    def _poll(self):
+        # fallback: one nvidia-smi call per sample
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out and self._on:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
     def __enter__(self):
+        self._stop = threading.Event()
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", f"-lms={self.period_ms}"],
+                 "--format=csv,noheader,nounits", f"--loop-ms={self.period_ms}"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
             self._first.wait(5.0)  # the sampler is live before the timed region opens
         except Exception:
             self._proc = None
+        if not self._first.is_set():  # no loop mode: poll instead
+            self._close_proc()
+            self._t = threading.Thread(target=self._poll, daemon=True)
+            self._t.start()
         self._on = True
         return self
 
-    def __exit__(self, *a):
-        self._on = False
+    def _close_proc(self):
         if self._proc is not None:
             self._proc.terminate()
             try:
                 self._proc.wait(timeout=5)
             except Exception:
                 self._proc.kill()
-            self._t.join(timeout=5)
+            self._proc = None
+
+    def __exit__(self, *a):
+        self._on = False
+        if not self.rows and self._proc is not None:  # the window fell between two samples
+            self._grab = True
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 0.5:
+                time.sleep(0.005)
+        self._stop.set()
+        self._close_proc()
+        if self._t is not None:
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.rows:
